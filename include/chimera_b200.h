@@ -1,0 +1,268 @@
+/*
+ * chimera_b200.h -- C-ABI of libchimera_sm100a.so, the B200 (sm_100a) per-tick
+ * scheduling hot path of Chimera (arxiv 2603.22206).
+ *
+ * Every entry point is stream-ordered and asynchronous: it enqueues kernels on
+ * `stream` and returns. Device buffers are plain pointers owned by the caller
+ * (the Python host layer allocates them as torch tensors); the library owns no
+ * device memory. Nothing in these signatures is a C++ or torch type.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/hetsched):
+ *   chm_prepare_rows       balancer.py:100-103   (assignment lookup `monitor.assignment`)
+ *   chm_encoder_forward    router.py:39-42       (Router.score -> ConfidenceVector)
+ *   chm_predict_*          predictor.py:22-27    (Predictor.predict) and the concrete
+ *                          predictors at predictor.py:30-45, 65-108
+ *   chm_schedule_rows      balancer.py:89-129    (schedule_request = Alg. 1), with
+ *                          estimate_load 49-60, select_model 63-77,
+ *                          monitor.py:55-63 (assign), 86-96 (record_dispatch),
+ *                          122-129 (in_flight_sum), engine.py:145-158 (enqueue)
+ *   chm_queue_tick         engine.py:309-374     (EngineSim._push/_pop_min/_iterate/
+ *                          _age_queued, QueueEntry.sort_key 55-69)
+ *
+ * Errors: functions return chm_status. Conditions the reference raises as
+ * exceptions inside a batch are detected on the device and reported in a
+ * caller-provided int32[4] error word {code, row, model, aux}; the host maps
+ * the code to the same hetsched.errors class (see paper_2603_22206_b200/errors.py).
+ */
+#ifndef CHIMERA_B200_H
+#define CHIMERA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHM_MAX_MODELS 8
+#define CHM_MAX_STAGES 32
+
+typedef enum chm_status {
+  CHM_OK = 0,
+  CHM_ERR_INVALID_ARG = 1,          /* bad sizes / null pointers (host-side check) */
+  CHM_ERR_VALIDATION = 2,           /* errors.ValidationError: score outside [0,1]
+                                       (router.py:27-28) or out_tokens < 0
+                                       (engine.py:285-286) */
+  CHM_ERR_NEGATIVE_PREDICTION = 3,  /* ValueError (monitor.py:89-90) */
+  CHM_ERR_DUPLICATE_REQUEST = 4,    /* errors.DuplicateRequest (monitor.py:91-94) */
+  CHM_ERR_TIME_BACKWARDS = 5,       /* ValueError (engine.py:140-143) */
+  CHM_ERR_NAN_PREDICTION = 6,       /* NaN predicted tokens: rejected (reference
+                                       behaviour is heap-order dependent) */
+  CHM_ERR_INVALID_STATE = 7,        /* device state violates an engine invariant */
+  CHM_ERR_CAPACITY = 8,             /* a queue segment exceeds its capacity */
+  CHM_ERR_UNSUPPORTED = 9,          /* option not implemented on device */
+  CHM_ERR_CUDA = 10,                /* CUDA launch / runtime failure */
+  CHM_ERR_UNKNOWN_REQUEST = 11,     /* errors.UnknownRequest (monitor.py:104-105) */
+  CHM_ERR_UNKNOWN_STAGE = 12        /* errors.UnknownStage (workload.py:143-147) */
+} chm_status;
+
+/* ---- static configuration ------------------------------------------------ */
+
+/* Pool (profiles.py:17-71). Index order MUST be sorted(model_id), the
+ * tie-break order everywhere in the reference (profiles.py:56-59). */
+typedef struct chm_pool {
+  int32_t n_models;
+  int32_t max_batch_size[CHM_MAX_MODELS];
+  double decode_ms_per_token[CHM_MAX_MODELS];
+} chm_pool;
+
+/* BalancerConfig (balancer.py:26-37). */
+typedef struct chm_balancer_cfg {
+  double latency_slack;
+  double confidence_margin;
+} chm_balancer_cfg;
+
+/* AgingConfig (engine.py:36-52). enabled=0 <=> starvation_threshold = inf. */
+typedef struct chm_aging_cfg {
+  int32_t enabled;
+  int32_t starvation_threshold;
+  int32_t running_quantum;
+  int32_t demote_while_queued;
+} chm_aging_cfg;
+
+/* ---- activity monitor + per-engine counters (device state) --------------- */
+
+typedef struct chm_monitor_state {
+  int32_t n_programs;
+  double* inflight_sum;      /* [K] Neumaier running sum of live predictions   */
+  double* inflight_comp;     /* [K] Neumaier compensation term                 */
+  int64_t* inflight_count;   /* [K] live in-flight entries                     */
+  int8_t* assignment;        /* [n_programs] model index, -1 = unassigned      */
+  uint32_t* stage_bits;      /* [n_programs] bit (stage-1) set while in flight */
+  uint64_t* batch_stamp;     /* [n_programs] scratch, init 0xff.. (repeat detection) */
+  double* engine_clock;      /* [K] EngineSim.now                              */
+  int64_t* engine_seq;       /* [K] next QueueEntry.seq                        */
+  int32_t* engine_running;   /* [K] len(EngineSim.running)                     */
+  int32_t* engine_queued;    /* [K] len(EngineSim._queued)                     */
+  int64_t* engine_iterations;/* [K] EngineSim.iterations                       */
+} chm_monitor_state;
+
+/* ---- one batch of requests, in arrival order ----------------------------- */
+
+typedef struct chm_rows {
+  int32_t n_rows;
+  const int32_t* program;    /* [B] dense program index                        */
+  const int32_t* stage;      /* [B] 1-based stage index                        */
+  const double* arrival;     /* [B] Request.arrival_time (ms)                  */
+  const int32_t* out_tokens; /* [B*K] rec.out_tokens(stage, m) per model       */
+  const int64_t* handle;     /* [B] opaque request handle stored in the queue  */
+} chm_rows;
+
+/* Scratch produced by chm_prepare_rows and consumed by chm_schedule_rows. */
+typedef struct chm_row_scratch {
+  int32_t* first_row;        /* [B] first row of the same program in the batch */
+  int8_t* pre_model;         /* [B] assignment before the batch (-1 none)      */
+  int32_t* route_rows;       /* [B] compacted rows that need the router        */
+  int32_t* n_route;          /* [1]                                            */
+  uint64_t* qual;            /* [B] per-row qualify masks (K*K bits)           */
+  uint32_t* rank;            /* [B] per-row packed descending-q rank (4b/model)*/
+  uint32_t* flags;           /* [B] per-row precomputed flags                  */
+} chm_row_scratch;
+
+typedef struct chm_decisions {
+  int32_t* model;            /* [B] Decision.model (index)                     */
+  double* priority;          /* [B] Decision.priority                          */
+  uint8_t* flags;            /* [B] bit0 used_cached_assignment, bit1 admitted
+                                    on enqueue, bit2 queued                    */
+  int64_t* seq;              /* [B] QueueEntry.seq on the chosen engine        */
+  double* loads;             /* [B*K] Decision.estimated_loads (NULL = skip)   */
+  int32_t* n_committed;      /* [1] rows fully applied                         */
+  int32_t* error;            /* [4] {code,row,model,aux}                       */
+} chm_decisions;
+
+/* ---- STJF + aging engine queues (device state, SoA, seq order) ----------- */
+
+typedef struct chm_queue_state {
+  int32_t capacity;          /* entries per engine segment                     */
+  double* priority;          /* [K*cap] QueueEntry.priority                    */
+  double* arrival;           /* [K*cap] QueueEntry.arrival                     */
+  int64_t* seq;              /* [K*cap] QueueEntry.seq                         */
+  int64_t* handle;           /* [K*cap]                                        */
+  int32_t* out_tokens;       /* [K*cap]                                        */
+  int32_t* level;            /* [K*cap] starvation_level                       */
+  int32_t* count;            /* [K*cap] starvation_count                       */
+  int32_t* quantum;          /* [K*cap] quantum_counter                        */
+  int32_t* order;            /* [K*cap] out: STJF order of the remaining queue */
+  int64_t* admitted;         /* [K*cap] out: handles admitted this call, in order */
+  int32_t* n_admitted;       /* [K] out                                        */
+  int32_t* n_promoted;       /* [K] out: promotions this call                  */
+  uint8_t* arrival_unsorted; /* [K] sticky: arrival not monotone in seq        */
+} chm_queue_state;
+
+/* ---- router encoder (BERT-style post-LN, CLS -> Linear(H,K) -> sigmoid) --- */
+
+typedef struct chm_encoder_cfg {
+  int32_t n_layers, hidden, n_heads, ffn, vocab, max_pos, n_models;
+  float ln_eps;
+} chm_encoder_cfg;
+
+/* bf16 weights, row-major [out_features, in_features] (nn.Linear layout). */
+typedef struct chm_encoder_weights {
+  const void* word_emb;      /* [vocab, H]  bf16 */
+  const void* pos_emb;       /* [max_pos, H] bf16 */
+  const void* type_emb;      /* [H] bf16 (token type 0) */
+  const float* emb_ln_g; const float* emb_ln_b;           /* [H] */
+  const void* const* w_qkv;  /* L x [3H, H] bf16 */
+  const float* const* b_qkv; /* L x [3H] */
+  const void* const* w_o;    /* L x [H, H] */
+  const float* const* b_o;   /* L x [H] */
+  const float* const* ln1_g; const float* const* ln1_b;   /* L x [H] */
+  const void* const* w_1;    /* L x [F, H] */
+  const float* const* b_1;   /* L x [F] */
+  const void* const* w_2;    /* L x [H, F] */
+  const float* const* b_2;   /* L x [H] */
+  const float* const* ln2_g; const float* const* ln2_b;   /* L x [H] */
+  const float* head_w;       /* [K, H] fp32 */
+  const float* head_b;       /* [K] */
+} chm_encoder_weights;
+
+/* Activation workspace for up to `max_tokens` = B*S tokens (bf16 unless noted). */
+typedef struct chm_encoder_workspace {
+  int64_t max_tokens;
+  void* x;                   /* [T, H]  residual stream                        */
+  void* qkv;                 /* [T, 3H]                                        */
+  void* ctx;                 /* [T, H]  attention output                       */
+  void* tmp;                 /* [T, H]  pre-LN sum                             */
+  void* ffn;                 /* [T, F]                                         */
+} chm_encoder_workspace;
+
+/* ---- entry points -------------------------------------------------------- */
+
+const char* chm_version(void);
+const char* chm_status_string(int32_t status);
+
+/* Number of SMs and compute capability of `device` (for diagnostics). */
+chm_status chm_device_info(int32_t device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* Resolve, per row, the pre-batch assignment (balancer.py:100-103), the first
+ * row of the same program inside the batch, and compact the rows that need
+ * the router (first occurrence, no assignment). `epoch_counter` is a device
+ * uint32 shared by every call on `mon->batch_stamp`; the kernel increments
+ * it, so the call can be replayed from a CUDA graph. */
+chm_status chm_prepare_rows(const chm_monitor_state* mon, const chm_rows* rows,
+                            const chm_row_scratch* scratch, uint32_t* epoch_counter,
+                            void* stream);
+
+/* K5: EmpiricalQuantilePredictor (predictor.py:65-108) as a dense table with
+ * the fallback chain resolved at build time: table[(wf*(S_cap+1) + st)*K + m],
+ * wf in [0, n_wf] (n_wf = unseen workflow), st in [0, S_cap] (0 = unseen stage).
+ * yhat[B*K] receives the prediction for every model. */
+chm_status chm_predict_quantile(const double* table, int32_t n_wf, int32_t s_cap,
+                                int32_t n_models, const int32_t* workflow,
+                                const int32_t* stage, int32_t n_rows, double* yhat,
+                                void* stream);
+/* K5: OraclePredictor (predictor.py:30-36): suffix sum of stage outputs,
+ * stage_out[(row*max_stages + j)*K + m], j 0-based. */
+chm_status chm_predict_oracle(const int32_t* stage_out, const int32_t* n_stages,
+                              const int32_t* stage, int32_t max_stages,
+                              int32_t n_models, int32_t n_rows, double* yhat,
+                              int32_t* error, void* stream);
+/* K5: InputLengthPredictor (predictor.py:39-45). */
+chm_status chm_predict_input_length(const int32_t* input_tokens, int32_t n_models,
+                                    int32_t n_rows, double* yhat, void* stream);
+
+/* K6: serial-exact fused monitor + load estimate + selection + dispatch for a
+ * batch (B calls of schedule_request in row order). `scores` [B*K] must hold
+ * router output for every routed row; `yhat` [B*K] the predictor output. */
+chm_status chm_schedule_rows(const chm_pool* pool, const chm_balancer_cfg* cfg,
+                             const chm_monitor_state* mon, const chm_rows* rows,
+                             const chm_row_scratch* scratch, const float* scores,
+                             const double* yhat, const chm_decisions* out,
+                             void* stream);
+
+/* K7 phase A: `n_complete[m]` running requests of engine m finish at `now`;
+ * each frees a slot and runs one scheduling iteration (engine.py:232-241,
+ * 328-338): admit the queue minimum, then age every queued entry. */
+chm_status chm_queue_complete(const chm_pool* pool, const chm_aging_cfg* aging,
+                              const chm_monitor_state* mon, const chm_queue_state* q,
+                              const int32_t* n_complete, int32_t* error,
+                              void* stream);
+
+/* K7 phase B: append the rows chm_schedule_rows marked `queued`, then run
+ * `n_iterations` explicit scheduling iterations per engine (admit into free
+ * slots, age the rest), and write the final STJF order of every queue. */
+chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* aging,
+                          const chm_monitor_state* mon, const chm_queue_state* q,
+                          const chm_rows* rows, const chm_decisions* dec,
+                          int32_t n_iterations, int32_t* error, void* stream);
+
+/* Router encoder forward over `n_seq` sequences of `seq_len` token ids, only
+ * for the rows listed in `rows` (NULL = all, n_seq rows). Writes
+ * q[rows[i]*K + m] = sigmoid(head(h_CLS)). `scratch_q` may be NULL. */
+chm_status chm_encoder_forward(const chm_encoder_cfg* cfg, const chm_encoder_weights* w,
+                               const chm_encoder_workspace* ws, const int32_t* token_ids,
+                               const int32_t* rows, const int32_t* n_rows_dev,
+                               int32_t n_seq, int32_t seq_len, float* q_out,
+                               void* stream);
+
+/* Standalone tcgen05 GEMM: C[M,N] = A[M,K] . B[N,K]^T (+bias[N]) (+GELU)
+ * (+residual[M,N]); bf16 in/out, fp32 accumulate. epilogue: 0 none, 1 bias,
+ * 2 bias+gelu, 3 bias+residual. */
+chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bias,
+                         const void* residual, int32_t M, int32_t N, int32_t K,
+                         int32_t epilogue, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHIMERA_B200_H */

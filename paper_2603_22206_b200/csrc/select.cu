@@ -1,0 +1,520 @@
+// K6 -- fused activity monitor + load estimate + confidence-gated slack
+// selection + dispatch, serial-exact.
+//
+// Reference semantics (hetsched, /root/reference/pkg/src/hetsched):
+//   schedule_request      balancer.py:89-129  (Algorithm 1)
+//   estimate_load         balancer.py:49-60   L[m] = (P_m * d_m) / b_m, fp64
+//   select_model          balancer.py:63-77   argmin (L, id); limit = (1+tau)*L_fast;
+//                                             first by (-q, id) with L<=limit and
+//                                             q >= q_fast + margin; else m_fast
+//   ActivityMonitor       monitor.py:52-63, 86-96, 122-129
+//                         P_m = sum(entries.values()) -- CPython >= 3.12 sums
+//                         floats with Neumaier compensation in insertion order,
+//                         so a running (s, c) pair per model reproduces every
+//                         intermediate P_m bit for bit.
+//   EngineSim.enqueue     engine.py:145-158, 135-143, 283-293 (clock, seq, admit)
+//
+// Decision i depends on P after decisions 0..i-1 (record_dispatch happens
+// inside schedule_request), so the recurrence is serial. Everything that does
+// not depend on P is precomputed in parallel: per-row rank of every model in
+// descending-q order and, per candidate m_fast, the mask of models that clear
+// the confidence margin. The serial step then needs only K fp64 compares for
+// argmin, one multiply for the limit, K compares for the slack mask, a few
+// integer ops, one Neumaier update and one mul+div for the changed model.
+//
+// Layout: one CTA of 256 threads. Lane 0 of warp 0 runs the chain with the K
+// (s, c, L) triples in registers; per-engine counters that do not feed back
+// into the selection live in shared memory. The other 7 warps stream the
+// next chunk of per-row inputs into a shared-memory double buffer while the
+// chain consumes the current one.
+#include "common.cuh"
+
+namespace chm {
+
+enum : uint32_t {
+  RF_CACHED_PRE = 1u,    // program already assigned before the batch
+  RF_REPEAT = 2u,        // an earlier row of this batch has the same program
+  RF_BAD_SCORE = 4u,     // routed row has a score outside [0,1] (or NaN)
+  RF_DUP_PRE = 8u,       // (program, stage) already in flight before the batch
+  RF_BAD_STAGE = 16u,    // stage outside [1, 32]
+  RF_BAD_PROGRAM = 32u,  // program index outside [0, n_programs)
+  RF_ROUTE = 64u,        // row takes the routing branch
+};
+
+enum : uint8_t { DF_CACHED = 1u, DF_ADMITTED = 2u, DF_QUEUED = 4u };
+
+// ---------------------------------------------------------------------------
+// chm_prepare_rows: assignment lookup + in-batch repeat detection + compaction
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) prepare_rows_kernel(chm_monitor_state mon,
+                                                            chm_rows rows,
+                                                            chm_row_scratch sc,
+                                                            uint32_t* epoch_counter) {
+  const int B = rows.n_rows;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_warps = blockDim.x >> 5;
+  const uint32_t epoch = *epoch_counter + 1u;
+  const unsigned long long hi = (unsigned long long)(~epoch) << 32;
+  // Newer epochs have smaller high words, so atomicMin keeps the first row of
+  // the current batch and overwrites any stale stamp.
+  for (int i = tid; i < B; i += blockDim.x) {
+    int p = rows.program[i];
+    if (p >= 0 && p < mon.n_programs)
+      atomicMin(reinterpret_cast<unsigned long long*>(mon.batch_stamp) + p,
+                hi | (unsigned long long)(uint32_t)i);
+  }
+  __syncthreads();
+  __shared__ int s_warp[32];
+  __shared__ int s_total;
+  int base_out = 0;
+  for (int base = 0; base < B; base += blockDim.x) {
+    const int i = base + tid;
+    bool route = false;
+    if (i < B) {
+      const int p = rows.program[i];
+      int first = i;
+      int8_t pre = -1;
+      if (p >= 0 && p < mon.n_programs) {
+        unsigned long long st =
+            __ldcg(reinterpret_cast<const unsigned long long*>(mon.batch_stamp) + p);
+        first = (int)(uint32_t)(st & 0xffffffffull);
+        pre = *(volatile int8_t*)(mon.assignment + p);
+        route = (first == i) && pre < 0;
+      }
+      sc.first_row[i] = first;
+      sc.pre_model[i] = pre;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, route);
+    const int wprefix = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < n_warps ? s_warp[lane] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < n_warps) s_warp[lane] = incl - v;
+      if (lane == 31) s_total = incl;
+    }
+    __syncthreads();
+    if (route) sc.route_rows[base_out + s_warp[warp] + wprefix] = i;
+    base_out += s_total;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *sc.n_route = base_out;
+    *epoch_counter = epoch;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// chm_schedule_rows
+// ---------------------------------------------------------------------------
+struct SelectParams {
+  double d[CHM_MAX_MODELS];       // decode_ms_per_token
+  double b[CHM_MAX_MODELS];       // float(max_batch_size)
+  double inv_b[CHM_MAX_MODELS];   // 1/b, used only when b is a power of two (exact)
+  int32_t b_int[CHM_MAX_MODELS];
+  uint32_t b_pow2_mask;
+  double one_plus_slack;          // (1.0 + cfg.latency_slack), balancer.py:72
+  double margin;                  // cfg.confidence_margin
+};
+
+constexpr int kChunk = 256;
+constexpr int kThreads = 256;
+
+template <int K>
+struct ChunkBuf {
+  uint64_t qual[kChunk];
+  double yhat[kChunk * K];
+  double arrival[kChunk];
+  uint32_t rank[kChunk];
+  uint32_t flags[kChunk];
+  int32_t out_tokens[kChunk * K];
+  int32_t first_row[kChunk];
+  int32_t pre_model[kChunk];
+};
+
+__device__ __forceinline__ double load_of(double P, double d, double b, double inv_b,
+                                          bool pow2) {
+  // (P * d) / b evaluated left to right in IEEE fp64 (balancer.py:57-59).
+  // For b = 2^k, x / b and x * 2^-k are the same exactly-rounded real.
+  double num = __dmul_rn(P, d);
+  return pow2 ? __dmul_rn(num, inv_b) : __ddiv_rn(num, b);
+}
+
+__device__ __forceinline__ double neumaier_value(double s, double c) {
+  // CPython 3.12 builtin sum(): `if (c && Py_IS_FINITE(c)) f_result += c`.
+  return (c != 0.0 && isfinite(c)) ? __dadd_rn(s, c) : s;
+}
+
+__device__ __forceinline__ void neumaier_add(double& s, double& c, double x) {
+  double t = __dadd_rn(s, x);
+  if (fabs(s) >= fabs(x))
+    c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), x));
+  else
+    c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), s));
+  s = t;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
+    SelectParams prm, chm_monitor_state mon, chm_rows rows, chm_row_scratch sc,
+    const float* __restrict__ scores, const double* __restrict__ yhat, chm_decisions out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ChunkBuf<K>* bufs = reinterpret_cast<ChunkBuf<K>*>(smem_raw);
+  __shared__ int s_committed;
+  const int B = rows.n_rows;
+  const int tid = threadIdx.x;
+
+  // ---- phase P: per-row precompute (independent of the in-flight state) ----
+  for (int i = tid; i < B; i += blockDim.x) {
+    const int p = rows.program[i];
+    const int st = rows.stage[i];
+    uint32_t fl = 0;
+    uint64_t qual = 0;
+    uint32_t rank = 0;
+    if (p < 0 || p >= mon.n_programs) {
+      fl |= RF_BAD_PROGRAM;
+    } else {
+      const int pre = sc.pre_model[i];
+      const int first = sc.first_row[i];
+      if (pre >= 0) fl |= RF_CACHED_PRE;
+      else if (first != i) fl |= RF_REPEAT;
+      else fl |= RF_ROUTE;
+      if (st < 1 || st > CHM_MAX_STAGES) {
+        fl |= RF_BAD_STAGE;
+      } else if (__ldcg(mon.stage_bits + p) & (1u << (st - 1))) {
+        fl |= RF_DUP_PRE;
+      }
+    }
+    if (fl & RF_ROUTE) {
+      double q[K];
+      bool bad = false;
+#pragma unroll
+      for (int m = 0; m < K; ++m) {
+        float qf = scores[(size_t)i * K + m];
+        // ConfidenceVector.__post_init__: `not 0.0 <= q <= 1.0` (NaN fails too).
+        if (!(qf >= 0.0f && qf <= 1.0f)) bad = true;
+        q[m] = (double)qf;
+      }
+      if (bad) fl |= RF_BAD_SCORE;
+      // rank[m] = position of m in sorted(models, key=(-q[m], m)).
+#pragma unroll
+      for (int m = 0; m < K; ++m) {
+        uint32_t r = 0;
+#pragma unroll
+        for (int o = 0; o < K; ++o)
+          r += (q[o] > q[m] || (q[o] == q[m] && o < m)) ? 1u : 0u;
+        rank |= r << (4 * m);
+      }
+      // qual[mf] = { m : q[m] >= q[mf] + margin } (balancer.py:73-75).
+#pragma unroll
+      for (int mf = 0; mf < K; ++mf) {
+        const double thr = __dadd_rn(q[mf], prm.margin);
+        uint64_t bits = 0;
+#pragma unroll
+        for (int m = 0; m < K; ++m) bits |= (q[m] >= thr ? 1ull : 0ull) << m;
+        qual |= bits << (K * mf);
+      }
+    }
+    sc.flags[i] = fl;
+    sc.qual[i] = qual;
+    sc.rank[i] = rank;
+  }
+  __syncthreads();
+
+  auto load_chunk = [&](int chunk, ChunkBuf<K>* buf, int t0, int nt) {
+    const int r0 = chunk * kChunk;
+    const int n = min(kChunk, B - r0);
+    if (n <= 0) return;
+    for (int j = t0; j < n; j += nt) {
+      buf->qual[j] = __ldcg(sc.qual + r0 + j);
+      buf->rank[j] = __ldcg(sc.rank + r0 + j);
+      buf->flags[j] = __ldcg(sc.flags + r0 + j);
+      buf->arrival[j] = rows.arrival[r0 + j];
+      buf->first_row[j] = sc.first_row[r0 + j];
+      buf->pre_model[j] = sc.pre_model[r0 + j];
+    }
+    for (int j = t0; j < n * K; j += nt) {
+      buf->yhat[j] = yhat[(size_t)r0 * K + j];
+      buf->out_tokens[j] = rows.out_tokens ? rows.out_tokens[(size_t)r0 * K + j] : 0;
+    }
+  };
+
+  const int n_chunks = (B + kChunk - 1) / kChunk;
+  if (n_chunks > 0) load_chunk(0, &bufs[0], tid, blockDim.x);
+  if (tid == 0) s_committed = B;
+  __syncthreads();
+
+  // Chain state (lane 0 of warp 0 only): the selection-critical triples in
+  // registers, the bookkeeping counters in shared memory.
+  double f[K], c[K], L[K];
+  __shared__ double clk[K];
+  __shared__ long long seq[K], cnt[K], iters[K];
+  __shared__ int run[K], que[K];
+  bool stop = false;
+  if (tid == 0) {
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      f[m] = mon.inflight_sum[m];
+      c[m] = mon.inflight_comp[m];
+      const bool pw = (prm.b_pow2_mask >> m) & 1u;
+      L[m] = load_of(neumaier_value(f[m], c[m]), prm.d[m], prm.b[m], prm.inv_b[m], pw);
+      clk[m] = mon.engine_clock[m];
+      seq[m] = mon.engine_seq[m];
+      cnt[m] = mon.inflight_count[m];
+      iters[m] = mon.engine_iterations[m];
+      run[m] = mon.engine_running[m];
+      que[m] = mon.engine_queued[m];
+      // Work conservation: free slots imply an empty queue (engine.py:328-338).
+      if (run[m] < prm.b_int[m] && que[m] > 0 && !stop) {
+        report_error(out.error, CHM_ERR_INVALID_STATE, 0, m, que[m]);
+        s_committed = 0;
+        stop = true;
+      }
+    }
+  }
+
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    ChunkBuf<K>* cur = &bufs[ch & 1];
+    if (tid >= 32) {
+      if (ch + 1 < n_chunks) load_chunk(ch + 1, &bufs[(ch + 1) & 1], tid - 32, blockDim.x - 32);
+    } else if (tid == 0 && !stop) {
+      const int r0 = ch * kChunk;
+      const int n = min(kChunk, B - r0);
+      for (int j = 0; j < n; ++j) {
+        const int i = r0 + j;
+        const uint32_t fl = cur->flags[j];
+        int err = 0, err_aux = 0;
+        // stage how far the reference got before raising:
+        // 0 nothing, 1 assigned, 2 + dispatched, 3 + clock advanced
+        int partial = 0;
+        if (fl & (RF_BAD_PROGRAM | RF_BAD_STAGE)) {
+          err = (fl & RF_BAD_PROGRAM) ? CHM_ERR_INVALID_ARG : CHM_ERR_UNSUPPORTED;
+          report_error(out.error, err, i, -1, 0);
+          s_committed = i;
+          stop = true;
+          break;
+        }
+        int m;
+        bool cached = true;
+        if (fl & RF_CACHED_PRE) {
+          m = cur->pre_model[j];
+        } else if (fl & RF_REPEAT) {
+          // The first occurrence (already decided by this thread) assigned it.
+          m = out.model[cur->first_row[j]];
+        } else {
+          if (fl & RF_BAD_SCORE) {
+            report_error(out.error, CHM_ERR_VALIDATION, i, -1, 1);
+            s_committed = i;
+            stop = true;
+            break;
+          }
+          cached = false;
+          int mf = 0;
+#pragma unroll
+          for (int k = 1; k < K; ++k)
+            if (L[k] < L[mf]) mf = k;
+          double lmf = L[0];
+#pragma unroll
+          for (int k = 1; k < K; ++k)
+            if (k == mf) lmf = L[k];
+          const double limit = __dmul_rn(prm.one_plus_slack, lmf);
+          uint32_t ok = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) ok |= (L[k] <= limit ? 1u : 0u) << k;
+          const uint32_t cand =
+              (uint32_t)(cur->qual[j] >> (K * mf)) & ok & ((1u << K) - 1u);
+          m = mf;
+          if (cand) {
+            const uint32_t rk = cur->rank[j];
+            uint32_t best = 16;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const uint32_t r = (rk >> (4 * k)) & 15u;
+              if (((cand >> k) & 1u) && r < best) {
+                best = r;
+                m = k;
+              }
+            }
+          }
+          if (out.loads) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) out.loads[(size_t)i * K + k] = L[k];
+          }
+          partial = 1;  // monitor.assign (balancer.py:113)
+        }
+        // predictor.predict + record_dispatch (balancer.py:115-116, monitor.py:86-96)
+        const double y = cur->yhat[j * K + m];
+        if (is_nan64(y)) err = CHM_ERR_NAN_PREDICTION;
+        else if (y < 0.0) err = CHM_ERR_NEGATIVE_PREDICTION;
+        else if (fl & RF_DUP_PRE) err = CHM_ERR_DUPLICATE_REQUEST;
+        else if (fl & RF_REPEAT) {
+          // Same (program, stage) earlier in this batch -> DuplicateRequest.
+          const int p = rows.program[i], st = rows.stage[i];
+          for (int o = cur->first_row[j]; o < i; ++o)
+            if (rows.program[o] == p && rows.stage[o] == st) {
+              err = CHM_ERR_DUPLICATE_REQUEST;
+              break;
+            }
+        }
+        if (!err) {
+          partial = 2;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (k == m) {
+              neumaier_add(f[k], c[k], y);
+              const bool pw = (prm.b_pow2_mask >> k) & 1u;
+              L[k] = load_of(neumaier_value(f[k], c[k]), prm.d[k], prm.b[k], prm.inv_b[k], pw);
+              cnt[k] += 1;
+            }
+          }
+          // EngineSim.enqueue: _advance_clock (engine.py:140-143), then
+          // _make_entry validates out_tokens (engine.py:285-286).
+          const double arr = cur->arrival[j];
+          double ck = clk[0];
+#pragma unroll
+          for (int k = 1; k < K; ++k)
+            if (k == m) ck = clk[k];
+          if (arr < __dsub_rn(ck, 1e-9)) {
+            err = CHM_ERR_TIME_BACKWARDS;
+          } else {
+            partial = 3;
+            const double nck = arr > ck ? arr : ck;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+              if (k == m) clk[k] = nck;
+            if (cur->out_tokens[j * K + m] < 0) {
+              err = CHM_ERR_VALIDATION;
+              err_aux = 2;
+            }
+          }
+        }
+        if (err) {
+          report_error(out.error, err, i, m, err_aux);
+          // Apply the side effects the reference performed before raising.
+          const int p = rows.program[i];
+          if (partial >= 1 && !cached) mon.assignment[p] = (int8_t)m;
+          if (partial >= 2) atomicOr(mon.stage_bits + p, 1u << (rows.stage[i] - 1));
+          s_committed = i;
+          stop = true;
+          break;
+        }
+        long long sq = 0;
+        uint8_t dfl = cached ? DF_CACHED : 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (k == m) {
+            sq = seq[k]++;
+            if (run[k] < prm.b_int[k]) {
+              // enqueue -> _iterate admits the only queued entry (engine.py:157-158)
+              run[k] += 1;
+              iters[k] += 1;
+              dfl |= DF_ADMITTED;
+            } else {
+              que[k] += 1;
+              dfl |= DF_QUEUED;
+            }
+          }
+        }
+        out.model[i] = m;
+        out.priority[i] = y;
+        out.flags[i] = dfl;
+        out.seq[i] = sq;
+      }
+    }
+    __syncthreads();
+  }
+
+  if (tid == 0) {
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      mon.inflight_sum[m] = f[m];
+      mon.inflight_comp[m] = c[m];
+      mon.engine_clock[m] = clk[m];
+      mon.engine_seq[m] = seq[m];
+      mon.inflight_count[m] = cnt[m];
+      mon.engine_iterations[m] = iters[m];
+      mon.engine_running[m] = run[m];
+      mon.engine_queued[m] = que[m];
+    }
+    *out.n_committed = s_committed;
+  }
+  __syncthreads();
+  // ---- post-pass: commit assignments and in-flight stage bits ----
+  const int n_ok = s_committed;
+  for (int i = tid; i < n_ok; i += blockDim.x) {
+    const int p = rows.program[i];
+    if (sc.flags[i] & RF_ROUTE) mon.assignment[p] = (int8_t)out.model[i];
+    atomicOr(mon.stage_bits + p, 1u << (rows.stage[i] - 1));
+  }
+}
+
+template <int K>
+static chm_status launch_schedule(const SelectParams& prm, const chm_monitor_state& mon,
+                                  const chm_rows& rows, const chm_row_scratch& sc,
+                                  const float* scores, const double* yhat,
+                                  const chm_decisions& out, cudaStream_t s) {
+  const size_t smem = 2 * sizeof(ChunkBuf<K>);
+  cudaFuncSetAttribute(schedule_rows_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  schedule_rows_kernel<K><<<1, kThreads, smem, s>>>(prm, mon, rows, sc, scores, yhat, out);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+}  // namespace chm
+
+extern "C" chm_status chm_prepare_rows(const chm_monitor_state* mon, const chm_rows* rows,
+                                       const chm_row_scratch* scratch,
+                                       uint32_t* epoch_counter, void* stream) {
+  if (!mon || !rows || !scratch || !epoch_counter || rows->n_rows < 0)
+    return CHM_ERR_INVALID_ARG;
+  chm::prepare_rows_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(*mon, *rows, *scratch,
+                                                                  epoch_counter);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_schedule_rows(const chm_pool* pool, const chm_balancer_cfg* cfg,
+                                        const chm_monitor_state* mon, const chm_rows* rows,
+                                        const chm_row_scratch* scratch, const float* scores,
+                                        const double* yhat, const chm_decisions* out,
+                                        void* stream) {
+  if (!pool || !cfg || !mon || !rows || !scratch || !out || !yhat || !scores)
+    return CHM_ERR_INVALID_ARG;
+  const int K = pool->n_models;
+  if (K < 1 || K > CHM_MAX_MODELS || rows->n_rows < 0) return CHM_ERR_INVALID_ARG;
+  if (!(cfg->latency_slack >= 0.0) || !(cfg->confidence_margin >= 0.0) ||
+      !(cfg->confidence_margin <= 1.0))
+    return CHM_ERR_INVALID_ARG;
+  chm::SelectParams prm{};
+  for (int m = 0; m < K; ++m) {
+    const int bi = pool->max_batch_size[m];
+    if (bi < 1 || !(pool->decode_ms_per_token[m] > 0.0)) return CHM_ERR_INVALID_ARG;
+    prm.d[m] = pool->decode_ms_per_token[m];
+    prm.b[m] = (double)bi;
+    prm.b_int[m] = bi;
+    if ((bi & (bi - 1)) == 0) {
+      prm.b_pow2_mask |= 1u << m;
+      prm.inv_b[m] = 1.0 / (double)bi;
+    }
+  }
+  prm.one_plus_slack = 1.0 + cfg->latency_slack;
+  prm.margin = cfg->confidence_margin;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (K) {
+    case 1: return chm::launch_schedule<1>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    case 2: return chm::launch_schedule<2>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    case 3: return chm::launch_schedule<3>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    case 4: return chm::launch_schedule<4>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    case 5: return chm::launch_schedule<5>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    case 6: return chm::launch_schedule<6>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    case 7: return chm::launch_schedule<7>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+    default: return chm::launch_schedule<8>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);
+  }
+}

@@ -1,0 +1,528 @@
+// K7 -- STJF + aging engine queues.
+//
+// Reference: EngineSim (engine.py:265-374). Queue order is ascending
+// QueueEntry.sort_key = (starvation_level, priority, arrival, seq)
+// (engine.py:55-69). A scheduling iteration (`_iterate`, engine.py:328-338)
+// admits the queue minimum while the running batch has free slots, then ages
+// every still-queued entry (`_age_queued`, engine.py:340-374): count += 1 and,
+// at count >= S, level -= 1, count = 0, quantum = 0.
+//
+// Device layout: engine m owns segment [m*cap, (m+1)*cap) of SoA arrays kept in
+// seq order, so "seq" comparisons are storage-index comparisons and a stable
+// sort over storage order needs no seq digits. One CTA per engine stages the
+// keys in shared memory and runs an LSD radix sort (8-bit digits, constant
+// digits skipped) by (count, level, priority[, arrival]). Entries with equal
+// count age in lock step, so each count group keeps its internal order for the
+// whole call: R iterations become R rounds of "admit the minimum of the group
+// heads, then shift each group's (count, level offset)". A final radix sort by
+// (level, priority[, arrival]) writes the STJF order of what remains.
+//
+// HBM bytes per queued entry per call (algorithmic): read 40 (priority 8,
+// arrival 8, seq-implicit, handle 8, out_tokens 4, level 4, count 4, quantum 4)
+// + write 40 + order 4.
+#include "common.cuh"
+
+namespace chm {
+
+constexpr int kQMax = 10240;       // entries per engine segment held in smem
+constexpr int kQThreads = 1024;
+constexpr int kQWarps = kQThreads / 32;
+constexpr int kMaxGroups = 256;
+constexpr uint16_t kAdmitted = 0xffffu;
+
+struct QueueSmem {
+  unsigned long long prio[kQMax];  // order-preserving bits of priority
+  uint16_t lvl[kQMax];             // starvation_level + 32768
+  uint16_t cnt[kQMax];             // starvation_count
+  uint16_t idx_a[kQMax];
+  uint16_t idx_b[kQMax];
+  uint16_t wcnt[kQWarps][256];
+  int base[256];
+  int g_start[kMaxGroups], g_end[kMaxGroups], g_cur[kMaxGroups];
+  int g_count[kMaxGroups], g_lvloff[kMaxGroups];
+  unsigned long long red_or[4], red_and[4];
+  int scan[kQWarps];
+  int misc[8];
+};
+
+__device__ __forceinline__ unsigned long long f64_key(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  // priorities/arrivals are >= 0 (validated upstream); -0.0 == 0.0 in Python.
+  return b == 0x8000000000000000ull ? 0ull : b;
+}
+
+// One stable LSD counting-sort pass over `n` indices.
+// src: 0 = arrival (global), 1 = priority, 2 = level, 3 = count; byte = digit index.
+__device__ void radix_pass(QueueSmem& s, const uint16_t* in, uint16_t* out, int n, int src,
+                           int byte, const double* __restrict__ arrival) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto digit = [&](int e) -> int {
+    unsigned long long v;
+    if (src == 0) v = f64_key(arrival[e]);
+    else if (src == 1) v = s.prio[e];
+    else if (src == 2) v = s.lvl[e];
+    else v = s.cnt[e];
+    return (int)((v >> (8 * byte)) & 255ull);
+  };
+  for (int d = tid; d < 256; d += blockDim.x) s.base[d] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&s.base[digit(in[i])], 1);
+  __syncthreads();
+  if (warp == 0) {
+    int v[8], tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { v[k] = s.base[lane * 8 + k]; tot += v[k]; }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int run = incl - tot;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { s.base[lane * 8 + k] = run; run += v[k]; }
+  }
+  __syncthreads();
+  for (int blk = 0; blk < n; blk += blockDim.x) {
+    const int i = blk + tid;
+    const bool valid = i < n;
+    const int e = valid ? in[i] : 0;
+    const int d = valid ? digit(e) : 256;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s.wcnt[warp][lane * 8 + k] = 0;
+    __syncwarp();
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank == 0) s.wcnt[warp][d] = (uint16_t)__popc(peers);
+    __syncthreads();
+    if (tid < 256) {
+      int run = s.base[tid];
+#pragma unroll 8
+      for (int w = 0; w < kQWarps; ++w) {
+        const int cnum = s.wcnt[w][tid];
+        s.wcnt[w][tid] = (uint16_t)(run & 0xffff);
+        run += cnum;
+      }
+      s.base[tid] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      // wcnt holds the low 16 bits of the destination base; n <= kQMax < 65536.
+      out[s.wcnt[warp][d] + rank] = (uint16_t)e;
+    }
+    __syncthreads();
+  }
+}
+
+// Stable sort of [0, n) by the given key sources (most significant last in
+// `srcs`), skipping digits that are equal across all entries.
+__device__ void radix_sort(QueueSmem& s, int n, const int* srcs, int n_srcs,
+                           const double* __restrict__ arrival, bool use_arrival,
+                           uint16_t*& sorted, uint16_t*& spare) {
+  const int tid = threadIdx.x;
+  if (tid < 4) { s.red_or[tid] = 0ull; s.red_and[tid] = ~0ull; }
+  for (int i = tid; i < n; i += blockDim.x) s.idx_a[i] = (uint16_t)i;
+  __syncthreads();
+  // Per-source OR / AND to find constant digits.
+  unsigned long long o[4] = {0, 0, 0, 0}, a[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+  for (int i = tid; i < n; i += blockDim.x) {
+    unsigned long long v0 = use_arrival ? f64_key(arrival[i]) : 0ull;
+    o[0] |= v0; a[0] &= v0;
+    o[1] |= s.prio[i]; a[1] &= s.prio[i];
+    o[2] |= s.lvl[i]; a[2] &= s.lvl[i];
+    o[3] |= s.cnt[i]; a[3] &= s.cnt[i];
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    for (int off = 16; off; off >>= 1) {
+      o[k] |= __shfl_xor_sync(0xffffffffu, o[k], off);
+      a[k] &= __shfl_xor_sync(0xffffffffu, a[k], off);
+    }
+  }
+  if ((tid & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { atomicOr(&s.red_or[k], o[k]); atomicAnd(&s.red_and[k], a[k]); }
+  }
+  __syncthreads();
+  uint16_t* in = s.idx_a;
+  uint16_t* out = s.idx_b;
+  for (int q = 0; q < n_srcs; ++q) {
+    const int src = srcs[q];
+    if (src == 0 && !use_arrival) continue;
+    const int n_bytes = (src <= 1) ? 8 : 2;
+    const unsigned long long diff = s.red_or[src] ^ s.red_and[src];
+    for (int byte = 0; byte < n_bytes; ++byte) {
+      if (((diff >> (8 * byte)) & 255ull) == 0) continue;
+      radix_pass(s, in, out, n, src, byte, arrival);
+      uint16_t* t = in; in = out; out = t;
+    }
+  }
+  sorted = in;
+  spare = out;
+}
+
+struct QueueParams {
+  int K;
+  int b[CHM_MAX_MODELS];
+  int aging_enabled;
+  int S;
+};
+
+// Lexicographic key of a group head: (level, priority, arrival?, storage idx).
+struct HeadKey {
+  int lvl;
+  unsigned long long prio;
+  unsigned long long arr;
+  int e;
+  int g;
+};
+
+__device__ __forceinline__ bool key_less(const HeadKey& x, const HeadKey& y) {
+  if (x.lvl != y.lvl) return x.lvl < y.lvl;
+  if (x.prio != y.prio) return x.prio < y.prio;
+  if (x.arr != y.arr) return x.arr < y.arr;
+  return x.e < y.e;
+}
+
+// mode 0: completions (R = n_complete[m], each frees one running slot first)
+// mode 1: tick (append queued rows, then R = n_iterations explicit iterations)
+__global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
+    QueueParams prm, chm_monitor_state mon, chm_queue_state q, chm_rows rows,
+    chm_decisions dec, const int32_t* __restrict__ n_complete, int n_iterations, int mode,
+    int32_t* err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QueueSmem& s = *reinterpret_cast<QueueSmem*>(smem_raw);
+  const int m = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t seg = (size_t)m * q.capacity;
+  const int cap = min(q.capacity, kQMax);
+  double* prio_g = q.priority + seg;
+  double* arr_g = q.arrival + seg;
+  int64_t* seq_g = q.seq + seg;
+  int64_t* handle_g = q.handle + seg;
+  int32_t* out_g = q.out_tokens + seg;
+  int32_t* lvl_g = q.level + seg;
+  int32_t* cnt_g = q.count + seg;
+  int32_t* qnt_g = q.quantum + seg;
+
+  int n = mon.engine_queued[m];
+  int run = mon.engine_running[m];
+  const int bmax = prm.b[m];
+
+  // ---- mode 1: append rows queued on this engine by chm_schedule_rows ----
+  if (mode == 1) {
+    const int n_rows = *dec.n_committed;
+    // rows queued this batch were already counted in engine_queued by K6
+    int n_new_total = 0;
+    {
+      // count first
+      int c = 0;
+      for (int i = tid; i < n_rows; i += blockDim.x)
+        c += (dec.model[i] == m && (dec.flags[i] & 4u)) ? 1 : 0;
+      for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+      if (lane == 0) s.scan[warp] = c;
+      __syncthreads();
+      if (tid == 0) {
+        int t = 0;
+        for (int w = 0; w < kQWarps; ++w) t += s.scan[w];
+        s.misc[0] = t;
+      }
+      __syncthreads();
+      n_new_total = s.misc[0];
+      __syncthreads();
+    }
+    const int n_old = n - n_new_total;
+    if (n_old < 0 || n > cap) {
+      if (tid == 0) report_error(err, n > cap ? CHM_ERR_CAPACITY : CHM_ERR_INVALID_STATE,
+                                 0, m, n);
+      return;
+    }
+    int pos_base = n_old;
+    for (int blk = 0; blk < n_rows; blk += blockDim.x) {
+      const int i = blk + tid;
+      const bool take = i < n_rows && dec.model[i] == m && (dec.flags[i] & 4u);
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (lane == 0) s.scan[warp] = __popc(bal);
+      __syncthreads();
+      if (warp == 0) {
+        int v = s.scan[lane], incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        s.scan[lane] = incl - v;
+        if (lane == 31) s.misc[1] = incl;
+      }
+      __syncthreads();
+      if (take) {
+        const int pos = pos_base + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
+        prio_g[pos] = dec.priority[i];
+        arr_g[pos] = rows.arrival[i];
+        seq_g[pos] = dec.seq[i];
+        handle_g[pos] = rows.handle ? rows.handle[i] : (int64_t)i;
+        out_g[pos] = rows.out_tokens ? rows.out_tokens[(size_t)i * prm.K + m] : 0;
+        lvl_g[pos] = 0;
+        cnt_g[pos] = 0;
+        qnt_g[pos] = 0;
+      }
+      pos_base += s.misc[1];
+      __syncthreads();
+    }
+    __threadfence_block();
+  } else {
+    if (n > cap) {
+      if (tid == 0) report_error(err, CHM_ERR_CAPACITY, 0, m, n);
+      return;
+    }
+  }
+  __syncthreads();
+
+  // ---- stage keys ----
+  int unsorted = 0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    s.prio[i] = f64_key(prio_g[i]);
+    const int lv = lvl_g[i];
+    s.lvl[i] = (uint16_t)(lv + 32768);
+    s.cnt[i] = (uint16_t)min(max(cnt_g[i], 0), 65535);
+    if (i > 0 && arr_g[i] < arr_g[i - 1]) unsorted = 1;
+  }
+  unsorted = __syncthreads_or(unsorted);
+  const bool use_arr = unsorted != 0;
+
+  const int R = (mode == 0) ? n_complete[m] : n_iterations;
+  // Admissions of this call are appended after those already reported since
+  // the host last zeroed n_admitted (completions and tick share the list).
+  const int n_adm0 = q.n_admitted[m];
+  int n_adm = 0, n_prom = 0;
+
+  if (R > 0) {
+    // ---- sort by (count, level, priority[, arrival]) and form count groups ----
+    const int srcs[4] = {0, 1, 2, 3};
+    uint16_t *sorted, *spare;
+    radix_sort(s, n, srcs, 4, arr_g, use_arr, sorted, spare);
+    if (tid == 0) s.misc[2] = 0;
+    __syncthreads();
+    // group boundaries: positions where count changes
+    for (int p = tid; p < n; p += blockDim.x) {
+      const bool head = (p == 0) || s.cnt[sorted[p]] != s.cnt[sorted[p - 1]];
+      if (head) {
+        const int g = atomicAdd(&s.misc[2], 1);
+        if (g < kMaxGroups) {
+          s.g_start[g] = p;
+          s.g_count[g] = s.cnt[sorted[p]];
+        }
+      }
+    }
+    __syncthreads();
+    const int G = s.misc[2];
+    if (G > kMaxGroups) {
+      if (tid == 0) report_error(err, CHM_ERR_UNSUPPORTED, 0, m, G);
+      return;
+    }
+    if (tid == 0) {
+      // groups were discovered out of order; insertion sort by start (G small)
+      for (int a = 1; a < G; ++a) {
+        int st = s.g_start[a], ct = s.g_count[a], b2 = a - 1;
+        while (b2 >= 0 && s.g_start[b2] > st) {
+          s.g_start[b2 + 1] = s.g_start[b2];
+          s.g_count[b2 + 1] = s.g_count[b2];
+          --b2;
+        }
+        s.g_start[b2 + 1] = st;
+        s.g_count[b2 + 1] = ct;
+      }
+      for (int g = 0; g < G; ++g) {
+        s.g_end[g] = (g + 1 < G) ? s.g_start[g + 1] : n;
+        s.g_cur[g] = s.g_start[g];
+        s.g_lvloff[g] = 0;
+      }
+    }
+    __syncthreads();
+
+    // ---- R scheduling iterations (warp 0) ----
+    if (warp == 0) {
+      int remaining = n;
+      for (int r = 0; r < R; ++r) {
+        if (mode == 0) run = max(run - 1, 0);
+        const int a = max(0, min(bmax - run, remaining));
+        for (int t = 0; t < a; ++t) {
+          HeadKey best;
+          best.g = -1;
+          for (int g0 = 0; g0 < G; g0 += 32) {
+            const int g = g0 + lane;
+            HeadKey k;
+            k.g = -1;
+            if (g < G && s.g_cur[g] < s.g_end[g]) {
+              const int e = sorted[s.g_cur[g]];
+              k.e = e;
+              k.g = g;
+              k.lvl = (int)s.lvl[e] - 32768 + s.g_lvloff[g];
+              k.prio = s.prio[e];
+              k.arr = use_arr ? f64_key(arr_g[e]) : 0ull;
+            }
+            for (int off = 16; off; off >>= 1) {
+              HeadKey o;
+              o.lvl = __shfl_xor_sync(0xffffffffu, k.lvl, off);
+              o.prio = __shfl_xor_sync(0xffffffffu, k.prio, off);
+              o.arr = __shfl_xor_sync(0xffffffffu, k.arr, off);
+              o.e = __shfl_xor_sync(0xffffffffu, k.e, off);
+              o.g = __shfl_xor_sync(0xffffffffu, k.g, off);
+              if (o.g >= 0 && (k.g < 0 || key_less(o, k))) k = o;
+            }
+            if (k.g >= 0 && (best.g < 0 || key_less(k, best))) best = k;
+          }
+          if (lane == 0) {
+            q.admitted[seg + n_adm0 + n_adm] = handle_g[best.e];
+            s.g_cur[best.g] += 1;
+          }
+          __syncwarp();
+          ++n_adm;
+          --remaining;
+        }
+        run += a;
+        if (prm.aging_enabled && remaining > 0) {
+          for (int g = lane; g < G; g += 32) {
+            if (s.g_cur[g] < s.g_end[g]) {
+              int c2 = s.g_count[g] + 1;
+              if (c2 >= prm.S) {
+                c2 = 0;
+                s.g_lvloff[g] -= 1;
+                n_prom += s.g_end[g] - s.g_cur[g];
+              }
+              s.g_count[g] = c2;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int off = 16; off; off >>= 1) n_prom += __shfl_xor_sync(0xffffffffu, n_prom, off);
+      if (lane == 0) { s.misc[3] = n_adm; s.misc[4] = n_prom; s.misc[5] = run; }
+    }
+    __syncthreads();
+    n_adm = s.misc[3];
+    n_prom = s.misc[4];
+    run = s.misc[5];
+    // ---- per-entry outcome: spare[e] = group or kAdmitted ----
+    for (int p = tid; p < n; p += blockDim.x) {
+      int lo = 0, hi = G - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s.g_start[mid] <= p) lo = mid; else hi = mid - 1;
+      }
+      const int e = sorted[p];
+      spare[e] = (p < s.g_cur[lo]) ? kAdmitted : (uint16_t)lo;
+    }
+    __syncthreads();
+    // ---- compact survivors in seq (storage) order, applying the aging ----
+    int out_base = 0;
+    for (int blk = 0; blk < n; blk += blockDim.x) {
+      const int i = blk + tid;
+      const bool valid = i < n;
+      const uint16_t g = valid ? spare[i] : kAdmitted;
+      const bool keep = valid && g != kAdmitted;
+      double pr = 0, ar = 0;
+      int64_t sq = 0, hd = 0;
+      int ot = 0, lv = 0, ct = 0, qn = 0;
+      unsigned long long pk = 0;
+      if (keep) {
+        pr = prio_g[i]; ar = arr_g[i]; sq = seq_g[i]; hd = handle_g[i]; ot = out_g[i];
+        lv = (int)s.lvl[i] - 32768 + s.g_lvloff[g];
+        ct = prm.aging_enabled ? s.g_count[g] : cnt_g[i];
+        qn = (s.g_lvloff[g] != 0) ? 0 : qnt_g[i];
+        pk = s.prio[i];
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) s.scan[warp] = __popc(bal);
+      __syncthreads();
+      if (warp == 0) {
+        int v = s.scan[lane], incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        s.scan[lane] = incl - v;
+        if (lane == 31) s.misc[6] = incl;
+      }
+      __syncthreads();
+      if (keep) {
+        const int pos = out_base + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
+        prio_g[pos] = pr; arr_g[pos] = ar; seq_g[pos] = sq; handle_g[pos] = hd;
+        out_g[pos] = ot; lvl_g[pos] = lv; cnt_g[pos] = ct; qnt_g[pos] = qn;
+        s.prio[pos] = pk;
+        s.lvl[pos] = (uint16_t)(lv + 32768);
+        s.cnt[pos] = (uint16_t)ct;
+      }
+      out_base += s.misc[6];
+      __syncthreads();
+    }
+    n = out_base;
+  }
+
+  // ---- final STJF order of the remaining queue: (level, priority[, arrival], seq) ----
+  {
+    int unsorted2 = 0;
+    for (int i = tid + 1; i < n; i += blockDim.x)
+      if (arr_g[i] < arr_g[i - 1]) unsorted2 = 1;
+    const bool ua = __syncthreads_or(unsorted2) != 0;
+    const int srcs[3] = {0, 1, 2};
+    uint16_t *sorted, *spare;
+    radix_sort(s, n, srcs, 3, arr_g, ua, sorted, spare);
+    for (int r = tid; r < n; r += blockDim.x) q.order[seg + r] = sorted[r];
+    if (tid == 0) q.arrival_unsorted[m] = ua ? 1 : 0;
+  }
+  if (tid == 0) {
+    q.n_admitted[m] = n_adm0 + n_adm;
+    q.n_promoted[m] += n_prom;
+    mon.engine_queued[m] = n;
+    mon.engine_running[m] = run;
+    mon.engine_iterations[m] += R;
+  }
+}
+
+static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
+                               const chm_monitor_state* mon, const chm_queue_state* q,
+                               const chm_rows* rows, const chm_decisions* dec,
+                               const int32_t* n_complete, int n_iterations, int mode,
+                               int32_t* err, cudaStream_t s) {
+  if (!pool || !aging || !mon || !q) return CHM_ERR_INVALID_ARG;
+  const int K = pool->n_models;
+  if (K < 1 || K > CHM_MAX_MODELS || q->capacity < 1) return CHM_ERR_INVALID_ARG;
+  if (aging->enabled && (aging->starvation_threshold < 1 || aging->starvation_threshold > 65535))
+    return CHM_ERR_UNSUPPORTED;
+  if (aging->enabled && aging->demote_while_queued) return CHM_ERR_UNSUPPORTED;
+  QueueParams prm{};
+  prm.K = K;
+  for (int m = 0; m < K; ++m) prm.b[m] = pool->max_batch_size[m];
+  prm.aging_enabled = aging->enabled;
+  prm.S = aging->starvation_threshold;
+  chm_rows r{};
+  chm_decisions d{};
+  if (rows) r = *rows;
+  if (dec) d = *dec;
+  const size_t smem = sizeof(QueueSmem);
+  cudaFuncSetAttribute(queue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  queue_kernel<<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete, n_iterations, mode,
+                                          err);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+}  // namespace chm
+
+extern "C" chm_status chm_queue_complete(const chm_pool* pool, const chm_aging_cfg* aging,
+                                         const chm_monitor_state* mon,
+                                         const chm_queue_state* q, const int32_t* n_complete,
+                                         int32_t* error, void* stream) {
+  if (!n_complete) return CHM_ERR_INVALID_ARG;
+  return chm::launch_queue(pool, aging, mon, q, nullptr, nullptr, n_complete, 0, 0, error,
+                           (cudaStream_t)stream);
+}
+
+extern "C" chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* aging,
+                                     const chm_monitor_state* mon, const chm_queue_state* q,
+                                     const chm_rows* rows, const chm_decisions* dec,
+                                     int32_t n_iterations, int32_t* error, void* stream) {
+  if (!rows || !dec || n_iterations < 0) return CHM_ERR_INVALID_ARG;
+  return chm::launch_queue(pool, aging, mon, q, rows, dec, nullptr, n_iterations, 1, error,
+                           (cudaStream_t)stream);
+}

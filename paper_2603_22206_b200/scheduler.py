@@ -1,0 +1,244 @@
+"""Batched drop-in for hetsched's scheduling hot path.
+
+`GpuScheduler.schedule_batch(reqs, recs)` returns exactly the list of
+`Decision`s that B serial calls of `hetsched.balancer.schedule_request`
+(balancer.py:89-129) would return, and leaves the activity monitor and the
+engine queues in the same state. Per batch it enqueues on one CUDA stream:
+
+  chm_queue_complete   (optional) engine completions freeing slots (K7 phase A)
+  chm_prepare_rows     assignment lookup, in-batch repeats, router row list
+  router.score_rows    K1-K4 encoder (or a lookup router) on the routed rows
+  predictor.predict_rows   K5
+  chm_schedule_rows    K6 serial-exact monitor + load + selection + dispatch
+  chm_queue_tick       K7 append + aging iterations + STJF order
+
+The columnar entry point `run_rows(RowBatch)` is the hot path (no per-request
+Python objects); `schedule_batch` converts reference-style Request/TraceRecord
+objects to columns first. Everything is asynchronous until results are read;
+the whole sequence is CUDA-graph capturable for a fixed batch shape
+(see tick.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import AgingConfig, BalancerConfig, Decision, Pool
+from .state import DeviceState, aging_struct, balancer_struct
+
+INT32_MAX = 2**31 - 1
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+@dataclass
+class RowBatch:
+    """Columnar batch of requests in arrival order (device tensors)."""
+
+    program: torch.Tensor        # i32[B] dense program index
+    stage: torch.Tensor          # i32[B] 1-based stage index
+    arrival: torch.Tensor        # f64[B]
+    out_tokens: torch.Tensor     # i32[B, K] rec.out_tokens(stage, m)
+    handle: torch.Tensor         # i64[B]
+    workflow: torch.Tensor | None = None      # i32[B] predictor workflow index
+    input_tokens: torch.Tensor | None = None  # i32[B]
+    token_ids: torch.Tensor | None = None     # i32[B, S] router input
+    n_stages: torch.Tensor | None = None      # i32[B] (oracle predictor)
+    stage_out: torch.Tensor | None = None     # i32[B, MAXST, K] (oracle predictor)
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.program.shape[0])
+
+    def rows_struct(self) -> _lib.Rows:
+        return _lib.Rows(self.n_rows, _p(self.program), _p(self.stage), _p(self.arrival),
+                         _p(self.out_tokens), _p(self.handle))
+
+    @staticmethod
+    def from_numpy(device, **cols) -> "RowBatch":
+        conv = {}
+        dtypes = dict(program=np.int32, stage=np.int32, arrival=np.float64,
+                      out_tokens=np.int32, handle=np.int64, workflow=np.int32,
+                      input_tokens=np.int32, token_ids=np.int32, n_stages=np.int32,
+                      stage_out=np.int32)
+        for k, v in cols.items():
+            if v is None:
+                conv[k] = None
+                continue
+            conv[k] = torch.as_tensor(np.ascontiguousarray(np.asarray(v, dtype=dtypes[k])),
+                                      device=device)
+        return RowBatch(**conv)
+
+
+class BatchBuffers:
+    """Per-batch scratch and outputs for up to `max_rows` rows."""
+
+    def __init__(self, K: int, max_rows: int, device):
+        d, B = device, int(max_rows)
+        self.K, self.max_rows = K, B
+        self.first_row = torch.empty(B, dtype=torch.int32, device=d)
+        self.pre_model = torch.empty(B, dtype=torch.int8, device=d)
+        self.route_rows = torch.empty(B, dtype=torch.int32, device=d)
+        self.n_route = torch.zeros(1, dtype=torch.int32, device=d)
+        self.qual = torch.empty(B, dtype=torch.int64, device=d)
+        self.rank = torch.empty(B, dtype=torch.int32, device=d)
+        self.flags = torch.empty(B, dtype=torch.int32, device=d)
+        self.scores = torch.zeros(B * K, dtype=torch.float32, device=d)
+        self.yhat = torch.zeros(B * K, dtype=torch.float64, device=d)
+        self.model = torch.full((B,), -1, dtype=torch.int32, device=d)
+        self.priority = torch.zeros(B, dtype=torch.float64, device=d)
+        self.dflags = torch.zeros(B, dtype=torch.uint8, device=d)
+        self.seq = torch.zeros(B, dtype=torch.int64, device=d)
+        self.loads = torch.zeros(B * K, dtype=torch.float64, device=d)
+        self.n_committed = torch.zeros(1, dtype=torch.int32, device=d)
+        self.error = torch.zeros(4, dtype=torch.int32, device=d)
+        self.error_init = torch.tensor([0, INT32_MAX, -1, 0], dtype=torch.int32, device=d)
+        self.scratch_c = _lib.RowScratch(
+            _p(self.first_row), _p(self.pre_model), _p(self.route_rows), _p(self.n_route),
+            _p(self.qual), _p(self.rank), _p(self.flags))
+
+    def decisions_struct(self, with_loads: bool = True) -> _lib.Decisions:
+        return _lib.Decisions(_p(self.model), _p(self.priority), _p(self.dflags), _p(self.seq),
+                              _p(self.loads) if with_loads else None, _p(self.n_committed),
+                              _p(self.error))
+
+
+class GpuScheduler:
+    """Serial-exact batched Algorithm 1 on one B200."""
+
+    def __init__(self, pool: Pool, balancer: BalancerConfig = BalancerConfig(),
+                 aging: AgingConfig = AgingConfig(), *, router=None, predictor=None,
+                 n_programs: int = 1 << 20, max_rows: int = 16384,
+                 queue_capacity: int = 10240, device="cuda"):
+        self.lib = _lib.load()
+        self.pool = pool
+        self.ids = pool.model_ids
+        self.K = len(self.ids)
+        self.cfg = balancer
+        self.aging = aging
+        self.router = router
+        self.predictor = predictor
+        self.device = torch.device(device)
+        self.state = DeviceState(pool, n_programs, queue_capacity, self.device)
+        self.buf = BatchBuffers(self.K, max_rows, self.device)
+        self.bal_c = balancer_struct(balancer)
+        self.aging_c = aging_struct(aging)
+        self._program_index: dict[str, int] = {}
+        self._handles: list = []
+
+    # ------------------------------------------------------------------ core
+    def run_rows(self, batch: RowBatch, n_iterations: int = 1, n_complete=None,
+                 with_loads: bool = True, stream=None) -> None:
+        """Enqueue one tick for `batch` on `stream` (default: current stream)."""
+        B = batch.n_rows
+        if B > self.buf.max_rows:
+            raise ValueError(f"batch of {B} rows exceeds max_rows={self.buf.max_rows}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        sh = s.cuda_stream
+        st, buf, lib = self.state, self.buf, self.lib
+        rows_c = batch.rows_struct()
+        dec_c = buf.decisions_struct(with_loads)
+        with torch.cuda.stream(s):
+            buf.error.copy_(buf.error_init)
+            st.q_n_admitted.zero_()
+            st.q_n_promoted.zero_()
+            if n_complete is not None:
+                _lib.check(lib.chm_queue_complete(st.pool_c, self.aging_c, st.monitor_c,
+                                                  st.queue_c, _p(n_complete), _p(buf.error),
+                                                  sh), "chm_queue_complete")
+            _lib.check(lib.chm_prepare_rows(st.monitor_c, rows_c, buf.scratch_c,
+                                            _p(st.epoch), sh), "chm_prepare_rows")
+            if self.router is None:
+                raise RuntimeError("GpuScheduler needs a router")
+            self.router.score_rows(batch, buf.route_rows, buf.n_route, buf.scores, s)
+            if self.predictor is None:
+                raise RuntimeError("GpuScheduler needs a predictor")
+            self.predictor.predict_rows(batch, self.K, buf.yhat, buf.error, s)
+            _lib.check(lib.chm_schedule_rows(st.pool_c, self.bal_c, st.monitor_c, rows_c,
+                                             buf.scratch_c, _p(buf.scores), _p(buf.yhat),
+                                             dec_c, sh), "chm_schedule_rows")
+            _lib.check(lib.chm_queue_tick(st.pool_c, self.aging_c, st.monitor_c, st.queue_c,
+                                          rows_c, dec_c, int(n_iterations), _p(buf.error), sh),
+                       "chm_queue_tick")
+
+    def check_errors(self, context: str = "") -> None:
+        _lib.raise_device_error(self.buf.error.cpu().tolist(), context)
+
+    # ------------------------------------------------------ reference-style API
+    def program_index(self, program_id: str) -> int:
+        idx = self._program_index.get(program_id)
+        if idx is None:
+            idx = len(self._program_index)
+            if idx >= self.state.n_programs:
+                raise ValueError("program index space exhausted (raise n_programs)")
+            self._program_index[program_id] = idx
+        return idx
+
+    def rows_from_requests(self, reqs, recs) -> RowBatch:
+        K = self.K
+        B = len(reqs)
+        prog = np.empty(B, np.int32)
+        stage = np.empty(B, np.int32)
+        arr = np.empty(B, np.float64)
+        out = np.empty((B, K), np.int32)
+        handle = np.empty(B, np.int64)
+        inp = np.empty(B, np.int32)
+        for i, (r, rec) in enumerate(zip(reqs, recs)):
+            prog[i] = self.program_index(r.program_id)
+            stage[i] = r.stage_index
+            arr[i] = r.arrival_time
+            out[i] = [rec.out_tokens(r.stage_index, mid) for mid in self.ids]
+            handle[i] = len(self._handles)
+            self._handles.append(r.request_id)
+            inp[i] = r.input_tokens
+        extra = {}
+        if hasattr(self.predictor, "columns_for"):
+            extra = self.predictor.columns_for(reqs, recs, self.ids)
+        if hasattr(self.router, "columns_for"):
+            extra.update(self.router.columns_for(reqs, recs))
+        return RowBatch.from_numpy(self.device, program=prog, stage=stage, arrival=arr,
+                                   out_tokens=out, handle=handle, input_tokens=inp, **extra)
+
+    def schedule_batch(self, reqs, recs, n_iterations: int = 0) -> list[Decision]:
+        """B serial schedule_request calls (balancer.py:89-129), batched.
+
+        n_iterations explicit EngineSim.scheduling_iteration calls per engine
+        follow the batch (0 = just the enqueues, like the reference loop)."""
+        batch = self.rows_from_requests(reqs, recs)
+        self.run_rows(batch, n_iterations=n_iterations)
+        return self.collect(batch)
+
+    def collect(self, batch: RowBatch) -> list[Decision]:
+        """Read back decisions (syncs) and raise the reference's exception, if any."""
+        buf, K = self.buf, self.K
+        B = batch.n_rows
+        n_ok = int(buf.n_committed.item())
+        model = buf.model[:n_ok].cpu().numpy()
+        prio = buf.priority[:n_ok].cpu().numpy()
+        fl = buf.dflags[:n_ok].cpu().numpy()
+        loads = buf.loads[:n_ok * K].view(-1, K).cpu().numpy() if n_ok else np.zeros((0, K))
+        scores = buf.scores[:n_ok * K].view(-1, K).cpu().numpy() if n_ok else np.zeros((0, K))
+        out = []
+        for i in range(n_ok):
+            cached = bool(fl[i] & 1)
+            out.append(Decision(
+                model=self.ids[int(model[i])],
+                priority=float(prio[i]),
+                estimated_loads={} if cached else {m: float(loads[i, k]) for k, m in enumerate(self.ids)},
+                used_cached_assignment=cached,
+                scores=None if cached else {m: float(scores[i, k]) for k, m in enumerate(self.ids)},
+            ))
+        try:
+            self.check_errors("schedule_batch")
+        except Exception as exc:  # the reference raised after applying rows < n_ok
+            exc.decisions = out
+            raise
+        if n_ok != B:
+            raise RuntimeError(f"batch stopped at row {n_ok} without an error code")
+        return out

@@ -1,0 +1,464 @@
+"""Generate golden vectors by running the UNMODIFIED reference (hetsched).
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports /root/reference/pkg/src/hetsched read-only and writes small .npz /
+.json fixtures next to this file. The GPU box has no /root/reference; the
+tests there read only these committed fixtures.
+
+Fixtures
+  select_kat.npz      select_model on SPEC examples + random instances
+                      (balancer.py:63-77, AC2 SPEC.md:533)
+  schedule_*.npz      sequences of schedule_request calls (balancer.py:89-129)
+                      fed precomputed scores/predictions through Router /
+                      Predictor shims, with pre-seeded in-flight state,
+                      pre-assigned programs, in-batch repeats and engines
+                      with free / full slots
+  errors.json         the exception class + row the reference raises
+  queue_*.npz         EngineSim STJF + aging: enqueue / iterate / complete
+                      scripts and the resulting admission and queue orders
+                      (engine.py:265-394)
+  quantile.npz        EmpiricalQuantilePredictor on synthesize_trace(2000, 1)
+                      (predictor.py:65-108) over a (wf, stage, model) grid
+  synth.json          fingerprints of synthesize_trace outputs (workload.py:334-416)
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+sys.dont_write_bytecode = True
+sys.path.insert(0, REF)
+
+from hetsched import balancer, engine, monitor, predictor, profiles, router, workload  # noqa: E402
+from hetsched.errors import SimError  # noqa: E402
+
+
+def model_ids(k):
+    return [f"m{i}" for i in range(k)]
+
+
+# ---------------------------------------------------------------- select KAT
+def make_select_kat():
+    rng = np.random.default_rng(7)
+    cases = []
+    # SPEC.md:319-321 examples (two models A<B as m0<m1)
+    cases.append(([0.4, 0.9], [100.0, 140.0], 0.5, 0.1))
+    cases.append(([0.4, 0.9], [100.0, 300.0], 0.5, 0.1))
+    cases.append(([0.3, 0.7, 0.5], [10.0, 10.0, 10.0], 0.5, 0.0))
+    for _ in range(4000):
+        k = int(rng.integers(1, 9))
+        q = rng.random(k).astype(np.float32).astype(np.float64)
+        if rng.random() < 0.3:  # ties in q
+            q[rng.integers(0, k, size=k)] = q[0]
+        if rng.random() < 0.5:
+            loads = rng.integers(0, 6, size=k).astype(np.float64) * 100.0  # ties in loads
+        else:
+            loads = rng.random(k) * 1000.0
+        tau = float(rng.choice([0.0, 0.25, 0.5, 1.0, 3.0, 1e6]))
+        dm = float(rng.choice([0.0, 0.05, 0.1, 0.3, 1.0]))
+        cases.append((list(q), list(loads), tau, dm))
+    K = 8
+    Q = np.full((len(cases), K), np.nan)
+    L = np.full((len(cases), K), np.nan)
+    meta = np.zeros((len(cases), 2))
+    kk = np.zeros(len(cases), dtype=np.int32)
+    out = np.zeros(len(cases), dtype=np.int32)
+    for i, (q, loads, tau, dm) in enumerate(cases):
+        k = len(q)
+        ids = model_ids(k)
+        cv = router.ConfidenceVector(dict(zip(ids, q)))
+        cfg = balancer.BalancerConfig(tau, dm)
+        sel = balancer.select_model(cv, dict(zip(ids, loads)), cfg)
+        Q[i, :k] = q
+        L[i, :k] = loads
+        meta[i] = (tau, dm)
+        kk[i] = k
+        out[i] = ids.index(sel)
+    np.savez_compressed(os.path.join(OUT, "select_kat.npz"), q=Q, loads=L, cfg=meta, k=kk,
+                        chosen=out)
+    return len(cases)
+
+
+# ----------------------------------------------------------- schedule shims
+class ShimRouter(router.Router):
+    name = "shim"
+
+    def __init__(self, table):
+        self.table = table  # request_id -> {model: q}
+
+    def _score_one(self, req, rec, model_id):
+        return self.table[req.request_id][model_id]
+
+
+class ShimPredictor(predictor.Predictor):
+    name = "shim"
+
+    def __init__(self, table):
+        self.table = table  # request_id -> {model: yhat}
+
+    def predict(self, req, rec, model_id):
+        return self.table[req.request_id][model_id]
+
+
+def build_scenario(seed, k, n_rows, *, dyadic=True, p0_entries=0, pre_assigned=0.0,
+                   repeats=0.0, batch=None, decode=None, pre_running=None, tau=0.5,
+                   margin=0.1, spread=1.0, tied_q=False):
+    rng = np.random.default_rng(seed)
+    ids = model_ids(k)
+    decode = decode or [5.0 * (i + 1) for i in range(k)]
+    batch = batch or [max(1, 32 >> i) for i in range(k)]
+    n_prog = n_rows + 8
+    # programs for rows: mostly distinct, some repeats (later stage of an earlier row)
+    prog = []
+    stage = []
+    used = {}
+    for i in range(n_rows):
+        if i > 0 and rng.random() < repeats:
+            p = int(prog[int(rng.integers(0, i))])
+            used[p] = used.get(p, 0) + 1
+            prog.append(p)
+            stage.append(used[p])
+        else:
+            p = i + 8
+            used[p] = 1
+            prog.append(p)
+            stage.append(1)
+    prog = np.array(prog, dtype=np.int32)
+    stage = np.array(stage, dtype=np.int32)
+    q = rng.random((n_rows, k))
+    q = 0.5 + (q - 0.5) * spread
+    if tied_q:
+        q = np.round(q * 4) / 4
+    q = np.clip(q, 0, 1).astype(np.float32)
+    if dyadic:
+        yhat = rng.integers(0, 4000, size=(n_rows, k)).astype(np.float64) / 2.0
+    else:
+        yhat = rng.lognormal(6.0, 1.0, size=(n_rows, k))
+    out_tok = rng.integers(0, 2000, size=(n_rows, k)).astype(np.int32)
+    arrival = np.sort(rng.random(n_rows) * 10.0) if rng.random() < 0.5 else np.full(n_rows, 3.0)
+    # initial in-flight entries on each model (request ids "seed:j")
+    p0 = []
+    for j in range(p0_entries):
+        m = int(rng.integers(0, k))
+        v = float(rng.integers(1, 3000)) / (1.0 if dyadic else 7.0)
+        p0.append((m, v))
+    # pre-assigned programs (programs 0..7 and some row programs)
+    pre = {}
+    for p in range(8):
+        pre[p] = int(rng.integers(0, k))
+    for p in set(prog.tolist()):
+        if rng.random() < pre_assigned:
+            pre[p] = int(rng.integers(0, k))
+    pre_running = pre_running if pre_running is not None else [0] * k
+    return dict(seed=seed, k=k, ids=ids, decode=decode, batch=batch, n_prog=n_prog,
+                prog=prog, stage=stage, q=q, yhat=yhat, out_tok=out_tok, arrival=arrival,
+                p0=p0, pre=pre, pre_running=pre_running, tau=tau, margin=margin)
+
+
+def run_reference(sc):
+    ids = sc["ids"]
+    k = sc["k"]
+    pool = profiles.Pool(tuple(profiles.ModelProfile(ids[i], sc["decode"][i], sc["batch"][i])
+                               for i in range(k)))
+    mon = monitor.ActivityMonitor(ids)
+    for j, (m, v) in enumerate(sc["p0"]):
+        mon.record_dispatch(ids[m], f"seed:{j}", v)
+    for p, m in sc["pre"].items():
+        mon.assign(f"p{p:06d}", ids[m])
+    aging = engine.AgingConfig()
+    engines = {mid: engine.EngineSim(pool[mid], aging=aging) for mid in ids}
+    for i, mid in enumerate(ids):
+        for j in range(sc["pre_running"][i]):
+            rq = workload.Request(f"r{i}x{j}", 1, 1, 0.0, "wf", "x")
+            engines[mid].enqueue(rq, priority=1.0, out_tokens=10 ** 6, now=0.0)
+    state = balancer.SchedulerState(pool=pool, monitor=mon, queues=engines)
+    n = len(sc["prog"])
+    qtab, ytab, recs, reqs = {}, {}, {}, []
+    for i in range(n):
+        pid = f"p{int(sc['prog'][i]):06d}"
+        st = int(sc["stage"][i])
+        req = workload.Request(pid, st, 10, float(sc["arrival"][i]), "wf", "r")
+        qtab[req.request_id] = {ids[m]: float(sc["q"][i, m]) for m in range(k)}
+        ytab[req.request_id] = {ids[m]: float(sc["yhat"][i, m]) for m in range(k)}
+        rec = recs.get(pid)
+        if rec is None or rec.n_stages < st:
+            stages = [] if rec is None else rec.stages
+            while len(stages) < st:
+                stages.append(workload.StageTrace(len(stages) + 1, "r", 10, {
+                    mid: workload.ModelStageOutput(0, 0) for mid in ids}))
+            rec = workload.TraceRecord(pid, "wf", 0.0, stages, {mid: 0 for mid in ids}, "easy")
+            recs[pid] = rec
+        rec.stages[st - 1].models = {
+            ids[m]: workload.ModelStageOutput(int(sc["out_tok"][i, m]), 0) for m in range(k)}
+        reqs.append(req)
+    rt, pr = ShimRouter(qtab), ShimPredictor(ytab)
+    cfg = balancer.BalancerConfig(sc["tau"], sc["margin"])
+    model = np.full(n, -1, dtype=np.int32)
+    prio = np.zeros(n)
+    cached = np.zeros(n, dtype=np.int8)
+    loads = np.full((n, k), np.nan)
+    seq = np.full(n, -1, dtype=np.int64)
+    admitted = np.zeros(n, dtype=np.int8)
+    err = None
+    for i, req in enumerate(reqs):
+        before = {mid: (engines[mid].running_count, engines[mid]._seq) for mid in ids}
+        try:
+            d = balancer.schedule_request(req, recs[req.program_id], state, rt, pr, cfg)
+        except (SimError, ValueError) as exc:
+            err = {"kind": type(exc).__name__, "row": i}
+            break
+        mi = ids.index(d.model)
+        model[i] = mi
+        prio[i] = d.priority
+        cached[i] = int(d.used_cached_assignment)
+        if d.estimated_loads:
+            loads[i] = [d.estimated_loads[mid] for mid in ids]
+        e = engines[d.model]
+        for s, rr in e.running.items():
+            if rr.entry.request.request_id == req.request_id:
+                seq[i], admitted[i] = s, 1
+        for s, qe in e._queued.items():
+            if qe.request.request_id == req.request_id:
+                seq[i] = s
+    final_p = np.array([mon.in_flight_sum(mid) for mid in ids], dtype=np.float64)
+    final_cnt = np.array([mon.in_flight_count(mid) for mid in ids], dtype=np.int64)
+    running = np.array([engines[mid].running_count for mid in ids], dtype=np.int32)
+    queued = np.array([engines[mid].waiting_count for mid in ids], dtype=np.int32)
+    assign = np.full(sc["n_prog"], -1, dtype=np.int8)
+    for p in range(sc["n_prog"]):
+        a = mon.assignment(f"p{p:06d}")
+        if a is not None:
+            assign[p] = ids.index(a)
+    return dict(model=model, priority=prio, cached=cached, loads=loads, seq=seq,
+                admitted=admitted, final_p=final_p, final_cnt=final_cnt, running=running,
+                queued=queued, assign=assign), err
+
+
+def save_scenario(name, sc, res, err):
+    p0 = np.array(sc["p0"], dtype=np.float64).reshape(-1, 2)
+    pre = np.array(sorted(sc["pre"].items()), dtype=np.int64).reshape(-1, 2)
+    np.savez_compressed(
+        os.path.join(OUT, f"schedule_{name}.npz"),
+        k=sc["k"], decode=np.array(sc["decode"]), batch=np.array(sc["batch"], dtype=np.int32),
+        n_prog=sc["n_prog"], prog=sc["prog"], stage=sc["stage"], q=sc["q"], yhat=sc["yhat"],
+        out_tok=sc["out_tok"], arrival=sc["arrival"], p0=p0, pre=pre,
+        pre_running=np.array(sc["pre_running"], dtype=np.int32), tau=sc["tau"],
+        margin=sc["margin"], err_kind=(err or {}).get("kind", ""),
+        err_row=(err or {}).get("row", -1), **{f"out_{k}": v for k, v in res.items()})
+
+
+def make_schedules():
+    specs = {
+        "k3_basic": dict(seed=1, k=3, n_rows=600),
+        "k5_dyadic_p0": dict(seed=2, k=5, n_rows=2000, p0_entries=3000),
+        "k5_nondyadic_p0": dict(seed=3, k=5, n_rows=2000, dyadic=False, p0_entries=500),
+        "k8_mixed": dict(seed=4, k=8, n_rows=3000, pre_assigned=0.2, repeats=0.15,
+                         dyadic=False, p0_entries=200),
+        "k5_nonpow2": dict(seed=5, k=5, n_rows=1500, batch=[3, 7, 12, 5, 1],
+                           decode=[4.7, 9.3, 13.1, 0.7, 21.0], dyadic=False, p0_entries=100),
+        "k4_ties": dict(seed=6, k=4, n_rows=1200, tied_q=True, margin=0.0, tau=0.0),
+        "k5_slack_big": dict(seed=7, k=5, n_rows=1000, tau=1e6, margin=0.0),
+        "k2_spread": dict(seed=8, k=2, n_rows=800, spread=0.2, pre_running=[31, 0]),
+        "k1_single": dict(seed=9, k=1, n_rows=300),
+        "k6_running": dict(seed=10, k=6, n_rows=1000, pre_running=[5, 16, 8, 0, 2, 1],
+                           repeats=0.1, pre_assigned=0.1),
+    }
+    out = {}
+    for name, spec in specs.items():
+        seed = spec.pop("seed")
+        k = spec.pop("k")
+        n = spec.pop("n_rows")
+        sc = build_scenario(seed, k, n, **spec)
+        res, err = run_reference(sc)
+        save_scenario(name, sc, res, err)
+        out[name] = err
+    return out
+
+
+def make_errors():
+    """Scenarios where the reference raises mid-batch."""
+    cases = {}
+    # ValidationError: score outside [0,1] at row 5
+    sc = build_scenario(21, 3, 20)
+    sc["q"][5, 1] = 1.5
+    res, err = run_reference(sc)
+    save_scenario("err_score", sc, res, err)
+    cases["err_score"] = err
+    # ValueError: negative prediction for the chosen model at row 7 (all models negative)
+    sc = build_scenario(22, 3, 20)
+    sc["yhat"][7, :] = -1.0
+    res, err = run_reference(sc)
+    save_scenario("err_negative", sc, res, err)
+    cases["err_negative"] = err
+    # DuplicateRequest: same (program, stage) twice
+    sc = build_scenario(23, 3, 20)
+    sc["prog"][9] = sc["prog"][4]
+    sc["stage"][9] = sc["stage"][4]
+    res, err = run_reference(sc)
+    save_scenario("err_duplicate", sc, res, err)
+    cases["err_duplicate"] = err
+    # ValueError: time going backwards (arrival decreases by > 1e-9)
+    sc = build_scenario(24, 3, 20)
+    sc["arrival"] = np.linspace(5, 10, 20)
+    sc["arrival"][12] = 1.0
+    sc["q"][:, :] = 0.5  # everything goes to the fastest model -> same engine
+    sc["margin"] = 0.1
+    res, err = run_reference(sc)
+    save_scenario("err_backwards", sc, res, err)
+    cases["err_backwards"] = err
+    # ValidationError: negative out_tokens
+    sc = build_scenario(25, 3, 20)
+    sc["out_tok"][11, :] = -3
+    res, err = run_reference(sc)
+    save_scenario("err_outtok", sc, res, err)
+    cases["err_outtok"] = err
+    with open(os.path.join(OUT, "errors.json"), "w") as fh:
+        json.dump(cases, fh, indent=1, sort_keys=True)
+    return cases
+
+
+# ------------------------------------------------------------------ queues
+def run_queue_script(seed, b, S, n_pre, script):
+    """Drive one EngineSim. `script` is a list of ("enq", n) / ("iter", n) /
+    ("complete", n) steps. Returns admission order and final queue order as
+    lists of request ordinals, plus the queued entries' (level, count)."""
+    rng = np.random.default_rng(seed)
+    prof = profiles.ModelProfile("m0", 1.0, b)
+    aging = engine.AgingConfig(starvation_threshold=S if S else math.inf)
+    eng = engine.EngineSim(prof, aging=aging)
+    t = 0.0
+    ordinal = 0
+    recs = []  # (ordinal, priority, out_tokens_completion_time)
+    admitted = []
+    prio_vals = rng.integers(1, 60, size=100000).astype(np.float64)
+    if seed % 2:
+        prio_vals = prio_vals / 3.0  # non-dyadic
+    # the first b requests fill the batch; completion time controlled by out_tokens
+    enq_log = []
+
+    def enqueue(n):
+        nonlocal ordinal
+        for _ in range(n):
+            p = float(prio_vals[ordinal])
+            rq = workload.Request(f"q{ordinal}", 1, 1, t, "wf", "x")
+            eng.enqueue(rq, priority=p, out_tokens=10 ** 9, now=t)
+            enq_log.append((ordinal, p, t))
+            ordinal += 1
+
+    admit_events = []
+    orig_admit = eng._admit
+
+    def spy(entry, now):
+        admit_events.append(int(entry.request.program_id[1:]))
+        rr = orig_admit(entry, now)
+        return rr
+    eng._admit = spy
+    enqueue(n_pre)
+    for op, n in script:
+        if op == "enq":
+            t += 1.0
+            enqueue(n)
+        elif op == "iter":
+            for _ in range(n):
+                t += 1.0
+                eng.scheduling_iteration(t)
+        elif op == "complete":
+            # complete the n earliest-admitted running requests at time t+1:
+            # shorten their stint so they end exactly then
+            t += 1.0
+            victims = sorted(eng.running)[:n]
+            for s in victims:
+                eng.running[s].stint_end = t
+            eng.advance_to(t)
+    order = [int(e.request.program_id[1:]) for e in sorted(eng._queued.values(),
+                                                             key=lambda e: e.sort_key())]
+    lv = {int(e.request.program_id[1:]): (e.starvation_level, e.starvation_count)
+          for e in eng._queued.values()}
+    return dict(enq=np.array(enq_log, dtype=np.float64), admitted=np.array(admit_events),
+                order=np.array(order), level=np.array([lv[o][0] for o in order]),
+                count=np.array([lv[o][1] for o in order]), running=eng.running_count,
+                iterations=eng.iterations)
+
+
+def make_queues():
+    scripts = {
+        "q_basic": (1, 4, 8, 20, [("iter", 3), ("enq", 10), ("iter", 2)]),
+        "q_promote": (2, 2, 3, 12, [("iter", 4), ("enq", 5), ("iter", 5)]),
+        "q_complete": (3, 8, 4, 60, [("iter", 2), ("complete", 3), ("enq", 7),
+                                      ("iter", 1), ("complete", 8), ("iter", 6)]),
+        "q_noaging": (4, 3, 0, 40, [("iter", 20), ("complete", 3), ("enq", 4), ("iter", 2)]),
+        "q_big": (5, 32, 8, 3000, [("iter", 7), ("complete", 32), ("enq", 500), ("iter", 3),
+                                   ("complete", 16), ("iter", 9), ("complete", 32)]),
+        "q_S1": (6, 2, 1, 30, [("iter", 3), ("complete", 2), ("iter", 2)]),
+    }
+    for name, (seed, b, S, n_pre, script) in scripts.items():
+        res = run_queue_script(seed, b, S, n_pre, script)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), seed=seed, b=b, S=S, n_pre=n_pre,
+                            script=json.dumps(script), **res)
+
+
+# ---------------------------------------------------------------- quantile
+MATH_STATS = {"m0": (606.0, 2587.0), "m1": (657.5, 1651.0), "m2": (709.0, 715.0)}
+MATH_SUCCESS = {"m0": {"easy": 0.55, "hard": 0.12}, "m1": {"easy": 0.72, "hard": 0.36},
+                "m2": {"easy": 0.9, "hard": 0.6}}
+
+
+def make_quantile():
+    stats = {m: workload.LengthStats(*v) for m, v in MATH_STATS.items()}
+    tr = workload.synthesize_trace(workload.MATH_WORKFLOWS, stats, MATH_SUCCESS, 2000, 1)
+    wfs = ["math-4stage", "math-2stage", "math-1stage", "unknown-wf"]
+    out = {}
+    for q in (0.5, 0.9, 0.37):
+        pr = predictor.EmpiricalQuantilePredictor(tr, q)
+        grid = np.zeros((len(wfs), 7, 3))
+        for a, wf in enumerate(wfs):
+            for st in range(1, 8):
+                for m in range(3):
+                    req = workload.Request("x", st, 1, 0.0, wf, "r")
+                    grid[a, st - 1, m] = pr.predict(req, None, f"m{m}")
+        out[f"q{q}"] = grid
+    np.savez_compressed(os.path.join(OUT, "quantile.npz"), wfs=np.array(wfs), **out)
+
+
+def trace_digest(tr):
+    h = hashlib.sha256()
+    for rec in tr:
+        h.update(json.dumps(rec.to_json_dict(), sort_keys=True).encode())
+    return h.hexdigest()
+
+
+def make_synth():
+    out = {}
+    stats = {m: workload.LengthStats(*v) for m, v in MATH_STATS.items()}
+    out["math_2000_1"] = trace_digest(
+        workload.synthesize_trace(workload.MATH_WORKFLOWS, stats, MATH_SUCCESS, 2000, 1))
+    code_stats = {"fast": workload.LengthStats(447, 1276), "strong": workload.LengthStats(649, 534)}
+    code_succ = {"fast": {"easy": 0.45, "hard": 0.08}, "strong": {"easy": 0.85, "hard": 0.55}}
+    out["code_500_3"] = trace_digest(
+        workload.synthesize_trace(workload.CODE_WORKFLOWS, code_stats, code_succ, 500, 3))
+    out["code_300_4_weights"] = trace_digest(workload.synthesize_trace(
+        workload.CODE_WORKFLOWS, code_stats, code_succ, 300, 4,
+        role_weights={"planner": 0.5, "coder": 2.0}, template_mix=[1, 2, 3]))
+    with open(os.path.join(OUT, "synth.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    print("select cases:", make_select_kat())
+    print("schedule:", make_schedules())
+    print("errors:", make_errors())
+    make_queues()
+    make_quantile()
+    make_synth()
+    print("done")
