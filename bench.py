@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the Chimera scheduling tick on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+One step = one scheduling tick over one batch of B synthetic requests already
+resident in HBM: chm_prepare_rows -> router encoder (tcgen05) -> quantile
+predictor -> serial-exact selection -> STJF+aging queue tick, from the same
+fresh monitor/queue state every tick (the reference CPU path is timed the same
+way). N > 1: one process per GPU (torchrun), weak scaling (B per GPU), the
+per-engine in-flight vector all-reduced over NCCL each tick (Mode A).
+
+Rank 0 prints ONE JSON line. `value` = decisions/s of the whole job, device
+timed (CUDA events, max over ranks); `e2e` = the same through the public API
+with host->device input copies and device->host decision reads inside the
+timed region (wall clock, synchronised); `roofline` = the dominant kernel
+(tcgen05 GEMM) timed live with CUDA events on its stream inside the timed
+region; `cpu_baseline` = the oracle port of the reference path + the fp32
+encoder restatement on this host's cores, on a bounded sample.
+
+--impl reference times that CPU path alone as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scheduling decisions/sec (router+predictor+select+STJF) at batch 4096; p50 tick latency"
+UNIT = "decisions/s"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="cfg3")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-clocks", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int, enabled: bool):
+        self.proc = None
+        self.path = None
+        if not enabled:
+            return
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[3], 16)
+            except ValueError:
+                continue
+            for b, name in REASON_BITS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- CPU reference path
+def cpu_reference_tick(wl, cols, q_rows, hp):
+    """One tick of the reference path through the oracle port: B calls of
+    schedule_request (balancer.py:89-129) + one scheduling_iteration per engine.
+    Scores come from a precomputed table (the reference's table-router cost)."""
+    ids = wl.pool.model_ids
+    recs = cols["records"]
+    mon = hp.PortMonitor(ids)
+    engines = {m: hp.PortEngine(wl.pool[m].max_batch_size) for m in ids}
+    pred = cols["_port_predictor"]
+    qtab = cols["_qtab"]
+    reqs = cols["_reqs"]
+    t0 = time.perf_counter()
+    hp.port_tick(reqs, recs, wl.pool, mon, engines, lambda r, rc: qtab[r.request_id], pred,
+                 wl.balancer.latency_slack, wl.balancer.confidence_margin, 1)
+    return time.perf_counter() - t0
+
+
+def prepare_cpu_inputs(wl, cols, q, hp):
+    from paper_2603_22206_b200.workload import first_stage_request
+    ids = wl.pool.model_ids
+    reqs = [first_stage_request(rec, float(cols["arrival"][i]))
+            for i, rec in enumerate(cols["records"])]
+    cols["_reqs"] = reqs
+    cols["_qtab"] = {r.request_id: {m: float(q[i, k]) for k, m in enumerate(ids)}
+                     for i, r in enumerate(reqs)}
+    cols["_port_predictor"] = hp.PortQuantilePredictor(wl.training, 0.5)
+    return cols
+
+
+_CPU_WEIGHTS = {}
+
+
+def cpu_router_sample(wl, n_sample: int, seed: int = 77):
+    """Seconds per request of the fp32 encoder restatement on the host CPU,
+    same architecture and weights as the device router (seed 0)."""
+    import torch
+
+    from oracle.encoder_ref import encoder_forward_fp32
+    from paper_2603_22206_b200.encoder import init_weights, synthetic_token_ids
+    cfg = wl.spec.encoder
+    K = len(wl.pool)
+    if cfg not in _CPU_WEIGHTS:
+        w = init_weights(cfg, K, seed=0, device="cpu")
+        _CPU_WEIGHTS[cfg] = {k: v.to(torch.float32) for k, v in w.items()}
+    w_cpu = _CPU_WEIGHTS[cfg]
+    ids = torch.as_tensor(synthetic_token_ids(n_sample, cfg.seq_len, seed, cfg.vocab))
+    with torch.no_grad():
+        encoder_forward_fp32(w_cpu, ids[:1], cfg.n_layers, cfg.n_heads, cfg.ln_eps,
+                             device="cpu")  # warm-up
+        t0 = time.perf_counter()
+        encoder_forward_fp32(w_cpu, ids, cfg.n_layers, cfg.n_heads, cfg.ln_eps, device="cpu")
+    return (time.perf_counter() - t0) / n_sample
+
+
+def cpu_baseline(wl, q_tick0, n_ticks=3, n_router=16):
+    """Bounded-sample CPU baseline: (i) oracle port of the reference selection
+    path on 1 thread over `n_ticks` full ticks, (ii) fp32 encoder restatement
+    on all host threads over `n_router` sequences, extrapolated per request."""
+    import torch
+
+    from oracle import hetsched_port as hp
+    B = wl.batch_size
+    sel = []
+    for t in range(n_ticks):
+        cols = prepare_cpu_inputs(wl, wl.host_columns(t), q_tick0, hp)
+        sel.append(cpu_reference_tick(wl, cols, q_tick0, hp))
+    t_sel = statistics.median(sel)
+    threads = torch.get_num_threads()
+    t_req = cpu_router_sample(wl, n_router)
+    tick = t_sel + B * t_req
+    return {
+        "value": B / tick, "unit": UNIT, "cores": threads, "kind": "port",
+        "sample": (f"selection+STJF: {n_ticks} full ticks of {B} rows through the oracle port "
+                   f"(1 thread, p50 {t_sel * 1e3:.1f} ms/tick); router: {n_router} of {B} "
+                   f"sequences through the fp32 encoder restatement on {threads} threads "
+                   f"({t_req * 1e3:.1f} ms/request), extrapolated to {B}"),
+        "selection_decisions_per_s": B / t_sel,
+        "router_ms_per_request": t_req * 1e3,
+        "cpu_model": _cpu_model(),
+        "affinity_cores": len(os.sched_getaffinity(0)),
+    }
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+
+    from oracle import hetsched_port as hp
+    from paper_2603_22206_b200 import synth
+    wl = synth.make_workload(args.config, device="cpu", with_router=False)
+    B = wl.batch_size
+    K = len(wl.pool)
+    rng = np.random.default_rng(0)
+    q = rng.random((B, K)).astype(np.float32)
+    n_router = 8 if wl.spec.encoder.hidden >= 768 else 64
+    times = []
+    for step in range(args.warmup + args.steps):
+        cols = prepare_cpu_inputs(wl, wl.host_columns(step), q, hp)
+        t_sel = cpu_reference_tick(wl, cols, q, hp)
+        t_req = cpu_router_sample(wl, n_router, seed=1000 + step)
+        if step >= args.warmup:
+            times.append(t_sel + B * t_req)
+    tick = statistics.median(times)
+    value = B / tick
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tick * 1e3,
+        "p50_tick_ms": tick * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32+fp64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {wl.spec.description}", "batch": B,
+                   "models": K, "router": _router_desc(wl)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": torch.get_num_threads(),
+                         "kind": "port",
+                         "sample": (f"per step: one full tick of {B} rows through the oracle "
+                                    f"port of the reference selection+STJF path (1 thread) + "
+                                    f"{n_router} sequences of the fp32 encoder restatement "
+                                    f"({torch.get_num_threads()} threads), extrapolated to {B}")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def _router_desc(wl):
+    c = wl.spec.encoder
+    return f"L{c.n_layers} H{c.hidden} A{c.n_heads} F{c.ffn} S{c.seq_len}"
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_22206_b200 import _lib, synth
+    from paper_2603_22206_b200.scheduler import GpuScheduler, HostStaging
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = synth.make_workload(args.config, device=dev)
+    B, K = wl.batch_size, len(wl.pool)
+    gs = GpuScheduler(wl.pool, wl.balancer, wl.aging, router=wl.router, predictor=wl.predictor,
+                      n_programs=wl.n_programs, max_rows=B, device=dev)
+    snap = gs.state.snapshot()
+    p0 = None
+    n_distinct = 4
+    host_cols = []
+    batches = []
+    for t in range(n_distinct):
+        cols = wl.host_columns(t + 1000 * rank)
+        host_cols.append(cols)
+        batches.append(wl.batch(t + 1000 * rank))
+    stream = torch.cuda.current_stream(dev)
+
+    def allreduce_inflight():
+        # Mode A: every GPU ran its shard's serial chain from the tick-start
+        # global P; the per-engine in-flight deltas are summed over NCCL.
+        nonlocal p0
+        st = gs.state
+        val = st.inflight_sum + torch.where(torch.isfinite(st.inflight_comp),
+                                            st.inflight_comp, torch.zeros_like(st.inflight_comp))
+        if p0 is None:
+            p0 = snap["inflight_sum"].clone()
+        delta = val - p0
+        dist.all_reduce(delta)
+        st.inflight_sum.copy_(p0 + delta)
+        st.inflight_comp.zero_()
+
+    def tick(i, batch=None):
+        gs.state.restore(snap)
+        gs.run_rows(batch if batch is not None else batches[i % n_distinct], n_iterations=1,
+                    stream=stream)
+        if world > 1:
+            allreduce_inflight()
+
+    for i in range(args.warmup):
+        tick(i)
+    torch.cuda.synchronize()
+    gs.check_errors("warmup")
+    q_tick0 = gs.buf.scores[:B * K].view(B, K).cpu().numpy().copy()
+
+    # ---------------- timed region (device) ----------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local, not args.no_clocks)
+    _lib.profile_read()  # reset timings
+    _lib.profile_enable(True)
+    launches0 = _lib.profile_read()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        tick(i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    clk = clocks.stop()
+    gs.check_errors("timed")
+    tick_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = args.steps * B * world / (total_ms / 1e3)
+    n_launch = sum(prof[k]["launches"] - launches0[k]["launches"] for k in prof)
+
+    # ---------------- end-to-end through the public API ----------------
+    e2e = None
+    if not args.no_e2e:
+        stages = [HostStaging({k: v for k, v in c.items() if k != "records"}, dev)
+                  for c in host_cols]
+        for i in range(2):
+            s = stages[i % n_distinct]
+            tick(i, s.upload())
+            s.download(gs.buf)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = []
+        for i in range(args.steps):
+            s = stages[i % n_distinct]
+            t0 = time.perf_counter()
+            tick(i, s.upload())
+            s.download(gs.buf)
+            torch.cuda.current_stream(dev).synchronize()
+            wall.append(time.perf_counter() - t0)
+        tw = torch.tensor([sum(wall)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.steps * B * world / float(tw.item()), "unit": UNIT,
+               "h2d_bytes_per_step": stages[0].h2d_bytes,
+               "d2h_bytes_per_step": stages[0].d2h_bytes,
+               "p50_step_ms": statistics.median(wall) * 1e3}
+
+    # ---------------- roofline of the dominant kernel ----------------
+    peaks, peak_src = load_peaks()
+    g = prof["gemm"]
+    gemm_tflops = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
+    peak_t = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.config)
+    roofline = {"bound": "tensor", "kernel": "chm::gemm::gemm_kernel (tcgen05 128x256x64, TMA)",
+                "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
+                "frac": gemm_tflops / peak_t if peak_t else None, "traffic": traffic,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (GEMMs run inside a long step)",
+                "launches_timed": g["timed"],
+                "share_of_step": (g["ms"] / args.steps) / statistics.mean(tick_ms)}
+    stage_ms = {k: v["ms"] / args.steps for k, v in prof.items() if v["timed"]}
+    router_flops = B * wl.spec.encoder.flops_per_request(K)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "p50_tick_ms": statistics.median(tick_ms),
+        "p99_tick_ms": sorted(tick_ms)[min(len(tick_ms) - 1, int(math.ceil(0.99 * len(tick_ms))) - 1)],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": ("synthetic: first-stage requests from synthesize_trace(B, seed=100+tick), "
+                 "[CLS]+U[1000,30522) token ids, BERT-init router weights (seed 0), "
+                 "quantile predictor trained on synthesize_trace(2000, seed=1)"),
+        "config": {"workload": f"{args.config}: {wl.spec.description}", "batch_per_gpu": B,
+                   "global_batch": B * world, "models": K, "router": _router_desc(wl),
+                   "parallelism": f"request-sharded x{world} (NCCL all-reduce of in-flight "
+                                  f"vector)" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (router activations >1 GB per layer)",
+                   "state": "fresh monitor/queues per tick (device-side restore, timed)"},
+        "roofline": roofline,
+        "gpu_launches": n_launch,
+        "stages_ms_per_tick": stage_ms,
+        "router_tflops_achieved": router_flops * args.steps /
+                                  ((prof["gemm"]["ms"] + prof["attention"]["ms"] +
+                                    prof["rowwise"]["ms"]) / 1e3) / 1e12,
+        "clocks": clk,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, q_tick0)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

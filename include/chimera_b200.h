@@ -262,6 +262,15 @@ chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bia
                          const void* residual, int32_t M, int32_t N, int32_t K,
                          int32_t epilogue, void* stream);
 
+/* Profiling: launch counters per kernel class (always on) and opt-in CUDA
+ * event timing around every launch on its own stream. Classes: 0 GEMM,
+ * 1 attention, 2 row-wise (embedding+LN, LayerNorm, head), 3 predictor,
+ * 4 prepare, 5 select, 6 queue. chm_profile_read synchronises on the recorded
+ * events, fills 7-entry arrays (timed launches, summed ms, summed algorithmic
+ * work -- FLOPs or bytes --, cumulative launch counts) and clears the timings. */
+chm_status chm_profile_enable(int32_t enable);
+chm_status chm_profile_read(int32_t* timed, double* total_ms, double* work, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

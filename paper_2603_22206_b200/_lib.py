@@ -205,7 +205,29 @@ _SIGNATURES = [
     ("chm_gemm_bf16", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
       c_void_p]),
+    ("chm_profile_enable", c_int32, [c_int32]),
+    ("chm_profile_read", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]
+
+PROFILE_KINDS = ["gemm", "attention", "rowwise", "predict", "prepare", "select", "queue"]
+
+
+def profile_enable(on: bool) -> None:
+    check(load().chm_profile_enable(1 if on else 0), "chm_profile_enable")
+
+
+def profile_read() -> dict:
+    """{kind: {"timed", "ms", "work", "launches"}} since the last read."""
+    n = len(PROFILE_KINDS)
+    timed = (ctypes.c_int32 * n)()
+    ms = (ctypes.c_double * n)()
+    work = (ctypes.c_double * n)()
+    launches = (ctypes.c_int64 * n)()
+    check(load().chm_profile_read(ctypes.addressof(timed), ctypes.addressof(ms),
+                                  ctypes.addressof(work), ctypes.addressof(launches)),
+          "chm_profile_read")
+    return {k: {"timed": timed[i], "ms": ms[i], "work": work[i], "launches": launches[i]}
+            for i, k in enumerate(PROFILE_KINDS)}
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]
 

@@ -1,0 +1,445 @@
+// Router encoder: K1 embedding + LayerNorm, K2 tcgen05
+// GEMMs (gemm.cu), K3 tcgen05 attention, post-LN LayerNorm, K4 CLS head.
+//
+// The reference has no neural router: router.py:34-45 only pins the contract
+// (one score per pool model, in [0,1], in pool.model_ids order). The paper's
+// router is an encoder with a sigmoid multi-label head on the [CLS] state
+// (PAPER.md:327-329); this is a BERT-style post-LN encoder with that head.
+// Its fp32 restatement is oracle/encoder_ref.py.
+//
+// Activations are bf16 in HBM, all accumulation and normalisation in fp32.
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "sm100.cuh"
+#include "prof.cuh"
+
+namespace chm {
+
+chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
+                     const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
+                     void* vt, int hidden, int seq_len);
+namespace gemm {
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows, uint32_t box_cols);
+}
+
+namespace enc {
+
+// ---------------------------------------------------------------------------
+// LayerNorm over H = 32 * 8 * VEC elements, one warp per row. Each lane owns
+// VEC 16-byte chunks (8 bf16 each).
+// ---------------------------------------------------------------------------
+template <int VEC>
+__device__ __forceinline__ void ln_row_store(float (&v)[VEC * 8], const float* __restrict__ g,
+                                             const float* __restrict__ b, float eps, int lane,
+                                             __nv_bfloat16* __restrict__ out) {
+  constexpr int H = 32 * 8 * VEC;
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < VEC * 8; ++j) sum += v[j];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum * (1.0f / H);
+  float var = 0.f;
+#pragma unroll
+  for (int j = 0; j < VEC * 8; ++j) {
+    const float d = v[j] - mean;
+    var += d * d;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+  const float rstd = rsqrtf(var * (1.0f / H) + eps);
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) {
+    const int col = (c * 32 + lane) * 8;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(g + col));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(g + col + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(b + col));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(b + col + 4));
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float x0 = (v[c * 8 + 2 * e] - mean) * rstd * gg[2 * e] + bb[2 * e];
+      const float x1 = (v[c * 8 + 2 * e + 1] - mean) * rstd * gg[2 * e + 1] + bb[2 * e + 1];
+      o[e] = __floats2bfloat162_rn(x0, x1);
+    }
+    *reinterpret_cast<uint4*>(out + col) = *reinterpret_cast<uint4*>(o);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ src, int lane,
+                                         float (&v)[VEC * 8]) {
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src + (c * 32 + lane) * 8));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      v[c * 8 + 2 * e] = f.x;
+      v[c * 8 + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+// K1: x[t] = LN(word_emb[id] + pos_emb[pos] + type_emb), t = seq*S + pos.
+// Sequence i reads token ids of batch row rows[i] (rows == nullptr: row i).
+template <int VEC>
+__global__ void __launch_bounds__(256) embed_ln_kernel(
+    const int32_t* __restrict__ ids, const int32_t* __restrict__ rows,
+    const int32_t* __restrict__ n_rows_dev, int n_seq, int S, int vocab,
+    const __nv_bfloat16* __restrict__ wemb, const __nv_bfloat16* __restrict__ pemb,
+    const __nv_bfloat16* __restrict__ temb, const float* __restrict__ g,
+    const float* __restrict__ b, float eps, __nv_bfloat16* __restrict__ x) {
+  constexpr int H = 32 * 8 * VEC;
+  const int lane = threadIdx.x & 31;
+  const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= (long long)n_seq * S) return;
+  const int seq = (int)(t / S), pos = (int)(t - (long long)seq * S);
+  const int n_live = n_rows_dev ? *n_rows_dev : n_seq;
+  int row = seq;
+  if (rows) row = rows[seq < n_live ? seq : 0];
+  int id = ids[(size_t)row * S + pos];
+  id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+  float v[VEC * 8], w[VEC * 8];
+  load_row<VEC>(wemb + (size_t)id * H, lane, v);
+  load_row<VEC>(pemb + (size_t)pos * H, lane, w);
+#pragma unroll
+  for (int j = 0; j < VEC * 8; ++j) v[j] += w[j];
+  load_row<VEC>(temb, lane, w);
+#pragma unroll
+  for (int j = 0; j < VEC * 8; ++j) v[j] += w[j];
+  ln_row_store<VEC>(v, g, b, eps, lane, x + (size_t)t * H);
+}
+
+// Post-LN: x[t] = LN(tmp[t]) (tmp already holds residual + sublayer output).
+template <int VEC>
+__global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __restrict__ in,
+                                                        long long n_rows,
+                                                        const float* __restrict__ g,
+                                                        const float* __restrict__ b, float eps,
+                                                        __nv_bfloat16* __restrict__ out) {
+  constexpr int H = 32 * 8 * VEC;
+  const int lane = threadIdx.x & 31;
+  const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= n_rows) return;
+  float v[VEC * 8];
+  load_row<VEC>(in + (size_t)t * H, lane, v);
+  ln_row_store<VEC>(v, g, b, eps, lane, out + (size_t)t * H);
+}
+
+// ---------------------------------------------------------------------------
+// K3 attention, one CTA per (sequence, head), S = 128, d = 64, tcgen05:
+//   S_tile = Q K^T  (M=128, N=128, K=64)   -> TMEM cols [0,128)
+//   softmax row-per-thread straight out of TMEM (no shuffles), unnormalised
+//   P = exp(s - max) written bf16 into a K-major 128B-swizzled smem tile
+//   O = P V        (M=128, N=64,  K=128)   -> TMEM cols [128,192)
+//   O / rowsum -> ctx (bf16)
+// Q is pre-scaled by 1/sqrt(d) in the QKV epilogue; V arrives transposed.
+// 5 warps: 0-3 softmax/epilogue (warp w owns TMEM lanes 32w..32w+31),
+// warp 4 issues TMA and MMA. ~81 KB smem -> two CTAs per SM overlap phases.
+// ---------------------------------------------------------------------------
+constexpr int kAttnS = 128;
+struct AttnSmem {
+  uint8_t q[kAttnS * 64 * 2];        // 16 KB, [128 rows][64] SW128
+  uint8_t k[kAttnS * 64 * 2];        // 16 KB
+  uint8_t vt[2][64 * 64 * 2];        // 2 x 8 KB, V^T [64 d][64 keys] per key half
+  uint8_t p[2][kAttnS * 64 * 2];     // 2 x 16 KB, P [128 rows][64 keys] per key half
+  uint64_t bar_load, bar_s, bar_p, bar_o;
+  uint32_t tmem_base;
+};
+constexpr size_t kAttnSmemBytes = sizeof(AttnSmem) + 1024;
+
+__global__ void __launch_bounds__(160, 2)
+    attention_kernel(const __grid_constant__ CUtensorMap tm_qk,
+                     const __grid_constant__ CUtensorMap tm_vt, int n_heads, int hidden,
+                     __nv_bfloat16* __restrict__ ctx) {
+  extern __shared__ uint8_t smem_raw[];
+  AttnSmem& s = *reinterpret_cast<AttnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x;
+  const int seq = item / n_heads, h = item - seq * n_heads;
+  if (warp == 4 && lane == 0) {
+    sm100::mbar_init(&s.bar_load, 1);
+    sm100::mbar_init(&s.bar_s, 1);
+    sm100::mbar_init(&s.bar_p, 128);
+    sm100::mbar_init(&s.bar_o, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<256>(&s.tmem_base);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      constexpr uint32_t kBytes = 2 * kAttnS * 64 * 2 + 2 * 64 * 64 * 2;
+      sm100::mbar_arrive_expect_tx(&s.bar_load, kBytes);
+      const int row0 = seq * kAttnS;
+      sm100::tma_load_2d(s.q, &tm_qk, &s.bar_load, h * 64, row0);
+      sm100::tma_load_2d(s.k, &tm_qk, &s.bar_load, hidden + h * 64, row0);
+      const int vrow = (seq * n_heads + h) * 64;
+      sm100::tma_load_2d(s.vt[0], &tm_vt, &s.bar_load, 0, vrow);
+      sm100::tma_load_2d(s.vt[1], &tm_vt, &s.bar_load, 64, vrow);
+      sm100::mbar_wait(&s.bar_load, 0);
+      sm100::tc_fence_after();
+      constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
+      const uint32_t qa = sm100::smem_u32(s.q), ka = sm100::smem_u32(s.k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sm100::mma_bf16(tmem, sm100::umma_desc_sw128(qa + k * 32),
+                        sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+      sm100::mma_commit(&s.bar_s);
+      sm100::mbar_wait(&s.bar_p, 0);
+      sm100::tc_fence_after();
+      constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t pa = sm100::smem_u32(s.p[kk >> 2]) + (kk & 3) * 32;
+        const uint32_t va = sm100::smem_u32(s.vt[kk >> 2]) + (kk & 3) * 32;
+        sm100::mma_bf16(tmem + 128, sm100::umma_desc_sw128(pa), sm100::umma_desc_sw128(va),
+                        idesc_o, kk);
+      }
+      sm100::mma_commit(&s.bar_o);
+    }
+    __syncwarp();
+  } else {
+    // softmax: thread = query row r
+    const int r = warp * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    sm100::mbar_wait(&s.bar_s, 0);
+    sm100::tc_fence_after();
+    uint32_t raw[4][32];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) sm100::tmem_ld_32x32b_x32(tmem + lane_base + c * 32, raw[c]);
+    sm100::tmem_ld_wait();
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(raw[c][j]));
+    const float mxl = mx * 1.4426950408889634f;
+    float sum = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      // keys [32c, 32c+32) -> half c/2, 16B chunks 4*(c&1) .. +3 of the 128B row
+      uint8_t* rowp = s.p[c >> 1] + r * 128;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = exp2f(fmaf(__uint_as_float(raw[c][q4 * 8 + 2 * e]), 1.4426950408889634f, -mxl));
+          const float p1 = exp2f(fmaf(__uint_as_float(raw[c][q4 * 8 + 2 * e + 1]), 1.4426950408889634f, -mxl));
+          o[e] = __floats2bfloat162_rn(p0, p1);
+          // accumulate the bf16-rounded values so the normaliser matches P
+          const float2 back = __bfloat1622float2(o[e]);
+          sum += back.x + back.y;
+        }
+        const int chunk = (c & 1) * 4 + q4;
+        *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
+            *reinterpret_cast<uint4*>(o);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    sm100::mbar_arrive(&s.bar_p);
+    sm100::mbar_wait(&s.bar_o, 0);
+    sm100::tc_fence_after();
+    uint32_t ov[2][32];
+    sm100::tmem_ld_32x32b_x32(tmem + lane_base + 128, ov[0]);
+    sm100::tmem_ld_32x32b_x32(tmem + lane_base + 160, ov[1]);
+    sm100::tmem_ld_wait();
+    const float inv = 1.0f / sum;
+    __nv_bfloat16* dst = ctx + ((size_t)seq * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          o[e] = __floats2bfloat162_rn(__uint_as_float(ov[c][q4 * 8 + 2 * e]) * inv,
+                                       __uint_as_float(ov[c][q4 * 8 + 2 * e + 1]) * inv);
+        *reinterpret_cast<uint4*>(dst + c * 32 + q4 * 8) = *reinterpret_cast<uint4*>(o);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<256>(tmem);
+  }
+}
+
+// K4: the last layer's output LayerNorm, fused for the [CLS] rows only and
+// kept in fp32, then q[rows[i]*K + m] = sigmoid(head_b[m] + <LN(tmp[i*S]), head_w[m]>)
+// for i < n_live. (Only the CLS state feeds the router head, so the last
+// LayerNorm is never materialised for the other S-1 tokens.)
+template <int VEC>
+__global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restrict__ tmp, int S,
+                                                   int n_seq, const int32_t* __restrict__ rows,
+                                                   const int32_t* __restrict__ n_rows_dev,
+                                                   const float* __restrict__ ln_g,
+                                                   const float* __restrict__ ln_b, float eps,
+                                                   const float* __restrict__ w,
+                                                   const float* __restrict__ bias, int K,
+                                                   float* __restrict__ q) {
+  constexpr int H = 32 * 8 * VEC;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int n_live = n_rows_dev ? *n_rows_dev : n_seq;
+  if (i >= n_seq || i >= n_live) return;
+  float v[VEC * 8];
+  load_row<VEC>(tmp + (size_t)i * S * H, lane, v);
+  {
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < VEC * 8; ++j) sum += v[j];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum * (1.0f / H);
+    float var = 0.f;
+#pragma unroll
+    for (int j = 0; j < VEC * 8; ++j) var += (v[j] - mean) * (v[j] - mean);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+    const float rstd = rsqrtf(var * (1.0f / H) + eps);
+#pragma unroll
+    for (int c = 0; c < VEC; ++c)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int col = (c * 32 + lane) * 8 + e;
+        v[c * 8 + e] = (v[c * 8 + e] - mean) * rstd * ln_g[col] + ln_b[col];
+      }
+  }
+  const int row = rows ? rows[i] : i;
+  for (int m = 0; m < K; ++m) {
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) {
+      const float* wp = w + (size_t)m * H + (c * 32 + lane) * 8;
+      const float4 w0 = __ldg(reinterpret_cast<const float4*>(wp));
+      const float4 w1 = __ldg(reinterpret_cast<const float4*>(wp + 4));
+      acc += v[c * 8 + 0] * w0.x + v[c * 8 + 1] * w0.y + v[c * 8 + 2] * w0.z +
+             v[c * 8 + 3] * w0.w + v[c * 8 + 4] * w1.x + v[c * 8 + 5] * w1.y +
+             v[c * 8 + 6] * w1.z + v[c * 8 + 7] * w1.w;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) q[(size_t)row * K + m] = 1.0f / (1.0f + __expf(-(acc + bias[m])));
+  }
+}
+
+template <int VEC>
+static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weights& w,
+                              const chm_encoder_workspace& ws, const int32_t* ids,
+                              const int32_t* rows, const int32_t* n_rows_dev, int n_seq, int S,
+                              float* q_out, cudaStream_t st) {
+  const int H = cfg.hidden, F = cfg.ffn, L = cfg.n_layers;
+  const long long T = (long long)n_seq * S;
+  auto* x = reinterpret_cast<__nv_bfloat16*>(ws.x);
+  auto* qk = reinterpret_cast<__nv_bfloat16*>(ws.qkv);
+  auto* ctx = reinterpret_cast<__nv_bfloat16*>(ws.ctx);
+  auto* tmp = reinterpret_cast<__nv_bfloat16*>(ws.tmp);
+  auto* ffn = reinterpret_cast<__nv_bfloat16*>(ws.ffn);
+  // V^T lives in the ctx-sized tail of the qkv workspace ([T, 3H]: Q|K use 2H).
+  auto* vt = qk + (size_t)T * 2 * H;
+  const int rows_per_cta = 256 / 32;
+  const unsigned grid_t = (unsigned)((T + rows_per_cta - 1) / rows_per_cta);
+  prof::begin(prof::K_ROWWISE, st);
+  embed_ln_kernel<VEC><<<grid_t, 256, 0, st>>>(
+      ids, rows, n_rows_dev, n_seq, S, cfg.vocab,
+      reinterpret_cast<const __nv_bfloat16*>(w.word_emb),
+      reinterpret_cast<const __nv_bfloat16*>(w.pos_emb),
+      reinterpret_cast<const __nv_bfloat16*>(w.type_emb), w.emb_ln_g, w.emb_ln_b, cfg.ln_eps, x);
+  prof::end(prof::K_ROWWISE, st, (double)T * (4.0 + 6.0 * H));
+  CHM_LAUNCH_CHECK();
+  CUtensorMap tm_qk, tm_vt;
+  if (!gemm::make_tmap_bf16(&tm_qk, qk, (uint64_t)T, (uint64_t)2 * H, 128, 64)) return CHM_ERR_CUDA;
+  if (!gemm::make_tmap_bf16(&tm_vt, vt, (uint64_t)n_seq * (H / 64) * 64, (uint64_t)S, 64, 64))
+    return CHM_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kAttnSmemBytes);
+    attr = true;
+  }
+  const int NH = H / 64;
+  chm_status rc;
+  for (int l = 0; l < L; ++l) {
+    rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, vt, H, S);
+    if (rc != CHM_OK) return rc;
+    prof::begin(prof::K_ATTENTION, st);
+    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qk, tm_vt, NH, H,
+                                                                         ctx);
+    prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
+    CHM_LAUNCH_CHECK();
+    rc = gemm_bf16(ctx, w.w_o[l], tmp, w.b_o[l], x, (int)T, H, H, 3, st, nullptr, 0, 0);
+    if (rc != CHM_OK) return rc;
+    prof::begin(prof::K_ROWWISE, st);
+    layernorm_kernel<VEC><<<grid_t, 256, 0, st>>>(tmp, T, w.ln1_g[l], w.ln1_b[l], cfg.ln_eps, x);
+    prof::end(prof::K_ROWWISE, st, (double)T * 4.0 * H);
+    CHM_LAUNCH_CHECK();
+    rc = gemm_bf16(x, w.w_1[l], ffn, w.b_1[l], nullptr, (int)T, F, H, 2, st, nullptr, 0, 0);
+    if (rc != CHM_OK) return rc;
+    rc = gemm_bf16(ffn, w.w_2[l], tmp, w.b_2[l], x, (int)T, H, F, 3, st, nullptr, 0, 0);
+    if (rc != CHM_OK) return rc;
+    if (l + 1 < L) {
+      prof::begin(prof::K_ROWWISE, st);
+      layernorm_kernel<VEC><<<grid_t, 256, 0, st>>>(tmp, T, w.ln2_g[l], w.ln2_b[l], cfg.ln_eps,
+                                                    x);
+      prof::end(prof::K_ROWWISE, st, (double)T * 4.0 * H);
+      CHM_LAUNCH_CHECK();
+    }
+  }
+  prof::begin(prof::K_ROWWISE, st);
+  head_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(
+      tmp, S, n_seq, rows, n_rows_dev, w.ln2_g[L - 1], w.ln2_b[L - 1], cfg.ln_eps, w.head_w,
+      w.head_b, cfg.n_models, q_out);
+  prof::end(prof::K_ROWWISE, st, (double)n_seq * (2.0 * H + 4.0 * cfg.n_models * H));
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+}  // namespace enc
+}  // namespace chm
+
+extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
+                                          const chm_encoder_weights* w,
+                                          const chm_encoder_workspace* ws,
+                                          const int32_t* token_ids, const int32_t* rows,
+                                          const int32_t* n_rows_dev, int32_t n_seq,
+                                          int32_t seq_len, float* q_out, void* stream) {
+  if (!cfg || !w || !ws || !token_ids || !q_out) return CHM_ERR_INVALID_ARG;
+  if (n_seq < 0) return CHM_ERR_INVALID_ARG;
+  if (n_seq == 0) return CHM_OK;
+  if (seq_len != chm::enc::kAttnS || seq_len > cfg->max_pos) return CHM_ERR_UNSUPPORTED;
+  if (cfg->n_heads * 64 != cfg->hidden || cfg->n_models < 1 ||
+      cfg->n_models > CHM_MAX_MODELS || cfg->ffn % 64 != 0)
+    return CHM_ERR_INVALID_ARG;
+  if ((long long)n_seq * seq_len > ws->max_tokens) return CHM_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (cfg->hidden) {
+    case 256:
+      return chm::enc::run_rowwise<1>(*cfg, *w, *ws, token_ids, rows, n_rows_dev, n_seq,
+                                      seq_len, q_out, st);
+    case 512:
+      return chm::enc::run_rowwise<2>(*cfg, *w, *ws, token_ids, rows, n_rows_dev, n_seq,
+                                      seq_len, q_out, st);
+    case 768:
+      return chm::enc::run_rowwise<3>(*cfg, *w, *ws, token_ids, rows, n_rows_dev, n_seq,
+                                      seq_len, q_out, st);
+    case 1024:
+      return chm::enc::run_rowwise<4>(*cfg, *w, *ws, token_ids, rows, n_rows_dev, n_seq,
+                                      seq_len, q_out, st);
+    default:
+      return CHM_ERR_UNSUPPORTED;
+  }
+}

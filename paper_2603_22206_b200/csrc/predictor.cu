@@ -9,6 +9,7 @@
 // HBM bytes per row (algorithmic): quantile 8 (wf, stage) + 8K (out);
 // oracle 8 + 4*max_stages*K + 8K; input-length 4 + 8K.
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace chm {
 
@@ -100,9 +101,11 @@ extern "C" chm_status chm_predict_quantile(const double* table, int32_t n_wf, in
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(chm::predict_quantile_kernel_dyn,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  chm::prof::begin(chm::prof::K_PREDICT, s);
   chm::predict_quantile_kernel_dyn<<<chm::grid_for((long long)n_rows * n_models, 256), 256,
                                      smem, s>>>(table, n_wf, s_cap, n_models, workflow,
                                                 stage, n_rows, yhat);
+  chm::prof::end(chm::prof::K_PREDICT, s, (double)n_rows * (8.0 + 8.0 * n_models));
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }
@@ -115,10 +118,13 @@ extern "C" chm_status chm_predict_oracle(const int32_t* stage_out, const int32_t
     return CHM_ERR_INVALID_ARG;
   if (n_rows == 0) return CHM_OK;
   if (!stage_out || !n_stages || !stage || !yhat) return CHM_ERR_INVALID_ARG;
+  chm::prof::begin(chm::prof::K_PREDICT, (cudaStream_t)stream);
   chm::predict_oracle_kernel<<<chm::grid_for((long long)n_rows * n_models, 256), 256, 0,
                                (cudaStream_t)stream>>>(stage_out, n_stages, stage,
                                                        max_stages, n_models, n_rows, yhat,
                                                        error);
+  chm::prof::end(chm::prof::K_PREDICT, (cudaStream_t)stream,
+                 (double)n_rows * (8.0 + 4.0 * max_stages * n_models + 8.0 * n_models));
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }
@@ -128,9 +134,11 @@ extern "C" chm_status chm_predict_input_length(const int32_t* input_tokens, int3
   if (n_rows < 0 || n_models < 1 || n_models > CHM_MAX_MODELS) return CHM_ERR_INVALID_ARG;
   if (n_rows == 0) return CHM_OK;
   if (!input_tokens || !yhat) return CHM_ERR_INVALID_ARG;
+  chm::prof::begin(chm::prof::K_PREDICT, (cudaStream_t)stream);
   chm::predict_input_length_kernel<<<chm::grid_for((long long)n_rows * n_models, 256), 256,
                                      0, (cudaStream_t)stream>>>(input_tokens, n_models,
                                                                 n_rows, yhat);
+  chm::prof::end(chm::prof::K_PREDICT, (cudaStream_t)stream, (double)n_rows * (4.0 + 8.0 * n_models));
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }

@@ -28,6 +28,7 @@
 // next chunk of per-row inputs into a shared-memory double buffer while the
 // chain consumes the current one.
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace chm {
 
@@ -462,7 +463,11 @@ static chm_status launch_schedule(const SelectParams& prm, const chm_monitor_sta
   const size_t smem = 2 * sizeof(ChunkBuf<K>);
   cudaFuncSetAttribute(schedule_rows_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  prof::begin(prof::K_SELECT, s);
   schedule_rows_kernel<K><<<1, kThreads, smem, s>>>(prm, mon, rows, sc, scores, yhat, out);
+  // bytes per row: q 4K + yhat 8K + out_tokens 4K + program/stage/arrival 16 +
+  // scratch 16 + outputs 21 (+ loads 8K)
+  prof::end(prof::K_SELECT, s, (double)rows.n_rows * (24.0 * K + 53.0));
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }
@@ -474,8 +479,10 @@ extern "C" chm_status chm_prepare_rows(const chm_monitor_state* mon, const chm_r
                                        uint32_t* epoch_counter, void* stream) {
   if (!mon || !rows || !scratch || !epoch_counter || rows->n_rows < 0)
     return CHM_ERR_INVALID_ARG;
+  chm::prof::begin(chm::prof::K_PREPARE, (cudaStream_t)stream);
   chm::prepare_rows_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(*mon, *rows, *scratch,
                                                                   epoch_counter);
+  chm::prof::end(chm::prof::K_PREPARE, (cudaStream_t)stream, (double)rows->n_rows * 26.0);
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }

@@ -21,6 +21,7 @@
 // arrival 8, seq-implicit, handle 8, out_tokens 4, level 4, count 4, quantum 4)
 // + write 40 + order 4.
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace chm {
 
@@ -501,8 +502,10 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   if (dec) d = *dec;
   const size_t smem = sizeof(QueueSmem);
   cudaFuncSetAttribute(queue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  prof::begin(prof::K_QUEUE, s);
   queue_kernel<<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete, n_iterations, mode,
                                           err);
+  prof::end(prof::K_QUEUE, s, 0.0);
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }

@@ -1,0 +1,168 @@
+"""Semantic router encoder on the device: config, weights, workspace, router.
+
+BERT-style post-LN encoder (embedding + LN, L x [QKV -> attention -> out-proj
++ residual -> LN -> FFN(GELU) + residual -> LN]) and the paper's router head:
+q[m] = sigmoid(Linear(h_[CLS]))[m]. Weights are bf16 in
+nn.Linear layout [out, in]; LN/bias/head parameters fp32. The forward runs
+entirely in libchimera_sm100a.so (chm_encoder_forward): tcgen05 GEMMs with
+fused epilogues, tcgen05 attention, warp-per-row LayerNorm.
+
+FLOPs per routed request (S tokens):
+  L * (8*S*H^2 + 4*S^2*H + 4*S*H*F) + 2*H*K
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class EncoderConfig:
+    n_layers: int = 12
+    hidden: int = 768
+    n_heads: int = 12
+    ffn: int = 3072
+    vocab: int = 30522
+    max_pos: int = 512
+    seq_len: int = 128
+    ln_eps: float = 1e-12
+
+    def flops_per_request(self, n_models: int) -> int:
+        L, S, H, F = self.n_layers, self.seq_len, self.hidden, self.ffn
+        return L * (8 * S * H * H + 4 * S * S * H + 4 * S * H * F) + 2 * H * n_models
+
+
+BERT_BASE = EncoderConfig()
+SMALL = EncoderConfig(n_layers=4, hidden=256, n_heads=4, ffn=1024)
+
+
+def init_weights(cfg: EncoderConfig, n_models: int, seed: int = 0, head_std: float = 0.02,
+                 device="cuda") -> dict:
+    """BERT initialisation: N(0, 0.02) matrices and embeddings, zero biases,
+    LN gamma=1 beta=0; the head uses `head_std` (also report a
+    spread variant 2/sqrt(H))."""
+    g = torch.Generator().manual_seed(seed)
+    H, F, L = cfg.hidden, cfg.ffn, cfg.n_layers
+
+    def n(*shape, std=0.02):
+        return torch.randn(*shape, generator=g) * std
+
+    w = {
+        "word_emb": n(cfg.vocab, H), "pos_emb": n(cfg.max_pos, H), "type_emb": n(H),
+        "emb_ln_g": torch.ones(H), "emb_ln_b": torch.zeros(H),
+        "head_w": n(n_models, H, std=head_std), "head_b": torch.zeros(n_models),
+    }
+    for i in range(L):
+        w[f"w_qkv.{i}"] = n(3 * H, H)
+        w[f"b_qkv.{i}"] = torch.zeros(3 * H)
+        w[f"w_o.{i}"] = n(H, H)
+        w[f"b_o.{i}"] = torch.zeros(H)
+        w[f"ln1_g.{i}"] = torch.ones(H)
+        w[f"ln1_b.{i}"] = torch.zeros(H)
+        w[f"w_1.{i}"] = n(F, H)
+        w[f"b_1.{i}"] = torch.zeros(F)
+        w[f"w_2.{i}"] = n(H, F)
+        w[f"b_2.{i}"] = torch.zeros(H)
+        w[f"ln2_g.{i}"] = torch.ones(H)
+        w[f"ln2_b.{i}"] = torch.zeros(H)
+    # matrices/embeddings live in bf16 on the device; keep the bf16-rounded
+    # values as the canonical weights so the fp32 restatement sees the same ones
+    out = {}
+    for k, v in w.items():
+        if k.startswith(("w_", "word_emb", "pos_emb", "type_emb")):
+            out[k] = v.to(torch.bfloat16).to(device)
+        else:
+            out[k] = v.float().to(device)
+    return out
+
+
+def synthetic_token_ids(n: int, seq_len: int, seed: int, vocab: int = 30522) -> np.ndarray:
+    """[CLS]=101 at position 0, then U[1000, vocab)."""
+    rng = np.random.default_rng(seed)
+    ids = rng.integers(1000, vocab, size=(n, seq_len), dtype=np.int32)
+    ids[:, 0] = 101
+    return ids
+
+
+class _PtrArray:
+    def __init__(self, tensors):
+        self.tensors = tensors
+        self.arr = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+
+    @property
+    def ptr(self):
+        return ctypes.cast(self.arr, ctypes.c_void_p).value
+
+
+class GpuEncoderRouter:
+    """Router backed by the sm_100a encoder (`score_rows` is the hot path)."""
+
+    name = "encoder"
+
+    def __init__(self, cfg: EncoderConfig, n_models: int, weights: dict | None = None,
+                 max_rows: int = 4096, seed: int = 0, head_std: float = 0.02, device="cuda"):
+        self.lib = _lib.load()
+        self.cfg = cfg
+        self.K = n_models
+        self.device = torch.device(device)
+        self.weights = weights if weights is not None else init_weights(
+            cfg, n_models, seed, head_std, self.device)
+        w, L = self.weights, cfg.n_layers
+        self._arrays = {name: _PtrArray([w[f"{name}.{i}"] for i in range(L)])
+                        for name in ("w_qkv", "b_qkv", "w_o", "b_o", "ln1_g", "ln1_b", "w_1",
+                                     "b_1", "w_2", "b_2", "ln2_g", "ln2_b")}
+        A = self._arrays
+        self.w_c = _lib.EncoderWeights(
+            w["word_emb"].data_ptr(), w["pos_emb"].data_ptr(), w["type_emb"].data_ptr(),
+            w["emb_ln_g"].data_ptr(), w["emb_ln_b"].data_ptr(),
+            A["w_qkv"].ptr, A["b_qkv"].ptr, A["w_o"].ptr, A["b_o"].ptr, A["ln1_g"].ptr,
+            A["ln1_b"].ptr, A["w_1"].ptr, A["b_1"].ptr, A["w_2"].ptr, A["b_2"].ptr,
+            A["ln2_g"].ptr, A["ln2_b"].ptr, w["head_w"].data_ptr(), w["head_b"].data_ptr())
+        self.cfg_c = _lib.EncoderCfg(cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.ffn, cfg.vocab,
+                                     cfg.max_pos, n_models, cfg.ln_eps)
+        self.max_rows = max_rows
+        T = max_rows * cfg.seq_len
+        bf = torch.bfloat16
+        H, F = cfg.hidden, cfg.ffn
+        self.ws = {
+            "x": torch.empty(T, H, dtype=bf, device=self.device),
+            "qkv": torch.empty(T, 3 * H, dtype=bf, device=self.device),
+            "ctx": torch.empty(T, H, dtype=bf, device=self.device),
+            "tmp": torch.empty(T, H, dtype=bf, device=self.device),
+            "ffn": torch.empty(T, F, dtype=bf, device=self.device),
+        }
+        self.ws_c = _lib.EncoderWorkspace(T, *(self.ws[k].data_ptr()
+                                               for k in ("x", "qkv", "ctx", "tmp", "ffn")))
+
+    def forward(self, token_ids: torch.Tensor, q_out: torch.Tensor, rows=None, n_rows=None,
+                n_seq: int | None = None, stream=None) -> None:
+        """q_out[row*K + m] for the listed rows (all rows when `rows` is None)."""
+        n_seq = token_ids.shape[0] if n_seq is None else n_seq
+        if n_seq > self.max_rows:
+            raise ValueError(f"{n_seq} sequences exceed max_rows={self.max_rows}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(self.lib.chm_encoder_forward(
+            self.cfg_c, self.w_c, self.ws_c, token_ids.data_ptr(),
+            None if rows is None else rows.data_ptr(),
+            None if n_rows is None else n_rows.data_ptr(), n_seq, token_ids.shape[1],
+            q_out.data_ptr(), s.cuda_stream), "chm_encoder_forward")
+
+    # scheduler router protocol
+    def score_rows(self, batch, route_rows, n_route, scores, stream) -> None:
+        if batch.token_ids is None:
+            raise ValueError("GpuEncoderRouter needs batch.token_ids")
+        self.forward(batch.token_ids, scores, rows=route_rows, n_rows=n_route,
+                     n_seq=batch.n_rows, stream=stream)
+
+    def score(self, req, rec, pool, token_ids: np.ndarray) -> dict:
+        """Single-request compatibility path (router.py:39-42)."""
+        ids = torch.as_tensor(token_ids.reshape(1, -1).astype(np.int32), device=self.device)
+        q = torch.empty(self.K, dtype=torch.float32, device=self.device)
+        self.forward(ids, q)
+        return dict(zip(pool.model_ids, q.cpu().tolist()))

@@ -76,6 +76,48 @@ class RowBatch:
         return RowBatch(**conv)
 
 
+class HostStaging:
+    """Pinned host columns of one batch + pinned decision outputs.
+
+    `upload()` enqueues the host->device copies of the batch, `download()` the
+    device->host copies of the decisions (model, priority, flags), both
+    asynchronous on the current stream: what an end-to-end caller pays per tick.
+    """
+
+    _DT = dict(program=np.int32, stage=np.int32, arrival=np.float64, out_tokens=np.int32,
+               handle=np.int64, workflow=np.int32, input_tokens=np.int32, token_ids=np.int32,
+               n_stages=np.int32, stage_out=np.int32)
+
+    def __init__(self, cols: dict, device):
+        self.host = {k: torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=self._DT[k])))
+                     .pin_memory() for k, v in cols.items() if v is not None}
+        self.batch = RowBatch(**{k: torch.empty(v.shape, dtype=v.dtype, device=device)
+                                 for k, v in self.host.items()})
+        B = self.batch.n_rows
+        self.model = torch.empty(B, dtype=torch.int32).pin_memory()
+        self.priority = torch.empty(B, dtype=torch.float64).pin_memory()
+        self.flags = torch.empty(B, dtype=torch.uint8).pin_memory()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.host.values())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.model, self.priority, self.flags))
+
+    def upload(self) -> RowBatch:
+        for k, h in self.host.items():
+            getattr(self.batch, k).copy_(h, non_blocking=True)
+        return self.batch
+
+    def download(self, buf: "BatchBuffers") -> None:
+        B = self.batch.n_rows
+        self.model.copy_(buf.model[:B], non_blocking=True)
+        self.priority.copy_(buf.priority[:B], non_blocking=True)
+        self.flags.copy_(buf.dflags[:B], non_blocking=True)
+
+
 class BatchBuffers:
     """Per-batch scratch and outputs for up to `max_rows` rows."""
 

@@ -158,6 +158,19 @@ class DeviceState:
         self.q_quantum[b:b + n].zero_()
         self.engine_queued[model] = n
 
+    # -- snapshot / restore (device-to-device copies, graph-capturable) ------
+    _MUTABLE = ("inflight_sum", "inflight_comp", "inflight_count", "assignment", "stage_bits",
+                "engine_clock", "engine_seq", "engine_running", "engine_queued",
+                "engine_iterations", "q_priority", "q_arrival", "q_seq", "q_handle",
+                "q_out_tokens", "q_level", "q_count", "q_quantum")
+
+    def snapshot(self) -> dict:
+        return {k: getattr(self, k).clone() for k in self._MUTABLE}
+
+    def restore(self, snap: dict) -> None:
+        for k in self._MUTABLE:
+            getattr(self, k).copy_(snap[k], non_blocking=True)
+
     # -- views ---------------------------------------------------------------
     def in_flight_sums(self) -> list[float]:
         s = self.inflight_sum.cpu().tolist()

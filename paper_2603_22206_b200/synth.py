@@ -1,0 +1,205 @@
+"""Synthetic workloads for BASELINE.json's configs, seeded.
+
+Pool: model m_i has decode_ms_per_token = 5*(i+1), max_batch_size =
+max(1, 32 >> i), prefill 0.02 (extends configs/pool_two_model.json, as
+SPEC.md:134 allows). Length and success statistics interpolate linearly
+between the paper's small and large model (APPS 447/1276 -> 649/534,
+MATH 606/2587 -> 709/715; configs/synth_*.json). The predictor is
+EmpiricalQuantilePredictor(q=0.5) trained on synthesize_trace(2000, seed=1),
+which keeps predictions dyadic. A tick's batch is the first-stage requests of
+B distinct programs from synthesize_trace(B, seed=100+tick), all arriving at
+the same time; token ids are [CLS] + U[1000, 30522) (seed 1234+tick); router
+weights are BERT-initialised from torch.manual_seed(0).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .config import AgingConfig, BalancerConfig, ModelProfile, Pool
+from .encoder import BERT_BASE, SMALL, EncoderConfig, GpuEncoderRouter, synthetic_token_ids
+from .predictor import GpuQuantilePredictor
+from .scheduler import RowBatch
+from . import workload as W
+
+APPS = ((447.0, 1276.0), (649.0, 534.0))
+MATH = ((606.0, 2587.0), (709.0, 715.0))
+CODE_SUCCESS = ({"easy": 0.45, "hard": 0.08}, {"easy": 0.85, "hard": 0.55})
+MATH_SUCCESS = ({"easy": 0.55, "hard": 0.12}, {"easy": 0.9, "hard": 0.6})
+CODE_3STAGE = W.workflow("code-3stage", "planner", "coder", "qa_agent")
+
+
+@dataclass
+class WorkloadSpec:
+    name: str
+    n_models: int
+    batch: int
+    encoder: EncoderConfig
+    templates: tuple
+    stats: tuple
+    success: tuple
+    description: str
+    n_pre_queued: int = 0      # cfg4: entries pre-queued over the engines
+    n_pre_inflight: int = 0    # cfg4: pre-existing in-flight entries
+    bursts: int = 1
+
+
+SPECS = {
+    "cfg1": WorkloadSpec("cfg1", 3, 1000, SMALL, (CODE_3STAGE,), APPS, CODE_SUCCESS,
+                         "reference CPU scheduler: 3-stage code-gen workflow, 3-model "
+                         "heterogeneous cluster, 1k requests, small router"),
+    "cfg2": WorkloadSpec("cfg2", 3, 4096, BERT_BASE, W.MATH_WORKFLOWS, MATH, MATH_SUCCESS,
+                         "math-reasoning workflow, 3-model cluster, batch 4096 scheduling "
+                         "tick on 1 B200"),
+    "cfg3": WorkloadSpec("cfg3", 5, 4096, BERT_BASE, W.MATH_WORKFLOWS + W.CODE_WORKFLOWS,
+                         MATH, MATH_SUCCESS,
+                         "5-model heterogeneous cluster, BERT-base-size router, batch 4096"),
+    "cfg4": WorkloadSpec("cfg4", 8, 4096, SMALL, W.MATH_WORKFLOWS, MATH, MATH_SUCCESS,
+                         "bursty arrival trace, 64k in-flight requests, 8 engines, "
+                         "STJF+aging sort stress", n_pre_queued=65536, n_pre_inflight=65536,
+                         bursts=16),
+    "smoke": WorkloadSpec("smoke", 3, 64, SMALL, W.MATH_WORKFLOWS, MATH, MATH_SUCCESS,
+                          "smoke: 64 requests, 3 models, small router"),
+}
+
+
+def make_pool(k: int) -> Pool:
+    return Pool(tuple(ModelProfile(f"m{i}", 5.0 * (i + 1), max(1, 32 >> i), 0.02)
+                      for i in range(k)))
+
+
+def interp_stats(k: int, pair) -> dict:
+    (m0, s0), (m1, s1) = pair
+    out = {}
+    for i in range(k):
+        t = i / (k - 1) if k > 1 else 1.0
+        out[f"m{i}"] = W.LengthStats(m0 + t * (m1 - m0), s0 + t * (s1 - s0))
+    return out
+
+
+def interp_success(k: int, pair) -> dict:
+    lo, hi = pair
+    out = {}
+    for i in range(k):
+        t = i / (k - 1) if k > 1 else 1.0
+        out[f"m{i}"] = {d: lo[d] + t * (hi[d] - lo[d]) for d in lo}
+    return out
+
+
+@dataclass
+class Workload:
+    spec: WorkloadSpec
+    pool: Pool
+    balancer: BalancerConfig
+    aging: AgingConfig
+    router: GpuEncoderRouter | None
+    predictor: GpuQuantilePredictor
+    training: list
+    device: torch.device
+    n_programs: int
+    host_batches: list = field(default_factory=list)
+    dev_batches: list = field(default_factory=list)
+
+    @property
+    def batch_size(self) -> int:
+        return self.spec.batch
+
+    def host_columns(self, tick: int) -> dict:
+        """Columnar numpy inputs of tick `tick` (what a caller hands the API)."""
+        sp = self.spec
+        k = len(self.pool)
+        stats = interp_stats(k, sp.stats)
+        succ = interp_success(k, sp.success)
+        recs = W.synthesize_trace(sp.templates, stats, succ, sp.batch, 100 + tick)
+        ids = self.pool.model_ids
+        B = sp.batch
+        out_tok = np.empty((B, k), np.int32)
+        for i, rec in enumerate(recs):
+            out_tok[i] = [rec.out_tokens(1, m) for m in ids]
+        arrival = np.full(B, 1000.0 * (tick + 1))
+        if sp.bursts > 1:  # bursts of B/bursts requests, each at one timestamp
+            arrival = 1000.0 * (tick + 1) + np.repeat(np.arange(sp.bursts),
+                                                      B // sp.bursts).astype(np.float64)
+        return dict(
+            program=(np.arange(B) + (tick % 4) * B).astype(np.int32),
+            stage=np.ones(B, np.int32),
+            arrival=arrival,
+            out_tokens=out_tok,
+            handle=(np.arange(B) + tick * B).astype(np.int64),
+            workflow=self.predictor.workflow_column([r.workflow_id for r in recs]),
+            input_tokens=np.array([r.stages[0].base_input_tokens for r in recs], np.int32),
+            token_ids=synthetic_token_ids(B, sp.encoder.seq_len, 1234 + tick, sp.encoder.vocab),
+            records=recs,
+        )
+
+    def batch(self, tick: int) -> RowBatch:
+        cols = dict(self.host_columns(tick))
+        cols.pop("records")
+        return RowBatch.from_numpy(self.device, **cols)
+
+    def router_reference(self, batch: RowBatch) -> np.ndarray:
+        from oracle.encoder_ref import encoder_forward_fp32  # test infrastructure
+        r = self.router
+        return encoder_forward_fp32(r.weights, batch.token_ids, r.cfg.n_layers, r.cfg.n_heads,
+                                    r.cfg.ln_eps).cpu().numpy()
+
+
+def make_workload(name: str, device="cuda", with_router: bool = True) -> Workload:
+    sp = SPECS[name]
+    pool = make_pool(sp.n_models)
+    stats = interp_stats(sp.n_models, sp.stats)
+    succ = interp_success(sp.n_models, sp.success)
+    training = W.synthesize_trace(sp.templates, stats, succ, 2000, 1)
+    dev = torch.device(device)
+    pred = GpuQuantilePredictor(training, pool.model_ids, 0.5, device=dev,
+                                extra_workflows=[t.workflow_id for t in sp.templates])
+    router = None
+    if with_router:
+        router = GpuEncoderRouter(sp.encoder, sp.n_models, max_rows=sp.batch, seed=0,
+                                  device=dev)
+    return Workload(sp, pool, BalancerConfig(0.5, 0.1), AgingConfig(8, 4), router, pred,
+                    training, dev, n_programs=4 * sp.batch)
+
+
+def oracle_tick(wl: Workload, batch: RowBatch, q: np.ndarray, hp, n_iterations: int = 1):
+    """Replay the batch through the CPU oracle (hp = oracle.hetsched_port) with
+    the GPU's router output as the scores. Returns models / priorities."""
+    ids = wl.pool.model_ids
+    mon = hp.PortMonitor(ids)
+    engines = {m: hp.PortEngine(wl.pool[m].max_batch_size) for m in ids}
+    port_pred = hp.PortQuantilePredictor(wl.training, 0.5)
+    prog = batch.program.cpu().numpy()
+    arr = batch.arrival.cpu().numpy()
+    wf_idx = batch.workflow.cpu().numpy()
+    inv_wf = {v: k for k, v in wl.predictor.workflow_index.items()}
+    out_tok = batch.out_tokens.cpu().numpy()
+
+    class _Req:
+        __slots__ = ("program_id", "stage_index", "arrival_time", "workflow_id", "request_id")
+
+    class _Rec:
+        def __init__(self, row):
+            self.row = row
+
+        def out_tokens(self, stage, m):
+            return int(out_tok[self.row, ids.index(m)])
+
+    models = np.empty(len(prog), np.int32)
+    prios = np.empty(len(prog))
+    for i in range(len(prog)):
+        r = _Req()
+        r.program_id = f"p{int(prog[i])}"
+        r.stage_index = 1
+        r.arrival_time = float(arr[i])
+        r.workflow_id = inv_wf.get(int(wf_idx[i]), "?")
+        r.request_id = f"{r.program_id}:1"
+        d = hp.port_schedule_request(
+            r, _Rec(i), wl.pool, mon, engines,
+            lambda rq, rc, i=i: {m: float(q[i, k]) for k, m in enumerate(ids)},
+            port_pred, wl.balancer.latency_slack, wl.balancer.confidence_margin)
+        models[i] = ids.index(d.model)
+        prios[i] = d.priority
+    return {"model": models, "priority": prios, "engines": engines, "monitor": mon}

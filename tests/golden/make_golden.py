@@ -305,6 +305,9 @@ def make_errors():
     sc = build_scenario(23, 3, 20)
     sc["prog"][9] = sc["prog"][4]
     sc["stage"][9] = sc["stage"][4]
+    # the shims key scores/predictions by request_id: keep both rows consistent
+    sc["q"][9] = sc["q"][4]
+    sc["yhat"][9] = sc["yhat"][4]
     res, err = run_reference(sc)
     save_scenario("err_duplicate", sc, res, err)
     cases["err_duplicate"] = err
