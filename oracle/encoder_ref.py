@@ -7,6 +7,7 @@ promoted to fp32), the same token ids, all arithmetic in fp32:
 
   x = LN(word_emb[id] + pos_emb[pos] + type_emb)
   per layer: x = LN(x + Attn(x) W_o^T + b_o);  x = LN(x + GELU(x W_1^T + b_1) W_2^T + b_2)
+  (GELU in its tanh form, the router model's activation)
   q = sigmoid(x[CLS] head_w^T + head_b)
 
 It runs on any device (CPU for the bench's cpu_baseline leg, which times it
@@ -41,7 +42,7 @@ def encoder_forward_fp32(weights: dict, token_ids: torch.Tensor, n_layers: int, 
         ctx = (att @ v).transpose(1, 2).reshape(B, S, H)
         x = F.layer_norm(x + ctx @ w[f"w_o.{i}"].T + w[f"b_o.{i}"], (H,), w[f"ln1_g.{i}"],
                          w[f"ln1_b.{i}"], eps)
-        h = F.gelu(x @ w[f"w_1.{i}"].T + w[f"b_1.{i}"])
+        h = F.gelu(x @ w[f"w_1.{i}"].T + w[f"b_1.{i}"], approximate="tanh")
         x = F.layer_norm(x + h @ w[f"w_2.{i}"].T + w[f"b_2.{i}"], (H,), w[f"ln2_g.{i}"],
                          w[f"ln2_b.{i}"], eps)
     return torch.sigmoid(x[:, 0] @ w["head_w"].T + w["head_b"])

@@ -21,7 +21,7 @@ chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                      void* vt, int hidden, int seq_len);
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
-                    uint32_t box_rows, uint32_t box_cols);
+                    uint32_t box_rows, uint32_t box_cols, uint64_t ld);
 }
 
 namespace enc {
@@ -362,8 +362,9 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   prof::end(prof::K_ROWWISE, st, (double)T * (4.0 + 6.0 * H));
   CHM_LAUNCH_CHECK();
   CUtensorMap tm_qk, tm_vt;
-  if (!gemm::make_tmap_bf16(&tm_qk, qk, (uint64_t)T, (uint64_t)2 * H, 128, 64)) return CHM_ERR_CUDA;
-  if (!gemm::make_tmap_bf16(&tm_vt, vt, (uint64_t)n_seq * (H / 64) * 64, (uint64_t)S, 64, 64))
+  if (!gemm::make_tmap_bf16(&tm_qk, qk, (uint64_t)T, (uint64_t)2 * H, 128, 64, 0))
+    return CHM_ERR_CUDA;
+  if (!gemm::make_tmap_bf16(&tm_vt, vt, (uint64_t)n_seq * (H / 64) * 64, (uint64_t)S, 64, 64, 0))
     return CHM_ERR_CUDA;
   static bool attr = false;
   if (!attr) {

@@ -316,14 +316,16 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
             break;
           }
           cached = false;
+          // min over (L, id): strict < keeps the lowest index on ties. The
+          // running minimum stays in a register (no dynamic register indexing).
           int mf = 0;
-#pragma unroll
-          for (int k = 1; k < K; ++k)
-            if (L[k] < L[mf]) mf = k;
           double lmf = L[0];
 #pragma unroll
           for (int k = 1; k < K; ++k)
-            if (k == mf) lmf = L[k];
+            if (L[k] < lmf) {
+              lmf = L[k];
+              mf = k;
+            }
           const double limit = __dmul_rn(prm.one_plus_slack, lmf);
           uint32_t ok = 0;
 #pragma unroll
