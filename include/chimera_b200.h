@@ -262,6 +262,14 @@ chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bia
                          const void* residual, int32_t M, int32_t N, int32_t K,
                          int32_t epilogue, void* stream);
 
+/* Fused post-LN sublayer: C = LayerNorm(A . B^T + bias + residual) * gamma + beta
+ * (fp32 statistics over the full row of N = 256*g columns, g <= 4; rows are
+ * spread over a cluster of 2g CTAs that exchange partial statistics through
+ * distributed shared memory). C may alias residual (in-place update). */
+chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, const float* bias,
+                            const void* residual, const float* gamma, const float* beta,
+                            float eps, int32_t M, int32_t N, int32_t K, void* stream);
+
 /* Profiling: launch counters per kernel class (always on) and opt-in CUDA
  * event timing around every launch on its own stream. Classes: 0 GEMM,
  * 1 attention, 2 row-wise (embedding+LN, LayerNorm, head), 3 predictor,

@@ -205,6 +205,9 @@ _SIGNATURES = [
     ("chm_gemm_bf16", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
       c_void_p]),
+    ("chm_gemm_bf16_ln", c_int32,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_int32,
+      c_int32, c_int32, c_void_p]),
     ("chm_profile_enable", c_int32, [c_int32]),
     ("chm_profile_read", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]

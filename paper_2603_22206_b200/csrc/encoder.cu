@@ -18,7 +18,8 @@ namespace chm {
 
 chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                      const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
-                     void* vt, int hidden, int seq_len);
+                     void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
+                     float eps);
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, uint64_t ld);
@@ -116,45 +117,30 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(
   ln_row_store<VEC>(v, g, b, eps, lane, x + (size_t)t * H);
 }
 
-// Post-LN: x[t] = LN(tmp[t]) (tmp already holds residual + sublayer output).
-template <int VEC>
-__global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __restrict__ in,
-                                                        long long n_rows,
-                                                        const float* __restrict__ g,
-                                                        const float* __restrict__ b, float eps,
-                                                        __nv_bfloat16* __restrict__ out) {
-  constexpr int H = 32 * 8 * VEC;
-  const int lane = threadIdx.x & 31;
-  const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= n_rows) return;
-  float v[VEC * 8];
-  load_row<VEC>(in + (size_t)t * H, lane, v);
-  ln_row_store<VEC>(v, g, b, eps, lane, out + (size_t)t * H);
-}
-
 // ---------------------------------------------------------------------------
 // K3 attention, one CTA per (sequence, head), S = 128, d = 64, tcgen05:
 //   S_tile = Q K^T  (M=128, N=128, K=64)   -> TMEM cols [0,128)
 //   softmax row-per-thread straight out of TMEM (no shuffles), unnormalised
 //   P = exp(s - max) written bf16 into a K-major 128B-swizzled smem tile
-//   O = P V        (M=128, N=64,  K=128)   -> TMEM cols [128,192)
+//   O = P V        (M=128, N=64,  K=128)   -> TMEM cols [0,64) (reuses S)
 //   O / rowsum -> ctx (bf16)
 // Q is pre-scaled by 1/sqrt(d) in the QKV epilogue; V arrives transposed.
 // 5 warps: 0-3 softmax/epilogue (warp w owns TMEM lanes 32w..32w+31),
-// warp 4 issues TMA and MMA. ~81 KB smem -> two CTAs per SM overlap phases.
+// warp 4 issues TMA and MMA. P overwrites the Q|K tiles once S is computed,
+// so a CTA needs 48 KB of smem and 128 TMEM columns: four CTAs per SM keep
+// loads, MMAs and softmax of different (sequence, head) items overlapped.
 // ---------------------------------------------------------------------------
 constexpr int kAttnS = 128;
 struct AttnSmem {
-  uint8_t q[kAttnS * 64 * 2];        // 16 KB, [128 rows][64] SW128
-  uint8_t k[kAttnS * 64 * 2];        // 16 KB
+  uint8_t qk[2][kAttnS * 64 * 2];    // Q then K tiles (16 KB each, [128][64] SW128);
+                                     // afterwards P key halves [128 rows][64 keys]
   uint8_t vt[2][64 * 64 * 2];        // 2 x 8 KB, V^T [64 d][64 keys] per key half
-  uint8_t p[2][kAttnS * 64 * 2];     // 2 x 16 KB, P [128 rows][64 keys] per key half
   uint64_t bar_load, bar_s, bar_p, bar_o;
   uint32_t tmem_base;
 };
 constexpr size_t kAttnSmemBytes = sizeof(AttnSmem) + 1024;
 
-__global__ void __launch_bounds__(160, 2)
+__global__ void __launch_bounds__(160, 4)
     attention_kernel(const __grid_constant__ CUtensorMap tm_qk,
                      const __grid_constant__ CUtensorMap tm_vt, int n_heads, int hidden,
                      __nv_bfloat16* __restrict__ ctx) {
@@ -171,7 +157,7 @@ __global__ void __launch_bounds__(160, 2)
     sm100::mbar_init(&s.bar_o, 1);
     sm100::fence_barrier_init();
   }
-  if (warp == 0) sm100::tmem_alloc<256>(&s.tmem_base);
+  if (warp == 0) sm100::tmem_alloc<128>(&s.tmem_base);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -182,15 +168,15 @@ __global__ void __launch_bounds__(160, 2)
       constexpr uint32_t kBytes = 2 * kAttnS * 64 * 2 + 2 * 64 * 64 * 2;
       sm100::mbar_arrive_expect_tx(&s.bar_load, kBytes);
       const int row0 = seq * kAttnS;
-      sm100::tma_load_2d(s.q, &tm_qk, &s.bar_load, h * 64, row0);
-      sm100::tma_load_2d(s.k, &tm_qk, &s.bar_load, hidden + h * 64, row0);
+      sm100::tma_load_2d(s.qk[0], &tm_qk, &s.bar_load, h * 64, row0);
+      sm100::tma_load_2d(s.qk[1], &tm_qk, &s.bar_load, hidden + h * 64, row0);
       const int vrow = (seq * n_heads + h) * 64;
       sm100::tma_load_2d(s.vt[0], &tm_vt, &s.bar_load, 0, vrow);
       sm100::tma_load_2d(s.vt[1], &tm_vt, &s.bar_load, 64, vrow);
       sm100::mbar_wait(&s.bar_load, 0);
       sm100::tc_fence_after();
       constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
-      const uint32_t qa = sm100::smem_u32(s.q), ka = sm100::smem_u32(s.k);
+      const uint32_t qa = sm100::smem_u32(s.qk[0]), ka = sm100::smem_u32(s.qk[1]);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         sm100::mma_bf16(tmem, sm100::umma_desc_sw128(qa + k * 32),
@@ -201,42 +187,47 @@ __global__ void __launch_bounds__(160, 2)
       constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const uint32_t pa = sm100::smem_u32(s.p[kk >> 2]) + (kk & 3) * 32;
+        const uint32_t pa = sm100::smem_u32(s.qk[kk >> 2]) + (kk & 3) * 32;
         const uint32_t va = sm100::smem_u32(s.vt[kk >> 2]) + (kk & 3) * 32;
-        sm100::mma_bf16(tmem + 128, sm100::umma_desc_sw128(pa), sm100::umma_desc_sw128(va),
+        sm100::mma_bf16(tmem, sm100::umma_desc_sw128(pa), sm100::umma_desc_sw128(va),
                         idesc_o, kk);
       }
       sm100::mma_commit(&s.bar_o);
     }
     __syncwarp();
   } else {
-    // softmax: thread = query row r
+    // softmax: thread = query row r, two passes over the TMEM row (max, then
+    // exp) so only 32 scores are live in registers at a time
     const int r = warp * 32 + lane;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     sm100::mbar_wait(&s.bar_s, 0);
     sm100::tc_fence_after();
-    uint32_t raw[4][32];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) sm100::tmem_ld_32x32b_x32(tmem + lane_base + c * 32, raw[c]);
-    sm100::tmem_ld_wait();
+    constexpr float kLog2e = 1.4426950408889634f;
     float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(raw[c][j]));
-    const float mxl = mx * 1.4426950408889634f;
-    float sum = 0.f;
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < 4; ++c) {
-      // keys [32c, 32c+32) -> half c/2, 16B chunks 4*(c&1) .. +3 of the 128B row
-      uint8_t* rowp = s.p[c >> 1] + r * 128;
+      uint32_t raw[32];
+      sm100::tmem_ld_32x32b_x32(tmem + lane_base + c * 32, raw);
+      sm100::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(raw[j]));
+    }
+    const float mxl = mx * kLog2e;
+    float sum = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t raw[32];
+      sm100::tmem_ld_32x32b_x32(tmem + lane_base + c * 32, raw);
+      sm100::tmem_ld_wait();
+      // keys [32c, 32c+32) -> P half c/2, 16B chunks 4*(c&1) .. +3 of the 128B row
+      uint8_t* rowp = s.qk[c >> 1] + r * 128;
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         __align__(16) __nv_bfloat162 o[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = exp2f(fmaf(__uint_as_float(raw[c][q4 * 8 + 2 * e]), 1.4426950408889634f, -mxl));
-          const float p1 = exp2f(fmaf(__uint_as_float(raw[c][q4 * 8 + 2 * e + 1]), 1.4426950408889634f, -mxl));
+          const float p0 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
+          const float p1 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
           o[e] = __floats2bfloat162_rn(p0, p1);
           // accumulate the bf16-rounded values so the normaliser matches P
           const float2 back = __bfloat1622float2(o[e]);
@@ -247,13 +238,14 @@ __global__ void __launch_bounds__(160, 2)
             *reinterpret_cast<uint4*>(o);
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    sm100::fence_proxy_async_smem();
+    sm100::tc_fence_before();  // S reads complete before O overwrites its columns
     sm100::mbar_arrive(&s.bar_p);
     sm100::mbar_wait(&s.bar_o, 0);
     sm100::tc_fence_after();
     uint32_t ov[2][32];
-    sm100::tmem_ld_32x32b_x32(tmem + lane_base + 128, ov[0]);
-    sm100::tmem_ld_32x32b_x32(tmem + lane_base + 160, ov[1]);
+    sm100::tmem_ld_32x32b_x32(tmem + lane_base, ov[0]);
+    sm100::tmem_ld_32x32b_x32(tmem + lane_base + 32, ov[1]);
     sm100::tmem_ld_wait();
     const float inv = 1.0f / sum;
     __nv_bfloat16* dst = ctx + ((size_t)seq * kAttnS + r) * hidden + h * 64;
@@ -274,20 +266,16 @@ __global__ void __launch_bounds__(160, 2)
   __syncthreads();
   if (warp == 0) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc<256>(tmem);
+    sm100::tmem_dealloc<128>(tmem);
   }
 }
 
-// K4: the last layer's output LayerNorm, fused for the [CLS] rows only and
-// kept in fp32, then q[rows[i]*K + m] = sigmoid(head_b[m] + <LN(tmp[i*S]), head_w[m]>)
-// for i < n_live. (Only the CLS state feeds the router head, so the last
-// LayerNorm is never materialised for the other S-1 tokens.)
+// K4: q[rows[i]*K + m] = sigmoid(head_b[m] + <x[i*S], head_w[m]>) for
+// i < n_live: the router head reads only the [CLS] state of each sequence.
 template <int VEC>
-__global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restrict__ tmp, int S,
+__global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restrict__ x, int S,
                                                    int n_seq, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ n_rows_dev,
-                                                   const float* __restrict__ ln_g,
-                                                   const float* __restrict__ ln_b, float eps,
                                                    const float* __restrict__ w,
                                                    const float* __restrict__ bias, int K,
                                                    float* __restrict__ q) {
@@ -297,28 +285,7 @@ __global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restri
   const int n_live = n_rows_dev ? *n_rows_dev : n_seq;
   if (i >= n_seq || i >= n_live) return;
   float v[VEC * 8];
-  load_row<VEC>(tmp + (size_t)i * S * H, lane, v);
-  {
-    float sum = 0.f;
-#pragma unroll
-    for (int j = 0; j < VEC * 8; ++j) sum += v[j];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float mean = sum * (1.0f / H);
-    float var = 0.f;
-#pragma unroll
-    for (int j = 0; j < VEC * 8; ++j) var += (v[j] - mean) * (v[j] - mean);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
-    const float rstd = rsqrtf(var * (1.0f / H) + eps);
-#pragma unroll
-    for (int c = 0; c < VEC; ++c)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int col = (c * 32 + lane) * 8 + e;
-        v[c * 8 + e] = (v[c * 8 + e] - mean) * rstd * ln_g[col] + ln_b[col];
-      }
-  }
+  load_row<VEC>(x + (size_t)i * S * H, lane, v);
   const int row = rows ? rows[i] : i;
   for (int m = 0; m < K; ++m) {
     float acc = 0.f;
@@ -375,35 +342,29 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   const int NH = H / 64;
   chm_status rc;
   for (int l = 0; l < L; ++l) {
-    rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, vt, H, S);
+    rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, vt, H, S,
+                   nullptr, nullptr, 0.f);
     if (rc != CHM_OK) return rc;
     prof::begin(prof::K_ATTENTION, st);
     attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qk, tm_vt, NH, H,
                                                                          ctx);
     prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
     CHM_LAUNCH_CHECK();
-    rc = gemm_bf16(ctx, w.w_o[l], tmp, w.b_o[l], x, (int)T, H, H, 3, st, nullptr, 0, 0);
+    // out-projection + residual + LayerNorm fused (x updated in place)
+    rc = gemm_bf16(ctx, w.w_o[l], x, w.b_o[l], x, (int)T, H, H, 5, st, nullptr, 0, 0,
+                   w.ln1_g[l], w.ln1_b[l], cfg.ln_eps);
     if (rc != CHM_OK) return rc;
-    prof::begin(prof::K_ROWWISE, st);
-    layernorm_kernel<VEC><<<grid_t, 256, 0, st>>>(tmp, T, w.ln1_g[l], w.ln1_b[l], cfg.ln_eps, x);
-    prof::end(prof::K_ROWWISE, st, (double)T * 4.0 * H);
-    CHM_LAUNCH_CHECK();
-    rc = gemm_bf16(x, w.w_1[l], ffn, w.b_1[l], nullptr, (int)T, F, H, 2, st, nullptr, 0, 0);
+    rc = gemm_bf16(x, w.w_1[l], ffn, w.b_1[l], nullptr, (int)T, F, H, 2, st, nullptr, 0, 0,
+                   nullptr, nullptr, 0.f);
     if (rc != CHM_OK) return rc;
-    rc = gemm_bf16(ffn, w.w_2[l], tmp, w.b_2[l], x, (int)T, H, F, 3, st, nullptr, 0, 0);
+    // FFN2 + residual + LayerNorm fused (x updated in place)
+    rc = gemm_bf16(ffn, w.w_2[l], x, w.b_2[l], x, (int)T, H, F, 5, st, nullptr, 0, 0,
+                   w.ln2_g[l], w.ln2_b[l], cfg.ln_eps);
     if (rc != CHM_OK) return rc;
-    if (l + 1 < L) {
-      prof::begin(prof::K_ROWWISE, st);
-      layernorm_kernel<VEC><<<grid_t, 256, 0, st>>>(tmp, T, w.ln2_g[l], w.ln2_b[l], cfg.ln_eps,
-                                                    x);
-      prof::end(prof::K_ROWWISE, st, (double)T * 4.0 * H);
-      CHM_LAUNCH_CHECK();
-    }
   }
   prof::begin(prof::K_ROWWISE, st);
   head_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(
-      tmp, S, n_seq, rows, n_rows_dev, w.ln2_g[L - 1], w.ln2_b[L - 1], cfg.ln_eps, w.head_w,
-      w.head_b, cfg.n_models, q_out);
+      x, S, n_seq, rows, n_rows_dev, w.head_w, w.head_b, cfg.n_models, q_out);
   prof::end(prof::K_ROWWISE, st, (double)n_seq * (2.0 * H + 4.0 * cfg.n_models * H));
   CHM_LAUNCH_CHECK();
   return CHM_OK;

@@ -1,28 +1,34 @@
 // K2 -- tcgen05 / TMEM / TMA GEMM for the router encoder.
 //
-//   C[M, N] = A[M, K] . B[N, K]^T  (+ bias[N]) (GELU) (+ residual[M, N])
+//   C[M, N] = A[M, K] . B[N, K]^T  (+ bias[N]) (GELU) (+ residual[M, N]) (LayerNorm)
 //   A: activations, B: nn.Linear weight [out, in]; both K-major bf16,
 //   fp32 accumulation in tensor memory, bf16 output.
 //
-// Structure: persistent CTA PAIRS (cluster 2x1, one CTA per SM, 384 threads).
-// A cluster owns a 256 x 256 output tile; CTA r of the pair stages rows
-// [128r, 128r+128) of the A tile and rows [128r, 128r+128) of the B tile
+// Structure: persistent clusters of CTA PAIRS (one CTA per SM, 384 threads).
+// A pair owns a 256 x 256 output tile; CTA x of the pair stages rows
+// [128x, 128x+128) of the A tile and rows [128x, 128x+128) of the B tile
 // (N half), so the pair MMA (tcgen05.mma.cta_group::2, M=256 N=256 K=16)
 // reads half of each operand from each SM's shared memory.
 //   warp 0      TMA producer (both CTAs): 4-stage ring of A 128x64 + B 128x64
-//               tiles (128B swizzle); completion counted on the leader's
+//               tiles (128B swizzle); completion counted on the pair leader's
 //               mbarrier (cta_group::2 TMA)
 //   warp 1      TMEM (512 cols, cta_group::2) alloc/dealloc in both CTAs; in
 //               the leader one elected thread issues the MMAs into a
 //               double-buffered accumulator; tcgen05.commit multicasts
-//               "stage free" / "accumulator full" to both CTAs
+//               "stage free" / "accumulator full" to both CTAs of the pair
 //   warps 4-11  epilogue (both CTAs): tcgen05.ld 32 lanes x 64 columns, bias
 //               / tanh-GELU / residual / QKV split in fp32, bf16 into a
 //               128B-swizzled smem box, TMA store (bulk group); residual
-//               boxes arrive by TMA into the same staging buffers. Two
-//               buffers per warp overlap the store of one chunk with the next.
-// Tiles go row-block-major over clusters so the A block is read from HBM once
-// and the weights stay L2 resident.
+//               boxes arrive by TMA into the same staging buffers.
+//
+// EPI_RESIDUAL_LN (post-LN sublayer output, N = 256 g, g <= 4): the cluster is
+// g pairs (2g CTAs; 6 for H = 768) covering one 256 x N row block, so every
+// output row lives in g CTAs. Each epilogue thread owns (row, 128 columns): pass 1 forms
+// v = acc + bias + residual and its (mean, M2); the partials are pushed to
+// the three CTAs of the row group through distributed shared memory and an
+// mbarrier; pass 2 re-reads TMEM and writes LayerNorm(v) in bf16. The sum
+// never round-trips through HBM (no separate LayerNorm kernel, no bf16
+// rounding of the pre-LN sum), and x is updated in place.
 //
 // FLOPs per launch: 2*M*N*K.
 #include <cudaTypedefs.h>
@@ -34,7 +40,7 @@
 namespace chm {
 namespace gemm {
 
-constexpr int BM = 256, BN = 256, BK = 64;  // cluster tile
+constexpr int BM = 256, BN = 256, BK = 64;  // pair tile
 constexpr int CM = 128, CN = 128;           // per-CTA operand rows (A half, B half)
 constexpr int kStages = 4;
 constexpr int kThreads = 384;
@@ -43,6 +49,7 @@ constexpr uint32_t kTileABytes = CM * BK * 2;  // 16 KB
 constexpr uint32_t kTileBBytes = CN * BK * 2;  // 16 KB
 constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
 constexpr uint32_t kBoxBytes = 32 * 128;       // 32 rows x 64 bf16, one epilogue box
+constexpr int kMaxLnGroups = 4;                // pairs per cluster in LN mode (N <= 1024)
 
 enum Epilogue : int {
   EPI_NONE = 0,
@@ -56,22 +63,30 @@ enum Epilogue : int {
   // 32 consecutive tokens of one sequence, so each transposed store is one
   // coalesced 64-byte segment.
   EPI_QKV = 4,
+  // C = LayerNorm(A.B^T + bias + residual) * gamma + beta, N = 256 g.
+  EPI_RESIDUAL_LN = 5,
 };
 
-struct QkvParams {
-  __nv_bfloat16* vt;  // [n_seq, n_heads, 64, seq_len]
-  int hidden;         // H
-  int seq_len;        // S (multiple of 128)
+struct EpiParams {
+  __nv_bfloat16* vt;   // QKV: [n_seq, n_heads, 64, seq_len]
+  int hidden;          // QKV: H
+  int seq_len;         // QKV: S (multiple of 128)
+  const float* gamma;  // LN
+  const float* beta;   // LN
+  float eps;           // LN
 };
 
 struct __align__(1024) Smem {
   uint8_t tiles[kStages][kStageBytes];          // A (16 KB) then B (16 KB) per stage
   uint8_t stage_out[kEpiWarps][2][kBoxBytes];   // epilogue boxes (SW128)
+  float2 stats[2][kMaxLnGroups][2][CM];         // LN partials [buf][src pair][half][row]
+  float ln_vec[3][BN];                          // LN: bias, gamma, beta of this CTA's columns
   uint64_t full[kStages];
   uint64_t empty[kStages];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint64_t res_bar[kEpiWarps][2];
+  uint64_t stats_bar[2];
   uint32_t tmem_base;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;  // + alignment slack
@@ -90,22 +105,65 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ void st_cluster_f2(uint32_t addr, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(sm100::smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// v[0..63] = acc + bias + residual for this thread's row and a 64-column chunk.
+// `bias_s` points at the chunk's first column in the staged shared-memory copy.
+__device__ __forceinline__ void load_chunk_ln(const uint32_t (&r0)[32], const uint32_t (&r1)[32],
+                                              const float* bias_s, const uint8_t* rowp, int lane,
+                                              float (&v)[64]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 b0 = *reinterpret_cast<const float4*>(bias_s + j * 8);
+    const float4 b1 = *reinterpret_cast<const float4*>(bias_s + j * 8 + 4);
+    const uint4 u = *reinterpret_cast<const uint4*>(rowp + ((j ^ (lane & 7)) << 4));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float acc = __uint_as_float(j < 4 ? r0[j * 8 + e] : r1[(j - 4) * 8 + e]);
+      const float2 f = __bfloat1622float2(h[e >> 1]);
+      v[j * 8 + e] = acc + bb[e] + ((e & 1) ? f.y : f.x);
+    }
+  }
+}
+
 template <int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                 const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c,
                 const __grid_constant__ CUtensorMap tmap_r, const float* __restrict__ bias,
-                int M, int N, int K, QkvParams qkv) {
+                int M, int N, int K, EpiParams ep) {
+  constexpr bool kLN = EPI == EPI_RESIDUAL_LN;
+  const int ln_groups = kLN ? N / BN : 1;
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
-  const bool leader = rank == 0;
+  const uint32_t px = rank & 1;          // position in the pair (M half)
+  const uint32_t pair = rank >> 1;       // pair index in the cluster (LN: N tile)
+  const uint32_t leader_rank = rank & ~1u;
+  const bool leader = px == 0;
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pair));
   const int cluster = (int)sm100::cluster_id_x();
   const int n_cl = (int)sm100::n_clusters_x();
-  const int n_tiles_n = (N + BN - 1) / BN;
+  // LN: a cluster tile is one 256-row block (all three N tiles); otherwise a
+  // pair tile (256 x 256), row-block major.
+  const int n_tiles_n = kLN ? 1 : (N + BN - 1) / BN;
   const int n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
   const int k_blocks = K / BK;
 
@@ -113,7 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     sm100::tma_prefetch(&tmap_a);
     sm100::tma_prefetch(&tmap_b);
     sm100::tma_prefetch(&tmap_c);
-    if (EPI == EPI_BIAS_RESIDUAL) sm100::tma_prefetch(&tmap_r);
+    if (EPI == EPI_BIAS_RESIDUAL || kLN) sm100::tma_prefetch(&tmap_r);
     for (int i = 0; i < kStages; ++i) {
       sm100::mbar_init(&s.full[i], 1);
       sm100::mbar_init(&s.empty[i], 1);
@@ -121,6 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&s.tmem_full[i], 1);
       sm100::mbar_init(&s.tmem_empty[i], 2 * kEpiWarps);  // epilogues of both CTAs
+      sm100::mbar_init(&s.stats_bar[i], ln_groups * kEpiWarps * 32);
     }
     for (int w = 0; w < kEpiWarps; ++w)
       for (int b = 0; b < 2; ++b) sm100::mbar_init(&s.res_bar[w][b], 1);
@@ -138,11 +197,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster; t < n_tiles; t += n_cl) {
-        const int m0 = (t / n_tiles_n) * BM + (int)rank * CM;
-        const int n0 = (t % n_tiles_n) * BN + (int)rank * CN;
+        const int m0 = (t / n_tiles_n) * BM + (int)px * CM;
+        const int n0 = (kLN ? (int)pair : (t % n_tiles_n)) * BN + (int)px * CN;
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
-          const uint32_t full_leader = sm100::mapa(sm100::smem_u32(&s.full[stage]), 0);
+          const uint32_t full_leader =
+              sm100::mapa(sm100::smem_u32(&s.full[stage]), leader_rank);
           if (leader) sm100::mbar_arrive_expect_tx(&s.full[stage], 2 * kStageBytes);
           uint8_t* base = s.tiles[stage];
           sm100::tma_load_2d_cg2(base, &tmap_a, full_leader, kb * BK, m0);
@@ -152,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (leader CTA) ----------------
+    // ---------------- MMA issuer (pair leader) ----------------
     if (leader) {
       constexpr uint32_t idesc = sm100::umma_idesc_bf16(BM, BN);
       int stage = 0;
@@ -175,8 +235,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint64_t bd = sm100::umma_desc_sw128(b_addr + k * 32);
               sm100::mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
             }
-            sm100::mma_commit_cg2_mc(&s.empty[stage], 0x3);
-            if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc(&s.tmem_full[acc], 0x3);
+            sm100::mma_commit_cg2_mc(&s.empty[stage], pair_mask);
+            if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc(&s.tmem_full[acc], pair_mask);
           }
           __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -189,107 +249,230 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int ew = warp - 4;       // 0..7
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int half = ew >> 2;      // which 128 of the 256 columns
-    const uint32_t empty_leader0 = sm100::mapa(sm100::smem_u32(&s.tmem_empty[0]), 0);
-    const uint32_t empty_leader1 = sm100::mapa(sm100::smem_u32(&s.tmem_empty[1]), 0);
+    const uint32_t empty_leader0 = sm100::mapa(sm100::smem_u32(&s.tmem_empty[0]), leader_rank);
+    const uint32_t empty_leader1 = sm100::mapa(sm100::smem_u32(&s.tmem_empty[1]), leader_rank);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t res_phase = 0;  // bit b = phase of res_bar[ew][b]
     int box = 0;             // alternates the two staging boxes
-    for (int t = cluster; t < n_tiles; t += n_cl) {
-      const int mrow0 = (t / n_tiles_n) * BM + (int)rank * CM + quarter * 32;
-      const int n_tile0 = (t % n_tiles_n) * BN + half * 128;
-      sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
-      sm100::tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        const int col0 = n_tile0 + c * 64;
-        uint8_t* sb = s.stage_out[ew][box];
-        // the box is free once the TMA store issued from it two chunks ago has
-        // finished reading shared memory
-        if (lane == 0) sm100::bulk_wait_read<1>();
-        __syncwarp();
-        if (EPI == EPI_BIAS_RESIDUAL && lane == 0 && col0 < N) {
-          sm100::mbar_arrive_expect_tx(&s.res_bar[ew][box], kBoxBytes);
-          sm100::tma_load_2d(sb, &tmap_r, &s.res_bar[ew][box], col0, mrow0);
-        }
-        uint32_t r0[32], r1[32];
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * 128 + c * 64;
-        sm100::tmem_ld_32x32b_x32(taddr, r0);
-        sm100::tmem_ld_32x32b_x32(taddr + 32, r1);
-        sm100::tmem_ld_wait();
-        if (c == 1) {
-          // accumulator fully read: hand it back to the leader's MMA warp
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive_cluster(acc ? empty_leader1 : empty_leader0);
-        }
-        if (col0 >= N) continue;
-        if (EPI == EPI_BIAS_RESIDUAL) {
-          sm100::mbar_wait(&s.res_bar[ew][box], (res_phase >> box) & 1);
-          res_phase ^= 1u << box;
-        }
-        const int row = mrow0 + lane;
-        if (EPI == EPI_QKV && col0 >= 2 * qkv.hidden) {
-          // V: transposed direct stores, one coalesced 64 B segment per column
-          if (row < M) {
-            const int hn = col0 - 2 * qkv.hidden, h = hn >> 6;
-            const int seq = row / qkv.seq_len, sp = row - seq * qkv.seq_len;
-            __nv_bfloat16* vp =
-                qkv.vt + ((size_t)(seq * (qkv.hidden >> 6) + h) * 64) * qkv.seq_len + sp;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              vp[(size_t)j * qkv.seq_len] =
-                  __float2bfloat16_rn(__uint_as_float(r0[j]) + __ldg(bias + col0 + j));
-              vp[(size_t)(j + 32) * qkv.seq_len] =
-                  __float2bfloat16_rn(__uint_as_float(r1[j]) + __ldg(bias + col0 + 32 + j));
-            }
-          }
-          continue;
-        }
-        const float qscale = (EPI == EPI_QKV && col0 < qkv.hidden) ? 0.125f : 1.0f;
-        uint8_t* rowp = sb + lane * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float v[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            v[e] = __uint_as_float(j < 4 ? r0[j * 8 + e] : r1[(j - 4) * 8 + e]);
-          if (EPI != EPI_NONE) {
-            const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + col0 + j * 8));
-            const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + col0 + j * 8 + 4));
-            v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
-            v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
-          }
-          uint4* slot = reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4));
-          if (EPI == EPI_BIAS_RESIDUAL) {
-            const uint4 u = *slot;
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h[e]);
-              v[2 * e] += f.x;
-              v[2 * e + 1] += f.y;
-            }
-          }
-          if (EPI == EPI_BIAS_GELU) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = gelu_tanh(v[e]);
-          }
-          uint4 o;
-          o.x = pack_bf16(v[0] * qscale, v[1] * qscale);
-          o.y = pack_bf16(v[2] * qscale, v[3] * qscale);
-          o.z = pack_bf16(v[4] * qscale, v[5] * qscale);
-          o.w = pack_bf16(v[6] * qscale, v[7] * qscale);
-          *slot = o;
-        }
-        sm100::fence_proxy_async_smem();
-        __syncwarp();
+    int it = 0;              // tiles processed by this CTA (LN stats buffer parity)
+    if constexpr (kLN) {
+      // this CTA's 256 columns are fixed for the whole launch: stage the
+      // per-column vectors once (epilogue warps only: named barrier 1)
+      const int et = threadIdx.x - 4 * 32;
+      const int nb = (int)pair * BN;
+      s.ln_vec[0][et] = bias[nb + et];
+      s.ln_vec[1][et] = ep.gamma[nb + et];
+      s.ln_vec[2][et] = ep.beta[nb + et];
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    }
+    for (int t = cluster; t < n_tiles; t += n_cl, ++it) {
+      const int mrow0 = (t / n_tiles_n) * BM + (int)px * CM + quarter * 32;
+      const int n_tile0 = (kLN ? (int)pair : (t % n_tiles_n)) * BN + half * 128;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN +
+                                 half * 128;
+      if constexpr (kLN) {
+        // ---- residual + LayerNorm epilogue ----
         if (lane == 0) {
-          sm100::tma_store_2d(&tmap_c, sb, col0, mrow0);
-          sm100::bulk_commit();
+          sm100::bulk_wait_read<0>();
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            sm100::mbar_arrive_expect_tx(&s.res_bar[ew][c], kBoxBytes);
+            sm100::tma_load_2d(s.stage_out[ew][c], &tmap_r, &s.res_bar[ew][c], n_tile0 + c * 64,
+                               mrow0);
+          }
         }
-        box ^= 1;
+        __syncwarp();
+        sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
+        sm100::tc_fence_after();
+        // pass 1: per-thread (mean, M2) over its 128 columns
+        float mean = 0.f, m2 = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r0[32], r1[32];
+          sm100::tmem_ld_32x32b_x32(lane_base + c * 64, r0);
+          sm100::tmem_ld_32x32b_x32(lane_base + c * 64 + 32, r1);
+          sm100::tmem_ld_wait();
+          sm100::mbar_wait(&s.res_bar[ew][c], (res_phase >> c) & 1);
+          float v[64];
+          load_chunk_ln(r0, r1, &s.ln_vec[0][half * 128 + c * 64], s.stage_out[ew][c] + lane * 128,
+                        lane, v);
+          float cs = 0.f;
+#pragma unroll
+          for (int j = 0; j < 64; ++j) cs += v[j];
+          const float cm = cs * (1.0f / 64.0f);
+          float cm2 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 64; ++j) cm2 = fmaf(v[j] - cm, v[j] - cm, cm2);
+          if (c == 0) {
+            mean = cm;
+            m2 = cm2;
+          } else {  // Chan merge of two equal-size groups
+            const float d = cm - mean;
+            mean = 0.5f * (mean + cm);
+            m2 = m2 + cm2 + d * d * 32.0f;
+          }
+        }
+        res_phase ^= 3u;
+        // push (mean, M2) to the CTAs holding this row (same pair position)
+        const int buf = it & 1;
+        const int row_local = quarter * 32 + lane;
+        for (int g = 0; g < ln_groups; ++g) {
+          const uint32_t dst_rank = px + 2 * g;
+          st_cluster_f2(sm100::mapa(sm100::smem_u32(&s.stats[buf][pair][half][row_local]),
+                                    dst_rank),
+                        make_float2(mean, m2));
+          sm100::mbar_arrive_cluster(sm100::mapa(sm100::smem_u32(&s.stats_bar[buf]), dst_rank));
+        }
+        mbar_wait_cluster(&s.stats_bar[buf], (it >> 1) & 1);
+        float gm = 0.f;
+        for (int g = 0; g < ln_groups; ++g)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) gm += s.stats[buf][g][hh][row_local].x;
+        gm *= 1.0f / (2 * ln_groups);
+        float gm2 = 0.f;
+        for (int g = 0; g < ln_groups; ++g)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float2 p = s.stats[buf][g][hh][row_local];
+            gm2 += p.y + 128.0f * (p.x - gm) * (p.x - gm);
+          }
+        const float rstd = rsqrtf(gm2 / (float)(2 * ln_groups * 128) + ep.eps);
+        // pass 2: normalise, write bf16 in place of the residual box, TMA store
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t r0[32], r1[32];
+          sm100::tmem_ld_32x32b_x32(lane_base + c * 64, r0);
+          sm100::tmem_ld_32x32b_x32(lane_base + c * 64 + 32, r1);
+          sm100::tmem_ld_wait();
+          if (c == 1) {
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive_cluster(acc ? empty_leader1 : empty_leader0);
+          }
+          const int col0 = n_tile0 + c * 64;
+          uint8_t* rowp = s.stage_out[ew][c] + lane * 128;
+          float v[64];
+          const int lc = half * 128 + c * 64;
+          load_chunk_ln(r0, r1, &s.ln_vec[0][lc], rowp, lane, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 g0 = *reinterpret_cast<const float4*>(&s.ln_vec[1][lc + j * 8]);
+            const float4 g1 = *reinterpret_cast<const float4*>(&s.ln_vec[1][lc + j * 8 + 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&s.ln_vec[2][lc + j * 8]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&s.ln_vec[2][lc + j * 8 + 4]);
+            const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            float o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = (v[j * 8 + e] - gm) * rstd * gg[e] + bb[e];
+            uint4 u;
+            u.x = pack_bf16(o[0], o[1]);
+            u.y = pack_bf16(o[2], o[3]);
+            u.z = pack_bf16(o[4], o[5]);
+            u.w = pack_bf16(o[6], o[7]);
+            *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = u;
+          }
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tmap_c, s.stage_out[ew][c], col0, mrow0);
+            sm100::bulk_commit();
+          }
+        }
+      } else {
+        // ---- pointwise epilogues ----
+        sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
+        sm100::tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          const int col0 = n_tile0 + c * 64;
+          uint8_t* sb = s.stage_out[ew][box];
+          // the box is free once the TMA store issued from it two chunks ago
+          // has finished reading shared memory
+          if (lane == 0) sm100::bulk_wait_read<1>();
+          __syncwarp();
+          if (EPI == EPI_BIAS_RESIDUAL && lane == 0 && col0 < N) {
+            sm100::mbar_arrive_expect_tx(&s.res_bar[ew][box], kBoxBytes);
+            sm100::tma_load_2d(sb, &tmap_r, &s.res_bar[ew][box], col0, mrow0);
+          }
+          uint32_t r0[32], r1[32];
+          sm100::tmem_ld_32x32b_x32(lane_base + c * 64, r0);
+          sm100::tmem_ld_32x32b_x32(lane_base + c * 64 + 32, r1);
+          sm100::tmem_ld_wait();
+          if (c == 1) {
+            // accumulator fully read: hand it back to the leader's MMA warp
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive_cluster(acc ? empty_leader1 : empty_leader0);
+          }
+          if (col0 >= N) continue;
+          if (EPI == EPI_BIAS_RESIDUAL) {
+            sm100::mbar_wait(&s.res_bar[ew][box], (res_phase >> box) & 1);
+            res_phase ^= 1u << box;
+          }
+          const int row = mrow0 + lane;
+          if (EPI == EPI_QKV && col0 >= 2 * ep.hidden) {
+            // V: transposed direct stores, one coalesced 64 B segment per column
+            if (row < M) {
+              const int hn = col0 - 2 * ep.hidden, h = hn >> 6;
+              const int seq = row / ep.seq_len, sp = row - seq * ep.seq_len;
+              __nv_bfloat16* vp =
+                  ep.vt + ((size_t)(seq * (ep.hidden >> 6) + h) * 64) * ep.seq_len + sp;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                vp[(size_t)j * ep.seq_len] =
+                    __float2bfloat16_rn(__uint_as_float(r0[j]) + __ldg(bias + col0 + j));
+                vp[(size_t)(j + 32) * ep.seq_len] =
+                    __float2bfloat16_rn(__uint_as_float(r1[j]) + __ldg(bias + col0 + 32 + j));
+              }
+            }
+            continue;
+          }
+          const float qscale = (EPI == EPI_QKV && col0 < ep.hidden) ? 0.125f : 1.0f;
+          uint8_t* rowp = sb + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[e] = __uint_as_float(j < 4 ? r0[j * 8 + e] : r1[(j - 4) * 8 + e]);
+            if (EPI != EPI_NONE) {
+              const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + col0 + j * 8));
+              const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + col0 + j * 8 + 4));
+              v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
+              v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+            }
+            uint4* slot = reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4));
+            if (EPI == EPI_BIAS_RESIDUAL) {
+              const uint4 u = *slot;
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                v[2 * e] += f.x;
+                v[2 * e + 1] += f.y;
+              }
+            }
+            if (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = gelu_tanh(v[e]);
+            }
+            uint4 o;
+            o.x = pack_bf16(v[0] * qscale, v[1] * qscale);
+            o.y = pack_bf16(v[2] * qscale, v[3] * qscale);
+            o.z = pack_bf16(v[4] * qscale, v[5] * qscale);
+            o.w = pack_bf16(v[6] * qscale, v[7] * qscale);
+            *slot = o;
+          }
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_2d(&tmap_c, sb, col0, mrow0);
+            sm100::bulk_commit();
+          }
+          box ^= 1;
+        }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -347,14 +530,14 @@ static int num_sms() {
 
 template <int EPI>
 static chm_status launch(const void* A, const void* B, void* C, const float* bias,
-                         const void* residual, int M, int N, int K, QkvParams qkv,
+                         const void* residual, int M, int N, int K, EpiParams ep,
                          cudaStream_t s) {
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_bf16(&ta, A, (uint64_t)M, (uint64_t)K, CM, BK, 0)) return CHM_ERR_CUDA;
   if (!make_tmap_bf16(&tb, B, (uint64_t)N, (uint64_t)K, CN, BK, 0)) return CHM_ERR_CUDA;
-  const uint64_t c_cols = (EPI == EPI_QKV) ? (uint64_t)2 * qkv.hidden : (uint64_t)N;
+  const uint64_t c_cols = (EPI == EPI_QKV) ? (uint64_t)2 * ep.hidden : (uint64_t)N;
   if (!make_tmap_bf16(&tc, C, (uint64_t)M, c_cols, 32, 64, 0)) return CHM_ERR_CUDA;
-  if (EPI == EPI_BIAS_RESIDUAL) {
+  if (EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESIDUAL_LN) {
     if (!make_tmap_bf16(&tr, residual, (uint64_t)M, (uint64_t)N, 32, 64, 0)) return CHM_ERR_CUDA;
   } else {
     tr = tc;
@@ -365,41 +548,75 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
                          (int)kSmemBytes);
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int cluster = (EPI == EPI_RESIDUAL_LN) ? 2 * (N / BN) : 2;
+  const int tiles = (EPI == EPI_RESIDUAL_LN) ? (M + BM - 1) / BM
+                                             : ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // Persistent grid: only as many clusters as can be co-resident (clusters
+  // must fit inside a GPC, so e.g. 6-CTA clusters cannot use every SM); a
+  // second partial wave would double the kernel time.
+  static int max_active[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (!max_active[cluster - 1]) {
+    cfg.gridDim = dim3(cluster * (num_sms() / cluster), 1, 1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI>, &cfg) != cudaSuccess || n < 1)
+      n = num_sms() / cluster;
+    max_active[cluster - 1] = n;
+  }
+  const int max_clusters = max_active[cluster - 1];
+  const int n_clusters = tiles < max_clusters ? tiles : max_clusters;
+  cfg.gridDim = dim3(cluster * n_clusters, 1, 1);
   prof::begin(prof::K_GEMM, s);
-  gemm_kernel<EPI><<<grid, kThreads, kSmemBytes, s>>>(ta, tb, tc, tr, bias, M, N, K, qkv);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<EPI>, ta, tb, tc, tr, bias, M, N, K, ep);
   prof::end(prof::K_GEMM, s, 2.0 * M * N * K);
+  if (e != cudaSuccess) return CHM_ERR_CUDA;
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }
 
 }  // namespace gemm
 
-// Internal entry (also used by the encoder): epilogue 4 = QKV split with V^T.
+// Internal entry (also used by the encoder). Epilogue 4 = QKV split with V^T
+// (vt/hidden/seq_len), 5 = residual + LayerNorm (gamma/beta/eps, N = 256 g, g <= 4).
 chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                      const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
-                     void* vt, int hidden, int seq_len) {
+                     void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
+                     float eps) {
   if (M <= 0 || N <= 0 || K <= 0) return M == 0 ? CHM_OK : CHM_ERR_INVALID_ARG;
   if (K % gemm::BK != 0 || N % 64 != 0) return CHM_ERR_INVALID_ARG;
   if (epilogue != gemm::EPI_NONE && !bias) return CHM_ERR_INVALID_ARG;
-  if (epilogue == gemm::EPI_BIAS_RESIDUAL && !residual) return CHM_ERR_INVALID_ARG;
-  gemm::QkvParams qkv{reinterpret_cast<__nv_bfloat16*>(vt), hidden, seq_len};
+  if ((epilogue == gemm::EPI_BIAS_RESIDUAL || epilogue == gemm::EPI_RESIDUAL_LN) && !residual)
+    return CHM_ERR_INVALID_ARG;
+  gemm::EpiParams ep{reinterpret_cast<__nv_bfloat16*>(vt), hidden, seq_len, gamma, beta, eps};
   if (epilogue == gemm::EPI_QKV &&
       (!vt || hidden % 64 != 0 || N != 3 * hidden || seq_len % 128 != 0 || M % seq_len != 0))
     return CHM_ERR_INVALID_ARG;
+  if (epilogue == gemm::EPI_RESIDUAL_LN &&
+      (N % gemm::BN != 0 || N / gemm::BN > gemm::kMaxLnGroups || !gamma || !beta))
+    return CHM_ERR_UNSUPPORTED;
   switch (epilogue) {
     case gemm::EPI_NONE:
-      return gemm::launch<gemm::EPI_NONE>(A, B, C, bias, residual, M, N, K, qkv, s);
+      return gemm::launch<gemm::EPI_NONE>(A, B, C, bias, residual, M, N, K, ep, s);
     case gemm::EPI_BIAS:
-      return gemm::launch<gemm::EPI_BIAS>(A, B, C, bias, residual, M, N, K, qkv, s);
+      return gemm::launch<gemm::EPI_BIAS>(A, B, C, bias, residual, M, N, K, ep, s);
     case gemm::EPI_BIAS_GELU:
-      return gemm::launch<gemm::EPI_BIAS_GELU>(A, B, C, bias, residual, M, N, K, qkv, s);
+      return gemm::launch<gemm::EPI_BIAS_GELU>(A, B, C, bias, residual, M, N, K, ep, s);
     case gemm::EPI_BIAS_RESIDUAL:
-      return gemm::launch<gemm::EPI_BIAS_RESIDUAL>(A, B, C, bias, residual, M, N, K, qkv, s);
+      return gemm::launch<gemm::EPI_BIAS_RESIDUAL>(A, B, C, bias, residual, M, N, K, ep, s);
     case gemm::EPI_QKV:
-      return gemm::launch<gemm::EPI_QKV>(A, B, C, bias, residual, M, N, K, qkv, s);
+      return gemm::launch<gemm::EPI_QKV>(A, B, C, bias, residual, M, N, K, ep, s);
+    case gemm::EPI_RESIDUAL_LN:
+      return gemm::launch<gemm::EPI_RESIDUAL_LN>(A, B, C, bias, residual, M, N, K, ep, s);
     default: return CHM_ERR_INVALID_ARG;
   }
 }
@@ -409,7 +626,16 @@ chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
 extern "C" chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                                     const void* residual, int32_t M, int32_t N, int32_t K,
                                     int32_t epilogue, void* stream) {
-  if (epilogue == chm::gemm::EPI_QKV) return CHM_ERR_INVALID_ARG;
+  if (epilogue == chm::gemm::EPI_QKV || epilogue == chm::gemm::EPI_RESIDUAL_LN)
+    return CHM_ERR_INVALID_ARG;
   return chm::gemm_bf16(A, B, C, bias, residual, M, N, K, epilogue, (cudaStream_t)stream,
-                        nullptr, 0, 0);
+                        nullptr, 0, 0, nullptr, nullptr, 0.f);
+}
+
+extern "C" chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, const float* bias,
+                                       const void* residual, const float* gamma,
+                                       const float* beta, float eps, int32_t M, int32_t N,
+                                       int32_t K, void* stream) {
+  return chm::gemm_bf16(A, B, C, bias, residual, M, N, K, chm::gemm::EPI_RESIDUAL_LN,
+                        (cudaStream_t)stream, nullptr, 0, 0, gamma, beta, eps);
 }

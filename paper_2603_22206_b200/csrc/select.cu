@@ -251,29 +251,37 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   if (tid == 0) s_committed = B;
   __syncthreads();
 
-  // Chain state (lane 0 of warp 0 only): the selection-critical triples in
-  // registers, the bookkeeping counters in shared memory.
-  double f[K], c[K], L[K];
-  __shared__ double clk[K];
-  __shared__ long long seq[K], cnt[K], iters[K];
-  __shared__ int run[K], que[K];
+  // Chain state (lane 0 of warp 0 only). The loads L[K] feed the next row's
+  // argmin, so they live in registers; everything else is indexed by the
+  // chosen model directly in shared memory (one LDS/STS each, no K-way
+  // predicated updates on the critical path).
+  double L[K];
+  __shared__ double s_f[K], s_c[K], s_clk[K], s_d[K], s_b[K], s_invb[K];
+  __shared__ long long s_seq[K], s_cnt[K], s_it[K];
+  __shared__ int s_run[K], s_que[K], s_bmax[K], s_pow2[K];
   bool stop = false;
   if (tid == 0) {
 #pragma unroll
     for (int m = 0; m < K; ++m) {
-      f[m] = mon.inflight_sum[m];
-      c[m] = mon.inflight_comp[m];
+      const double f = mon.inflight_sum[m], c = mon.inflight_comp[m];
       const bool pw = (prm.b_pow2_mask >> m) & 1u;
-      L[m] = load_of(neumaier_value(f[m], c[m]), prm.d[m], prm.b[m], prm.inv_b[m], pw);
-      clk[m] = mon.engine_clock[m];
-      seq[m] = mon.engine_seq[m];
-      cnt[m] = mon.inflight_count[m];
-      iters[m] = mon.engine_iterations[m];
-      run[m] = mon.engine_running[m];
-      que[m] = mon.engine_queued[m];
+      L[m] = load_of(neumaier_value(f, c), prm.d[m], prm.b[m], prm.inv_b[m], pw);
+      s_f[m] = f;
+      s_c[m] = c;
+      s_d[m] = prm.d[m];
+      s_b[m] = prm.b[m];
+      s_invb[m] = prm.inv_b[m];
+      s_pow2[m] = pw;
+      s_bmax[m] = prm.b_int[m];
+      s_clk[m] = mon.engine_clock[m];
+      s_seq[m] = mon.engine_seq[m];
+      s_cnt[m] = mon.inflight_count[m];
+      s_it[m] = mon.engine_iterations[m];
+      s_run[m] = mon.engine_running[m];
+      s_que[m] = mon.engine_queued[m];
       // Work conservation: free slots imply an empty queue (engine.py:328-338).
-      if (run[m] < prm.b_int[m] && que[m] > 0 && !stop) {
-        report_error(out.error, CHM_ERR_INVALID_STATE, 0, m, que[m]);
+      if (s_run[m] < prm.b_int[m] && s_que[m] > 0 && !stop) {
+        report_error(out.error, CHM_ERR_INVALID_STATE, 0, m, s_que[m]);
         s_committed = 0;
         stop = true;
       }
@@ -367,30 +375,24 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
         }
         if (!err) {
           partial = 2;
+          double fs = s_f[m], cs = s_c[m];
+          neumaier_add(fs, cs, y);
+          s_f[m] = fs;
+          s_c[m] = cs;
+          const double lm = load_of(neumaier_value(fs, cs), s_d[m], s_b[m], s_invb[m],
+                                    s_pow2[m] != 0);
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (k == m) {
-              neumaier_add(f[k], c[k], y);
-              const bool pw = (prm.b_pow2_mask >> k) & 1u;
-              L[k] = load_of(neumaier_value(f[k], c[k]), prm.d[k], prm.b[k], prm.inv_b[k], pw);
-              cnt[k] += 1;
-            }
-          }
+          for (int k = 0; k < K; ++k) L[k] = (k == m) ? lm : L[k];
+          s_cnt[m] += 1;
           // EngineSim.enqueue: _advance_clock (engine.py:140-143), then
           // _make_entry validates out_tokens (engine.py:285-286).
           const double arr = cur->arrival[j];
-          double ck = clk[0];
-#pragma unroll
-          for (int k = 1; k < K; ++k)
-            if (k == m) ck = clk[k];
+          const double ck = s_clk[m];
           if (arr < __dsub_rn(ck, 1e-9)) {
             err = CHM_ERR_TIME_BACKWARDS;
           } else {
             partial = 3;
-            const double nck = arr > ck ? arr : ck;
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-              if (k == m) clk[k] = nck;
+            s_clk[m] = arr > ck ? arr : ck;
             if (cur->out_tokens[j * K + m] < 0) {
               err = CHM_ERR_VALIDATION;
               err_aux = 2;
@@ -407,22 +409,18 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
           stop = true;
           break;
         }
-        long long sq = 0;
+        const long long sq = s_seq[m];
+        s_seq[m] = sq + 1;
         uint8_t dfl = cached ? DF_CACHED : 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if (k == m) {
-            sq = seq[k]++;
-            if (run[k] < prm.b_int[k]) {
-              // enqueue -> _iterate admits the only queued entry (engine.py:157-158)
-              run[k] += 1;
-              iters[k] += 1;
-              dfl |= DF_ADMITTED;
-            } else {
-              que[k] += 1;
-              dfl |= DF_QUEUED;
-            }
-          }
+        const int rn = s_run[m];
+        if (rn < s_bmax[m]) {
+          // enqueue -> _iterate admits the only queued entry (engine.py:157-158)
+          s_run[m] = rn + 1;
+          s_it[m] += 1;
+          dfl |= DF_ADMITTED;
+        } else {
+          s_que[m] += 1;
+          dfl |= DF_QUEUED;
         }
         out.model[i] = m;
         out.priority[i] = y;
@@ -436,14 +434,14 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   if (tid == 0) {
 #pragma unroll
     for (int m = 0; m < K; ++m) {
-      mon.inflight_sum[m] = f[m];
-      mon.inflight_comp[m] = c[m];
-      mon.engine_clock[m] = clk[m];
-      mon.engine_seq[m] = seq[m];
-      mon.inflight_count[m] = cnt[m];
-      mon.engine_iterations[m] = iters[m];
-      mon.engine_running[m] = run[m];
-      mon.engine_queued[m] = que[m];
+      mon.inflight_sum[m] = s_f[m];
+      mon.inflight_comp[m] = s_c[m];
+      mon.engine_clock[m] = s_clk[m];
+      mon.engine_seq[m] = s_seq[m];
+      mon.inflight_count[m] = s_cnt[m];
+      mon.engine_iterations[m] = s_it[m];
+      mon.engine_running[m] = s_run[m];
+      mon.engine_queued[m] = s_que[m];
     }
     *out.n_committed = s_committed;
   }

@@ -53,6 +53,29 @@ def test_gemm(M, N, K, epilogue):
     torch.testing.assert_close(C.float(), ref, rtol=GEMM_RTOL, atol=GEMM_ATOL)
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (1000, 768, 768), (4096, 768, 3072),
+                                   (777, 512, 128), (2048, 1024, 256)])
+@pytest.mark.parametrize("in_place", [False, True])
+def test_gemm_residual_layernorm(M, N, K, in_place):
+    """C = LN(A.B^T + bias + residual): fp32 statistics over the full row,
+    rows spread over a 2N/256-CTA cluster (DSMEM exchange)."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    bias = 0.1 * torch.randn(N, device="cuda", generator=g)
+    res = (torch.randn(M, N, device="cuda", generator=g) + 0.5).to(torch.bfloat16)
+    gamma = 1 + 0.1 * torch.randn(N, device="cuda", generator=g)
+    beta = 0.1 * torch.randn(N, device="cuda", generator=g)
+    ref = F.layer_norm(A.float() @ B.float().T + bias + res.float(), (N,), gamma, beta, 1e-12)
+    C = res if in_place else torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.load().chm_gemm_bf16_ln(
+        A.data_ptr(), B.data_ptr(), C.data_ptr(), bias.data_ptr(), res.data_ptr(),
+        gamma.data_ptr(), beta.data_ptr(), 1e-12, M, N, K,
+        torch.cuda.current_stream().cuda_stream), "gemm_ln")
+    torch.cuda.synchronize()
+    torch.testing.assert_close(C.float(), ref, rtol=GEMM_RTOL, atol=GEMM_ATOL)
+
+
 def _ref_q(router, ids):
     from oracle.encoder_ref import encoder_forward_fp32
     return encoder_forward_fp32(router.weights, ids, router.cfg.n_layers, router.cfg.n_heads,
