@@ -389,7 +389,8 @@ def run_ours(args):
                 "launches_timed": g["timed"],
                 "share_of_step": (g["ms"] / args.steps) / statistics.mean(tick_ms)}
     stage_ms = {k: v["ms"] / args.steps for k, v in prof.items() if v["timed"]}
-    router_flops = B * wl.spec.encoder.flops_per_request(K)
+    # executed (trimmed) FLOPs: the last layer is computed for the CLS row only
+    router_flops = B * wl.spec.encoder.flops_executed_per_request(K)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -19,7 +19,7 @@ namespace chm {
 chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                      const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
                      void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
-                     float eps);
+                     float eps, long long res_ld = 0);
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, uint64_t ld);
@@ -270,6 +270,83 @@ __global__ void __launch_bounds__(160, 4)
   }
 }
 
+// Last layer, [CLS] query only: the router head reads h_[CLS] alone, so after
+// the last QKV projection only the CLS row of every (sequence, head) needs
+// attention (all S keys/values). One warp per (sequence, head): 128 q.k dot
+// products (4 keys per lane), warp softmax in fp32, o = sum_j p_j v_j with
+// V^T rows (2 dims per lane). Memory bound: 32 KB of K/V per item.
+constexpr int kClsWarps = 8;
+__global__ void __launch_bounds__(kClsWarps * 32)
+    attention_cls_kernel(const __nv_bfloat16* __restrict__ qk,
+                         const __nv_bfloat16* __restrict__ vt, int n_items, int n_heads,
+                         int hidden, __nv_bfloat16* __restrict__ ctx_c) {
+  __shared__ float s_q[kClsWarps][64];
+  __shared__ float s_p[kClsWarps][kAttnS];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kClsWarps + w;
+  if (item >= n_items) return;
+  const int seq = item / n_heads, h = item - seq * n_heads;
+  const size_t ld = 2 * (size_t)hidden;
+  const __nv_bfloat162 q2 = *reinterpret_cast<const __nv_bfloat162*>(
+      qk + (size_t)seq * kAttnS * ld + h * 64 + 2 * lane);
+  const float2 qf = __bfloat1622float2(q2);
+  s_q[w][2 * lane] = qf.x;
+  s_q[w][2 * lane + 1] = qf.y;
+  __syncwarp();
+  float sc[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint4* kp = reinterpret_cast<const uint4*>(
+        qk + ((size_t)seq * kAttnS + lane + 32 * t) * ld + hidden + h * 64);
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 u = __ldg(kp + c);
+      const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 kf = __bfloat1622float2(k2[e]);
+        acc = fmaf(s_q[w][c * 8 + 2 * e], kf.x, acc);
+        acc = fmaf(s_q[w][c * 8 + 2 * e + 1], kf.y, acc);
+      }
+    }
+    sc[t] = acc;
+  }
+  float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float p = __expf(sc[t] - mx);
+    s_p[w][lane + 32 * t] = p;
+    sum += p;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  __syncwarp();
+  const float inv = 1.0f / sum;
+#pragma unroll
+  for (int dd = 0; dd < 2; ++dd) {
+    const int d = lane + 32 * dd;
+    const uint4* vp =
+        reinterpret_cast<const uint4*>(vt + ((size_t)(seq * n_heads + h) * 64 + d) * kAttnS);
+    float acc = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < kAttnS / 8; ++c) {
+      const uint4 u = __ldg(vp + c);
+      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 vf = __bfloat1622float2(v2[e]);
+        acc = fmaf(s_p[w][c * 8 + 2 * e], vf.x, acc);
+        acc = fmaf(s_p[w][c * 8 + 2 * e + 1], vf.y, acc);
+      }
+    }
+    ctx_c[(size_t)seq * hidden + h * 64 + d] = __float2bfloat16_rn(acc * inv);
+  }
+}
+
 // K4: q[rows[i]*K + m] = sigmoid(head_b[m] + <x[i*S], head_w[m]>) for
 // i < n_live: the router head reads only the [CLS] state of each sequence.
 template <int VEC>
@@ -345,6 +422,29 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
     rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, vt, H, S,
                    nullptr, nullptr, 0.f);
     if (rc != CHM_OK) return rc;
+    if (l == L - 1) {
+      // Last layer: only h_[CLS] reaches the router head, so attention runs
+      // for the CLS query of every (sequence, head) and the rest of the layer
+      // for n_seq rows. ctx_c = ctx[:n_seq], xc = tmp[:n_seq] (compact).
+      auto* ctx_c = ctx;
+      auto* xc = tmp;
+      const int items = n_seq * NH;
+      prof::begin(prof::K_ATTENTION, st);
+      attention_cls_kernel<<<(unsigned)((items + kClsWarps - 1) / kClsWarps), kClsWarps * 32, 0,
+                             st>>>(qk, vt, items, NH, H, ctx_c);
+      prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
+      CHM_LAUNCH_CHECK();
+      rc = gemm_bf16(ctx_c, w.w_o[l], xc, w.b_o[l], x, n_seq, H, H, 5, st, nullptr, 0, 0,
+                     w.ln1_g[l], w.ln1_b[l], cfg.ln_eps, (long long)S * H);
+      if (rc != CHM_OK) return rc;
+      rc = gemm_bf16(xc, w.w_1[l], ffn, w.b_1[l], nullptr, n_seq, F, H, 2, st, nullptr, 0, 0,
+                     nullptr, nullptr, 0.f, 0);
+      if (rc != CHM_OK) return rc;
+      rc = gemm_bf16(ffn, w.w_2[l], xc, w.b_2[l], xc, n_seq, H, F, 5, st, nullptr, 0, 0,
+                     w.ln2_g[l], w.ln2_b[l], cfg.ln_eps, 0);
+      if (rc != CHM_OK) return rc;
+      break;
+    }
     prof::begin(prof::K_ATTENTION, st);
     attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qk, tm_vt, NH, H,
                                                                          ctx);
@@ -364,7 +464,7 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   }
   prof::begin(prof::K_ROWWISE, st);
   head_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(
-      x, S, n_seq, rows, n_rows_dev, w.head_w, w.head_b, cfg.n_models, q_out);
+      tmp, 1, n_seq, rows, n_rows_dev, w.head_w, w.head_b, cfg.n_models, q_out);
   prof::end(prof::K_ROWWISE, st, (double)n_seq * (2.0 * H + 4.0 * cfg.n_models * H));
   CHM_LAUNCH_CHECK();
   return CHM_OK;

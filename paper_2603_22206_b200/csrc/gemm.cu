@@ -74,6 +74,7 @@ struct EpiParams {
   const float* gamma;  // LN
   const float* beta;   // LN
   float eps;           // LN
+  long long res_ld;    // residual row pitch in elements (0 = N)
 };
 
 struct __align__(1024) Smem {
@@ -538,7 +539,8 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   const uint64_t c_cols = (EPI == EPI_QKV) ? (uint64_t)2 * ep.hidden : (uint64_t)N;
   if (!make_tmap_bf16(&tc, C, (uint64_t)M, c_cols, 32, 64, 0)) return CHM_ERR_CUDA;
   if (EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESIDUAL_LN) {
-    if (!make_tmap_bf16(&tr, residual, (uint64_t)M, (uint64_t)N, 32, 64, 0)) return CHM_ERR_CUDA;
+    if (!make_tmap_bf16(&tr, residual, (uint64_t)M, (uint64_t)N, 32, 64, (uint64_t)ep.res_ld))
+      return CHM_ERR_CUDA;
   } else {
     tr = tc;
   }
@@ -591,13 +593,15 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
 chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                      const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
                      void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
-                     float eps) {
+                     float eps, long long res_ld) {
   if (M <= 0 || N <= 0 || K <= 0) return M == 0 ? CHM_OK : CHM_ERR_INVALID_ARG;
   if (K % gemm::BK != 0 || N % 64 != 0) return CHM_ERR_INVALID_ARG;
   if (epilogue != gemm::EPI_NONE && !bias) return CHM_ERR_INVALID_ARG;
   if ((epilogue == gemm::EPI_BIAS_RESIDUAL || epilogue == gemm::EPI_RESIDUAL_LN) && !residual)
     return CHM_ERR_INVALID_ARG;
-  gemm::EpiParams ep{reinterpret_cast<__nv_bfloat16*>(vt), hidden, seq_len, gamma, beta, eps};
+  if (res_ld != 0 && res_ld < N) return CHM_ERR_INVALID_ARG;
+  gemm::EpiParams ep{reinterpret_cast<__nv_bfloat16*>(vt), hidden, seq_len, gamma,
+                     beta, eps,    res_ld};
   if (epilogue == gemm::EPI_QKV &&
       (!vt || hidden % 64 != 0 || N != 3 * hidden || seq_len % 128 != 0 || M % seq_len != 0))
     return CHM_ERR_INVALID_ARG;
@@ -629,7 +633,7 @@ extern "C" chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const
   if (epilogue == chm::gemm::EPI_QKV || epilogue == chm::gemm::EPI_RESIDUAL_LN)
     return CHM_ERR_INVALID_ARG;
   return chm::gemm_bf16(A, B, C, bias, residual, M, N, K, epilogue, (cudaStream_t)stream,
-                        nullptr, 0, 0, nullptr, nullptr, 0.f);
+                        nullptr, 0, 0, nullptr, nullptr, 0.f, 0);
 }
 
 extern "C" chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, const float* bias,
@@ -637,5 +641,5 @@ extern "C" chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, co
                                        const float* beta, float eps, int32_t M, int32_t N,
                                        int32_t K, void* stream) {
   return chm::gemm_bf16(A, B, C, bias, residual, M, N, K, chm::gemm::EPI_RESIDUAL_LN,
-                        (cudaStream_t)stream, nullptr, 0, 0, gamma, beta, eps);
+                        (cudaStream_t)stream, nullptr, 0, 0, gamma, beta, eps, 0);
 }

@@ -133,6 +133,7 @@ struct ChunkBuf {
   double yhat[kChunk * K];
   double arrival[kChunk];
   uint32_t rank[kChunk];
+  uint32_t perm[kChunk];
   uint32_t flags[kChunk];
   int32_t out_tokens[kChunk * K];
   int32_t first_row[kChunk];
@@ -161,6 +162,20 @@ __device__ __forceinline__ void neumaier_add(double& s, double& c, double x) {
   s = t;
 }
 
+// v[m] for a run-time m in [0, K) as a log-depth select tree over registers
+// (dynamic indexing would spill the array to local memory).
+template <int K>
+__device__ __forceinline__ double tree_select(const double (&v)[K], int m) {
+  double a[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) a[k] = v[k];
+#pragma unroll
+  for (int step = 1; step < K; step *= 2)
+#pragma unroll
+    for (int k = 0; k + step < K; k += 2 * step) a[k] = (m & step) ? a[k + step] : a[k];
+  return a[0];
+}
+
 template <int K>
 __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     SelectParams prm, chm_monitor_state mon, chm_rows rows, chm_row_scratch sc,
@@ -172,9 +187,26 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   const int tid = threadIdx.x;
 
   // ---- phase P: per-row precompute (independent of the in-flight state) ----
+  // It also decides the chain mode: the fast chain defers the engine
+  // bookkeeping (seq, admission, clock) to a parallel post-pass, which is
+  // exact unless a row could raise inside EngineSim.enqueue (clock going
+  // backwards, negative out_tokens) or needs the in-batch duplicate scan.
+  double max_clk0 = 0.0;
+#pragma unroll
+  for (int m = 0; m < K; ++m) max_clk0 = fmax(max_clk0, mon.engine_clock[m]);
+  int slow = 0;
   for (int i = tid; i < B; i += blockDim.x) {
     const int p = rows.program[i];
     const int st = rows.stage[i];
+    {
+      const double a = rows.arrival[i];
+      const double prev = i ? rows.arrival[i - 1] : max_clk0;
+      if (i ? (a < prev) : (a < __dsub_rn(prev, 1e-9))) slow = 1;
+      if (rows.out_tokens) {
+#pragma unroll
+        for (int m = 0; m < K; ++m) slow |= rows.out_tokens[(size_t)i * K + m] < 0;
+      }
+    }
     uint32_t fl = 0;
     uint64_t qual = 0;
     uint32_t rank = 0;
@@ -222,11 +254,12 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
         qual |= bits << (K * mf);
       }
     }
+    if (fl & ~(RF_ROUTE | RF_CACHED_PRE)) slow = 1;
     sc.flags[i] = fl;
     sc.qual[i] = qual;
     sc.rank[i] = rank;
   }
-  __syncthreads();
+  const bool exact = __syncthreads_or(slow) != 0;
 
   auto load_chunk = [&](int chunk, ChunkBuf<K>* buf, int t0, int nt) {
     const int r0 = chunk * kChunk;
@@ -234,7 +267,12 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     if (n <= 0) return;
     for (int j = t0; j < n; j += nt) {
       buf->qual[j] = __ldcg(sc.qual + r0 + j);
-      buf->rank[j] = __ldcg(sc.rank + r0 + j);
+      const uint32_t rk = __ldcg(sc.rank + r0 + j);
+      buf->rank[j] = rk;
+      uint32_t pm = 0;  // perm: rank r -> model (inverse of rank)
+#pragma unroll
+      for (int k = 0; k < K; ++k) pm |= (uint32_t)k << (4 * ((rk >> (4 * k)) & 15u));
+      buf->perm[j] = pm;
       buf->flags[j] = __ldcg(sc.flags + r0 + j);
       buf->arrival[j] = rows.arrival[r0 + j];
       buf->first_row[j] = sc.first_row[r0 + j];
@@ -287,12 +325,108 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       }
     }
   }
+  // Fast-chain state: everything the serial step touches lives in registers.
+  // Loads are compared as IEEE bit patterns (all non-negative), which orders
+  // them exactly like the fp64 values, with integer compares.
+  unsigned long long Lb[K];
+  double fr[K], cv[K], dd[K], bdiv[K];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    Lb[m] = (unsigned long long)__double_as_longlong(L[m]);
+    fr[m] = s_f[m];
+    cv[m] = s_c[m];
+    dd[m] = prm.d[m];
+    bdiv[m] = ((prm.b_pow2_mask >> m) & 1u) ? prm.inv_b[m] : prm.b[m];
+  }
+  const uint32_t pow2_mask = prm.b_pow2_mask;
 
   for (int ch = 0; ch < n_chunks; ++ch) {
     ChunkBuf<K>* cur = &bufs[ch & 1];
     if (tid >= 32) {
       if (ch + 1 < n_chunks) load_chunk(ch + 1, &bufs[(ch + 1) & 1], tid - 32, blockDim.x - 32);
-    } else if (tid == 0 && !stop) {
+    } else if (tid == 0 && !stop && !exact) {
+      // ---------------- fast chain ----------------
+      const int r0 = ch * kChunk;
+      const int n = min(kChunk, B - r0);
+      for (int j = 0; j < n; ++j) {
+        const int i = r0 + j;
+        const uint32_t fl = cur->flags[j];
+        double yr[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) yr[k] = cur->yhat[j * K + k];
+        int m;
+        bool cached;
+        if (fl & RF_CACHED_PRE) {
+          m = cur->pre_model[j];
+          cached = true;
+        } else {
+          if (fl & RF_BAD_SCORE) {
+            report_error(out.error, CHM_ERR_VALIDATION, i, -1, 1);
+            s_committed = i;
+            stop = true;
+            break;
+          }
+          cached = false;
+          unsigned long long tv[K];
+          int ti[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            tv[k] = Lb[k];
+            ti[k] = k;
+          }
+#pragma unroll
+          for (int step = 1; step < K; step *= 2)
+#pragma unroll
+            for (int k = 0; k + step < K; k += 2 * step)
+              if (tv[k + step] < tv[k]) {
+                tv[k] = tv[k + step];
+                ti[k] = ti[k + step];
+              }
+          const int mf = ti[0];
+          const unsigned long long limb = (unsigned long long)__double_as_longlong(
+              __dmul_rn(prm.one_plus_slack, __longlong_as_double((long long)tv[0])));
+          uint32_t ok = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) ok |= (Lb[k] <= limb ? 1u : 0u) << k;
+          const uint32_t cand = (uint32_t)(cur->qual[j] >> (K * mf)) & ok;
+          const uint32_t rk = cur->rank[j];
+          uint32_t crk = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) crk |= ((cand >> k) & 1u) << ((rk >> (4 * k)) & 15u);
+          m = crk ? (int)((cur->perm[j] >> (4 * (__ffs(crk) - 1))) & 15u) : mf;
+          if (out.loads) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+              out.loads[(size_t)i * K + k] = __longlong_as_double((long long)Lb[k]);
+          }
+        }
+        const double y = tree_select<K>(yr, m);
+        if (!(y >= 0.0)) {  // NaN or negative prediction (monitor.py:89-90)
+          report_error(out.error, y < 0.0 ? CHM_ERR_NEGATIVE_PREDICTION : CHM_ERR_NAN_PREDICTION,
+                       i, m, 0);
+          if (!cached) mon.assignment[rows.program[i]] = (int8_t)m;
+          s_committed = i;
+          stop = true;
+          break;
+        }
+        double fm = tree_select<K>(fr, m), cm = tree_select<K>(cv, m);
+        neumaier_add(fm, cm, y);
+        const double num = __dmul_rn(neumaier_value(fm, cm), tree_select<K>(dd, m));
+        const double bdm = tree_select<K>(bdiv, m);
+        const double lm = ((pow2_mask >> m) & 1u) ? __dmul_rn(num, bdm) : __ddiv_rn(num, bdm);
+        const unsigned long long lmb = (unsigned long long)__double_as_longlong(lm);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const bool hit = k == m;
+          fr[k] = hit ? fm : fr[k];
+          cv[k] = hit ? cm : cv[k];
+          Lb[k] = hit ? lmb : Lb[k];
+        }
+        out.model[i] = m;
+        out.priority[i] = y;
+        out.flags[i] = cached ? DF_CACHED : 0;  // admission bits: post-pass
+      }
+    } else if (tid == 0 && !stop && exact) {
       const int r0 = ch * kChunk;
       const int n = min(kChunk, B - r0);
       for (int j = 0; j < n; ++j) {
@@ -324,35 +458,38 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
             break;
           }
           cached = false;
-          // min over (L, id): strict < keeps the lowest index on ties. The
-          // running minimum stays in a register (no dynamic register indexing).
-          int mf = 0;
-          double lmf = L[0];
+          // min over (L, id) as a log-depth tournament; the left operand always
+          // carries the lower indices, so strict < keeps the lowest index on
+          // ties (balancer.py:71).
+          double tv[K];
+          int ti[K];
 #pragma unroll
-          for (int k = 1; k < K; ++k)
-            if (L[k] < lmf) {
-              lmf = L[k];
-              mf = k;
-            }
-          const double limit = __dmul_rn(prm.one_plus_slack, lmf);
+          for (int k = 0; k < K; ++k) {
+            tv[k] = L[k];
+            ti[k] = k;
+          }
+#pragma unroll
+          for (int step = 1; step < K; step *= 2)
+#pragma unroll
+            for (int k = 0; k + step < K; k += 2 * step)
+              if (tv[k + step] < tv[k]) {
+                tv[k] = tv[k + step];
+                ti[k] = ti[k + step];
+              }
+          const int mf = ti[0];
+          const double limit = __dmul_rn(prm.one_plus_slack, tv[0]);
           uint32_t ok = 0;
 #pragma unroll
           for (int k = 0; k < K; ++k) ok |= (L[k] <= limit ? 1u : 0u) << k;
-          const uint32_t cand =
-              (uint32_t)(cur->qual[j] >> (K * mf)) & ok & ((1u << K) - 1u);
-          m = mf;
-          if (cand) {
-            const uint32_t rk = cur->rank[j];
-            uint32_t best = 16;
+          const uint32_t cand = (uint32_t)(cur->qual[j] >> (K * mf)) & ok;
+          // the first qualifying model in descending-q order = the candidate
+          // with the smallest rank: move the candidate bits to rank space and
+          // take the lowest set bit
+          const uint32_t rk = cur->rank[j];
+          uint32_t cr = 0;
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-              const uint32_t r = (rk >> (4 * k)) & 15u;
-              if (((cand >> k) & 1u) && r < best) {
-                best = r;
-                m = k;
-              }
-            }
-          }
+          for (int k = 0; k < K; ++k) cr |= ((cand >> k) & 1u) << ((rk >> (4 * k)) & 15u);
+          m = cr ? (int)((cur->perm[j] >> (4 * (__ffs(cr) - 1))) & 15u) : mf;
           if (out.loads) {
 #pragma unroll
             for (int k = 0; k < K; ++k) out.loads[(size_t)i * K + k] = L[k];
@@ -427,6 +564,83 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
         out.flags[i] = dfl;
         out.seq[i] = sq;
       }
+    }
+    __syncthreads();
+  }
+
+  if (!exact) {
+    // ---- fast-chain bookkeeping, in parallel (EngineSim.enqueue effects) ----
+    // Rows choosing engine m take consecutive seq numbers; the first
+    // max(0, b - running) of them are admitted by the enqueue-triggered
+    // iteration, the rest queue; the engine clock ends at the arrival of the
+    // last row it received (arrivals are non-decreasing in fast mode).
+    __shared__ int s_cntm[K][kThreads];
+    __shared__ int s_lastm[K][kThreads];
+    __shared__ int s_tot[K], s_last[K];
+    if (tid == 0) {
+#pragma unroll
+      for (int m = 0; m < K; ++m) {
+        s_f[m] = fr[m];
+        s_c[m] = cv[m];
+      }
+    }
+    const int n_ok = s_committed;
+    const int per = (n_ok + kThreads - 1) / kThreads;
+    const int lo = min(tid * per, n_ok), hi = min(lo + per, n_ok);
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      s_cntm[m][tid] = 0;
+      s_lastm[m][tid] = -1;
+    }
+    for (int i = lo; i < hi; ++i) {
+      const int m = out.model[i];
+      s_cntm[m][tid] += 1;
+      s_lastm[m][tid] = i;
+    }
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp < K) {
+      int v[kThreads / 32], sum = 0, last = -1;
+#pragma unroll
+      for (int e = 0; e < kThreads / 32; ++e) {
+        v[e] = s_cntm[warp][lane * (kThreads / 32) + e];
+        sum += v[e];
+        last = max(last, s_lastm[warp][lane * (kThreads / 32) + e]);
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+      int run = incl - sum;
+#pragma unroll
+      for (int e = 0; e < kThreads / 32; ++e) {
+        s_cntm[warp][lane * (kThreads / 32) + e] = run;
+        run += v[e];
+      }
+      if (lane == 31) s_tot[warp] = incl;
+      if (lane == 0) s_last[warp] = last;
+    }
+    __syncthreads();
+    for (int i = lo; i < hi; ++i) {
+      const int m = out.model[i];
+      const int r = s_cntm[m][tid]++;
+      out.seq[i] = s_seq[m] + r;
+      out.flags[i] |= (s_run[m] + r < s_bmax[m]) ? DF_ADMITTED : DF_QUEUED;
+    }
+    __syncthreads();
+    if (tid < K) {
+      const int m = tid, tot = s_tot[m];
+      const int adm = min(max(s_bmax[m] - s_run[m], 0), tot);
+      s_seq[m] += tot;
+      s_run[m] += adm;
+      s_que[m] += tot - adm;
+      s_it[m] += adm;
+      s_cnt[m] += tot;
+      if (tot) s_clk[m] = fmax(s_clk[m], rows.arrival[s_last[m]]);
     }
     __syncthreads();
   }
