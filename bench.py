@@ -50,6 +50,11 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true")
+    p.add_argument("--mode", default="A", choices=["A", "B"],
+                   help="N>1 decision semantics: A all-reduce (north star), B serial-exact relay")
+    p.add_argument("--graph", action="store_true",
+                   help="replay the tick as a CUDA graph (1 GPU; per-kernel timing from an "
+                        "eager profiled pass)")
     return p.parse_args()
 
 
@@ -263,7 +268,9 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2603_22206_b200 import _lib, synth
+    from paper_2603_22206_b200.dist import ShardedScheduler
     from paper_2603_22206_b200.scheduler import GpuScheduler, HostStaging
+    from paper_2603_22206_b200.tick import TickGraph
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -277,7 +284,6 @@ def run_ours(args):
     gs = GpuScheduler(wl.pool, wl.balancer, wl.aging, router=wl.router, predictor=wl.predictor,
                       n_programs=wl.n_programs, max_rows=B, device=dev)
     snap = gs.state.snapshot()
-    p0 = None
     n_distinct = 4
     host_cols = []
     batches = []
@@ -286,27 +292,24 @@ def run_ours(args):
         host_cols.append(cols)
         batches.append(wl.batch(t + 1000 * rank))
     stream = torch.cuda.current_stream(dev)
-
-    def allreduce_inflight():
-        # Mode A: every GPU ran its shard's serial chain from the tick-start
-        # global P; the per-engine in-flight deltas are summed over NCCL.
-        nonlocal p0
-        st = gs.state
-        val = st.inflight_sum + torch.where(torch.isfinite(st.inflight_comp),
-                                            st.inflight_comp, torch.zeros_like(st.inflight_comp))
-        if p0 is None:
-            p0 = snap["inflight_sum"].clone()
-        delta = val - p0
-        dist.all_reduce(delta)
-        st.inflight_sum.copy_(p0 + delta)
-        st.inflight_comp.zero_()
+    # N > 1: request-sharded ticks; Mode A all-reduces the per-engine in-flight
+    # vector over NCCL after each GPU's chain, Mode B relays it (serial-exact).
+    sched = ShardedScheduler(gs, args.mode) if world > 1 else gs
+    graph = None
+    if args.graph and world == 1:
+        gbatch = wl.batch(0)
+        graph = TickGraph(gs, gbatch, n_iterations=1, restore_snapshot=snap)
 
     def tick(i, batch=None):
+        src = batch if batch is not None else batches[i % n_distinct]
+        if graph is not None:
+            for name in ("program", "stage", "arrival", "out_tokens", "handle", "workflow",
+                         "input_tokens", "token_ids"):
+                getattr(graph.batch, name).copy_(getattr(src, name), non_blocking=True)
+            graph.replay()
+            return
         gs.state.restore(snap)
-        gs.run_rows(batch if batch is not None else batches[i % n_distinct], n_iterations=1,
-                    stream=stream)
-        if world > 1:
-            allreduce_inflight()
+        sched.run_rows(src, n_iterations=1, stream=stream)
 
     for i in range(args.warmup):
         tick(i)
@@ -320,7 +323,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local, not args.no_clocks)
     _lib.profile_read()  # reset timings
-    _lib.profile_enable(True)
+    _lib.profile_enable(graph is None)
     launches0 = _lib.profile_read()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -335,6 +338,17 @@ def run_ours(args):
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     clk = clocks.stop()
+    if graph is not None:
+        # graph replays bypass the host-side launch hooks: time the same
+        # ticks eagerly once more for the per-kernel breakdown / roofline
+        launches0 = _lib.profile_read()
+        _lib.profile_enable(True)
+        for i in range(args.steps):
+            gs.state.restore(snap)
+            gs.run_rows(batches[i % n_distinct], n_iterations=1, stream=stream)
+        torch.cuda.synchronize()
+        prof = _lib.profile_read()
+        _lib.profile_enable(False)
     gs.check_errors("timed")
     tick_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
@@ -403,8 +417,10 @@ def run_ours(args):
                  "quantile predictor trained on synthesize_trace(2000, seed=1)"),
         "config": {"workload": f"{args.config}: {wl.spec.description}", "batch_per_gpu": B,
                    "global_batch": B * world, "models": K, "router": _router_desc(wl),
-                   "parallelism": f"request-sharded x{world} (NCCL all-reduce of in-flight "
-                                  f"vector)" if world > 1 else "single GPU",
+                   "parallelism": (f"request-sharded x{world}, mode {args.mode} "
+                                   f"({'NCCL all-reduce' if args.mode == 'A' else 'NCCL relay'}"
+                                   f" of the in-flight vector)") if world > 1 else "single GPU",
+                   "cuda_graph": graph is not None,
                    "l2": "inputs larger than L2 (router activations >1 GB per layer)",
                    "state": "fresh monitor/queues per tick (device-side restore, timed)"},
         "roofline": roofline,

@@ -124,7 +124,9 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(
 //   P = exp(s - max) written bf16 into a K-major 128B-swizzled smem tile
 //   O = P V        (M=128, N=64,  K=128)   -> TMEM cols [0,64) (reuses S)
 //   O / rowsum -> ctx (bf16)
-// Q is pre-scaled by 1/sqrt(d) in the QKV epilogue; V arrives transposed.
+// Q is pre-scaled by 1/sqrt(d) in the QKV epilogue. V is read row-major
+// ([keys][d], the layout the QKV GEMM writes) and fed to the P.V MMA as an
+// MN-major B operand (N = d contiguous), so no transpose pass exists.
 // 5 warps: 0-3 softmax/epilogue (warp w owns TMEM lanes 32w..32w+31),
 // warp 4 issues TMA and MMA. P overwrites the Q|K tiles once S is computed,
 // so a CTA needs 48 KB of smem and 128 TMEM columns: four CTAs per SM keep
@@ -134,15 +136,14 @@ constexpr int kAttnS = 128;
 struct AttnSmem {
   uint8_t qk[2][kAttnS * 64 * 2];    // Q then K tiles (16 KB each, [128][64] SW128);
                                      // afterwards P key halves [128 rows][64 keys]
-  uint8_t vt[2][64 * 64 * 2];        // 2 x 8 KB, V^T [64 d][64 keys] per key half
+  uint8_t v[kAttnS * 64 * 2];        // V [128 keys][64 d] SW128 (MN-major B operand)
   uint64_t bar_load, bar_s, bar_p, bar_o;
   uint32_t tmem_base;
 };
 constexpr size_t kAttnSmemBytes = sizeof(AttnSmem) + 1024;
 
 __global__ void __launch_bounds__(160, 4)
-    attention_kernel(const __grid_constant__ CUtensorMap tm_qk,
-                     const __grid_constant__ CUtensorMap tm_vt, int n_heads, int hidden,
+    attention_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
                      __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ uint8_t smem_raw[];
   AttnSmem& s = *reinterpret_cast<AttnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -165,14 +166,12 @@ __global__ void __launch_bounds__(160, 4)
 
   if (warp == 4) {
     if (lane == 0) {
-      constexpr uint32_t kBytes = 2 * kAttnS * 64 * 2 + 2 * 64 * 64 * 2;
+      constexpr uint32_t kBytes = 3 * kAttnS * 64 * 2;
       sm100::mbar_arrive_expect_tx(&s.bar_load, kBytes);
       const int row0 = seq * kAttnS;
-      sm100::tma_load_2d(s.qk[0], &tm_qk, &s.bar_load, h * 64, row0);
-      sm100::tma_load_2d(s.qk[1], &tm_qk, &s.bar_load, hidden + h * 64, row0);
-      const int vrow = (seq * n_heads + h) * 64;
-      sm100::tma_load_2d(s.vt[0], &tm_vt, &s.bar_load, 0, vrow);
-      sm100::tma_load_2d(s.vt[1], &tm_vt, &s.bar_load, 64, vrow);
+      sm100::tma_load_2d(s.qk[0], &tm_qkv, &s.bar_load, h * 64, row0);
+      sm100::tma_load_2d(s.qk[1], &tm_qkv, &s.bar_load, hidden + h * 64, row0);
+      sm100::tma_load_2d(s.v, &tm_qkv, &s.bar_load, 2 * hidden + h * 64, row0);
       sm100::mbar_wait(&s.bar_load, 0);
       sm100::tc_fence_after();
       constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
@@ -184,12 +183,14 @@ __global__ void __launch_bounds__(160, 4)
       sm100::mma_commit(&s.bar_s);
       sm100::mbar_wait(&s.bar_p, 0);
       sm100::tc_fence_after();
-      constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64);
+      // B = V, MN-major: a K=16 step covers 16 key rows = two 8-row swizzle
+      // atoms (2 KB); the atom stride along K is the SBO (1024 B).
+      constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);
+      const uint32_t va = sm100::smem_u32(s.v);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t pa = sm100::smem_u32(s.qk[kk >> 2]) + (kk & 3) * 32;
-        const uint32_t va = sm100::smem_u32(s.vt[kk >> 2]) + (kk & 3) * 32;
-        sm100::mma_bf16(tmem, sm100::umma_desc_sw128(pa), sm100::umma_desc_sw128(va),
+        sm100::mma_bf16(tmem, sm100::umma_desc_sw128(pa), sm100::umma_desc_sw128(va + kk * 2048),
                         idesc_o, kk);
       }
       sm100::mma_commit(&s.bar_o);
@@ -273,12 +274,11 @@ __global__ void __launch_bounds__(160, 4)
 // Last layer, [CLS] query only: the router head reads h_[CLS] alone, so after
 // the last QKV projection only the CLS row of every (sequence, head) needs
 // attention (all S keys/values). One warp per (sequence, head): 128 q.k dot
-// products (4 keys per lane), warp softmax in fp32, o = sum_j p_j v_j with
-// V^T rows (2 dims per lane). Memory bound: 32 KB of K/V per item.
+// products (4 keys per lane), warp softmax in fp32, o = sum_j p_j v_j (2 dims
+// per lane). Memory bound: 32 KB of K/V per item.
 constexpr int kClsWarps = 8;
 __global__ void __launch_bounds__(kClsWarps * 32)
-    attention_cls_kernel(const __nv_bfloat16* __restrict__ qk,
-                         const __nv_bfloat16* __restrict__ vt, int n_items, int n_heads,
+    attention_cls_kernel(const __nv_bfloat16* __restrict__ qk, int n_items, int n_heads,
                          int hidden, __nv_bfloat16* __restrict__ ctx_c) {
   __shared__ float s_q[kClsWarps][64];
   __shared__ float s_p[kClsWarps][kAttnS];
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kClsWarps * 32)
   const int item = blockIdx.x * kClsWarps + w;
   if (item >= n_items) return;
   const int seq = item / n_heads, h = item - seq * n_heads;
-  const size_t ld = 2 * (size_t)hidden;
+  const size_t ld = 3 * (size_t)hidden;
   const __nv_bfloat162 q2 = *reinterpret_cast<const __nv_bfloat162*>(
       qk + (size_t)seq * kAttnS * ld + h * 64 + 2 * lane);
   const float2 qf = __bfloat1622float2(q2);
@@ -326,25 +326,20 @@ __global__ void __launch_bounds__(kClsWarps * 32)
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   __syncwarp();
   const float inv = 1.0f / sum;
-#pragma unroll
-  for (int dd = 0; dd < 2; ++dd) {
-    const int d = lane + 32 * dd;
-    const uint4* vp =
-        reinterpret_cast<const uint4*>(vt + ((size_t)(seq * n_heads + h) * 64 + d) * kAttnS);
-    float acc = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < kAttnS / 8; ++c) {
-      const uint4 u = __ldg(vp + c);
-      const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 vf = __bfloat1622float2(v2[e]);
-        acc = fmaf(s_p[w][c * 8 + 2 * e], vf.x, acc);
-        acc = fmaf(s_p[w][c * 8 + 2 * e + 1], vf.y, acc);
-      }
-    }
-    ctx_c[(size_t)seq * hidden + h * 64 + d] = __float2bfloat16_rn(acc * inv);
+  // o[d] = sum_j p_j V[j][d]: lane owns d = 2*lane, 2*lane+1; each key row is
+  // one coalesced 128-byte warp load
+  const __nv_bfloat16* vbase = qk + (size_t)seq * kAttnS * ld + 2 * hidden + h * 64 + 2 * lane;
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+  for (int j = 0; j < kAttnS; ++j) {
+    const float2 vf =
+        __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vbase + (size_t)j * ld));
+    const float p = s_p[w][j];
+    a0 = fmaf(p, vf.x, a0);
+    a1 = fmaf(p, vf.y, a1);
   }
+  *reinterpret_cast<__nv_bfloat162*>(ctx_c + (size_t)seq * hidden + h * 64 + 2 * lane) =
+      __floats2bfloat162_rn(a0 * inv, a1 * inv);
 }
 
 // K4: q[rows[i]*K + m] = sigmoid(head_b[m] + <x[i*S], head_w[m]>) for
@@ -393,8 +388,6 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   auto* ctx = reinterpret_cast<__nv_bfloat16*>(ws.ctx);
   auto* tmp = reinterpret_cast<__nv_bfloat16*>(ws.tmp);
   auto* ffn = reinterpret_cast<__nv_bfloat16*>(ws.ffn);
-  // V^T lives in the ctx-sized tail of the qkv workspace ([T, 3H]: Q|K use 2H).
-  auto* vt = qk + (size_t)T * 2 * H;
   const int rows_per_cta = 256 / 32;
   const unsigned grid_t = (unsigned)((T + rows_per_cta - 1) / rows_per_cta);
   prof::begin(prof::K_ROWWISE, st);
@@ -405,10 +398,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       reinterpret_cast<const __nv_bfloat16*>(w.type_emb), w.emb_ln_g, w.emb_ln_b, cfg.ln_eps, x);
   prof::end(prof::K_ROWWISE, st, (double)T * (4.0 + 6.0 * H));
   CHM_LAUNCH_CHECK();
-  CUtensorMap tm_qk, tm_vt;
-  if (!gemm::make_tmap_bf16(&tm_qk, qk, (uint64_t)T, (uint64_t)2 * H, 128, 64, 0))
-    return CHM_ERR_CUDA;
-  if (!gemm::make_tmap_bf16(&tm_vt, vt, (uint64_t)n_seq * (H / 64) * 64, (uint64_t)S, 64, 64, 0))
+  CUtensorMap tm_qkv;
+  if (!gemm::make_tmap_bf16(&tm_qkv, qk, (uint64_t)T, (uint64_t)3 * H, 128, 64, 0))
     return CHM_ERR_CUDA;
   static bool attr = false;
   if (!attr) {
@@ -419,8 +410,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   const int NH = H / 64;
   chm_status rc;
   for (int l = 0; l < L; ++l) {
-    rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, vt, H, S,
-                   nullptr, nullptr, 0.f);
+    rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, nullptr, H,
+                   S, nullptr, nullptr, 0.f);
     if (rc != CHM_OK) return rc;
     if (l == L - 1) {
       // Last layer: only h_[CLS] reaches the router head, so attention runs
@@ -431,7 +422,7 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       const int items = n_seq * NH;
       prof::begin(prof::K_ATTENTION, st);
       attention_cls_kernel<<<(unsigned)((items + kClsWarps - 1) / kClsWarps), kClsWarps * 32, 0,
-                             st>>>(qk, vt, items, NH, H, ctx_c);
+                             st>>>(qk, items, NH, H, ctx_c);
       prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
       CHM_LAUNCH_CHECK();
       rc = gemm_bf16(ctx_c, w.w_o[l], xc, w.b_o[l], x, n_seq, H, H, 5, st, nullptr, 0, 0,
@@ -446,8 +437,7 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       break;
     }
     prof::begin(prof::K_ATTENTION, st);
-    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qk, tm_vt, NH, H,
-                                                                         ctx);
+    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx);
     prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
     CHM_LAUNCH_CHECK();
     // out-projection + residual + LayerNorm fused (x updated in place)

@@ -56,12 +56,8 @@ enum Epilogue : int {
   EPI_BIAS = 1,
   EPI_BIAS_GELU = 2,
   EPI_BIAS_RESIDUAL = 3,
-  // QKV projection: columns [0, H) are Q (pre-scaled by 1/sqrt(64), exact in
-  // bf16), [H, 2H) are K -> C with row stride 2H; columns [2H, 3H) are V,
-  // written transposed per (sequence, head) as vt[seq][head][d][s] so the
-  // attention kernel's P.V MMA reads V^T K-major. A 32-lane TMEM quarter holds
-  // 32 consecutive tokens of one sequence, so each transposed store is one
-  // coalesced 64-byte segment.
+  // QKV projection: bias, and columns [0, H) (Q) pre-scaled by 1/sqrt(64)
+  // (exact in bf16) so attention needs no score scaling.
   EPI_QKV = 4,
   // C = LayerNorm(A.B^T + bias + residual) * gamma + beta, N = 256 g.
   EPI_RESIDUAL_LN = 5,
@@ -412,24 +408,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::mbar_wait(&s.res_bar[ew][box], (res_phase >> box) & 1);
             res_phase ^= 1u << box;
           }
-          const int row = mrow0 + lane;
-          if (EPI == EPI_QKV && col0 >= 2 * ep.hidden) {
-            // V: transposed direct stores, one coalesced 64 B segment per column
-            if (row < M) {
-              const int hn = col0 - 2 * ep.hidden, h = hn >> 6;
-              const int seq = row / ep.seq_len, sp = row - seq * ep.seq_len;
-              __nv_bfloat16* vp =
-                  ep.vt + ((size_t)(seq * (ep.hidden >> 6) + h) * 64) * ep.seq_len + sp;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                vp[(size_t)j * ep.seq_len] =
-                    __float2bfloat16_rn(__uint_as_float(r0[j]) + __ldg(bias + col0 + j));
-                vp[(size_t)(j + 32) * ep.seq_len] =
-                    __float2bfloat16_rn(__uint_as_float(r1[j]) + __ldg(bias + col0 + 32 + j));
-              }
-            }
-            continue;
-          }
           const float qscale = (EPI == EPI_QKV && col0 < ep.hidden) ? 0.125f : 1.0f;
           uint8_t* rowp = sb + lane * 128;
 #pragma unroll
@@ -536,8 +514,7 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   CUtensorMap ta, tb, tc, tr;
   if (!make_tmap_bf16(&ta, A, (uint64_t)M, (uint64_t)K, CM, BK, 0)) return CHM_ERR_CUDA;
   if (!make_tmap_bf16(&tb, B, (uint64_t)N, (uint64_t)K, CN, BK, 0)) return CHM_ERR_CUDA;
-  const uint64_t c_cols = (EPI == EPI_QKV) ? (uint64_t)2 * ep.hidden : (uint64_t)N;
-  if (!make_tmap_bf16(&tc, C, (uint64_t)M, c_cols, 32, 64, 0)) return CHM_ERR_CUDA;
+  if (!make_tmap_bf16(&tc, C, (uint64_t)M, (uint64_t)N, 32, 64, 0)) return CHM_ERR_CUDA;
   if (EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESIDUAL_LN) {
     if (!make_tmap_bf16(&tr, residual, (uint64_t)M, (uint64_t)N, 32, 64, (uint64_t)ep.res_ld))
       return CHM_ERR_CUDA;
@@ -602,8 +579,7 @@ chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
   if (res_ld != 0 && res_ld < N) return CHM_ERR_INVALID_ARG;
   gemm::EpiParams ep{reinterpret_cast<__nv_bfloat16*>(vt), hidden, seq_len, gamma,
                      beta, eps,    res_ld};
-  if (epilogue == gemm::EPI_QKV &&
-      (!vt || hidden % 64 != 0 || N != 3 * hidden || seq_len % 128 != 0 || M % seq_len != 0))
+  if (epilogue == gemm::EPI_QKV && (hidden % 64 != 0 || N != 3 * hidden))
     return CHM_ERR_INVALID_ARG;
   if (epilogue == gemm::EPI_RESIDUAL_LN &&
       (N % gemm::BN != 0 || N / gemm::BN > gemm::kMaxLnGroups || !gamma || !beta))

@@ -1,0 +1,110 @@
+"""Request-sharded multi-GPU scheduling: one process per GPU.
+
+Requests shard by program (`shard_of`), so every stage of a program lands on
+the same GPU and the assignment map stays local. Router, predictor and the
+per-row precompute are shard-local; the only cross-GPU state is the
+per-engine in-flight predicted-token vector P (K doubles, Neumaier (s, c)).
+
+Two decision semantics (the caller picks one):
+
+  Mode A (north-star literal): every GPU runs its shard's serial chain from
+      the tick-start global P; afterwards the per-engine deltas are summed
+      with one all-reduce (NCCL over NVLink, 64 B for K = 8). Decisions equal
+      G independent serial replays that all start from P0.
+  Mode B (serial-exact relay): the chains run in rank order; rank g receives
+      (s, c) from rank g-1 before its selection kernel, sends its final
+      (s, c) to rank g+1, and the last rank broadcasts the tick-end state.
+      Decisions equal ONE serial replay of the concatenated batch (rank 0's
+      rows, then rank 1's, ...) -- bit for bit, because (s, c) is exactly
+      the reference's Neumaier state. Routers and predictors still run in
+      parallel; only the short serial chains are ordered.
+
+The functions below operate on torch tensors on any device, so the same
+protocol code runs over NCCL on GPUs and over gloo on CPUs (tests).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import torch
+import torch.distributed as dist
+
+
+def shard_of(program_id: str, world: int) -> int:
+    """Stable program -> rank map (all stages of a program on one GPU)."""
+    h = hashlib.blake2b(program_id.encode("utf-8"), digest_size=8).digest()
+    return int.from_bytes(h, "big") % world
+
+
+def neumaier_value_t(s: torch.Tensor, c: torch.Tensor) -> torch.Tensor:
+    """Elementwise CPython-sum value of (s, c): s + c when c is finite and != 0."""
+    use = torch.isfinite(c) & (c != 0)
+    return torch.where(use, s + c, s)
+
+
+def mode_a_allreduce(s: torch.Tensor, c: torch.Tensor, s0: torch.Tensor,
+                     c0: torch.Tensor, group=None) -> None:
+    """Mode A tick end: P = P0 + sum_g (P_g - P0); (s, c) <- (P, 0) in place."""
+    p0 = neumaier_value_t(s0, c0)
+    delta = neumaier_value_t(s, c) - p0
+    dist.all_reduce(delta, group=group)
+    s.copy_(p0 + delta)
+    c.zero_()
+
+
+def relay_receive(state: torch.Tensor, group=None) -> None:
+    """Mode B: before the selection chain, rank g > 0 receives the packed
+    monitor state [2K] = (s, c) from rank g-1 (in place)."""
+    rank = dist.get_rank(group)
+    if rank > 0:
+        dist.recv(state, src=_global(rank - 1, group), group=group)
+
+
+def relay_forward(state: torch.Tensor, group=None) -> None:
+    """Mode B: after the chain, pass (s, c) on; the last rank broadcasts the
+    tick-end state so every rank starts the next tick from it."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    if rank + 1 < world:
+        dist.send(state, dst=_global(rank + 1, group), group=group)
+    dist.broadcast(state, src=_global(world - 1, group), group=group)
+
+
+def _global(rank: int, group) -> int:
+    return rank if group is None else dist.get_global_rank(group, rank)
+
+
+class ShardedScheduler:
+    """Wraps a per-rank GpuScheduler with the Mode A / Mode B exchange."""
+
+    def __init__(self, scheduler, mode: str = "B", group=None):
+        if mode not in ("A", "B"):
+            raise ValueError("mode must be 'A' or 'B'")
+        self.gs = scheduler
+        self.mode = mode
+        self.group = group
+        st = scheduler.state
+        self.packed = torch.empty(2 * st.K, dtype=torch.float64, device=st.device)
+
+    def run_rows(self, batch, n_iterations: int = 1, **kw) -> None:
+        st = self.gs.state
+        K = st.K
+        if self.mode == "A":
+            s0 = st.inflight_sum.clone()
+            c0 = st.inflight_comp.clone()
+            self.gs.run_rows(batch, n_iterations=n_iterations, **kw)
+            mode_a_allreduce(st.inflight_sum, st.inflight_comp, s0, c0, self.group)
+            return
+        # Mode B: receive the predecessor's (s, c), run, forward.
+        self.packed[:K].copy_(st.inflight_sum)
+        self.packed[K:].copy_(st.inflight_comp)
+        relay_receive(self.packed, self.group)
+        st.inflight_sum.copy_(self.packed[:K])
+        st.inflight_comp.copy_(self.packed[K:])
+        self.gs.run_rows(batch, n_iterations=n_iterations, **kw)
+        self.packed[:K].copy_(st.inflight_sum)
+        self.packed[K:].copy_(st.inflight_comp)
+        relay_forward(self.packed, self.group)
+        st.inflight_sum.copy_(self.packed[:K])
+        st.inflight_comp.copy_(self.packed[K:])
