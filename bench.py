@@ -282,7 +282,10 @@ def run_ours(args):
     wl = synth.make_workload(args.config, device=dev)
     B, K = wl.batch_size, len(wl.pool)
     gs = GpuScheduler(wl.pool, wl.balancer, wl.aging, router=wl.router, predictor=wl.predictor,
-                      n_programs=wl.n_programs, max_rows=B, device=dev)
+                      n_programs=wl.n_programs, max_rows=B, device=dev,
+                      queue_capacity=wl.queue_capacity)
+    wl.seed_state(gs.state)  # cfg4: 64k in flight + 64k queued, engines full
+    n_complete = wl.completions()
     snap = gs.state.snapshot()
     n_distinct = 4
     host_cols = []
@@ -298,7 +301,8 @@ def run_ours(args):
     graph = None
     if args.graph and world == 1:
         gbatch = wl.batch(0)
-        graph = TickGraph(gs, gbatch, n_iterations=1, restore_snapshot=snap)
+        graph = TickGraph(gs, gbatch, n_iterations=1, restore_snapshot=snap,
+                          n_complete=n_complete)
 
     def tick(i, batch=None):
         src = batch if batch is not None else batches[i % n_distinct]
@@ -309,7 +313,7 @@ def run_ours(args):
             graph.replay()
             return
         gs.state.restore(snap)
-        sched.run_rows(src, n_iterations=1, stream=stream)
+        sched.run_rows(src, n_iterations=1, n_complete=n_complete, stream=stream)
 
     for i in range(args.warmup):
         tick(i)
@@ -345,7 +349,8 @@ def run_ours(args):
         _lib.profile_enable(True)
         for i in range(args.steps):
             gs.state.restore(snap)
-            gs.run_rows(batches[i % n_distinct], n_iterations=1, stream=stream)
+            gs.run_rows(batches[i % n_distinct], n_iterations=1, n_complete=n_complete,
+                        stream=stream)
         torch.cuda.synchronize()
         prof = _lib.profile_read()
         _lib.profile_enable(False)

@@ -146,7 +146,10 @@ typedef struct chm_queue_state {
   int64_t* admitted;         /* [K*cap] out: handles admitted this call, in order */
   int32_t* n_admitted;       /* [K] out                                        */
   int32_t* n_promoted;       /* [K] out: promotions this call                  */
-  uint8_t* arrival_unsorted; /* [K] sticky: arrival not monotone in seq        */
+  uint8_t* arrival_unsorted; /* [K] out: arrival not monotone in seq           */
+  void* scratch;             /* K*cap*20 bytes of sort-key scratch; required
+                                when capacity > 10240 (keys then live in L2/HBM
+                                instead of shared memory)                      */
 } chm_queue_state;
 
 /* ---- router encoder (BERT-style post-LN, CLS -> Linear(H,K) -> sigmoid) --- */

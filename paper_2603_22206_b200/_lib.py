@@ -127,7 +127,11 @@ class QueueState(ctypes.Structure):
         ("n_admitted", c_void_p),
         ("n_promoted", c_void_p),
         ("arrival_unsorted", c_void_p),
+        ("scratch", c_void_p),
     ]
+
+QUEUE_SMEM_CAPACITY = 10240        # entries per engine sorted in shared memory
+QUEUE_SCRATCH_BYTES_PER_ENTRY = 20  # larger segments: global sort-key scratch
 
 
 class EncoderCfg(ctypes.Structure):

@@ -271,33 +271,227 @@ __global__ void __launch_bounds__(160, 4)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 attention for S = 128 * n_kb > 128 (long prompts, cfg5 S = 512): one CTA
+// per (sequence, head, 128-query block), flash-style loop over 128-key
+// blocks with an online softmax. Per key block: S = Q K^T (TMEM cols
+// [0,128)), running max / rescale in registers, P bf16 to smem, O_blk = P V
+// (TMEM cols [128,192), fresh each block), o = o * alpha + O_blk in
+// registers. K/V blocks are double-buffered so the next block's TMA overlaps
+// this block's softmax.
+// ---------------------------------------------------------------------------
+struct AttnLongSmem {
+  uint8_t q[kAttnS * 64 * 2];         // Q block [128][64]
+  uint8_t kv[2][2][kAttnS * 64 * 2];  // [buf][K|V] [128 keys][64]
+  uint8_t p[2][kAttnS * 64 * 2];      // P key halves [128][64]
+  uint64_t bar_q, bar_kv[2], bar_s, bar_p, bar_o;
+  uint32_t tmem_base;
+};
+constexpr size_t kAttnLongSmemBytes = sizeof(AttnLongSmem) + 1024;
+
+__global__ void __launch_bounds__(160, 1)
+    attention_long_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
+                          int S, __nv_bfloat16* __restrict__ ctx) {
+  extern __shared__ uint8_t smem_raw[];
+  AttnLongSmem& s = *reinterpret_cast<AttnLongSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_qb = S / kAttnS, n_kb = S / kAttnS;
+  const int item = blockIdx.x;
+  const int qb = item % n_qb;
+  const int sh = item / n_qb;
+  const int seq = sh / n_heads, h = sh - seq * n_heads;
+  const int row0 = seq * S;
+  if (warp == 4 && lane == 0) {
+    sm100::mbar_init(&s.bar_q, 1);
+    sm100::mbar_init(&s.bar_kv[0], 1);
+    sm100::mbar_init(&s.bar_kv[1], 1);
+    sm100::mbar_init(&s.bar_s, 1);
+    sm100::mbar_init(&s.bar_p, 128);
+    sm100::mbar_init(&s.bar_o, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 0) sm100::tmem_alloc<256>(&s.tmem_base);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  constexpr uint32_t kTile = kAttnS * 64 * 2;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      auto load_kv = [&](int kb) {
+        const int b = kb & 1;
+        sm100::mbar_arrive_expect_tx(&s.bar_kv[b], 2 * kTile);
+        sm100::tma_load_2d(s.kv[b][0], &tm_qkv, &s.bar_kv[b], hidden + h * 64,
+                           row0 + kb * kAttnS);
+        sm100::tma_load_2d(s.kv[b][1], &tm_qkv, &s.bar_kv[b], 2 * hidden + h * 64,
+                           row0 + kb * kAttnS);
+      };
+      sm100::mbar_arrive_expect_tx(&s.bar_q, kTile);
+      sm100::tma_load_2d(s.q, &tm_qkv, &s.bar_q, h * 64, row0 + qb * kAttnS);
+      load_kv(0);
+      if (n_kb > 1) load_kv(1);
+      sm100::mbar_wait(&s.bar_q, 0);
+      constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
+      constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);
+      const uint32_t qa = sm100::smem_u32(s.q);
+      for (int kb = 0; kb < n_kb; ++kb) {
+        const int b = kb & 1;
+        sm100::mbar_wait(&s.bar_kv[b], (kb >> 1) & 1);
+        sm100::tc_fence_after();
+        const uint32_t ka = sm100::smem_u32(s.kv[b][0]), va = sm100::smem_u32(s.kv[b][1]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          sm100::mma_bf16(tmem, sm100::umma_desc_sw128(qa + k * 32),
+                          sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+        sm100::mma_commit(&s.bar_s);
+        sm100::mbar_wait(&s.bar_p, kb & 1);
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t pa = sm100::smem_u32(s.p[kk >> 2]) + (kk & 3) * 32;
+          sm100::mma_bf16(tmem + 128, sm100::umma_desc_sw128(pa),
+                          sm100::umma_desc_sw128(va + kk * 2048), idesc_o, kk);
+        }
+        sm100::mma_commit(&s.bar_o);
+        // K/V buffer b is free once this block's MMAs completed
+        if (kb + 2 < n_kb) {
+          sm100::mbar_wait(&s.bar_o, kb & 1);
+          load_kv(kb + 2);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int r = warp * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    constexpr float kLog2e = 1.4426950408889634f;
+    float m_run = -INFINITY, l_run = 0.f;
+    float o[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) o[j] = 0.f;
+    for (int kb = 0; kb < n_kb; ++kb) {
+      sm100::mbar_wait(&s.bar_s, kb & 1);
+      sm100::tc_fence_after();
+      float mx = m_run;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t raw[32];
+        sm100::tmem_ld_32x32b_x32(tmem + lane_base + c * 32, raw);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(raw[j]));
+      }
+      const float alpha = exp2f((m_run - mx) * kLog2e);  // 0 on the first block
+      const float mxl = mx * kLog2e;
+      float sum = 0.f;
+      // P of the previous block may still be read by its P.V MMA
+      if (kb > 0) sm100::mbar_wait(&s.bar_o, (kb - 1) & 1);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t raw[32];
+        sm100::tmem_ld_32x32b_x32(tmem + lane_base + c * 32, raw);
+        sm100::tmem_ld_wait();
+        uint8_t* rowp = s.p[c >> 1] + r * 128;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          __align__(16) __nv_bfloat162 pv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float p0 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
+            const float p1 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
+            pv[e] = __floats2bfloat162_rn(p0, p1);
+            const float2 back = __bfloat1622float2(pv[e]);
+            sum += back.x + back.y;
+          }
+          const int chunk = (c & 1) * 4 + q4;
+          *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
+              *reinterpret_cast<uint4*>(pv);
+        }
+      }
+      if (kb > 0) {
+        // fold the previous block's O_blk (still in TMEM cols [128,192))
+        uint32_t ov[2][32];
+        sm100::tmem_ld_32x32b_x32(tmem + lane_base + 128, ov[0]);
+        sm100::tmem_ld_32x32b_x32(tmem + lane_base + 160, ov[1]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          o[j] += __uint_as_float(ov[0][j]);
+          o[32 + j] += __uint_as_float(ov[1][j]);
+        }
+      }
+      // rescale the running output to the new max, then add this block later
+#pragma unroll
+      for (int j = 0; j < 64; ++j) o[j] *= alpha;
+      l_run = l_run * alpha + sum;
+      m_run = mx;
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.bar_p);
+    }
+    sm100::mbar_wait(&s.bar_o, (n_kb - 1) & 1);
+    sm100::tc_fence_after();
+    {
+      uint32_t ov[2][32];
+      sm100::tmem_ld_32x32b_x32(tmem + lane_base + 128, ov[0]);
+      sm100::tmem_ld_32x32b_x32(tmem + lane_base + 160, ov[1]);
+      sm100::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        o[j] += __uint_as_float(ov[0][j]);
+        o[32 + j] += __uint_as_float(ov[1][j]);
+      }
+    }
+    const float inv = 1.0f / l_run;
+    __nv_bfloat16* dst = ctx + ((size_t)row0 + qb * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        pk[e] = __floats2bfloat162_rn(o[c * 8 + 2 * e] * inv, o[c * 8 + 2 * e + 1] * inv);
+      *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pk);
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<256>(tmem);
+  }
+}
+
 // Last layer, [CLS] query only: the router head reads h_[CLS] alone, so after
 // the last QKV projection only the CLS row of every (sequence, head) needs
 // attention (all S keys/values). One warp per (sequence, head): 128 q.k dot
 // products (4 keys per lane), warp softmax in fp32, o = sum_j p_j v_j (2 dims
 // per lane). Memory bound: 32 KB of K/V per item.
 constexpr int kClsWarps = 8;
+template <int S>
 __global__ void __launch_bounds__(kClsWarps * 32)
     attention_cls_kernel(const __nv_bfloat16* __restrict__ qk, int n_items, int n_heads,
                          int hidden, __nv_bfloat16* __restrict__ ctx_c) {
+  constexpr int KPL = S / 32;  // keys per lane
   __shared__ float s_q[kClsWarps][64];
-  __shared__ float s_p[kClsWarps][kAttnS];
+  __shared__ float s_p[kClsWarps][S];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kClsWarps + w;
   if (item >= n_items) return;
   const int seq = item / n_heads, h = item - seq * n_heads;
   const size_t ld = 3 * (size_t)hidden;
   const __nv_bfloat162 q2 = *reinterpret_cast<const __nv_bfloat162*>(
-      qk + (size_t)seq * kAttnS * ld + h * 64 + 2 * lane);
+      qk + (size_t)seq * S * ld + h * 64 + 2 * lane);
   const float2 qf = __bfloat1622float2(q2);
   s_q[w][2 * lane] = qf.x;
   s_q[w][2 * lane + 1] = qf.y;
   __syncwarp();
-  float sc[4];
+  float sc[KPL];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < KPL; ++t) {
     const uint4* kp = reinterpret_cast<const uint4*>(
-        qk + ((size_t)seq * kAttnS + lane + 32 * t) * ld + hidden + h * 64);
+        qk + ((size_t)seq * S + lane + 32 * t) * ld + hidden + h * 64);
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -312,12 +506,14 @@ __global__ void __launch_bounds__(kClsWarps * 32)
     }
     sc[t] = acc;
   }
-  float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+  float mx = sc[0];
+#pragma unroll
+  for (int t = 1; t < KPL; ++t) mx = fmaxf(mx, sc[t]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float sum = 0.f;
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < KPL; ++t) {
     const float p = __expf(sc[t] - mx);
     s_p[w][lane + 32 * t] = p;
     sum += p;
@@ -328,10 +524,10 @@ __global__ void __launch_bounds__(kClsWarps * 32)
   const float inv = 1.0f / sum;
   // o[d] = sum_j p_j V[j][d]: lane owns d = 2*lane, 2*lane+1; each key row is
   // one coalesced 128-byte warp load
-  const __nv_bfloat16* vbase = qk + (size_t)seq * kAttnS * ld + 2 * hidden + h * 64 + 2 * lane;
+  const __nv_bfloat16* vbase = qk + (size_t)seq * S * ld + 2 * hidden + h * 64 + 2 * lane;
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll 8
-  for (int j = 0; j < kAttnS; ++j) {
+  for (int j = 0; j < S; ++j) {
     const float2 vf =
         __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vbase + (size_t)j * ld));
     const float p = s_p[w][j];
@@ -405,6 +601,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   if (!attr) {
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kAttnSmemBytes);
+    cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kAttnLongSmemBytes);
     attr = true;
   }
   const int NH = H / 64;
@@ -420,9 +618,14 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       auto* ctx_c = ctx;
       auto* xc = tmp;
       const int items = n_seq * NH;
+      const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
       prof::begin(prof::K_ATTENTION, st);
-      attention_cls_kernel<<<(unsigned)((items + kClsWarps - 1) / kClsWarps), kClsWarps * 32, 0,
-                             st>>>(qk, items, NH, H, ctx_c);
+      switch (S) {
+        case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
+        case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
+        case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
+        default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
+      }
       prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
       CHM_LAUNCH_CHECK();
       rc = gemm_bf16(ctx_c, w.w_o[l], xc, w.b_o[l], x, n_seq, H, H, 5, st, nullptr, 0, 0,
@@ -437,7 +640,11 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       break;
     }
     prof::begin(prof::K_ATTENTION, st);
-    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx);
+    if (S == kAttnS)
+      attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx);
+    else
+      attention_long_kernel<<<(unsigned)(n_seq * NH * (S / kAttnS)), 160, kAttnLongSmemBytes,
+                              st>>>(tm_qkv, NH, H, S, ctx);
     prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
     CHM_LAUNCH_CHECK();
     // out-projection + residual + LayerNorm fused (x updated in place)
@@ -472,7 +679,8 @@ extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
   if (!cfg || !w || !ws || !token_ids || !q_out) return CHM_ERR_INVALID_ARG;
   if (n_seq < 0) return CHM_ERR_INVALID_ARG;
   if (n_seq == 0) return CHM_OK;
-  if (seq_len != chm::enc::kAttnS || seq_len > cfg->max_pos) return CHM_ERR_UNSUPPORTED;
+  if (seq_len % chm::enc::kAttnS != 0 || seq_len > 512 || seq_len > cfg->max_pos)
+    return CHM_ERR_UNSUPPORTED;
   if (cfg->n_heads * 64 != cfg->hidden || cfg->n_models < 1 ||
       cfg->n_models > CHM_MAX_MODELS || cfg->ffn % 64 != 0)
     return CHM_ERR_INVALID_ARG;

@@ -9,17 +9,22 @@
 //
 // Device layout: engine m owns segment [m*cap, (m+1)*cap) of SoA arrays kept in
 // seq order, so "seq" comparisons are storage-index comparisons and a stable
-// sort over storage order needs no seq digits. One CTA per engine stages the
-// keys in shared memory and runs an LSD radix sort (8-bit digits, constant
-// digits skipped) by (count, level, priority[, arrival]). Entries with equal
-// count age in lock step, so each count group keeps its internal order for the
-// whole call: R iterations become R rounds of "admit the minimum of the group
-// heads, then shift each group's (count, level offset)". A final radix sort by
+// sort over storage order needs no seq digits. One CTA per engine runs an LSD
+// radix sort (8-bit digits, digits equal across the segment skipped) by
+// (count, level, priority[, arrival]). Entries with equal count age in lock
+// step, so each count group keeps its internal order for the whole call: R
+// iterations become R rounds of "admit the minimum of the group heads, then
+// shift each group's (count, level offset)". A final radix sort by
 // (level, priority[, arrival]) writes the STJF order of what remains.
 //
+// Key storage: segments up to kQMax entries keep the sort keys in shared
+// memory (16-bit indices); larger segments (the 64k-entry cfg4 stress) keep
+// them in a global scratch area (32-bit indices, L2 resident) with the same
+// algorithm -- chosen on the host from the segment capacity.
+//
 // HBM bytes per queued entry per call (algorithmic): read 40 (priority 8,
-// arrival 8, seq-implicit, handle 8, out_tokens 4, level 4, count 4, quantum 4)
-// + write 40 + order 4.
+// arrival 8, handle 8, out_tokens 4, level 4, count 4, quantum 4; seq is
+// implicit) + write 40 + order 4.
 #include "common.cuh"
 #include "prof.cuh"
 
@@ -29,21 +34,36 @@ constexpr int kQMax = 10240;       // entries per engine segment held in smem
 constexpr int kQThreads = 1024;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxGroups = 256;
-constexpr uint16_t kAdmitted = 0xffffu;
+constexpr uint32_t kAdmitted = 0xffffffffu;
+constexpr size_t kScratchBytesPerEntry = 8 + 2 + 2 + 4 + 4;  // prio, lvl, cnt, idx a/b
 
-struct QueueSmem {
-  unsigned long long prio[kQMax];  // order-preserving bits of priority
-  uint16_t lvl[kQMax];             // starvation_level + 32768
-  uint16_t cnt[kQMax];             // starvation_count
-  uint16_t idx_a[kQMax];
-  uint16_t idx_b[kQMax];
-  uint16_t wcnt[kQWarps][256];
+// Shared control state (both storage modes).
+struct QueueCtl {
+  int wcnt[kQWarps][256];
   int base[256];
   int g_start[kMaxGroups], g_end[kMaxGroups], g_cur[kMaxGroups];
   int g_count[kMaxGroups], g_lvloff[kMaxGroups];
   unsigned long long red_or[4], red_and[4];
   int scan[kQWarps];
   int misc[8];
+};
+
+template <typename Idx>
+struct Keys {
+  unsigned long long* prio;  // order-preserving bits of priority
+  uint16_t* lvl;             // starvation_level + 32768
+  uint16_t* cnt;             // starvation_count
+  Idx* a;
+  Idx* b;
+};
+
+// Small segments: keys right after the control block in shared memory.
+struct SmallKeysSmem {
+  unsigned long long prio[kQMax];
+  uint16_t lvl[kQMax];
+  uint16_t cnt[kQMax];
+  uint16_t a[kQMax];
+  uint16_t b[kQMax];
 };
 
 __device__ __forceinline__ unsigned long long f64_key(double x) {
@@ -54,15 +74,16 @@ __device__ __forceinline__ unsigned long long f64_key(double x) {
 
 // One stable LSD counting-sort pass over `n` indices.
 // src: 0 = arrival (global), 1 = priority, 2 = level, 3 = count; byte = digit index.
-__device__ void radix_pass(QueueSmem& s, const uint16_t* in, uint16_t* out, int n, int src,
-                           int byte, const double* __restrict__ arrival) {
+template <typename Idx>
+__device__ void radix_pass(QueueCtl& s, const Keys<Idx>& k, const Idx* in, Idx* out, int n,
+                           int src, int byte, const double* __restrict__ arrival) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto digit = [&](int e) -> int {
     unsigned long long v;
     if (src == 0) v = f64_key(arrival[e]);
-    else if (src == 1) v = s.prio[e];
-    else if (src == 2) v = s.lvl[e];
-    else v = s.cnt[e];
+    else if (src == 1) v = k.prio[e];
+    else if (src == 2) v = k.lvl[e];
+    else v = k.cnt[e];
     return (int)((v >> (8 * byte)) & 255ull);
   };
   for (int d = tid; d < 256; d += blockDim.x) s.base[d] = 0;
@@ -72,7 +93,7 @@ __device__ void radix_pass(QueueSmem& s, const uint16_t* in, uint16_t* out, int 
   if (warp == 0) {
     int v[8], tot = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { v[k] = s.base[lane * 8 + k]; tot += v[k]; }
+    for (int j = 0; j < 8; ++j) { v[j] = s.base[lane * 8 + j]; tot += v[j]; }
     int incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -81,81 +102,78 @@ __device__ void radix_pass(QueueSmem& s, const uint16_t* in, uint16_t* out, int 
     }
     int run = incl - tot;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { s.base[lane * 8 + k] = run; run += v[k]; }
+    for (int j = 0; j < 8; ++j) { s.base[lane * 8 + j] = run; run += v[j]; }
   }
   __syncthreads();
   for (int blk = 0; blk < n; blk += blockDim.x) {
     const int i = blk + tid;
     const bool valid = i < n;
-    const int e = valid ? in[i] : 0;
-    const int d = valid ? digit(e) : 256;
+    const Idx e = valid ? in[i] : (Idx)0;
+    const int d = valid ? digit((int)e) : 256;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s.wcnt[warp][lane * 8 + k] = 0;
+    for (int j = 0; j < 8; ++j) s.wcnt[warp][lane * 8 + j] = 0;
     __syncwarp();
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const int rank = __popc(peers & ((1u << lane) - 1u));
-    if (valid && rank == 0) s.wcnt[warp][d] = (uint16_t)__popc(peers);
+    if (valid && rank == 0) s.wcnt[warp][d] = __popc(peers);
     __syncthreads();
     if (tid < 256) {
       int run = s.base[tid];
 #pragma unroll 8
       for (int w = 0; w < kQWarps; ++w) {
         const int cnum = s.wcnt[w][tid];
-        s.wcnt[w][tid] = (uint16_t)(run & 0xffff);
+        s.wcnt[w][tid] = run;
         run += cnum;
       }
       s.base[tid] = run;
     }
     __syncthreads();
-    if (valid) {
-      // wcnt holds the low 16 bits of the destination base; n <= kQMax < 65536.
-      out[s.wcnt[warp][d] + rank] = (uint16_t)e;
-    }
+    if (valid) out[s.wcnt[warp][d] + rank] = e;
     __syncthreads();
   }
 }
 
 // Stable sort of [0, n) by the given key sources (most significant last in
 // `srcs`), skipping digits that are equal across all entries.
-__device__ void radix_sort(QueueSmem& s, int n, const int* srcs, int n_srcs,
-                           const double* __restrict__ arrival, bool use_arrival,
-                           uint16_t*& sorted, uint16_t*& spare) {
+template <typename Idx>
+__device__ void radix_sort(QueueCtl& s, const Keys<Idx>& k, int n, const int* srcs, int n_srcs,
+                           const double* __restrict__ arrival, bool use_arrival, Idx*& sorted,
+                           Idx*& spare) {
   const int tid = threadIdx.x;
   if (tid < 4) { s.red_or[tid] = 0ull; s.red_and[tid] = ~0ull; }
-  for (int i = tid; i < n; i += blockDim.x) s.idx_a[i] = (uint16_t)i;
+  for (int i = tid; i < n; i += blockDim.x) k.a[i] = (Idx)i;
   __syncthreads();
-  // Per-source OR / AND to find constant digits.
   unsigned long long o[4] = {0, 0, 0, 0}, a[4] = {~0ull, ~0ull, ~0ull, ~0ull};
   for (int i = tid; i < n; i += blockDim.x) {
-    unsigned long long v0 = use_arrival ? f64_key(arrival[i]) : 0ull;
+    const unsigned long long v0 = use_arrival ? f64_key(arrival[i]) : 0ull;
     o[0] |= v0; a[0] &= v0;
-    o[1] |= s.prio[i]; a[1] &= s.prio[i];
-    o[2] |= s.lvl[i]; a[2] &= s.lvl[i];
-    o[3] |= s.cnt[i]; a[3] &= s.cnt[i];
+    o[1] |= k.prio[i]; a[1] &= k.prio[i];
+    o[2] |= k.lvl[i]; a[2] &= k.lvl[i];
+    o[3] |= k.cnt[i]; a[3] &= k.cnt[i];
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int j = 0; j < 4; ++j) {
     for (int off = 16; off; off >>= 1) {
-      o[k] |= __shfl_xor_sync(0xffffffffu, o[k], off);
-      a[k] &= __shfl_xor_sync(0xffffffffu, a[k], off);
+      o[j] |= __shfl_xor_sync(0xffffffffu, o[j], off);
+      a[j] &= __shfl_xor_sync(0xffffffffu, a[j], off);
     }
   }
   if ((tid & 31) == 0) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) { atomicOr(&s.red_or[k], o[k]); atomicAnd(&s.red_and[k], a[k]); }
+    for (int j = 0; j < 4; ++j) { atomicOr(&s.red_or[j], o[j]); atomicAnd(&s.red_and[j], a[j]); }
   }
   __syncthreads();
-  uint16_t* in = s.idx_a;
-  uint16_t* out = s.idx_b;
-  for (int q = 0; q < n_srcs; ++q) {
-    const int src = srcs[q];
+  Idx* in = k.a;
+  Idx* out = k.b;
+  for (int qi = 0; qi < n_srcs; ++qi) {
+    const int src = srcs[qi];
     if (src == 0 && !use_arrival) continue;
     const int n_bytes = (src <= 1) ? 8 : 2;
     const unsigned long long diff = s.red_or[src] ^ s.red_and[src];
     for (int byte = 0; byte < n_bytes; ++byte) {
       if (((diff >> (8 * byte)) & 255ull) == 0) continue;
-      radix_pass(s, in, out, n, src, byte, arrival);
-      uint16_t* t = in; in = out; out = t;
+      radix_pass(s, k, in, out, n, src, byte, arrival);
+      Idx* t = in; in = out; out = t;
     }
   }
   sorted = in;
@@ -167,6 +185,7 @@ struct QueueParams {
   int b[CHM_MAX_MODELS];
   int aging_enabled;
   int S;
+  int cap_limit;  // largest segment this kernel variant can hold
 };
 
 // Lexicographic key of a group head: (level, priority, arrival?, storage idx).
@@ -187,16 +206,35 @@ __device__ __forceinline__ bool key_less(const HeadKey& x, const HeadKey& y) {
 
 // mode 0: completions (R = n_complete[m], each frees one running slot first)
 // mode 1: tick (append queued rows, then R = n_iterations explicit iterations)
+template <typename Idx, bool kBig>
 __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
     QueueParams prm, chm_monitor_state mon, chm_queue_state q, chm_rows rows,
     chm_decisions dec, const int32_t* __restrict__ n_complete, int n_iterations, int mode,
     int32_t* err) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  QueueSmem& s = *reinterpret_cast<QueueSmem*>(smem_raw);
+  QueueCtl& s = *reinterpret_cast<QueueCtl*>(smem_raw);
   const int m = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t seg = (size_t)m * q.capacity;
-  const int cap = min(q.capacity, kQMax);
+  const int cap = min(q.capacity, prm.cap_limit);
+  Keys<Idx> k;
+  if constexpr (kBig) {
+    uint8_t* base = reinterpret_cast<uint8_t*>(q.scratch) +
+                    (size_t)m * q.capacity * kScratchBytesPerEntry;
+    const size_t C = (size_t)q.capacity;
+    k.prio = reinterpret_cast<unsigned long long*>(base);
+    k.lvl = reinterpret_cast<uint16_t*>(base + 8 * C);
+    k.cnt = reinterpret_cast<uint16_t*>(base + 10 * C);
+    k.a = reinterpret_cast<Idx*>(base + 12 * C);
+    k.b = reinterpret_cast<Idx*>(base + 16 * C);
+  } else {
+    SmallKeysSmem& ks = *reinterpret_cast<SmallKeysSmem*>(smem_raw + sizeof(QueueCtl));
+    k.prio = ks.prio;
+    k.lvl = ks.lvl;
+    k.cnt = ks.cnt;
+    k.a = reinterpret_cast<Idx*>(ks.a);
+    k.b = reinterpret_cast<Idx*>(ks.b);
+  }
   double* prio_g = q.priority + seg;
   double* arr_g = q.arrival + seg;
   int64_t* seq_g = q.seq + seg;
@@ -214,24 +252,20 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   if (mode == 1) {
     const int n_rows = *dec.n_committed;
     // rows queued this batch were already counted in engine_queued by K6
-    int n_new_total = 0;
-    {
-      // count first
-      int c = 0;
-      for (int i = tid; i < n_rows; i += blockDim.x)
-        c += (dec.model[i] == m && (dec.flags[i] & 4u)) ? 1 : 0;
-      for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-      if (lane == 0) s.scan[warp] = c;
-      __syncthreads();
-      if (tid == 0) {
-        int t = 0;
-        for (int w = 0; w < kQWarps; ++w) t += s.scan[w];
-        s.misc[0] = t;
-      }
-      __syncthreads();
-      n_new_total = s.misc[0];
-      __syncthreads();
+    int c = 0;
+    for (int i = tid; i < n_rows; i += blockDim.x)
+      c += (dec.model[i] == m && (dec.flags[i] & 4u)) ? 1 : 0;
+    for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if (lane == 0) s.scan[warp] = c;
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < kQWarps; ++w) t += s.scan[w];
+      s.misc[0] = t;
     }
+    __syncthreads();
+    const int n_new_total = s.misc[0];
+    __syncthreads();
     const int n_old = n - n_new_total;
     if (n_old < 0 || n > cap) {
       if (tid == 0) report_error(err, n > cap ? CHM_ERR_CAPACITY : CHM_ERR_INVALID_STATE,
@@ -281,10 +315,9 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   // ---- stage keys ----
   int unsorted = 0;
   for (int i = tid; i < n; i += blockDim.x) {
-    s.prio[i] = f64_key(prio_g[i]);
-    const int lv = lvl_g[i];
-    s.lvl[i] = (uint16_t)(lv + 32768);
-    s.cnt[i] = (uint16_t)min(max(cnt_g[i], 0), 65535);
+    k.prio[i] = f64_key(prio_g[i]);
+    k.lvl[i] = (uint16_t)(lvl_g[i] + 32768);
+    k.cnt[i] = (uint16_t)min(max(cnt_g[i], 0), 65535);
     if (i > 0 && arr_g[i] < arr_g[i - 1]) unsorted = 1;
   }
   unsorted = __syncthreads_or(unsorted);
@@ -299,18 +332,17 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   if (R > 0) {
     // ---- sort by (count, level, priority[, arrival]) and form count groups ----
     const int srcs[4] = {0, 1, 2, 3};
-    uint16_t *sorted, *spare;
-    radix_sort(s, n, srcs, 4, arr_g, use_arr, sorted, spare);
+    Idx *sorted, *spare;
+    radix_sort(s, k, n, srcs, 4, arr_g, use_arr, sorted, spare);
     if (tid == 0) s.misc[2] = 0;
     __syncthreads();
-    // group boundaries: positions where count changes
     for (int p = tid; p < n; p += blockDim.x) {
-      const bool head = (p == 0) || s.cnt[sorted[p]] != s.cnt[sorted[p - 1]];
+      const bool head = (p == 0) || k.cnt[sorted[p]] != k.cnt[sorted[p - 1]];
       if (head) {
         const int g = atomicAdd(&s.misc[2], 1);
         if (g < kMaxGroups) {
           s.g_start[g] = p;
-          s.g_count[g] = s.cnt[sorted[p]];
+          s.g_count[g] = k.cnt[sorted[p]];
         }
       }
     }
@@ -351,26 +383,26 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
           best.g = -1;
           for (int g0 = 0; g0 < G; g0 += 32) {
             const int g = g0 + lane;
-            HeadKey k;
-            k.g = -1;
+            HeadKey hk;
+            hk.g = -1;
             if (g < G && s.g_cur[g] < s.g_end[g]) {
-              const int e = sorted[s.g_cur[g]];
-              k.e = e;
-              k.g = g;
-              k.lvl = (int)s.lvl[e] - 32768 + s.g_lvloff[g];
-              k.prio = s.prio[e];
-              k.arr = use_arr ? f64_key(arr_g[e]) : 0ull;
+              const int e = (int)sorted[s.g_cur[g]];
+              hk.e = e;
+              hk.g = g;
+              hk.lvl = (int)k.lvl[e] - 32768 + s.g_lvloff[g];
+              hk.prio = k.prio[e];
+              hk.arr = use_arr ? f64_key(arr_g[e]) : 0ull;
             }
             for (int off = 16; off; off >>= 1) {
               HeadKey o;
-              o.lvl = __shfl_xor_sync(0xffffffffu, k.lvl, off);
-              o.prio = __shfl_xor_sync(0xffffffffu, k.prio, off);
-              o.arr = __shfl_xor_sync(0xffffffffu, k.arr, off);
-              o.e = __shfl_xor_sync(0xffffffffu, k.e, off);
-              o.g = __shfl_xor_sync(0xffffffffu, k.g, off);
-              if (o.g >= 0 && (k.g < 0 || key_less(o, k))) k = o;
+              o.lvl = __shfl_xor_sync(0xffffffffu, hk.lvl, off);
+              o.prio = __shfl_xor_sync(0xffffffffu, hk.prio, off);
+              o.arr = __shfl_xor_sync(0xffffffffu, hk.arr, off);
+              o.e = __shfl_xor_sync(0xffffffffu, hk.e, off);
+              o.g = __shfl_xor_sync(0xffffffffu, hk.g, off);
+              if (o.g >= 0 && (hk.g < 0 || key_less(o, hk))) hk = o;
             }
-            if (k.g >= 0 && (best.g < 0 || key_less(k, best))) best = k;
+            if (hk.g >= 0 && (best.g < 0 || key_less(hk, best))) best = hk;
           }
           if (lane == 0) {
             q.admitted[seg + n_adm0 + n_adm] = handle_g[best.e];
@@ -410,8 +442,8 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
         const int mid = (lo + hi + 1) >> 1;
         if (s.g_start[mid] <= p) lo = mid; else hi = mid - 1;
       }
-      const int e = sorted[p];
-      spare[e] = (p < s.g_cur[lo]) ? kAdmitted : (uint16_t)lo;
+      const int e = (int)sorted[p];
+      spare[e] = (p < s.g_cur[lo]) ? (Idx)kAdmitted : (Idx)lo;
     }
     __syncthreads();
     // ---- compact survivors in seq (storage) order, applying the aging ----
@@ -419,18 +451,18 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
     for (int blk = 0; blk < n; blk += blockDim.x) {
       const int i = blk + tid;
       const bool valid = i < n;
-      const uint16_t g = valid ? spare[i] : kAdmitted;
-      const bool keep = valid && g != kAdmitted;
+      const Idx g = valid ? spare[i] : (Idx)kAdmitted;
+      const bool keep = valid && g != (Idx)kAdmitted;
       double pr = 0, ar = 0;
       int64_t sq = 0, hd = 0;
       int ot = 0, lv = 0, ct = 0, qn = 0;
       unsigned long long pk = 0;
       if (keep) {
         pr = prio_g[i]; ar = arr_g[i]; sq = seq_g[i]; hd = handle_g[i]; ot = out_g[i];
-        lv = (int)s.lvl[i] - 32768 + s.g_lvloff[g];
+        lv = (int)k.lvl[i] - 32768 + s.g_lvloff[g];
         ct = prm.aging_enabled ? s.g_count[g] : cnt_g[i];
         qn = (s.g_lvloff[g] != 0) ? 0 : qnt_g[i];
-        pk = s.prio[i];
+        pk = k.prio[i];
       }
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
       if (lane == 0) s.scan[warp] = __popc(bal);
@@ -449,9 +481,9 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
         const int pos = out_base + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
         prio_g[pos] = pr; arr_g[pos] = ar; seq_g[pos] = sq; handle_g[pos] = hd;
         out_g[pos] = ot; lvl_g[pos] = lv; cnt_g[pos] = ct; qnt_g[pos] = qn;
-        s.prio[pos] = pk;
-        s.lvl[pos] = (uint16_t)(lv + 32768);
-        s.cnt[pos] = (uint16_t)ct;
+        k.prio[pos] = pk;
+        k.lvl[pos] = (uint16_t)(lv + 32768);
+        k.cnt[pos] = (uint16_t)ct;
       }
       out_base += s.misc[6];
       __syncthreads();
@@ -466,9 +498,9 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
       if (arr_g[i] < arr_g[i - 1]) unsorted2 = 1;
     const bool ua = __syncthreads_or(unsorted2) != 0;
     const int srcs[3] = {0, 1, 2};
-    uint16_t *sorted, *spare;
-    radix_sort(s, n, srcs, 3, arr_g, ua, sorted, spare);
-    for (int r = tid; r < n; r += blockDim.x) q.order[seg + r] = sorted[r];
+    Idx *sorted, *spare;
+    radix_sort(s, k, n, srcs, 3, arr_g, ua, sorted, spare);
+    for (int r = tid; r < n; r += blockDim.x) q.order[seg + r] = (int32_t)sorted[r];
     if (tid == 0) q.arrival_unsorted[m] = ua ? 1 : 0;
   }
   if (tid == 0) {
@@ -491,20 +523,32 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   if (aging->enabled && (aging->starvation_threshold < 1 || aging->starvation_threshold > 65535))
     return CHM_ERR_UNSUPPORTED;
   if (aging->enabled && aging->demote_while_queued) return CHM_ERR_UNSUPPORTED;
+  const bool big = q->capacity > kQMax;
+  if (big && !q->scratch) return CHM_ERR_INVALID_ARG;
   QueueParams prm{};
   prm.K = K;
   for (int m = 0; m < K; ++m) prm.b[m] = pool->max_batch_size[m];
   prm.aging_enabled = aging->enabled;
   prm.S = aging->starvation_threshold;
+  prm.cap_limit = big ? 0x7fffffff : kQMax;
   chm_rows r{};
   chm_decisions d{};
   if (rows) r = *rows;
   if (dec) d = *dec;
-  const size_t smem = sizeof(QueueSmem);
-  cudaFuncSetAttribute(queue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   prof::begin(prof::K_QUEUE, s);
-  queue_kernel<<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete, n_iterations, mode,
-                                          err);
+  if (big) {
+    const size_t smem = sizeof(QueueCtl);
+    cudaFuncSetAttribute(queue_kernel<uint32_t, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    queue_kernel<uint32_t, true><<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete,
+                                                             n_iterations, mode, err);
+  } else {
+    const size_t smem = sizeof(QueueCtl) + sizeof(SmallKeysSmem);
+    cudaFuncSetAttribute(queue_kernel<uint16_t, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    queue_kernel<uint16_t, false><<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete,
+                                                              n_iterations, mode, err);
+  }
   prof::end(prof::K_QUEUE, s, 0.0);
   CHM_LAUNCH_CHECK();
   return CHM_OK;

@@ -93,6 +93,10 @@ class DeviceState:
         self.q_n_admitted = torch.zeros(K, dtype=i32, device=d)
         self.q_n_promoted = torch.zeros(K, dtype=i32, device=d)
         self.q_arrival_unsorted = torch.zeros(K, dtype=torch.uint8, device=d)
+        self.q_scratch = None
+        if C > _lib.QUEUE_SMEM_CAPACITY:
+            self.q_scratch = torch.empty(n * _lib.QUEUE_SCRATCH_BYTES_PER_ENTRY,
+                                         dtype=torch.uint8, device=d)
         self.pool_c = _lib.Pool()
         self.pool_c.n_models = K
         for i, mid in enumerate(self.ids):
@@ -108,7 +112,7 @@ class DeviceState:
             _ptr(self.q_handle), _ptr(self.q_out_tokens), _ptr(self.q_level),
             _ptr(self.q_count), _ptr(self.q_quantum), _ptr(self.q_order),
             _ptr(self.q_admitted), _ptr(self.q_n_admitted), _ptr(self.q_n_promoted),
-            _ptr(self.q_arrival_unsorted))
+            _ptr(self.q_arrival_unsorted), _ptr(self.q_scratch))
 
     # -- host-side setup (not on the tick path) ------------------------------
     def seed_inflight(self, per_model_values: dict[str, list[float]]) -> None:

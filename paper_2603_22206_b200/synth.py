@@ -61,6 +61,11 @@ SPECS = {
                          "bursty arrival trace, 64k in-flight requests, 8 engines, "
                          "STJF+aging sort stress", n_pre_queued=65536, n_pre_inflight=65536,
                          bursts=16),
+    # cfg5 is quoted for 8 GPUs (16k requests/tick); per GPU that is 2048
+    "cfg5": WorkloadSpec("cfg5", 5, 2048, EncoderConfig(seq_len=512), W.MATH_WORKFLOWS,
+                         MATH, MATH_SUCCESS,
+                         "long-prompt router inputs (seq 512), 2048 requests/tick per GPU "
+                         "(16k over 8 B200), NCCL in-flight all-reduce"),
     "smoke": WorkloadSpec("smoke", 3, 64, SMALL, W.MATH_WORKFLOWS, MATH, MATH_SUCCESS,
                           "smoke: 64 requests, 3 models, small router"),
 }
@@ -139,6 +144,47 @@ class Workload:
         cols = dict(self.host_columns(tick))
         cols.pop("records")
         return RowBatch.from_numpy(self.device, **cols)
+
+    @property
+    def queue_capacity(self) -> int:
+        sp = self.spec
+        if not sp.n_pre_queued:
+            return 10240
+        per = sp.n_pre_queued // sp.n_models
+        return 1 << int(np.ceil(np.log2(per + sp.batch)))
+
+    def seed_state(self, state, seed: int = 7) -> None:
+        """cfg4: pre-existing in-flight predictions and pre-queued entries
+        (integer lognormal predictions from the MATH stats), engines running
+        full, so each tick exercises completions, admission and aging at scale."""
+        sp = self.spec
+        if not (sp.n_pre_queued or sp.n_pre_inflight):
+            return
+        rng = np.random.default_rng(seed)
+        K = sp.n_models
+        ids = self.pool.model_ids
+        mu, sigma = np.log(650.0) - 0.5, 1.0
+        if sp.n_pre_inflight:
+            owner = rng.integers(0, K, sp.n_pre_inflight)
+            vals = np.maximum(1, np.round(rng.lognormal(mu, sigma, sp.n_pre_inflight)))
+            state.seed_inflight({ids[m]: vals[owner == m].tolist() for m in range(K)})
+        per = sp.n_pre_queued // K
+        for m in range(K):
+            prio = np.maximum(1, np.round(rng.lognormal(mu, sigma, per)))
+            arr = np.sort(rng.random(per) * 900.0)
+            state.load_queue(m, prio, arr, np.arange(per), np.arange(per) + (m << 40),
+                             out_tokens=rng.integers(1, 2000, per),
+                             count=rng.integers(0, int(self.aging.starvation_threshold), per))
+        state.set_engine_counters(
+            running=[self.pool[i].max_batch_size for i in ids],
+            seq=[per] * K, clock=[900.0] * K)
+
+    def completions(self):
+        """cfg4: every engine's running batch turns over once per tick."""
+        if not self.spec.n_pre_queued:
+            return None
+        return torch.tensor([self.pool[m].max_batch_size for m in self.pool.model_ids],
+                            dtype=torch.int32, device=self.device)
 
     def router_reference(self, batch: RowBatch) -> np.ndarray:
         from oracle.encoder_ref import encoder_forward_fp32  # test infrastructure

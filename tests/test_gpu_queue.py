@@ -67,10 +67,11 @@ def replay_on_gpu(qd, capacity=10240):
     )
 
 
+@pytest.mark.parametrize("capacity", [10240, 20480])  # smem keys / global-scratch keys
 @pytest.mark.parametrize("name", H.queue_names())
-def test_queue_matches_reference(name):
+def test_queue_matches_reference(name, capacity):
     qd = H.load_queue(name)
-    res = replay_on_gpu(qd)
+    res = replay_on_gpu(qd, capacity)
     np.testing.assert_array_equal(res["admitted"], qd["admitted"])
     np.testing.assert_array_equal(res["order"], qd["order"])
     np.testing.assert_array_equal(res["level"], qd["level"])
@@ -79,13 +80,14 @@ def test_queue_matches_reference(name):
     assert res["iterations"] == qd["iterations"]
 
 
-def test_queue_order_random_large():
-    """Full-size STJF order vs a numpy lexsort of (level, priority, arrival, seq)."""
+@pytest.mark.parametrize("n,capacity", [(9000, 10240), (70000, 72000)])
+def test_queue_order_random_large(n, capacity):
+    """Full-size STJF order vs a numpy lexsort of (level, priority, arrival, seq);
+    70k entries per engine exercises the global-scratch path (cfg4 stress)."""
     rng = np.random.default_rng(5)
-    n = 9000
     pool = Pool((ModelProfile("m0", 1.0, 4), ModelProfile("m1", 2.0, 4)))
     gs = GpuScheduler(pool, router=ScoreTableRouter(), predictor=PrecomputedPredictor(),
-                      n_programs=16, max_rows=16, queue_capacity=10240)
+                      n_programs=16, max_rows=16, queue_capacity=capacity)
     st = gs.state
     for m in range(2):
         prio = rng.lognormal(5, 2, n)

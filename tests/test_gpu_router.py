@@ -98,6 +98,21 @@ def test_encoder_matches_fp32(cfg, head_std):
     assert np.all((got >= 0) & (got <= 1))
 
 
+@pytest.mark.parametrize("S", [256, 512])
+def test_encoder_long_prompts(S):
+    """S > 128: flash-style key-block loop with online softmax (cfg5 S=512)."""
+    from dataclasses import replace
+    cfg = replace(SMALL, seq_len=S)
+    K, B = 5, 6
+    r = GpuEncoderRouter(cfg, K, max_rows=B, seed=8, head_std=2 / math.sqrt(256))
+    ids = torch.as_tensor(synthetic_token_ids(B, S, seed=21), device="cuda")
+    q = torch.zeros(B * K, dtype=torch.float32, device="cuda")
+    r.forward(ids, q)
+    torch.cuda.synchronize()
+    err = np.abs(q.view(B, K).cpu().numpy() - _ref_q(r, ids)).max()
+    assert err <= Q_TOL, err
+
+
 def test_encoder_routed_rows_only():
     """Only rows listed in route_rows[:n_route] are written (balancer.py:104-114)."""
     K, B = 3, 16
