@@ -74,9 +74,16 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 
 
 class ClockSampler:
+    """nvidia-smi clock / throttle-reason samples every 100 ms. Started before
+    the warm-up so it is already sampling when the timed region opens; stop()
+    keeps the samples whose host timestamp falls inside the timed window
+    (mark_start / mark_end), or -- for timed regions shorter than the sampling
+    period -- the samples nearest to it, and says which."""
+
     def __init__(self, index: int, enabled: bool):
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
         if not enabled:
             return
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -84,13 +91,23 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        if self.proc is not None and self.t1 - self.t0 < 0.25:
+            time.sleep(0.25)  # let the sample after the window land
+
     def stop(self):
+        import datetime
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -98,23 +115,32 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        rows = []
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 4:
+            if len(parts) < 5:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                bits = int(parts[3], 16)
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), int(parts[4], 16)))
             except ValueError:
                 continue
-            for b, name in REASON_BITS.items():
-                if bits & b and name != "gpu_idle":
-                    reasons.add(name)
-        if not sm:
+        if not rows:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+        window = "timed"
+        sel = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        if not sel and self.t0 is not None:
+            # timed region shorter than the sampling period: nearest samples
+            mid = 0.5 * (self.t0 + self.t1)
+            sel = sorted(rows, key=lambda r: abs(r[0] - mid))[:2]
+            window = "nearest to the timed region (shorter than the 100 ms period)"
+        reasons = set()
+        for r in sel:
+            for b, name in REASON_BITS.items():
+                if r[3] & b and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[1] for r in sel),
+                "sm_max_mhz": max(r[2] for r in sel), "samples": len(sel), "window": window,
                 "reasons": sorted(reasons)}
 
 
@@ -315,6 +341,7 @@ def run_ours(args):
         gs.state.restore(snap)
         sched.run_rows(src, n_iterations=1, n_complete=n_complete, stream=stream)
 
+    clocks = ClockSampler(local, not args.no_clocks)
     for i in range(args.warmup):
         tick(i)
     torch.cuda.synchronize()
@@ -325,7 +352,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local, not args.no_clocks)
+    clocks.mark_start()
     _lib.profile_read()  # reset timings
     _lib.profile_enable(graph is None)
     launches0 = _lib.profile_read()
@@ -339,6 +366,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    clocks.mark_end()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     clk = clocks.stop()
