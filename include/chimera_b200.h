@@ -157,7 +157,13 @@ typedef struct chm_queue_state {
 typedef struct chm_encoder_cfg {
   int32_t n_layers, hidden, n_heads, ffn, vocab, max_pos, n_models;
   float ln_eps;
+  int32_t flags;  /* CHM_ENC_* */
 } chm_encoder_cfg;
+
+/* chm_encoder_cfg.flags: run the QKV projection and attention as two kernels
+ * (QKV written to HBM) instead of the fused S = 128 kernel. Same numerics;
+ * kept for A/B measurement and parity tests. */
+#define CHM_ENC_UNFUSED_ATTENTION 1
 
 /* bf16 weights, row-major [out_features, in_features] (nn.Linear layout). */
 typedef struct chm_encoder_weights {
@@ -272,6 +278,20 @@ chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bia
 chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, const float* bias,
                             const void* residual, const float* gamma, const float* beta,
                             float eps, int32_t M, int32_t N, int32_t K, void* stream);
+
+/* Encoder self-attention sublayer core (no mask, head dim 64), the kernel the
+ * encoder runs between its QKV projection and out-projection:
+ *   ctx[t, h*64:(h+1)*64] = softmax(Q_h K_h^T) V_h  per sequence,
+ * qkv = [n_seq*seq_len, 3*hidden] bf16 with Q pre-scaled by 1/8, ctx =
+ * [n_seq*seq_len, hidden] bf16. seq_len % 128 == 0, <= 512. */
+chm_status chm_attention_bf16(const void* qkv, void* ctx, int32_t n_seq, int32_t seq_len,
+                              int32_t hidden, void* stream);
+
+/* Fused QKV projection + attention (S = 128 only): ctx as chm_attention_bf16
+ * of qkv = x . w_qkv^T + b_qkv (Q columns scaled by 1/8), without writing qkv
+ * to HBM. x = [n_seq*128, hidden] bf16, w_qkv = [3*hidden, hidden] bf16. */
+chm_status chm_qkv_attention_bf16(const void* x, const void* w_qkv, const float* b_qkv,
+                                  void* ctx, int32_t n_seq, int32_t hidden, void* stream);
 
 /* Profiling: launch counters per kernel class (always on) and opt-in CUDA
  * event timing around every launch on its own stream. Classes: 0 GEMM,

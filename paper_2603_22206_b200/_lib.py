@@ -144,7 +144,11 @@ class EncoderCfg(ctypes.Structure):
         ("max_pos", c_int32),
         ("n_models", c_int32),
         ("ln_eps", c_float),
+        ("flags", c_int32),
     ]
+
+
+ENC_UNFUSED_ATTENTION = 1
 
 
 class EncoderWeights(ctypes.Structure):
@@ -212,6 +216,10 @@ _SIGNATURES = [
     ("chm_gemm_bf16_ln", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_int32,
       c_int32, c_int32, c_void_p]),
+    ("chm_attention_bf16", c_int32,
+     [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p]),
+    ("chm_qkv_attention_bf16", c_int32,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
     ("chm_profile_enable", c_int32, [c_int32]),
     ("chm_profile_read", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]

@@ -20,6 +20,8 @@ chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                      const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
                      void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
                      float eps, long long res_ld = 0);
+chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv, void* ctx,
+                         int n_seq, int hidden, cudaStream_t st);
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, uint64_t ld);
@@ -463,6 +465,252 @@ __global__ void __launch_bounds__(160, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 attention for S = 256 n (cfg5 S = 512): persistent, one CTA per SM.
+// An item is (sequence, head, 256-query chunk) = two 128-query tiles that
+// share every K/V block, so each K/V block is loaded once for 256 queries.
+//   warp 0      TMA: Q (double-buffered across items), K/V ring of 2 blocks
+//   warp 1      MMA issuer, ping-pong over the two tiles:
+//                 S0(0) S1(0) | O0(j) S0(j+1) | O1(j) S1(j+1) | ...
+//               so the tensor pipe works on one tile while the other tile's
+//               softmax runs (j = flat (item, key block) index)
+//   warps 4-7   online softmax of tile 0, warps 8-11 of tile 1 (thread =
+//               query row; warp w reads TMEM lanes 32(w%4)..+31)
+// TMEM: S_g in cols [128g, 128g+128), O_blk,g in [256+64g, 256+64g+64).
+// The running output o (64 fp32 per row) and (m, l) live in registers; each
+// block's O_blk = P V is folded in after the next block's P is written.
+// ---------------------------------------------------------------------------
+constexpr int kFlashThreads = 384;
+struct FlashSmem {
+  uint8_t q[2][2][kAttnS * 64 * 2];   // [item parity][tile] Q [128][64] SW128
+  uint8_t kv[2][2][kAttnS * 64 * 2];  // [stage][K | V] [128 keys][64]
+  uint8_t p[2][2][kAttnS * 64 * 2];   // [tile][key half] P [128 rows][64 keys]
+  uint64_t q_full[2], q_empty[2], kv_full[2], kv_empty[2];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kFlashSmemBytes = sizeof(FlashSmem) + 1024;
+
+__global__ void __launch_bounds__(kFlashThreads, 1)
+    attention_flash_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
+                           int S, int n_items, __nv_bfloat16* __restrict__ ctx) {
+  extern __shared__ uint8_t smem_raw[];
+  FlashSmem& s = *reinterpret_cast<FlashSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_kb = S / kAttnS;
+  const int n_qp = S / (2 * kAttnS);
+  constexpr uint32_t kTile = kAttnS * 64 * 2;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s.q_full[i], 1);
+      sm100::mbar_init(&s.q_empty[i], 1);
+      sm100::mbar_init(&s.kv_full[i], 1);
+      sm100::mbar_init(&s.kv_empty[i], 1);
+      sm100::mbar_init(&s.s_full[i], 1);
+      sm100::mbar_init(&s.p_full[i], 128);
+      sm100::mbar_init(&s.o_full[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t kv_phase = 0;
+      for (int it = 0; it < n_my; ++it) {
+        const int item = (int)blockIdx.x + it * (int)gridDim.x;
+        const int qp = item % n_qp, sh = item / n_qp;
+        const int seq = sh / n_heads, h = sh - seq * n_heads;
+        const int row0 = seq * S;
+        const int qb = it & 1;
+        sm100::mbar_wait(&s.q_empty[qb], ((it >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&s.q_full[qb], 2 * kTile);
+        sm100::tma_load_2d(s.q[qb][0], &tm_qkv, &s.q_full[qb], h * 64, row0 + qp * 256);
+        sm100::tma_load_2d(s.q[qb][1], &tm_qkv, &s.q_full[qb], h * 64, row0 + qp * 256 + 128);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          sm100::mbar_wait(&s.kv_empty[stage], kv_phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&s.kv_full[stage], 2 * kTile);
+          sm100::tma_load_2d(s.kv[stage][0], &tm_qkv, &s.kv_full[stage], hidden + h * 64,
+                             row0 + kb * kAttnS);
+          sm100::tma_load_2d(s.kv[stage][1], &tm_qkv, &s.kv_full[stage], 2 * hidden + h * 64,
+                             row0 + kb * kAttnS);
+          if (++stage == 2) { stage = 0; kv_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
+      constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
+      const int J = n_my * n_kb;
+      auto issue_s = [&](int g, int j) {
+        const int it = j / n_kb, kb = j - it * n_kb;
+        const int qb = it & 1, stage = j & 1;
+        if (g == 0) {
+          if (kb == 0) sm100::mbar_wait(&s.q_full[qb], (it >> 1) & 1);
+          sm100::mbar_wait(&s.kv_full[stage], (j >> 1) & 1);
+        }
+        // S_g columns are free once softmax g has consumed S_g(j-1)
+        if (j > 0) sm100::mbar_wait(&s.p_full[g], (j - 1) & 1);
+        sm100::tc_fence_after();
+        const uint32_t qa = sm100::smem_u32(s.q[qb][g]), ka = sm100::smem_u32(s.kv[stage][0]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          sm100::mma_bf16(tmem + 128 * g, sm100::umma_desc_sw128(qa + k * 32),
+                          sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+        sm100::mma_commit(&s.s_full[g]);
+        if (g == 1 && kb == n_kb - 1) sm100::mma_commit(&s.q_empty[qb]);
+      };
+      auto issue_o = [&](int g, int j) {
+        const int stage = j & 1;
+        sm100::mbar_wait(&s.p_full[g], j & 1);
+        sm100::tc_fence_after();
+        const uint32_t va = sm100::smem_u32(s.kv[stage][1]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t pa = sm100::smem_u32(s.p[g][kk >> 2]) + (kk & 3) * 32;
+          sm100::mma_bf16(tmem + 256 + 64 * g, sm100::umma_desc_sw128(pa),
+                          sm100::umma_desc_sw128(va + kk * 2048), idesc_o, kk);
+        }
+        sm100::mma_commit(&s.o_full[g]);
+        if (g == 1) sm100::mma_commit(&s.kv_empty[stage]);
+      };
+      if (J > 0) {
+        issue_s(0, 0);
+        issue_s(1, 0);
+      }
+      for (int j = 0; j < J; ++j) {
+        issue_o(0, j);
+        if (j + 1 < J) issue_s(0, j + 1);
+        issue_o(1, j);
+        if (j + 1 < J) issue_s(1, j + 1);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------- online softmax, tile g ----------------
+    const int g = (warp - 4) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_tm = tmem + lane_base + 128 * g;
+    const uint32_t o_tm = tmem + lane_base + 256 + 64 * g;
+    constexpr float kLog2e = 1.4426950408889634f;
+    int j = 0;
+    for (int it = 0; it < n_my; ++it) {
+      const int item = (int)blockIdx.x + it * (int)gridDim.x;
+      const int qp = item % n_qp, sh = item / n_qp;
+      const int seq = sh / n_heads, h = sh - seq * n_heads;
+      float m_run = -INFINITY, l_run = 0.f;
+      float o[64];
+#pragma unroll
+      for (int e = 0; e < 64; ++e) o[e] = 0.f;
+      for (int kb = 0; kb < n_kb; ++kb, ++j) {
+        sm100::mbar_wait(&s.s_full[g], j & 1);
+        sm100::tc_fence_after();
+        float mx = m_run;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          sm100::tmem_ld_32x32b_x32(s_tm + c * 32, raw);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(raw[e]));
+        }
+        const float alpha = sm100::ex2_approx((m_run - mx) * kLog2e);  // 0 on the first block
+        const float mxl = mx * kLog2e;
+        float sum = 0.f;
+        // P_g of the previous block is free once its P.V MMA completed
+        if (kb > 0) {
+          sm100::mbar_wait(&s.o_full[g], (j - 1) & 1);
+          sm100::tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          sm100::tmem_ld_32x32b_x32(s_tm + c * 32, raw);
+          sm100::tmem_ld_wait();
+          uint8_t* rowp = s.p[g][c >> 1] + r * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            __align__(16) __nv_bfloat162 pv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float p0 = sm100::ex2_approx(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
+              const float p1 = sm100::ex2_approx(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
+              pv[e] = __floats2bfloat162_rn(p0, p1);
+              const float2 back = __bfloat1622float2(pv[e]);
+              sum += back.x + back.y;
+            }
+            const int chunk = (c & 1) * 4 + q4;
+            *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
+                *reinterpret_cast<uint4*>(pv);
+          }
+        }
+        if (kb > 0) {
+          uint32_t ov[2][32];
+          sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+          sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            o[e] += __uint_as_float(ov[0][e]);
+            o[32 + e] += __uint_as_float(ov[1][e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 64; ++e) o[e] *= alpha;
+        l_run = l_run * alpha + sum;
+        m_run = mx;
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.p_full[g]);
+      }
+      sm100::mbar_wait(&s.o_full[g], (j - 1) & 1);
+      sm100::tc_fence_after();
+      {
+        uint32_t ov[2][32];
+        sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+        sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          o[e] += __uint_as_float(ov[0][e]);
+          o[32 + e] += __uint_as_float(ov[1][e]);
+        }
+      }
+      sm100::tc_fence_before();
+      const float inv = 1.0f / l_run;
+      __nv_bfloat16* dst =
+          ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          pk[e] = __floats2bfloat162_rn(o[c * 8 + 2 * e] * inv, o[c * 8 + 2 * e + 1] * inv);
+        *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pk);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
 // Last layer, [CLS] query only: the router head reads h_[CLS] alone, so after
 // the last QKV projection only the CLS row of every (sequence, head) needs
 // attention (all S keys/values). One warp per (sequence, head): 128 q.k dot
@@ -572,6 +820,51 @@ __global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restri
   }
 }
 
+static int n_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// ctx = attention(qkv) for n_seq sequences of S tokens (S % 128 == 0, <= 512).
+chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq, int S, int H,
+                         cudaStream_t st) {
+  const long long T = (long long)n_seq * S;
+  CUtensorMap tm_qkv;
+  if (!gemm::make_tmap_bf16(&tm_qkv, qk, (uint64_t)T, (uint64_t)3 * H, 128, 64, 0))
+    return CHM_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kAttnSmemBytes);
+    cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kAttnLongSmemBytes);
+    cudaFuncSetAttribute(attention_flash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kFlashSmemBytes);
+    attr = true;
+  }
+  const int NH = H / 64;
+  prof::begin(prof::K_ATTENTION, st);
+  if (S == kAttnS) {
+    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx);
+  } else if (S % (2 * kAttnS) == 0) {
+    const int items = n_seq * NH * (S / (2 * kAttnS));
+    const unsigned grid = (unsigned)(items < n_sms() ? items : n_sms());
+    attention_flash_kernel<<<grid, kFlashThreads, kFlashSmemBytes, st>>>(tm_qkv, NH, H, S,
+                                                                         items, ctx);
+  } else {
+    attention_long_kernel<<<(unsigned)(n_seq * NH * (S / kAttnS)), 160, kAttnLongSmemBytes,
+                            st>>>(tm_qkv, NH, H, S, ctx);
+  }
+  prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
 template <int VEC>
 static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weights& w,
                               const chm_encoder_workspace& ws, const int32_t* ids,
@@ -594,23 +887,19 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       reinterpret_cast<const __nv_bfloat16*>(w.type_emb), w.emb_ln_g, w.emb_ln_b, cfg.ln_eps, x);
   prof::end(prof::K_ROWWISE, st, (double)T * (4.0 + 6.0 * H));
   CHM_LAUNCH_CHECK();
-  CUtensorMap tm_qkv;
-  if (!gemm::make_tmap_bf16(&tm_qkv, qk, (uint64_t)T, (uint64_t)3 * H, 128, 64, 0))
-    return CHM_ERR_CUDA;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kAttnSmemBytes);
-    cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kAttnLongSmemBytes);
-    attr = true;
-  }
   const int NH = H / 64;
   chm_status rc;
+  const bool fused = S == kAttnS && !(cfg.flags & CHM_ENC_UNFUSED_ATTENTION);
   for (int l = 0; l < L; ++l) {
-    rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, nullptr, H,
-                   S, nullptr, nullptr, 0.f);
-    if (rc != CHM_OK) return rc;
+    if (fused && l < L - 1) {
+      // QKV projection + attention in one kernel (qkv_attn.cu)
+      rc = qkv_attention(x, w.w_qkv[l], w.b_qkv[l], ctx, n_seq, H, st);
+      if (rc != CHM_OK) return rc;
+    } else {
+      rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, nullptr,
+                     H, S, nullptr, nullptr, 0.f);
+      if (rc != CHM_OK) return rc;
+    }
     if (l == L - 1) {
       // Last layer: only h_[CLS] reaches the router head, so attention runs
       // for the CLS query of every (sequence, head) and the rest of the layer
@@ -639,14 +928,10 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       if (rc != CHM_OK) return rc;
       break;
     }
-    prof::begin(prof::K_ATTENTION, st);
-    if (S == kAttnS)
-      attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx);
-    else
-      attention_long_kernel<<<(unsigned)(n_seq * NH * (S / kAttnS)), 160, kAttnLongSmemBytes,
-                              st>>>(tm_qkv, NH, H, S, ctx);
-    prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
-    CHM_LAUNCH_CHECK();
+    if (!fused) {
+      rc = run_attention(qk, ctx, n_seq, S, H, st);
+      if (rc != CHM_OK) return rc;
+    }
     // out-projection + residual + LayerNorm fused (x updated in place)
     rc = gemm_bf16(ctx, w.w_o[l], x, w.b_o[l], x, (int)T, H, H, 5, st, nullptr, 0, 0,
                    w.ln1_g[l], w.ln1_b[l], cfg.ln_eps);
@@ -702,4 +987,14 @@ extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
     default:
       return CHM_ERR_UNSUPPORTED;
   }
+}
+
+extern "C" chm_status chm_attention_bf16(const void* qkv, void* ctx, int32_t n_seq,
+                                         int32_t seq_len, int32_t hidden, void* stream) {
+  if (!qkv || !ctx || n_seq < 0 || hidden <= 0 || hidden % 64 != 0) return CHM_ERR_INVALID_ARG;
+  if (seq_len <= 0 || seq_len % chm::enc::kAttnS != 0 || seq_len > 512) return CHM_ERR_UNSUPPORTED;
+  if (n_seq == 0) return CHM_OK;
+  return chm::enc::run_attention(reinterpret_cast<const __nv_bfloat16*>(qkv),
+                                 reinterpret_cast<__nv_bfloat16*>(ctx), n_seq, seq_len, hidden,
+                                 (cudaStream_t)stream);
 }

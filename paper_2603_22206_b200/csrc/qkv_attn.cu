@@ -1,0 +1,464 @@
+// K2+K3 fused: QKV projection + self-attention for S = 128 (the headline
+// router shape), one pass, Q/K/V never written to HBM.
+//
+// An item is one (sequence, head): its 128 tokens are one MMA M tile, so the
+// projection of that head is a 128 x 192 x H GEMM (rows = tokens, columns =
+// the head's 64 Q + 64 K + 64 V output features of W_qkv), and its attention
+// consumes the result straight from tensor memory.
+//
+// Operand traffic: a lone CTA would stream 40 KB (x 16 KB + W 24 KB) from L2
+// per 384 tensor cycles, ~2x what L2 can deliver to every SM at once. CTAs
+// are therefore grouped in clusters of CS sequences x CH heads: the CH CTAs
+// of one sequence share its x tile and the CS CTAs of one head share its W
+// tile, each CTA loading a 1/CH slice of x and a 1/CS slice of W and
+// multicasting it to the sharers (TMA .multicast::cluster). Stage reuse is
+// released cluster-wide: each CTA's MMA commit arrives on the "empty"
+// barrier of every CTA that writes into its stages (tcgen05.commit multicast).
+//
+//   warp 0      TMA producer: 4-stage ring of x[128 x 64] + W[192 x 64]
+//   warp 1      MMA issuer (one thread). GEMM(i+1) is issued while item i's
+//               attention runs: between k-blocks of GEMM(i+1) it polls
+//               (mbarrier test_wait) for "Q/K/V of item i staged" and
+//               "P of item i written" and slots S(i) = Q K^T and O(i) = P V
+//               into the tensor pipe as soon as they are ready
+//   warps 2-9   epilogue, 2 threads per token row (column halves hf = 0/1):
+//               (1) acc(i) + bias -> bf16 Q (x 1/8), K, V tiles in smem
+//                   (128B swizzle, the UMMA operand layout), accumulator freed
+//               (2) softmax of S(i) (row max / sum exchanged between the two
+//                   halves through smem), P bf16 over the Q|K tiles
+//               (3) O(i) / rowsum -> ctx (bf16, HBM)
+//
+// TMEM (512 columns): accumulators acc[0] = [0,192), acc[1] = [192,384)
+// (double-buffered across items), S = [384,512), O = [384,448) (after S is
+// consumed). Numerics equal the unfused path (chm_gemm QKV epilogue + K3):
+// fp32 accumulation, bias in fp32, bf16 Q/K/V, exp2-based softmax with the
+// normaliser summed over the bf16-rounded P.
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "prof.cuh"
+#include "sm100.cuh"
+
+namespace chm {
+namespace gemm {
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
+                    uint32_t box_rows, uint32_t box_cols, uint64_t ld);
+}
+namespace qa {
+
+constexpr int kS = 128;                        // tokens per sequence = MMA M
+constexpr int kStages = 4;
+constexpr int kThreads = 320;                  // 10 warps
+constexpr uint32_t kATile = kS * 64 * 2;       // x   [128][64] bf16, 16 KB
+constexpr uint32_t kBTile = 192 * 64 * 2;      // W   [192][64] (Q | K | V rows), 24 KB
+constexpr uint32_t kStageBytes = kATile + kBTile;  // 40 KB
+constexpr uint32_t kWBox = 32;                 // W rows per TMA box (6 per head)
+constexpr uint32_t kHeadTile = kS * 64 * 2;    // Q/K/V [128][64] bf16, 16 KB
+constexpr uint32_t kAccCols = 192;
+constexpr uint32_t kSCol = 384;
+
+struct __align__(1024) Smem {
+  uint8_t stages[kStages][kStageBytes];
+  uint8_t qkv[3][kHeadTile];  // Q, K, V; P key halves [0,64) / [64,128) overwrite Q / K
+  float red_max[2][kS];
+  float red_sum[2][kS];
+  uint64_t full[kStages], empty[kStages], kdone[kStages];
+  uint64_t acc_full[2], acc_empty[2];
+  uint64_t qkv_ready, s_full, p_ready, o_full;
+  uint32_t tmem_base;
+};
+constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void epi_sync() {
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+// Cluster items: (group of CS sequences) x (group of CH heads). CTA (i, j) of
+// the cluster (rank = i*CH + j) owns sequence sg*CS + i, head hg*CH + j.
+// lag > 0: the MMA issuer keeps at most `lag` projection k-blocks queued on
+// the tensor pipe, so S(i) / O(i) slotted between them start soon.
+template <int CS, int CH>
+__global__ void __launch_bounds__(kThreads, 1)
+    qkv_attention_kernel(const __grid_constant__ CUtensorMap tm_x,
+                         const __grid_constant__ CUtensorMap tm_w,
+                         const float* __restrict__ b_qkv, int n_seq, int n_heads, int hidden,
+                         __nv_bfloat16* __restrict__ ctx, int lag, int dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                     ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k_blocks = hidden / 64;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const int ci = (int)rank / CH, cj = (int)rank % CH;
+  const uint16_t row_mask = (uint16_t)(((1u << CH) - 1) << (ci * CH));  // same sequence
+  uint16_t col_mask = 0;                                                 // same head
+#pragma unroll
+  for (int i = 0; i < CS; ++i) col_mask |= (uint16_t)(1u << (i * CH + cj));
+  const int head_groups = n_heads / CH;
+  const int n_citems = ((n_seq + CS - 1) / CS) * head_groups;
+  const int cl = (int)sm100::cluster_id_x(), n_cl = (int)sm100::n_clusters_x();
+  const int n_my = cl < n_citems ? (n_citems - 1 - cl) / n_cl + 1 : 0;
+  auto item_of = [&](int it, int& seq, int& h) {
+    const int c = cl + it * n_cl;
+    const int sg = c / head_groups, hg = c - sg * head_groups;
+    seq = sg * CS + ci;
+    h = hg * CH + cj;
+  };
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_x);
+    sm100::tma_prefetch(&tm_w);
+    for (int i = 0; i < kStages; ++i) {
+      sm100::mbar_init(&s.full[i], 1);
+      sm100::mbar_init(&s.empty[i], CS + CH - 1);  // consumers of this CTA's slices
+      sm100::mbar_init(&s.kdone[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s.acc_full[i], 1);
+      sm100::mbar_init(&s.acc_empty[i], 256);
+    }
+    sm100::mbar_init(&s.qkv_ready, 256);
+    sm100::mbar_init(&s.s_full, 1);
+    sm100::mbar_init(&s.p_ready, 256);
+    sm100::mbar_init(&s.o_full, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: this CTA's slices, multicast ----------------
+    if (lane == 0) {
+      constexpr int kARows = kS / CH;        // x rows this CTA loads
+      constexpr int kBoxes = 6 / CS;         // 32-row W boxes this CTA loads
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = 0; it < n_my; ++it) {
+        int seq, h;
+        item_of(it, seq, h);
+        const int a_row = seq * kS + cj * kARows;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          // every sharer of this stage has consumed its previous contents
+          sm100::mbar_wait(&s.empty[stage], phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&s.full[stage], kStageBytes);
+          uint8_t* st = s.stages[stage];
+          sm100::tma_load_2d_mc(st + cj * kARows * 128, &tm_x, &s.full[stage], kb * 64, a_row,
+                                row_mask);
+#pragma unroll
+          for (int bb = 0; bb < kBoxes; ++bb) {
+            const int b = ci * kBoxes + bb;  // box of the head's 6: part b/2, half b%2
+            sm100::tma_load_2d_mc(st + kATile + b * kWBox * 128, &tm_w, &s.full[stage], kb * 64,
+                                  (b >> 1) * hidden + h * 64 + (b & 1) * kWBox, col_mask);
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc_g = sm100::umma_idesc_bf16(128, 192);
+      constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
+      constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
+      const uint16_t share_mask = row_mask | col_mask;
+      const uint32_t q_addr = sm100::smem_u32(s.qkv[0]);
+      const uint32_t k_addr = sm100::smem_u32(s.qkv[1]);
+      const uint32_t v_addr = sm100::smem_u32(s.qkv[2]);
+      int stage = 0;
+      uint32_t phase = 0;
+      int g = 0;  // projection k-blocks issued so far
+      auto gemm_kb = [&](int it, int kb) {
+        if (lag > 0 && g >= lag) {
+          const int d = g - lag;
+          sm100::mbar_wait(&s.kdone[d % kStages], (d / kStages) & 1);
+        }
+        sm100::mbar_wait(&s.full[stage], phase);
+        sm100::tc_fence_after();
+        const uint32_t a = sm100::smem_u32(s.stages[stage]);
+        const uint32_t b = a + kATile;
+        const uint32_t d = tmem + (uint32_t)(it & 1) * kAccCols;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          sm100::mma_bf16(d, sm100::umma_desc_sw128(a + k * 32), sm100::umma_desc_sw128(b + k * 32),
+                          idesc_g, (kb | k) != 0);
+        sm100::mma_commit_mc(&s.empty[stage], share_mask);
+        if (lag > 0) sm100::mma_commit(&s.kdone[stage]);
+        ++g;
+        if (kb == k_blocks - 1) sm100::mma_commit(&s.acc_full[it & 1]);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      };
+      auto acc_wait = [&](int it) {
+        sm100::mbar_wait(&s.acc_empty[it & 1], ((it >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+      };
+      auto issue_s = [&]() {
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
+                          sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+        sm100::mma_commit(&s.s_full);
+      };
+      auto issue_o = [&]() {
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t pa = ((kk >> 2) ? k_addr : q_addr) + (kk & 3) * 32;
+          sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(pa),
+                          sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+        }
+        sm100::mma_commit(&s.o_full);
+      };
+      if (n_my > 0) {
+        acc_wait(0);
+        for (int kb = 0; kb < k_blocks; ++kb) gemm_kb(0, kb);
+      }
+      for (int it = 0; it < n_my; ++it) {
+        const uint32_t par = it & 1;
+        bool s_done = dbg != 0, o_done = dbg != 0;
+        if (it + 1 < n_my) {
+          acc_wait(it + 1);
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            gemm_kb(it + 1, kb);
+            if (!s_done) {
+              if (sm100::mbar_test(&s.qkv_ready, par)) {
+                issue_s();
+                s_done = true;
+              }
+            } else if (!o_done && sm100::mbar_test(&s.p_ready, par)) {
+              issue_o();
+              o_done = true;
+            }
+          }
+        }
+        if (!s_done) {
+          sm100::mbar_wait(&s.qkv_ready, par);
+          issue_s();
+        }
+        if (!o_done) {
+          sm100::mbar_wait(&s.p_ready, par);
+          issue_o();
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue / softmax (warps 2-9) ----------------
+    const int quarter = warp & 3;       // TMEM lane quarter this warp may access
+    const int hf = (warp - 2) >> 2;     // column half
+    const int r = quarter * 32 + lane;  // token row of the item
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    constexpr float kLog2e = 1.4426950408889634f;
+    for (int it = 0; it < n_my; ++it) {
+      int seq, h;
+      item_of(it, seq, h);
+      const uint32_t par = it & 1;
+      const int a = it & 1;
+      // (1) acc + bias -> bf16 Q/K/V tiles. Chunk c (32 columns) of the 192:
+      // part t = c/2 (Q, K, V), columns (c&1)*32.. of that part.
+      sm100::mbar_wait(&s.acc_full[a], (it >> 1) & 1);
+      sm100::tc_fence_after();
+      if (dbg == 1) {
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.acc_empty[a]);
+        continue;
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < 3; ++cc) {
+        const int c = hf * 3 + cc;
+        const int t = c >> 1, c32 = c & 1;
+        uint32_t raw[32];
+        sm100::tmem_ld_32x32b_x32(lane_base + (uint32_t)a * kAccCols + c * 32, raw);
+        sm100::tmem_ld_wait();
+        const float* bp = b_qkv + t * hidden + h * 64 + c32 * 32;
+        const float scale = t == 0 ? 0.125f : 1.0f;
+        uint8_t* rowp = s.qkv[t] + r * 128;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + q4 * 8));
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(bp + q4 * 8 + 4));
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = (__uint_as_float(raw[q4 * 8 + e]) + bb[e]) * scale;
+          uint4 u;
+          u.x = pack_bf16(v[0], v[1]);
+          u.y = pack_bf16(v[2], v[3]);
+          u.z = pack_bf16(v[4], v[5]);
+          u.w = pack_bf16(v[6], v[7]);
+          const int piece = c32 * 4 + q4;
+          *reinterpret_cast<uint4*>(rowp + ((piece ^ (r & 7)) << 4)) = u;
+        }
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.acc_empty[a]);
+      sm100::fence_proxy_async_smem();
+      sm100::mbar_arrive(&s.qkv_ready);
+      if (dbg == 2) continue;
+      // (2) softmax over this thread's 64 keys [64 hf, 64 hf + 64)
+      sm100::mbar_wait(&s.s_full, par);
+      sm100::tc_fence_after();
+      uint32_t sv[2][32];
+      sm100::tmem_ld_32x32b_x32(lane_base + kSCol + hf * 64, sv[0]);
+      sm100::tmem_ld_32x32b_x32(lane_base + kSCol + hf * 64 + 32, sv[1]);
+      sm100::tmem_ld_wait();
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        mx = fmaxf(mx, fmaxf(__uint_as_float(sv[0][e]), __uint_as_float(sv[1][e])));
+      s.red_max[hf][r] = mx;
+      epi_sync();
+      mx = fmaxf(mx, s.red_max[hf ^ 1][r]);
+      const float mxl = mx * kLog2e;
+      float sum = 0.f;
+      uint8_t* prow = s.qkv[hf] + r * 128;  // P keys [64 hf, +64) over the Q (hf 0) / K tile
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        __align__(16) __nv_bfloat162 pv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = exp2f(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e]), kLog2e, -mxl));
+          const float p1 =
+              exp2f(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e + 1]), kLog2e, -mxl));
+          pv[e] = __floats2bfloat162_rn(p0, p1);
+          const float2 back = __bfloat1622float2(pv[e]);
+          sum += back.x + back.y;
+        }
+        *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) = *reinterpret_cast<uint4*>(pv);
+      }
+      s.red_sum[hf][r] = sum;
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.p_ready);
+      // (3) O / rowsum -> ctx, this thread's 32 of the head's 64 features
+      sm100::mbar_wait(&s.o_full, par);
+      sm100::tc_fence_after();
+      uint32_t ov[32];
+      sm100::tmem_ld_32x32b_x32(lane_base + kSCol + hf * 32, ov);
+      sm100::tmem_ld_wait();
+      epi_sync();
+      const float inv = 1.0f / (sum + s.red_sum[hf ^ 1][r]);
+      if (seq < n_seq) {  // the last sequence group may be padded
+        __nv_bfloat16* dst = ctx + ((size_t)seq * kS + r) * hidden + h * 64 + hf * 32;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(ov[q4 * 8 + 0]) * inv, __uint_as_float(ov[q4 * 8 + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(ov[q4 * 8 + 2]) * inv, __uint_as_float(ov[q4 * 8 + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(ov[q4 * 8 + 4]) * inv, __uint_as_float(ov[q4 * 8 + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(ov[q4 * 8 + 6]) * inv, __uint_as_float(ov[q4 * 8 + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + q4 * 8) = u;
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  // no CTA may leave while a sharer can still multicast into it or arrive on
+  // its barriers
+  sm100::cluster_sync();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
+static int n_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+}  // namespace qa
+
+// Diagnostic overrides (measurement only): CHM_QA_DEBUG=1 projection alone,
+// 2 + Q/K/V staging; CHM_QA_CLUSTER = "<CS><CH>"; CHM_QA_LAG = issue lag.
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int CS, int CH>
+static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv, void* ctx,
+                         int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
+  const int n_heads = hidden / 64;
+  if (n_heads % CH != 0) return CHM_ERR_UNSUPPORTED;
+  constexpr int kCluster = CS * CH;
+  const long long T = (long long)n_seq * qa::kS;
+  CUtensorMap tm_x, tm_w;
+  if (!gemm::make_tmap_bf16(&tm_x, x, (uint64_t)T, (uint64_t)hidden, qa::kS / CH, 64, 0))
+    return CHM_ERR_CUDA;
+  if (!gemm::make_tmap_bf16(&tm_w, w_qkv, (uint64_t)3 * hidden, (uint64_t)hidden, qa::kWBox, 64,
+                            0))
+    return CHM_ERR_CUDA;
+  auto kern = qa::qkv_attention_kernel<CS, CH>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(qa::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = qa::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int max_clusters = 0;
+  if (!max_clusters) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qa::kSmemBytes);
+    cfg.gridDim = dim3(kCluster * (qa::n_sms() / kCluster), 1, 1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1)
+      n = qa::n_sms() / kCluster;
+    max_clusters = n;
+  }
+  const int citems = ((n_seq + CS - 1) / CS) * (n_heads / CH);
+  const int n_cl = citems < max_clusters ? citems : max_clusters;
+  cfg.gridDim = dim3(kCluster * n_cl, 1, 1);
+  prof::begin(prof::K_GEMM, st);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, n_seq, n_heads, hidden,
+                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg);
+  // tensor work: the projection (2 T 3H H) + S and O (4 S^2 64 per item)
+  prof::end(prof::K_GEMM, st,
+            2.0 * T * 3.0 * hidden * hidden + 4.0 * qa::kS * qa::kS * 64.0 * n_seq * n_heads);
+  if (e != cudaSuccess) return CHM_ERR_CUDA;
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+// ctx = attention(x . w_qkv^T + b_qkv) for n_seq sequences of 128 tokens.
+chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv, void* ctx,
+                         int n_seq, int hidden, cudaStream_t st) {
+  static const int cluster = env_int("CHM_QA_CLUSTER", 21);
+  static const int lag = env_int("CHM_QA_LAG", 0);
+  static const int dbg = env_int("CHM_QA_DEBUG", 0);
+  switch (cluster) {
+    case 11: return launch<1, 1>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
+    case 12: return launch<1, 2>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
+    case 21: return launch<2, 1>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
+    case 24: return launch<2, 4>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
+    default: return launch<2, 2>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
+  }
+}
+
+}  // namespace chm
+
+extern "C" chm_status chm_qkv_attention_bf16(const void* x, const void* w_qkv,
+                                             const float* b_qkv, void* ctx, int32_t n_seq,
+                                             int32_t hidden, void* stream) {
+  if (!x || !w_qkv || !b_qkv || !ctx || n_seq < 0) return CHM_ERR_INVALID_ARG;
+  if (hidden <= 0 || hidden % 64 != 0) return CHM_ERR_INVALID_ARG;
+  if (n_seq == 0) return CHM_OK;
+  return chm::qkv_attention(x, w_qkv, b_qkv, ctx, n_seq, hidden, (cudaStream_t)stream);
+}

@@ -135,7 +135,7 @@ class GpuEncoderRouter:
             A["ln1_b"].ptr, A["w_1"].ptr, A["b_1"].ptr, A["w_2"].ptr, A["b_2"].ptr,
             A["ln2_g"].ptr, A["ln2_b"].ptr, w["head_w"].data_ptr(), w["head_b"].data_ptr())
         self.cfg_c = _lib.EncoderCfg(cfg.n_layers, cfg.hidden, cfg.n_heads, cfg.ffn, cfg.vocab,
-                                     cfg.max_pos, n_models, cfg.ln_eps)
+                                     cfg.max_pos, n_models, cfg.ln_eps, 0)
         self.max_rows = max_rows
         T = max_rows * cfg.seq_len
         bf = torch.bfloat16

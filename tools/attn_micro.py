@@ -1,0 +1,69 @@
+"""Micro-benchmark of the S = 128 attention sublayer core at the cfg3 shape:
+fused QKV+attention kernel vs QKV GEMM + attention kernel (CUDA events).
+
+  python tools/attn_micro.py [--n-seq 4096] [--hidden 768] [--reps 10] [--only fused|unfused]
+"""
+
+import argparse
+import math
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_22206_b200 import _lib  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n-seq", type=int, default=4096)
+    ap.add_argument("--hidden", type=int, default=768)
+    ap.add_argument("--seq-len", type=int, default=128)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    lib = _lib.load()
+    n, H, S = a.n_seq, a.hidden, a.seq_len
+    T = n * S
+    dev = "cuda"
+    x = torch.randn(T, H, device=dev).to(torch.bfloat16)
+    w = (torch.randn(3 * H, H, device=dev) / math.sqrt(H)).to(torch.bfloat16)
+    b = torch.randn(3 * H, device=dev) * 0.1
+    qkv = torch.empty(T, 3 * H, dtype=torch.bfloat16, device=dev)
+    ctx = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def fused():
+        _lib.check(lib.chm_qkv_attention_bf16(x.data_ptr(), w.data_ptr(), b.data_ptr(),
+                                              ctx.data_ptr(), n, H, st), "fused")
+
+    def gemm():
+        _lib.check(lib.chm_gemm_bf16(x.data_ptr(), w.data_ptr(), qkv.data_ptr(), b.data_ptr(),
+                                     None, T, 3 * H, H, 1, st), "gemm")
+
+    def attn():
+        _lib.check(lib.chm_attention_bf16(qkv.data_ptr(), ctx.data_ptr(), n, S, H, st), "attn")
+
+    flops_g = 2.0 * T * 3 * H * H
+    flops_a = 4.0 * S * S * 64 * n * (H // 64)
+    cases = {"fused": (fused, flops_g + flops_a), "gemm": (gemm, flops_g),
+             "attention": (attn, flops_a)}
+    for name, (fn, fl) in cases.items():
+        if a.only and a.only not in name:
+            continue
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        print(f"{name:10s} {ms:8.3f} ms  {fl / ms / 1e9:8.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()
