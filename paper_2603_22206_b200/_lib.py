@@ -258,7 +258,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    # CHM_LIB: an alternative build of the same library (A/B measurement)
+    path = path or os.environ.get("CHM_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(
             f"{path} is missing: build it with `python -m paper_2603_22206_b200.build` "

@@ -102,9 +102,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__device__ __forceinline__ void st_cluster_f2(uint32_t addr, float2 v) {
-  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y)
-               : "memory");
+__device__ __forceinline__ void st_async_f2(uint32_t addr, float2 v, uint32_t bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+          addr),
+      "f"(v.x), "f"(v.y), "r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&s.tmem_full[i], 1);
       sm100::mbar_init(&s.tmem_empty[i], 2 * kEpiWarps);  // epilogues of both CTAs
-      sm100::mbar_init(&s.stats_bar[i], ln_groups * kEpiWarps * 32);
+      sm100::mbar_init(&s.stats_bar[i], 1);  // local arm; pushes complete tx bytes
     }
     for (int w = 0; w < kEpiWarps; ++w)
       for (int b = 0; b < 2; ++b) sm100::mbar_init(&s.res_bar[w][b], 1);
@@ -314,12 +317,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // push (mean, M2) to the CTAs holding this row (same pair position)
         const int buf = it & 1;
         const int row_local = quarter * 32 + lane;
+        // st.async: each 8-byte push completes bytes on the destination's
+        // barrier (armed locally for ln_groups x 256 pushes), no fences
+        if (ew == 0 && lane == 0)
+          sm100::mbar_arrive_expect_tx(&s.stats_bar[buf], ln_groups * kEpiWarps * 32 * 8);
         for (int g = 0; g < ln_groups; ++g) {
           const uint32_t dst_rank = px + 2 * g;
-          st_cluster_f2(sm100::mapa(sm100::smem_u32(&s.stats[buf][pair][half][row_local]),
-                                    dst_rank),
-                        make_float2(mean, m2));
-          sm100::mbar_arrive_cluster(sm100::mapa(sm100::smem_u32(&s.stats_bar[buf]), dst_rank));
+          st_async_f2(sm100::mapa(sm100::smem_u32(&s.stats[buf][pair][half][row_local]), dst_rank),
+                      make_float2(mean, m2),
+                      sm100::mapa(sm100::smem_u32(&s.stats_bar[buf]), dst_rank));
         }
         mbar_wait_cluster(&s.stats_bar[buf], (it >> 1) & 1);
         float gm = 0.f;
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c == 1) {
             sm100::tc_fence_before();
             __syncwarp();
-            if (lane == 0) sm100::mbar_arrive_cluster(acc ? empty_leader1 : empty_leader0);
+            if (lane == 0) sm100::mbar_arrive_remote(acc ? empty_leader1 : empty_leader0);
           }
           const int col0 = n_tile0 + c * 64;
           uint8_t* rowp = s.stage_out[ew][c] + lane * 128;
@@ -401,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // accumulator fully read: hand it back to the leader's MMA warp
             sm100::tc_fence_before();
             __syncwarp();
-            if (lane == 0) sm100::mbar_arrive_cluster(acc ? empty_leader1 : empty_leader0);
+            if (lane == 0) sm100::mbar_arrive_remote(acc ? empty_leader1 : empty_leader0);
           }
           if (col0 >= N) continue;
           if (EPI == EPI_BIAS_RESIDUAL) {
