@@ -147,10 +147,17 @@ typedef struct chm_queue_state {
   int32_t* n_admitted;       /* [K] out                                        */
   int32_t* n_promoted;       /* [K] out: promotions this call                  */
   uint8_t* arrival_unsorted; /* [K] out: arrival not monotone in seq           */
-  void* scratch;             /* K*cap*20 bytes of sort-key scratch; required
-                                when capacity > 10240 (keys then live in L2/HBM
-                                instead of shared memory)                      */
+  void* scratch;             /* K * chm_queue_scratch_bytes(cap) bytes; required
+                                when capacity > 10240 (sort keys then live in
+                                L2/HBM instead of shared memory)               */
 } chm_queue_state;
+
+/* Per-engine scratch bytes chm_queue_* need for a segment capacity: 0 up to
+ * 10240 entries (keys in shared memory, one CTA per engine), 20/entry up to
+ * 2^18 (keys in global memory, one CTA per engine), above that the
+ * grid-wide path (radix passes over 4096-entry tiles, staging copy for the
+ * compaction): ~68/entry. */
+uint64_t chm_queue_scratch_bytes(int32_t capacity);
 
 /* ---- router encoder (BERT-style post-LN, CLS -> Linear(H,K) -> sigmoid) --- */
 

@@ -130,8 +130,6 @@ class QueueState(ctypes.Structure):
         ("scratch", c_void_p),
     ]
 
-QUEUE_SMEM_CAPACITY = 10240        # entries per engine sorted in shared memory
-QUEUE_SCRATCH_BYTES_PER_ENTRY = 20  # larger segments: global sort-key scratch
 
 
 class EncoderCfg(ctypes.Structure):
@@ -216,6 +214,7 @@ _SIGNATURES = [
     ("chm_gemm_bf16_ln", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_int32,
       c_int32, c_int32, c_void_p]),
+    ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
     ("chm_attention_bf16", c_int32,
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p]),
     ("chm_qkv_attention_bf16", c_int32,

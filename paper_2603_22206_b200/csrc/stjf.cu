@@ -27,15 +27,21 @@
 // implicit) + write 40 + order 4.
 #include "common.cuh"
 #include "prof.cuh"
+#include "stjf_common.cuh"
 
 namespace chm {
 
 constexpr int kQMax = 10240;       // entries per engine segment held in smem
 constexpr int kQThreads = 1024;
 constexpr int kQWarps = kQThreads / 32;
-constexpr int kMaxGroups = 256;
-constexpr uint32_t kAdmitted = 0xffffffffu;
 constexpr size_t kScratchBytesPerEntry = 8 + 2 + 2 + 4 + 4;  // prio, lvl, cnt, idx a/b
+constexpr int kQHuge = 1 << 18;    // larger segments: grid-wide passes (stjf_huge.cu)
+
+size_t queue_huge_scratch_bytes(int capacity);
+chm_status launch_queue_huge(const QueueParams& prm, const chm_monitor_state& mon,
+                             const chm_queue_state& q, const chm_rows& rows,
+                             const chm_decisions& dec, const int32_t* n_complete,
+                             int n_iterations, int mode, int32_t* err, cudaStream_t s);
 
 // Shared control state (both storage modes).
 struct QueueCtl {
@@ -65,12 +71,6 @@ struct SmallKeysSmem {
   uint16_t a[kQMax];
   uint16_t b[kQMax];
 };
-
-__device__ __forceinline__ unsigned long long f64_key(double x) {
-  unsigned long long b = (unsigned long long)__double_as_longlong(x);
-  // priorities/arrivals are >= 0 (validated upstream); -0.0 == 0.0 in Python.
-  return b == 0x8000000000000000ull ? 0ull : b;
-}
 
 // One stable LSD counting-sort pass over `n` indices.
 // src: 0 = arrival (global), 1 = priority, 2 = level, 3 = count; byte = digit index.
@@ -180,30 +180,6 @@ __device__ void radix_sort(QueueCtl& s, const Keys<Idx>& k, int n, const int* sr
   spare = out;
 }
 
-struct QueueParams {
-  int K;
-  int b[CHM_MAX_MODELS];
-  int aging_enabled;
-  int S;
-  int cap_limit;  // largest segment this kernel variant can hold
-};
-
-// Lexicographic key of a group head: (level, priority, arrival?, storage idx).
-struct HeadKey {
-  int lvl;
-  unsigned long long prio;
-  unsigned long long arr;
-  int e;
-  int g;
-};
-
-__device__ __forceinline__ bool key_less(const HeadKey& x, const HeadKey& y) {
-  if (x.lvl != y.lvl) return x.lvl < y.lvl;
-  if (x.prio != y.prio) return x.prio < y.prio;
-  if (x.arr != y.arr) return x.arr < y.arr;
-  return x.e < y.e;
-}
-
 // mode 0: completions (R = n_complete[m], each frees one running slot first)
 // mode 1: tick (append queued rows, then R = n_iterations explicit iterations)
 template <typename Idx, bool kBig>
@@ -250,59 +226,15 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
 
   // ---- mode 1: append rows queued on this engine by chm_schedule_rows ----
   if (mode == 1) {
-    const int n_rows = *dec.n_committed;
     // rows queued this batch were already counted in engine_queued by K6
-    int c = 0;
-    for (int i = tid; i < n_rows; i += blockDim.x)
-      c += (dec.model[i] == m && (dec.flags[i] & 4u)) ? 1 : 0;
-    for (int off = 16; off; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-    if (lane == 0) s.scan[warp] = c;
-    __syncthreads();
-    if (tid == 0) {
-      int t = 0;
-      for (int w = 0; w < kQWarps; ++w) t += s.scan[w];
-      s.misc[0] = t;
-    }
-    __syncthreads();
-    const int n_new_total = s.misc[0];
-    __syncthreads();
+    const int n_new_total = count_queued_rows(m, dec, s.scan, s.misc);
     const int n_old = n - n_new_total;
     if (n_old < 0 || n > cap) {
       if (tid == 0) report_error(err, n > cap ? CHM_ERR_CAPACITY : CHM_ERR_INVALID_STATE,
                                  0, m, n);
       return;
     }
-    int pos_base = n_old;
-    for (int blk = 0; blk < n_rows; blk += blockDim.x) {
-      const int i = blk + tid;
-      const bool take = i < n_rows && dec.model[i] == m && (dec.flags[i] & 4u);
-      const unsigned bal = __ballot_sync(0xffffffffu, take);
-      if (lane == 0) s.scan[warp] = __popc(bal);
-      __syncthreads();
-      if (warp == 0) {
-        int v = s.scan[lane], incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-          int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        s.scan[lane] = incl - v;
-        if (lane == 31) s.misc[1] = incl;
-      }
-      __syncthreads();
-      if (take) {
-        const int pos = pos_base + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
-        prio_g[pos] = dec.priority[i];
-        arr_g[pos] = rows.arrival[i];
-        seq_g[pos] = dec.seq[i];
-        handle_g[pos] = rows.handle ? rows.handle[i] : (int64_t)i;
-        out_g[pos] = rows.out_tokens ? rows.out_tokens[(size_t)i * prm.K + m] : 0;
-        lvl_g[pos] = 0;
-        cnt_g[pos] = 0;
-        qnt_g[pos] = 0;
-      }
-      pos_base += s.misc[1];
-      __syncthreads();
-    }
+    append_queued_rows(m, prm.K, rows, dec, seg, q, n_old, s.scan, s.misc);
     __threadfence_block();
   } else {
     if (n > cap) {
@@ -525,6 +457,7 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   if (aging->enabled && aging->demote_while_queued) return CHM_ERR_UNSUPPORTED;
   const bool big = q->capacity > kQMax;
   if (big && !q->scratch) return CHM_ERR_INVALID_ARG;
+  const bool huge = q->capacity > kQHuge;
   QueueParams prm{};
   prm.K = K;
   for (int m = 0; m < K; ++m) prm.b[m] = pool->max_batch_size[m];
@@ -536,6 +469,12 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   if (rows) r = *rows;
   if (dec) d = *dec;
   prof::begin(prof::K_QUEUE, s);
+  if (huge) {
+    const chm_status rc = launch_queue_huge(prm, *mon, *q, r, d, n_complete, n_iterations, mode,
+                                            err, s);
+    prof::end(prof::K_QUEUE, s, 0.0);
+    return rc;
+  }
   if (big) {
     const size_t smem = sizeof(QueueCtl);
     cudaFuncSetAttribute(queue_kernel<uint32_t, true>,
@@ -555,6 +494,12 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
 }
 
 }  // namespace chm
+
+extern "C" uint64_t chm_queue_scratch_bytes(int32_t capacity) {
+  if (capacity <= chm::kQMax) return 0;
+  if (capacity <= chm::kQHuge) return (uint64_t)capacity * chm::kScratchBytesPerEntry;
+  return (uint64_t)chm::queue_huge_scratch_bytes(capacity);
+}
 
 extern "C" chm_status chm_queue_complete(const chm_pool* pool, const chm_aging_cfg* aging,
                                          const chm_monitor_state* mon,

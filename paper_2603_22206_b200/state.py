@@ -94,9 +94,9 @@ class DeviceState:
         self.q_n_promoted = torch.zeros(K, dtype=i32, device=d)
         self.q_arrival_unsorted = torch.zeros(K, dtype=torch.uint8, device=d)
         self.q_scratch = None
-        if C > _lib.QUEUE_SMEM_CAPACITY:
-            self.q_scratch = torch.empty(n * _lib.QUEUE_SCRATCH_BYTES_PER_ENTRY,
-                                         dtype=torch.uint8, device=d)
+        per_engine = int(_lib.load().chm_queue_scratch_bytes(C))
+        if per_engine:
+            self.q_scratch = torch.empty(K * per_engine, dtype=torch.uint8, device=d)
         self.pool_c = _lib.Pool()
         self.pool_c.n_models = K
         for i, mid in enumerate(self.ids):

@@ -67,7 +67,7 @@ def replay_on_gpu(qd, capacity=10240):
     )
 
 
-@pytest.mark.parametrize("capacity", [10240, 20480])  # smem keys / global-scratch keys
+@pytest.mark.parametrize("capacity", [10240, 20480, 300000])  # smem / global keys / grid-wide
 @pytest.mark.parametrize("name", H.queue_names())
 def test_queue_matches_reference(name, capacity):
     qd = H.load_queue(name)
@@ -80,7 +80,67 @@ def test_queue_matches_reference(name, capacity):
     assert res["iterations"] == qd["iterations"]
 
 
-@pytest.mark.parametrize("n,capacity", [(9000, 10240), (70000, 72000)])
+def _stress_state(capacity, n, seed, b=(64, 16), S=3):
+    """Two engines with n queued entries each: ties, mixed levels/counts, and
+    engines with free slots so iterations admit and age at scale."""
+    rng = np.random.default_rng(seed)
+    pool = Pool((ModelProfile("m0", 1.0, b[0]), ModelProfile("m1", 2.0, b[1])))
+    gs = GpuScheduler(pool, BalancerConfig(), AgingConfig(starvation_threshold=S),
+                      router=ScoreTableRouter(), predictor=PrecomputedPredictor(),
+                      n_programs=16, max_rows=16, queue_capacity=capacity)
+    st = gs.state
+    for m in range(2):
+        prio = np.round(rng.lognormal(5, 2, n))
+        prio[rng.random(n) < 0.2] = 37.0  # ties
+        arr = np.sort(rng.random(n) * 100)
+        st.load_queue(m, prio, arr, np.arange(n), np.arange(n) + (m << 40),
+                      level=-rng.integers(0, 3, n), count=rng.integers(0, S, n))
+    st.set_engine_counters(running=[b[0] // 2, b[1]])
+    gs.router.set(torch.zeros((0, 2), device=gs.device))
+    gs.predictor.set(torch.zeros((0, 2), dtype=torch.float64, device=gs.device))
+    return gs
+
+
+def _snapshot_queue(gs):
+    st = gs.state
+    out = {"running": st.engine_running.cpu().numpy().copy(),
+           "queued": st.engine_queued.cpu().numpy().copy(),
+           "iterations": st.engine_iterations.cpu().numpy().copy(),
+           "promoted": st.q_n_promoted.cpu().numpy().copy()}
+    for m in range(2):
+        nq = int(st.engine_queued[m])
+        b = m * st.capacity
+        order = st.q_order[b:b + nq].long()
+        out[f"admitted{m}"] = st.admitted(m)
+        out[f"order{m}"] = st.q_handle[b:b + nq][order].cpu().numpy()
+        for f in ("level", "count", "quantum", "priority", "handle"):
+            out[f"{f}{m}"] = getattr(st, f"q_{f}")[b:b + nq].cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("n", [150000, 250000])
+def test_queue_grid_wide_matches_single_cta(n):
+    """The grid-wide path (capacity > 2^18) against the single-CTA global-key
+    path (itself pinned to the reference goldens above) on the same state:
+    completions, then a tick with 3 iterations (admission + aging + promotion)."""
+    res = []
+    for capacity in (262144, 300000):
+        gs = _stress_state(capacity, n, seed=n)
+        e = RowBatch.from_numpy(gs.device, program=np.zeros(0), stage=np.zeros(0),
+                                arrival=np.zeros(0), out_tokens=np.zeros((0, 2)),
+                                handle=np.zeros(0))
+        nc = torch.tensor([5, 3], dtype=torch.int32, device=gs.device)
+        gs.run_rows(e, n_iterations=3, n_complete=nc)
+        gs.check_errors()
+        res.append(_snapshot_queue(gs))
+    small, huge = res
+    assert small.keys() == huge.keys()
+    for k in small:
+        np.testing.assert_array_equal(small[k], huge[k], err_msg=k)
+    assert small["promoted"].sum() > 0 and len(small["admitted0"]) > 0
+
+
+@pytest.mark.parametrize("n,capacity", [(9000, 10240), (70000, 72000), (2000000, 2097152)])
 def test_queue_order_random_large(n, capacity):
     """Full-size STJF order vs a numpy lexsort of (level, priority, arrival, seq);
     70k entries per engine exercises the global-scratch path (cfg4 stress)."""
