@@ -95,6 +95,14 @@ typedef struct chm_monitor_state {
   int32_t* engine_running;   /* [K] len(EngineSim.running)                     */
   int32_t* engine_queued;    /* [K] len(EngineSim._queued)                     */
   int64_t* engine_iterations;/* [K] EngineSim.iterations                       */
+  /* Optional live in-flight log (ActivityMonitor._in_flight, monitor.py:43-48,
+   * 86-106): per model, the live entries in insertion order, [K * cap] each;
+   * inflight_count[m] entries are live. Needed by chm_monitor_complete; NULL
+   * keys disable it. key = program * 32 + (stage - 1) for dispatched rows
+   * (negative keys: entries seeded by the caller). */
+  int32_t inflight_capacity;
+  int64_t* inflight_key;
+  double* inflight_yhat;
 } chm_monitor_state;
 
 /* ---- one batch of requests, in arrival order ----------------------------- */
@@ -245,6 +253,17 @@ chm_status chm_schedule_rows(const chm_pool* pool, const chm_balancer_cfg* cfg,
                              const chm_row_scratch* scratch, const float* scores,
                              const double* yhat, const chm_decisions* out,
                              void* stream);
+
+/* Completion path (ActivityMonitor.record_completion, monitor.py:98-106): the
+ * n requests (model[j], key[j]) finished; each is removed from model[j]'s
+ * in-flight log (insertion order of the rest kept), its (program, stage)
+ * in-flight bit cleared, and the model's Neumaier (sum, comp) recomputed over
+ * the survivors exactly as builtin sum() would. n_complete[m] (optional, [K])
+ * receives the per-model counts, ready for chm_queue_complete. Device errors:
+ * UNKNOWN_REQUEST (not in flight on that model), VALIDATION (model index). */
+chm_status chm_monitor_complete(const chm_pool* pool, const chm_monitor_state* mon,
+                                const int32_t* model, const int64_t* key, int32_t n,
+                                int32_t* n_complete, int32_t* error, void* stream);
 
 /* K7 phase A: `n_complete[m]` running requests of engine m finish at `now`;
  * each frees a slot and runs one scheduling iteration (engine.py:232-241,

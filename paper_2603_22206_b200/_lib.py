@@ -73,6 +73,9 @@ class MonitorState(ctypes.Structure):
         ("engine_running", c_void_p),
         ("engine_queued", c_void_p),
         ("engine_iterations", c_void_p),
+        ("inflight_capacity", c_int32),
+        ("inflight_key", c_void_p),
+        ("inflight_yhat", c_void_p),
     ]
 
 
@@ -215,6 +218,9 @@ _SIGNATURES = [
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_int32,
       c_int32, c_int32, c_void_p]),
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
+    ("chm_monitor_complete", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+      c_void_p]),
     ("chm_attention_bf16", c_int32,
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p]),
     ("chm_qkv_attention_bf16", c_int32,

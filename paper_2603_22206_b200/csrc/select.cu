@@ -127,6 +127,21 @@ struct SelectParams {
 constexpr int kChunk = 256;
 constexpr int kThreads = 256;
 
+// record_dispatch's insertion into _in_flight[model] (monitor.py:95): the
+// live log keeps insertion order, position = live count at dispatch.
+__device__ __forceinline__ void log_append(const chm_monitor_state& mon, int m, long long pos,
+                                           int program, int stage, double y, int32_t* err,
+                                           int row) {
+  if (!mon.inflight_key) return;
+  if (pos >= mon.inflight_capacity) {
+    report_error(err, CHM_ERR_CAPACITY, row, m, (int)mon.inflight_capacity);
+    return;
+  }
+  const size_t at = (size_t)m * mon.inflight_capacity + pos;
+  mon.inflight_key[at] = (long long)program * 32 + (stage - 1);
+  mon.inflight_yhat[at] = y;
+}
+
 template <int K>
 struct ChunkBuf {
   uint64_t qual[kChunk];
@@ -520,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
                                     s_pow2[m] != 0);
 #pragma unroll
           for (int k = 0; k < K; ++k) L[k] = (k == m) ? lm : L[k];
+          log_append(mon, m, s_cnt[m], rows.program[i], rows.stage[i], y, out.error, i);
           s_cnt[m] += 1;
           // EngineSim.enqueue: _advance_clock (engine.py:140-143), then
           // _make_entry validates out_tokens (engine.py:285-286).
@@ -628,6 +644,8 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     for (int i = lo; i < hi; ++i) {
       const int m = out.model[i];
       const int r = s_cntm[m][tid]++;
+      log_append(mon, m, s_cnt[m] + r, rows.program[i], rows.stage[i], yhat[(size_t)i * K + m],
+                 out.error, i);
       out.seq[i] = s_seq[m] + r;
       out.flags[i] |= (s_run[m] + r < s_bmax[m]) ? DF_ADMITTED : DF_QUEUED;
     }

@@ -139,6 +139,7 @@ class BatchBuffers:
         self.seq = torch.zeros(B, dtype=torch.int64, device=d)
         self.loads = torch.zeros(B * K, dtype=torch.float64, device=d)
         self.n_committed = torch.zeros(1, dtype=torch.int32, device=d)
+        self.n_complete = torch.zeros(K, dtype=torch.int32, device=d)
         self.error = torch.zeros(4, dtype=torch.int32, device=d)
         self.error_init = torch.tensor([0, INT32_MAX, -1, 0], dtype=torch.int32, device=d)
         self.scratch_c = _lib.RowScratch(
@@ -157,7 +158,7 @@ class GpuScheduler:
     def __init__(self, pool: Pool, balancer: BalancerConfig = BalancerConfig(),
                  aging: AgingConfig = AgingConfig(), *, router=None, predictor=None,
                  n_programs: int = 1 << 20, max_rows: int = 16384,
-                 queue_capacity: int = 10240, device="cuda"):
+                 queue_capacity: int = 10240, device="cuda", inflight_capacity=None):
         self.lib = _lib.load()
         self.pool = pool
         self.ids = pool.model_ids
@@ -167,7 +168,8 @@ class GpuScheduler:
         self.router = router
         self.predictor = predictor
         self.device = torch.device(device)
-        self.state = DeviceState(pool, n_programs, queue_capacity, self.device)
+        self.state = DeviceState(pool, n_programs, queue_capacity, self.device,
+                                 inflight_capacity=inflight_capacity)
         self.buf = BatchBuffers(self.K, max_rows, self.device)
         self.bal_c = balancer_struct(balancer)
         self.aging_c = aging_struct(aging)
@@ -176,8 +178,14 @@ class GpuScheduler:
 
     # ------------------------------------------------------------------ core
     def run_rows(self, batch: RowBatch, n_iterations: int = 1, n_complete=None,
-                 with_loads: bool = True, stream=None) -> None:
-        """Enqueue one tick for `batch` on `stream` (default: current stream)."""
+                 with_loads: bool = True, stream=None, completions=None) -> None:
+        """Enqueue one tick for `batch` on `stream` (default: current stream).
+
+        completions: optional (model int32[n], key int64[n]) device tensors of
+        requests that finished since the last tick (key = request_key(program,
+        stage)): removed from the in-flight log (record_completion) and their
+        engines' slots freed, before the batch is scheduled. n_complete: the
+        engine side only (int32[K] finished-per-engine counts)."""
         B = batch.n_rows
         if B > self.buf.max_rows:
             raise ValueError(f"batch of {B} rows exceeds max_rows={self.buf.max_rows}")
@@ -190,6 +198,16 @@ class GpuScheduler:
             buf.error.copy_(buf.error_init)
             st.q_n_admitted.zero_()
             st.q_n_promoted.zero_()
+            if completions is not None:
+                # monitor side (record_completion) -> per-engine counts -> engines
+                if n_complete is not None:
+                    raise ValueError("give either completions or n_complete")
+                c_model, c_key = completions
+                _lib.check(lib.chm_monitor_complete(st.pool_c, st.monitor_c, _p(c_model),
+                                                    _p(c_key), int(c_model.numel()),
+                                                    _p(buf.n_complete), _p(buf.error), sh),
+                           "chm_monitor_complete")
+                n_complete = buf.n_complete
             if n_complete is not None:
                 _lib.check(lib.chm_queue_complete(st.pool_c, self.aging_c, st.monitor_c,
                                                   st.queue_c, _p(n_complete), _p(buf.error),

@@ -56,7 +56,7 @@ class DeviceState:
     """Monitor + engine + queue state for one pool on one device."""
 
     def __init__(self, pool: Pool, n_programs: int, queue_capacity: int = 10240,
-                 device: str | torch.device = "cuda"):
+                 device: str | torch.device = "cuda", inflight_capacity: int | None = None):
         self.pool = pool
         self.ids = pool.model_ids
         self.K = len(self.ids)
@@ -79,6 +79,11 @@ class DeviceState:
         self.engine_running = torch.zeros(K, dtype=i32, device=d)
         self.engine_queued = torch.zeros(K, dtype=i32, device=d)
         self.engine_iterations = torch.zeros(K, dtype=i64, device=d)
+        # live in-flight log (insertion order) for the completion path
+        self.inflight_capacity = int(inflight_capacity if inflight_capacity is not None
+                                     else min(max(NP, 65536), 1 << 22))
+        self.inflight_key = torch.zeros(K * self.inflight_capacity, dtype=i64, device=d)
+        self.inflight_yhat = torch.zeros(K * self.inflight_capacity, dtype=f64, device=d)
         n = K * C
         self.q_priority = torch.zeros(n, dtype=f64, device=d)
         self.q_arrival = torch.zeros(n, dtype=f64, device=d)
@@ -106,7 +111,8 @@ class DeviceState:
             NP, _ptr(self.inflight_sum), _ptr(self.inflight_comp), _ptr(self.inflight_count),
             _ptr(self.assignment), _ptr(self.stage_bits), _ptr(self.batch_stamp),
             _ptr(self.engine_clock), _ptr(self.engine_seq), _ptr(self.engine_running),
-            _ptr(self.engine_queued), _ptr(self.engine_iterations))
+            _ptr(self.engine_queued), _ptr(self.engine_iterations), self.inflight_capacity,
+            _ptr(self.inflight_key), _ptr(self.inflight_yhat))
         self.queue_c = _lib.QueueState(
             C, _ptr(self.q_priority), _ptr(self.q_arrival), _ptr(self.q_seq),
             _ptr(self.q_handle), _ptr(self.q_out_tokens), _ptr(self.q_level),
@@ -120,6 +126,7 @@ class DeviceState:
         s = self.inflight_sum.cpu().numpy()
         c = self.inflight_comp.cpu().numpy()
         n = self.inflight_count.cpu().numpy()
+        cap = self.inflight_capacity
         for mid, vals in per_model_values.items():
             k = self.ids.index(mid)
             ss, cc = float(s[k]), float(c[k])
@@ -128,7 +135,16 @@ class DeviceState:
                 t = ss + x
                 cc += ((ss - t) + x) if abs(ss) >= abs(x) else ((x - t) + ss)
                 ss = t
-            s[k], c[k], n[k] = ss, cc, n[k] + len(vals)
+            n0 = int(n[k])
+            if n0 + len(vals) > cap:
+                raise ValueError(f"in-flight log of {mid} exceeds capacity {cap}")
+            # log entries keyed -(n0 + j + 1): seeded requests (see seed_key)
+            b = k * cap + n0
+            self.inflight_key[b:b + len(vals)] = torch.arange(
+                -(n0 + 1), -(n0 + len(vals) + 1), -1, dtype=torch.int64)
+            self.inflight_yhat[b:b + len(vals)] = torch.as_tensor(
+                np.asarray(vals, dtype=np.float64))
+            s[k], c[k], n[k] = ss, cc, n0 + len(vals)
         self.inflight_sum.copy_(torch.from_numpy(s))
         self.inflight_comp.copy_(torch.from_numpy(c))
         self.inflight_count.copy_(torch.from_numpy(n))
@@ -163,7 +179,8 @@ class DeviceState:
         self.engine_queued[model] = n
 
     # -- snapshot / restore (device-to-device copies, graph-capturable) ------
-    _MUTABLE = ("inflight_sum", "inflight_comp", "inflight_count", "assignment", "stage_bits",
+    _MUTABLE = ("inflight_sum", "inflight_comp", "inflight_count", "inflight_key",
+                "inflight_yhat", "assignment", "stage_bits",
                 "engine_clock", "engine_seq", "engine_running", "engine_queued",
                 "engine_iterations", "q_priority", "q_arrival", "q_seq", "q_handle",
                 "q_out_tokens", "q_level", "q_count", "q_quantum")
@@ -192,6 +209,11 @@ class DeviceState:
         n = int(self.q_n_admitted[model])
         b = model * self.capacity
         return self.q_admitted[b:b + n].cpu().numpy()
+
+
+def request_key(program: int, stage: int) -> int:
+    """In-flight log key of request (program, stage) (request_id "p:stage")."""
+    return int(program) * 32 + (int(stage) - 1)
 
 
 def balancer_struct(cfg: BalancerConfig) -> _lib.BalancerCfg:

@@ -457,7 +457,141 @@ def make_synth():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def _reference_rows(sc, ids, state, engines, recs, rt_tab, pr_tab):
+    """schedule_request over sc's rows against a live SchedulerState."""
+    k = len(ids)
+    n = len(sc["prog"])
+    reqs = []
+    for i in range(n):
+        pid = f"p{int(sc['prog'][i]):06d}"
+        st = int(sc["stage"][i])
+        req = workload.Request(pid, st, 10, float(sc["arrival"][i]), "wf", "r")
+        rt_tab[req.request_id] = {ids[m]: float(sc["q"][i, m]) for m in range(k)}
+        pr_tab[req.request_id] = {ids[m]: float(sc["yhat"][i, m]) for m in range(k)}
+        rec = recs.get(pid)
+        if rec is None:
+            rec = workload.TraceRecord(pid, "wf", 0.0, [], {mid: 0 for mid in ids}, "easy")
+            recs[pid] = rec
+        while rec.n_stages < st:
+            rec.stages.append(workload.StageTrace(rec.n_stages + 1, "r", 10, {
+                mid: workload.ModelStageOutput(0, 0) for mid in ids}))
+        rec.stages[st - 1].models = {
+            ids[m]: workload.ModelStageOutput(int(sc["out_tok"][i, m]), 0) for m in range(k)}
+        reqs.append(req)
+    rt, pr = ShimRouter(rt_tab), ShimPredictor(pr_tab)
+    cfg = balancer.BalancerConfig(sc["tau"], sc["margin"])
+    model = np.full(n, -1, dtype=np.int32)
+    prio = np.zeros(n)
+    cached = np.zeros(n, dtype=np.int8)
+    loads = np.full((n, k), np.nan)
+    err = None
+    for i, req in enumerate(reqs):
+        try:
+            d = balancer.schedule_request(req, recs[req.program_id], state, rt, pr, cfg)
+        except (SimError, ValueError) as exc:
+            err = {"kind": type(exc).__name__, "row": i}
+            break
+        model[i] = ids.index(d.model)
+        prio[i] = d.priority
+        cached[i] = int(d.used_cached_assignment)
+        if d.estimated_loads:
+            loads[i] = [d.estimated_loads[mid] for mid in ids]
+    return dict(model=model, priority=prio, cached=cached, loads=loads), err
+
+
+def make_completions():
+    """Completion path (monitor.py:98-129): batch 1 through schedule_request,
+    then record_completion for a random subset of the live requests (batch-1
+    rows and pre-seeded entries, shuffled), then batch 2 -- fresh programs and
+    later stages of batch-1 programs -- against the reduced in-flight sums."""
+    specs = {
+        "c5_dyadic": dict(seed=21, k=5, n1=1500, n2=1500, p0=800, dyadic=True, frac=0.4),
+        "c3_nondyadic": dict(seed=22, k=3, n1=1000, n2=800, p0=200, dyadic=False, frac=0.5),
+        "c8_mixed": dict(seed=23, k=8, n1=2000, n2=1500, p0=300, dyadic=False, frac=0.3),
+        "c4_all": dict(seed=24, k=4, n1=600, n2=600, p0=100, dyadic=True, frac=1.0),
+    }
+    out = {}
+    for name, sp in specs.items():
+        rng = np.random.default_rng(sp["seed"] + 1000)
+        k, n1, n2 = sp["k"], sp["n1"], sp["n2"]
+        sc1 = build_scenario(sp["seed"], k, n1, dyadic=sp["dyadic"], p0_entries=sp["p0"],
+                             pre_assigned=0.1)
+        sc2 = build_scenario(sp["seed"] + 100, k, n2, dyadic=sp["dyadic"])
+        # batch 2 programs: half fresh, half the next stage of a batch-1 program
+        last_stage = {}
+        for p, s in zip(sc1["prog"].tolist(), sc1["stage"].tolist()):
+            last_stage[p] = max(last_stage.get(p, 0), s)
+        b1_progs = sorted(last_stage)
+        prog2, stage2 = [], []
+        for i in range(n2):
+            if rng.random() < 0.5:
+                p = int(b1_progs[int(rng.integers(0, len(b1_progs)))])
+                last_stage[p] += 1
+                prog2.append(p)
+                stage2.append(last_stage[p])
+            else:
+                p = n1 + 16 + i
+                last_stage[p] = 1
+                prog2.append(p)
+                stage2.append(1)
+        sc2["prog"] = np.array(prog2, dtype=np.int32)
+        sc2["stage"] = np.array(stage2, dtype=np.int32)
+        sc2["arrival"] = np.sort(rng.random(n2) * 10.0) + 20.0
+        n_prog = n1 + n2 + 32
+        ids = sc1["ids"]
+        pool = profiles.Pool(tuple(profiles.ModelProfile(ids[i], sc1["decode"][i],
+                                                         sc1["batch"][i]) for i in range(k)))
+        mon = monitor.ActivityMonitor(ids)
+        seed_pos = {m: 0 for m in range(k)}
+        seed_keys = []
+        for j, (m, v) in enumerate(sc1["p0"]):
+            mon.record_dispatch(ids[m], f"seed:{j}", v)
+            seed_pos[m] += 1
+            seed_keys.append((m, -seed_pos[m], f"seed:{j}"))
+        for p, m in sc1["pre"].items():
+            mon.assign(f"p{p:06d}", ids[m])
+        engines = {mid: engine.EngineSim(pool[mid], aging=engine.AgingConfig()) for mid in ids}
+        state = balancer.SchedulerState(pool=pool, monitor=mon, queues=engines)
+        recs, rt_tab, pr_tab = {}, {}, {}
+        res1, err1 = _reference_rows(sc1, ids, state, engines, recs, rt_tab, pr_tab)
+        assert err1 is None, err1
+        live = [(int(res1["model"][i]), int(sc1["prog"][i]) * 32 + int(sc1["stage"][i]) - 1,
+                 f"p{int(sc1['prog'][i]):06d}:{int(sc1['stage'][i])}") for i in range(n1)]
+        live += seed_keys
+        pick = [c for c in live if rng.random() < sp["frac"]]
+        rng.shuffle(pick)
+        for m, _, rid in pick:
+            mon.record_completion(ids[m], rid, 0, 0.0)
+        mid_p = np.array([mon.in_flight_sum(mid) for mid in ids], dtype=np.float64)
+        mid_cnt = np.array([mon.in_flight_count(mid) for mid in ids], dtype=np.int64)
+        res2, err2 = _reference_rows(sc2, ids, state, engines, recs, rt_tab, pr_tab)
+        final_p = np.array([mon.in_flight_sum(mid) for mid in ids], dtype=np.float64)
+        final_cnt = np.array([mon.in_flight_count(mid) for mid in ids], dtype=np.int64)
+        p0 = np.array(sc1["p0"], dtype=np.float64).reshape(-1, 2)
+        pre = np.array(sorted(sc1["pre"].items()), dtype=np.int64).reshape(-1, 2)
+        np.savez_compressed(
+            os.path.join(OUT, f"complete_{name}.npz"),
+            k=k, decode=np.array(sc1["decode"]), batch=np.array(sc1["batch"], dtype=np.int32),
+            n_prog=n_prog, tau=sc1["tau"], margin=sc1["margin"], p0=p0, pre=pre,
+            prog1=sc1["prog"], stage1=sc1["stage"], q1=sc1["q"], yhat1=sc1["yhat"],
+            out_tok1=sc1["out_tok"], arrival1=sc1["arrival"],
+            prog2=sc2["prog"], stage2=sc2["stage"], q2=sc2["q"], yhat2=sc2["yhat"],
+            out_tok2=sc2["out_tok"], arrival2=sc2["arrival"],
+            c_model=np.array([c[0] for c in pick], dtype=np.int32),
+            c_key=np.array([c[1] for c in pick], dtype=np.int64),
+            mid_p=mid_p, mid_cnt=mid_cnt, final_p=final_p, final_cnt=final_cnt,
+            err2_kind=(err2 or {}).get("kind", ""), err2_row=(err2 or {}).get("row", -1),
+            **{f"out1_{kk}": v for kk, v in res1.items()},
+            **{f"out2_{kk}": v for kk, v in res2.items()})
+        out[name] = (len(pick), err2)
+    return out
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["completions"]:
+        print("completions:", make_completions())
+        sys.exit(0)
+    print("completions:", make_completions())
     print("select cases:", make_select_kat())
     print("schedule:", make_schedules())
     print("errors:", make_errors())

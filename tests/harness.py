@@ -116,6 +116,84 @@ def run_port_schedule(sc):
     return res, err
 
 
+# ----------------------------------------------------------------- completions
+def complete_names():
+    return schedule_names(prefix="complete_")
+
+
+def load_complete(name):
+    """A completion golden as two schedule-like batches sharing one state."""
+    z = np.load(os.path.join(GOLDEN, f"complete_{name}.npz"), allow_pickle=False)
+    d = {k: z[k] for k in z.files}
+    k = int(d["k"])
+    common = dict(k=k, decode=d["decode"], batch=d["batch"], n_prog=int(d["n_prog"]),
+                  tau=float(d["tau"]), margin=float(d["margin"]), p0=d["p0"], pre=d["pre"],
+                  pre_running=np.zeros(k, np.int32), ids=[f"m{i}" for i in range(k)])
+    b1 = dict(common, prog=d["prog1"], stage=d["stage1"], q=d["q1"], yhat=d["yhat1"],
+              out_tok=d["out_tok1"], arrival=d["arrival1"])
+    b2 = dict(common, prog=d["prog2"], stage=d["stage2"], q=d["q2"], yhat=d["yhat2"],
+              out_tok=d["out_tok2"], arrival=d["arrival2"], p0=np.zeros((0, 2)),
+              pre=np.zeros((0, 2), np.int64))
+    return d, b1, b2
+
+
+def seed_request_ids(p0, k):
+    """(model, log key) -> request id "seed:j" of the pre-seeded entries."""
+    pos = {m: 0 for m in range(k)}
+    out = {}
+    for j, (m, _) in enumerate(p0):
+        m = int(m)
+        pos[m] += 1
+        out[(m, -pos[m])] = f"seed:{j}"
+    return out
+
+
+def run_port_complete(name):
+    """Replay a completion golden on the oracle port: batch 1, the
+    record_completion list, batch 2 (one monitor / engine set throughout)."""
+    d, b1, b2 = load_complete(name)
+    ids, k = b1["ids"], b1["k"]
+    pool = pool_of(b1)
+    mon = hp.PortMonitor(ids)
+    for j, (m, v) in enumerate(b1["p0"]):
+        mon.record_dispatch(ids[int(m)], f"seed:{j}", float(v))
+    for p, m in b1["pre"]:
+        mon.assign(f"p{int(p):06d}", ids[int(m)])
+    engines = {mid: hp.PortEngine(pool[mid].max_batch_size) for mid in ids}
+    seeds = seed_request_ids(b1["p0"], k)
+
+    def run(sc):
+        reqs, recs = requests_of(sc)
+        qtab = {r.request_id: {ids[m]: float(sc["q"][i, m]) for m in range(k)}
+                for i, r in enumerate(reqs)}
+        ytab = {r.request_id: {ids[m]: float(sc["yhat"][i, m]) for m in range(k)}
+                for i, r in enumerate(reqs)}
+        n = len(reqs)
+        res = dict(model=np.full(n, -1, np.int32), priority=np.zeros(n),
+                   cached=np.zeros(n, np.int8), loads=np.full((n, k), np.nan))
+        for i, (r, rec) in enumerate(zip(reqs, recs)):
+            dd = hp.port_schedule_request(r, rec, pool, mon, engines,
+                                          lambda rq, rc: qtab[rq.request_id],
+                                          lambda rq, rc, m: ytab[rq.request_id][m],
+                                          sc["tau"], sc["margin"])
+            res["model"][i] = ids.index(dd.model)
+            res["priority"][i] = dd.priority
+            res["cached"][i] = int(dd.used_cached_assignment)
+            if dd.estimated_loads:
+                res["loads"][i] = [dd.estimated_loads[m] for m in ids]
+        return res
+
+    r1 = run(b1)
+    for m, key in zip(d["c_model"].tolist(), d["c_key"].tolist()):
+        rid = seeds[(m, key)] if key < 0 else f"p{key // 32:06d}:{key % 32 + 1}"
+        mon.record_completion(ids[m], rid)
+    mid_p = np.array([mon.in_flight_sum(m) for m in ids], dtype=np.float64)
+    mid_cnt = np.array([len(mon.live[m]) for m in ids], dtype=np.int64)
+    r2 = run(b2)
+    final_p = np.array([mon.in_flight_sum(m) for m in ids], dtype=np.float64)
+    return d, r1, r2, mid_p, mid_cnt, final_p
+
+
 # ----------------------------------------------------------------- queues
 def queue_names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "q_*.npz")))

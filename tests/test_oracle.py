@@ -52,6 +52,20 @@ def test_schedule_port_matches_reference(name):
         np.testing.assert_array_equal(res[key], sc[f"out_{key}"], err_msg=key)
 
 
+@pytest.mark.parametrize("name", H.complete_names())
+def test_completion_port_matches_reference(name):
+    """record_completion + the recomputed Neumaier sums + the next batch's
+    decisions, against the real reference (tests/golden/complete_*.npz)."""
+    d, r1, r2, mid_p, mid_cnt, final_p = H.run_port_complete(name)
+    for key in ("model", "priority", "cached"):
+        np.testing.assert_array_equal(r1[key], d[f"out1_{key}"], err_msg=key)
+        np.testing.assert_array_equal(r2[key], d[f"out2_{key}"], err_msg=key)
+    np.testing.assert_array_equal(r2["loads"], d["out2_loads"])
+    assert mid_p.tobytes() == d["mid_p"].tobytes()
+    np.testing.assert_array_equal(mid_cnt, d["mid_cnt"])
+    assert final_p.tobytes() == d["final_p"].tobytes()
+
+
 @pytest.mark.parametrize("name", H.queue_names())
 def test_queue_port_matches_reference(name):
     qd = H.load_queue(name)
