@@ -316,7 +316,13 @@ def run_ours(args):
                       n_programs=wl.n_programs, max_rows=B, device=dev,
                       queue_capacity=wl.queue_capacity)
     wl.seed_state(gs.state)  # cfg4: 64k in flight + 64k queued, engines full
-    n_complete = wl.completions()
+    # cfg4: each tick the engines' running batches finish (record_completion
+    # on the in-flight log + freed slots); sharded runs free the slots only
+    completions = wl.completions()
+    n_complete = None
+    if completions is not None and world > 1:
+        n_complete = torch.bincount(completions[0].long(), minlength=K).to(torch.int32)
+        completions = None
     snap = gs.state.snapshot()
     n_distinct = 4
     host_cols = []
@@ -333,7 +339,7 @@ def run_ours(args):
     if args.graph and world == 1:
         gbatch = wl.batch(0)
         graph = TickGraph(gs, gbatch, n_iterations=1, restore_snapshot=snap,
-                          n_complete=n_complete)
+                          n_complete=n_complete, completions=completions)
 
     def tick(i, batch=None):
         src = batch if batch is not None else batches[i % n_distinct]
@@ -344,7 +350,8 @@ def run_ours(args):
             graph.replay()
             return
         gs.state.restore(snap)
-        sched.run_rows(src, n_iterations=1, n_complete=n_complete, stream=stream)
+        kw = {"completions": completions} if completions is not None else {}
+        sched.run_rows(src, n_iterations=1, n_complete=n_complete, stream=stream, **kw)
 
     clocks = ClockSampler(local, not args.no_clocks)
     for i in range(args.warmup):
@@ -383,7 +390,7 @@ def run_ours(args):
         for i in range(args.steps):
             gs.state.restore(snap)
             gs.run_rows(batches[i % n_distinct], n_iterations=1, n_complete=n_complete,
-                        stream=stream)
+                        stream=stream, completions=completions)
         torch.cuda.synchronize()
         prof = _lib.profile_read()
         _lib.profile_enable(False)

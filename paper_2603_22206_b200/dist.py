@@ -90,6 +90,11 @@ class ShardedScheduler:
     def run_rows(self, batch, n_iterations: int = 1, **kw) -> None:
         st = self.gs.state
         K = st.K
+        if kw.get("completions") is not None:
+            # each GPU's log holds only its own dispatches while (s, c) carries
+            # the global volume: recomputing from the local log would drop the
+            # other shards' contributions
+            raise NotImplementedError("monitor completions are single-GPU; pass n_complete")
         if self.mode == "A":
             s0 = st.inflight_sum.clone()
             c0 = st.inflight_comp.clone()

@@ -180,11 +180,20 @@ class Workload:
             seq=[per] * K, clock=[900.0] * K)
 
     def completions(self):
-        """cfg4: every engine's running batch turns over once per tick."""
+        """cfg4: every engine's running batch turns over once per tick: the
+        b_m oldest in-flight requests of engine m finish (record_completion
+        through chm_monitor_complete, then their slots free up). Returns
+        (model int32[n], key int64[n]) device tensors; the pre-seeded
+        entries of engine m have keys -1, -2, ... in insertion order."""
         if not self.spec.n_pre_queued:
             return None
-        return torch.tensor([self.pool[m].max_batch_size for m in self.pool.model_ids],
-                            dtype=torch.int32, device=self.device)
+        models, keys = [], []
+        for k, mid in enumerate(self.pool.model_ids):
+            b = self.pool[mid].max_batch_size
+            models += [k] * b
+            keys += list(range(-1, -b - 1, -1))
+        return (torch.tensor(models, dtype=torch.int32, device=self.device),
+                torch.tensor(keys, dtype=torch.int64, device=self.device))
 
     def router_reference(self, batch: RowBatch) -> np.ndarray:
         from oracle.encoder_ref import encoder_forward_fp32  # test infrastructure

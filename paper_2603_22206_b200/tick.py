@@ -19,12 +19,14 @@ from .scheduler import RowBatch
 
 class TickGraph:
     def __init__(self, scheduler, batch: RowBatch, n_iterations: int = 1,
-                 restore_snapshot: dict | None = None, warmup: int = 1, n_complete=None):
+                 restore_snapshot: dict | None = None, warmup: int = 1, n_complete=None,
+                 completions=None):
         self.gs = scheduler
         self.batch = batch
         self.snapshot = restore_snapshot
         self.n_iterations = n_iterations
         self.n_complete = n_complete
+        self.completions = completions
         dev = scheduler.device
         self.stream = torch.cuda.Stream(dev)
         _lib.profile_enable(False)
@@ -44,7 +46,7 @@ class TickGraph:
         if self.snapshot is not None:
             self.gs.state.restore(self.snapshot)
         self.gs.run_rows(self.batch, n_iterations=self.n_iterations, n_complete=self.n_complete,
-                         stream=torch.cuda.current_stream())
+                         stream=torch.cuda.current_stream(), completions=self.completions)
 
     def replay(self) -> None:
         self.graph.replay()
