@@ -45,7 +45,13 @@ def main():
                                                        b.data_ptr(), x.data_ptr(), g.data_ptr(),
                                                        be.data_ptr(), 1e-12, M, H, K, st), "ln")
 
+    def cublas(A, W, C):
+        return lambda: torch.matmul(A, W.t(), out=C)
+
     cases = {
+        "cublas_qkv": (cublas(x, w["qkv"], out_q), 2.0 * M * 3 * H * H),
+        "cublas_ffn1": (cublas(x, w["1"], out_f), 2.0 * M * F * H),
+        "cublas_ffn2": (cublas(f, w["2"], out_h), 2.0 * M * H * F),
         "qkv": (plain(x, w["qkv"], out_q, 3 * H, H, 1), 2.0 * M * 3 * H * H),
         "out_ln": (ln(out_h, w["o"], out_h, H), 2.0 * M * H * H),
         "ffn1_gelu": (plain(x, w["1"], out_f, F, H, 2), 2.0 * M * F * H),
