@@ -322,8 +322,8 @@ chm_status chm_qkv_attention_bf16(const void* x, const void* w_qkv, const float*
 /* Profiling: launch counters per kernel class (always on) and opt-in CUDA
  * event timing around every launch on its own stream. Classes: 0 GEMM,
  * 1 attention, 2 row-wise (embedding+LN, LayerNorm, head), 3 predictor,
- * 4 prepare, 5 select, 6 queue. chm_profile_read synchronises on the recorded
- * events, fills 7-entry arrays (timed launches, summed ms, summed algorithmic
+ * 4 prepare, 5 select, 6 queue, 7 fused QKV+attention. chm_profile_read
+ * synchronises on the recorded events, fills 8-entry arrays (timed launches, summed ms, summed algorithmic
  * work -- FLOPs or bytes --, cumulative launch counts) and clears the timings. */
 chm_status chm_profile_enable(int32_t enable);
 chm_status chm_profile_read(int32_t* timed, double* total_ms, double* work, int64_t* launches);

@@ -229,7 +229,8 @@ _SIGNATURES = [
     ("chm_profile_read", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]
 
-PROFILE_KINDS = ["gemm", "attention", "rowwise", "predict", "prepare", "select", "queue"]
+PROFILE_KINDS = ["gemm", "attention", "rowwise", "predict", "prepare", "select", "queue",
+                 "qkv_attention"]
 
 
 def profile_enable(on: bool) -> None:

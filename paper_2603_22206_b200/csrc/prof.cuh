@@ -16,7 +16,8 @@ enum Kind : int {
   K_PREPARE = 4,
   K_SELECT = 5,
   K_QUEUE = 6,
-  K_NUM = 7
+  K_QKV_ATTENTION = 7,  // fused QKV projection + attention (qkv_attn.cu)
+  K_NUM = 8
 };
 
 // Call around one kernel launch on `s`. `work` is the algorithmic FLOPs

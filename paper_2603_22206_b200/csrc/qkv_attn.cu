@@ -426,11 +426,11 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv, v
   const int citems = ((n_seq + CS - 1) / CS) * (n_heads / CH);
   const int n_cl = citems < max_clusters ? citems : max_clusters;
   cfg.gridDim = dim3(kCluster * n_cl, 1, 1);
-  prof::begin(prof::K_GEMM, st);
+  prof::begin(prof::K_QKV_ATTENTION, st);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, n_seq, n_heads, hidden,
                                      reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg);
   // tensor work: the projection (2 T 3H H) + S and O (4 S^2 64 per item)
-  prof::end(prof::K_GEMM, st,
+  prof::end(prof::K_QKV_ATTENTION, st,
             2.0 * T * 3.0 * hidden * hidden + 4.0 * qa::kS * qa::kS * 64.0 * n_seq * n_heads);
   if (e != cudaSuccess) return CHM_ERR_CUDA;
   CHM_LAUNCH_CHECK();
