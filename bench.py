@@ -249,6 +249,9 @@ def run_reference(args):
     import numpy as np
     import torch
 
+    # all host threads (torchrun sets OMP_NUM_THREADS=1 for its workers)
+    torch.set_num_threads(max(1, len(os.sched_getaffinity(0))))
+
     from oracle import hetsched_port as hp
     from paper_2603_22206_b200 import synth
     wl = synth.make_workload(args.config, device="cpu", with_router=False)
@@ -304,10 +307,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CHM_DIST_BACKEND=gloo: validation of the N > 1 flow on a box with fewer
+    # GPUs than ranks (ranks share devices); the measured path is NCCL
+    backend = os.environ.get("CHM_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     wl = synth.make_workload(args.config, device=dev)
     if args.attention == "unfused":
         wl.router.cfg_c.flags |= _lib.ENC_UNFUSED_ATTENTION

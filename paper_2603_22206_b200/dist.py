@@ -53,12 +53,22 @@ def mode_a_allreduce(s: torch.Tensor, c: torch.Tensor, s0: torch.Tensor,
     c.zero_()
 
 
+def _p2p_buffer(state: torch.Tensor, group) -> torch.Tensor:
+    # gloo point-to-point needs host tensors (NCCL takes the device tensor)
+    if state.is_cuda and dist.get_backend(group) == "gloo":
+        return state.cpu()
+    return state
+
+
 def relay_receive(state: torch.Tensor, group=None) -> None:
     """Mode B: before the selection chain, rank g > 0 receives the packed
     monitor state [2K] = (s, c) from rank g-1 (in place)."""
     rank = dist.get_rank(group)
     if rank > 0:
-        dist.recv(state, src=_global(rank - 1, group), group=group)
+        buf = _p2p_buffer(state, group)
+        dist.recv(buf, src=_global(rank - 1, group), group=group)
+        if buf is not state:
+            state.copy_(buf)
 
 
 def relay_forward(state: torch.Tensor, group=None) -> None:
@@ -66,9 +76,12 @@ def relay_forward(state: torch.Tensor, group=None) -> None:
     tick-end state so every rank starts the next tick from it."""
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
+    buf = _p2p_buffer(state, group)
     if rank + 1 < world:
-        dist.send(state, dst=_global(rank + 1, group), group=group)
-    dist.broadcast(state, src=_global(world - 1, group), group=group)
+        dist.send(buf, dst=_global(rank + 1, group), group=group)
+    dist.broadcast(buf, src=_global(world - 1, group), group=group)
+    if buf is not state:
+        state.copy_(buf)
 
 
 def _global(rank: int, group) -> int:
