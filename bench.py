@@ -55,6 +55,9 @@ def parse_args():
     p.add_argument("--attention", default="fused", choices=["fused", "unfused"],
                    help="S=128 router layers: fused QKV+attention kernel or QKV GEMM + "
                         "attention kernel (A/B measurement)")
+    p.add_argument("--layernorm", default="deferred", choices=["deferred", "cluster"],
+                   help="post-LN sublayers: deferred LayerNorm folded into the next GEMM "
+                        "(default) or normalised in a cluster-row GEMM epilogue (A/B)")
     p.add_argument("--graph", action="store_true",
                    help="replay the tick as a CUDA graph (1 GPU; per-kernel timing from an "
                         "eager profiled pass)")
@@ -322,6 +325,8 @@ def run_ours(args):
     wl = synth.make_workload(args.config, device=dev)
     if args.attention == "unfused":
         wl.router.cfg_c.flags |= _lib.ENC_UNFUSED_ATTENTION
+    if args.layernorm == "cluster":
+        wl.router.cfg_c.flags |= _lib.ENC_CLUSTER_LN
     B, K = wl.batch_size, len(wl.pool)
     gs = GpuScheduler(wl.pool, wl.balancer, wl.aging, router=wl.router, predictor=wl.predictor,
                       n_programs=wl.n_programs, max_rows=B, device=dev,
@@ -486,6 +491,7 @@ def run_ours(args):
                                    f"({'NCCL all-reduce' if args.mode == 'A' else 'NCCL relay'}"
                                    f" of the in-flight vector)") if world > 1 else "single GPU",
                    "cuda_graph": graph is not None,
+                   "layernorm": args.layernorm,
                    "attention": (args.attention if wl.spec.encoder.seq_len == 128
                                  else "flash (S>128)"),
                    "l2": "inputs larger than L2 (router activations >1 GB per layer)",

@@ -179,6 +179,10 @@ typedef struct chm_encoder_cfg {
  * (QKV written to HBM) instead of the fused S = 128 kernel. Same numerics;
  * kept for A/B measurement and parity tests. */
 #define CHM_ENC_UNFUSED_ATTENTION 1
+/* chm_encoder_cfg.flags: normalise every post-LN sublayer inside its own GEMM
+ * epilogue (rows owned by clusters of 2H/256 CTAs exchanging statistics over
+ * DSMEM) instead of the deferred LayerNorm. Same math; A/B measurement. */
+#define CHM_ENC_CLUSTER_LN 2
 
 /* bf16 weights, row-major [out_features, in_features] (nn.Linear layout). */
 typedef struct chm_encoder_weights {
@@ -208,6 +212,11 @@ typedef struct chm_encoder_workspace {
   void* ctx;                 /* [T, H]  attention output                       */
   void* tmp;                 /* [T, H]  pre-LN sum                             */
   void* ffn;                 /* [T, F]                                         */
+  void* stats;               /* chm_encoder_stats_bytes(): deferred-LayerNorm row
+                                statistics, (mean, M2) fp32 per 128 columns    */
+  void* folded;              /* chm_encoder_folded_bytes(): LayerNorm-folded
+                                QKV / FFN1 weights, written by
+                                chm_encoder_fold_weights()                      */
 } chm_encoder_workspace;
 
 /* ---- entry points -------------------------------------------------------- */
@@ -281,6 +290,18 @@ chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* aging,
                           const chm_rows* rows, const chm_decisions* dec,
                           int32_t n_iterations, int32_t* error, void* stream);
 
+/* Deferred LayerNorm. The encoder does not normalise a sublayer output where
+ * it is produced: out-projection and FFN2 write the pre-LN sum plus per-row
+ * partial statistics, and the next projection folds the LayerNorm in
+ * (LN(x).W^T + b = rstd (x.W'^T) - rstd mean c + b', W' = W diag(gamma),
+ * c = W' row sums, b' = b + W beta). The folded QKV / FFN1 weights live in
+ * the workspace; chm_encoder_fold_weights() (re)computes them and must run
+ * after the weights are loaded or changed, before chm_encoder_forward. */
+uint64_t chm_encoder_folded_bytes(const chm_encoder_cfg* cfg);
+uint64_t chm_encoder_stats_bytes(const chm_encoder_cfg* cfg, int64_t max_tokens);
+chm_status chm_encoder_fold_weights(const chm_encoder_cfg* cfg, const chm_encoder_weights* w,
+                                    const chm_encoder_workspace* ws, void* stream);
+
 /* Router encoder forward over `n_seq` sequences of `seq_len` token ids, only
  * for the rows listed in `rows` (NULL = all, n_seq rows). Writes
  * q[rows[i]*K + m] = sigmoid(head(h_CLS)). `scratch_q` may be NULL. */
@@ -304,6 +325,19 @@ chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bia
 chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, const float* bias,
                             const void* residual, const float* gamma, const float* beta,
                             float eps, int32_t M, int32_t N, int32_t K, void* stream);
+
+/* Deferred-LayerNorm GEMMs (the encoder's sublayers):
+ *  epilogue 1 / 2 (bias / bias+GELU) with stats_in: C = [GELU](rstd (A.B^T)
+ *      - rstd mean colsum + bias), i.e. the LayerNorm of A's rows folded in
+ *      (B, colsum, bias from chm_encoder_fold_weights' rule);
+ *  epilogue 6: C = A.B^T + bias + R, R = residual, or LN(residual) with
+ *      gamma/beta when stats_in is given; writes stats_out[M][N/128].
+ * stats_in = [M][n_part] (mean, M2) partials over 128 columns each. */
+chm_status chm_gemm_bf16_deferred_ln(const void* A, const void* B, void* C, const float* bias,
+                                     int32_t epilogue, const void* residual, const float* gamma,
+                                     const float* beta, const void* stats_in, int32_t n_part,
+                                     const float* colsum, void* stats_out, float eps, int32_t M,
+                                     int32_t N, int32_t K, void* stream);
 
 /* Encoder self-attention sublayer core (no mask, head dim 64), the kernel the
  * encoder runs between its QKV projection and out-projection:

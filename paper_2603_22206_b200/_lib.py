@@ -150,6 +150,7 @@ class EncoderCfg(ctypes.Structure):
 
 
 ENC_UNFUSED_ATTENTION = 1
+ENC_CLUSTER_LN = 2
 
 
 class EncoderWeights(ctypes.Structure):
@@ -184,6 +185,8 @@ class EncoderWorkspace(ctypes.Structure):
         ("ctx", c_void_p),
         ("tmp", c_void_p),
         ("ffn", c_void_p),
+        ("stats", c_void_p),
+        ("folded", c_void_p),
     ]
 
 
@@ -217,6 +220,13 @@ _SIGNATURES = [
     ("chm_gemm_bf16_ln", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_int32,
       c_int32, c_int32, c_void_p]),
+    ("chm_gemm_bf16_deferred_ln", c_int32,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_int32, c_void_p, c_void_p, c_float, c_int32, c_int32, c_int32, c_void_p]),
+    ("chm_encoder_folded_bytes", ctypes.c_uint64, [POINTER(EncoderCfg)]),
+    ("chm_encoder_stats_bytes", ctypes.c_uint64, [POINTER(EncoderCfg), ctypes.c_int64]),
+    ("chm_encoder_fold_weights", c_int32,
+     [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p]),
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
     ("chm_monitor_complete", c_int32,
      [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_int32, c_void_p, c_void_p,

@@ -11,17 +11,16 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include "common.cuh"
+#include "deferred_ln.cuh"
+#include "gemm.cuh"
 #include "sm100.cuh"
 #include "prof.cuh"
 
 namespace chm {
 
-chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
-                     const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
-                     void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
-                     float eps, long long res_ld = 0);
-chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv, void* ctx,
-                         int n_seq, int hidden, cudaStream_t st);
+chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
+                         const float* c_qkv, const float2* stats_in, int n_part, float eps,
+                         void* ctx, int n_seq, int hidden, cudaStream_t st);
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, uint64_t ld);
@@ -820,6 +819,103 @@ __global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restri
   }
 }
 
+// Deferred-LayerNorm weight folding (once per weight load, not per tick):
+//   W'[n,k] = bf16(W[n,k] * gamma[k]),  c[n] = sum_k W'[n,k] (fp32 over the
+//   bf16 values the tensor cores multiply),  b'[n] = b[n] + sum_k W[n,k] beta[k],
+// so that LN(x) . W^T + b = rstd (x . W'^T) - rstd mean c + b' per row.
+// gamma == nullptr: identity (W' = W, b' = b). One warp per output row.
+__global__ void __launch_bounds__(256) fold_ln_kernel(const __nv_bfloat16* __restrict__ W,
+                                                      const float* __restrict__ b,
+                                                      const float* __restrict__ g,
+                                                      const float* __restrict__ be, int N,
+                                                      int K, __nv_bfloat16* __restrict__ Wf,
+                                                      float* __restrict__ c,
+                                                      float* __restrict__ bf) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * 8 + warp;
+  if (n >= N) return;
+  float cs = 0.f, bs = 0.f;
+  for (int k0 = lane * 8; k0 < K; k0 += 256) {
+    const uint4 u = *reinterpret_cast<const uint4*>(W + (size_t)n * K + k0);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      const int k = k0 + 2 * e;
+      const __nv_bfloat162 pk =
+          g ? __floats2bfloat162_rn(f.x * g[k], f.y * g[k + 1]) : h[e];
+      const float2 pf = __bfloat1622float2(pk);
+      cs += pf.x + pf.y;
+      if (be) bs += f.x * be[k] + f.y * be[k + 1];
+      o[e] = pk;
+    }
+    *reinterpret_cast<uint4*>(Wf + (size_t)n * K + k0) = *reinterpret_cast<uint4*>(o);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    bs += __shfl_xor_sync(0xffffffffu, bs, o);
+  }
+  if (lane == 0) {
+    c[n] = cs;
+    bf[n] = b[n] + bs;
+  }
+}
+
+// out[i] = LN(x[i*S]) for the [CLS] row of every sequence, from the deferred
+// statistics (stats == nullptr: the row is already normalised, plain gather).
+// Residual input of the last layer's CLS-only sublayers. Warp per row.
+template <int VEC>
+__global__ void __launch_bounds__(256) ln_rows_kernel(const __nv_bfloat16* __restrict__ x, int S,
+                                                      int n_seq, const float2* __restrict__ stats,
+                                                      int P, const float* __restrict__ g,
+                                                      const float* __restrict__ be, float eps,
+                                                      __nv_bfloat16* __restrict__ out) {
+  constexpr int H = 32 * 8 * VEC;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= n_seq) return;
+  float v[VEC * 8];
+  load_row<VEC>(x + (size_t)i * S * H, lane, v);
+  float a = 1.f, b = 0.f;
+  if (stats) row_affine(stats + (size_t)i * S * P, P, eps, a, b);
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) {
+    const int col = (c * 32 + lane) * 8;
+    __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float x0 = v[c * 8 + 2 * e], x1 = v[c * 8 + 2 * e + 1];
+      if (stats) {
+        x0 = fmaf(fmaf(a, x0, b), g[col + 2 * e], be[col + 2 * e]);
+        x1 = fmaf(fmaf(a, x1, b), g[col + 2 * e + 1], be[col + 2 * e + 1]);
+      }
+      o[e] = __floats2bfloat162_rn(x0, x1);
+    }
+    *reinterpret_cast<uint4*>(out + (size_t)i * H + col) = *reinterpret_cast<uint4*>(o);
+  }
+}
+
+// Per-layer block of folded weights inside chm_encoder_workspace.folded.
+struct FoldedLayout {
+  size_t wqkv, cqkv, bqkv, w1, c1, b1, per_layer;
+};
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+static FoldedLayout folded_layout(const chm_encoder_cfg& c) {
+  const size_t H = (size_t)c.hidden, F = (size_t)c.ffn;
+  FoldedLayout f;
+  size_t o = 0;
+  f.wqkv = o; o = align256(o + 3 * H * H * 2);
+  f.cqkv = o; o = align256(o + 3 * H * 4);
+  f.bqkv = o; o = align256(o + 3 * H * 4);
+  f.w1 = o;   o = align256(o + F * H * 2);
+  f.c1 = o;   o = align256(o + F * 4);
+  f.b1 = o;   o = align256(o + F * 4);
+  f.per_layer = o;
+  return f;
+}
+
 static int n_sms() {
   static int n = 0;
   if (!n) {
@@ -888,24 +984,55 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   prof::end(prof::K_ROWWISE, st, (double)T * (4.0 + 6.0 * H));
   CHM_LAUNCH_CHECK();
   const int NH = H / 64;
+  const int P = H / kLnPartCols;
+  const float eps = cfg.ln_eps;
+  // Deferred LayerNorm (deferred_ln.cuh): x holds the pre-LN2 stream u_l with
+  // row statistics st_u, tmp the pre-LN1 sum v_l with st_v. The QKV projection
+  // and FFN1 fold the pending LayerNorm into their epilogues (folded weights),
+  // out-projection and FFN2 normalise their residual box and emit the
+  // statistics of their own output: no sublayer needs a whole row per cluster.
+  float2* st_u = reinterpret_cast<float2*>(ws.stats);
+  float2* st_v = st_u + (size_t)ws.max_tokens * P;
+  const FoldedLayout FL = folded_layout(cfg);
   chm_status rc;
   const bool fused = S == kAttnS && !(cfg.flags & CHM_ENC_UNFUSED_ATTENTION);
+  // A/B measurement: the cluster-LayerNorm path (each post-LN sublayer
+  // normalised in its own GEMM epilogue, rows owned by 2H/256-CTA clusters)
+  const bool cluster_ln = (cfg.flags & CHM_ENC_CLUSTER_LN) != 0;
   for (int l = 0; l < L; ++l) {
+    const uint8_t* fb = reinterpret_cast<const uint8_t*>(ws.folded) + (size_t)l * FL.per_layer;
+    const void* wq = cluster_ln ? w.w_qkv[l] : fb + FL.wqkv;
+    const float* cq = reinterpret_cast<const float*>(fb + FL.cqkv);
+    const float* bq = cluster_ln ? w.b_qkv[l] : reinterpret_cast<const float*>(fb + FL.bqkv);
+    // layer 0 reads the embedding LayerNorm's (normalised) output
+    const float2* st_in = (l == 0 || cluster_ln) ? nullptr : st_u;
+    const float* g_prev = l == 0 ? nullptr : w.ln2_g[l - 1];
+    const float* b_prev = l == 0 ? nullptr : w.ln2_b[l - 1];
     if (fused && l < L - 1) {
       // QKV projection + attention in one kernel (qkv_attn.cu)
-      rc = qkv_attention(x, w.w_qkv[l], w.b_qkv[l], ctx, n_seq, H, st);
+      rc = qkv_attention(x, wq, bq, cq, st_in, P, eps, ctx, n_seq, H, st);
       if (rc != CHM_OK) return rc;
     } else {
-      rc = gemm_bf16(x, w.w_qkv[l], qk, w.b_qkv[l], nullptr, (int)T, 3 * H, H, 4, st, nullptr,
-                     H, S, nullptr, nullptr, 0.f);
+      GemmArgs g;
+      g.epilogue = 4;
+      g.bias = bq;
+      g.hidden = H;
+      g.stats_in = st_in;
+      g.n_part = P;
+      g.colsum = cq;
+      g.eps = eps;
+      rc = gemm_run(x, wq, qk, (int)T, 3 * H, H, g, st);
       if (rc != CHM_OK) return rc;
     }
     if (l == L - 1) {
       // Last layer: only h_[CLS] reaches the router head, so attention runs
       // for the CLS query of every (sequence, head) and the rest of the layer
-      // for n_seq rows. ctx_c = ctx[:n_seq], xc = tmp[:n_seq] (compact).
+      // for n_seq rows. ctx_c = ctx[:n_seq], xc = tmp[:n_seq], hc = the
+      // normalised layer input of the CLS rows (in the qkv buffer, free once
+      // the CLS attention has read it).
       auto* ctx_c = ctx;
       auto* xc = tmp;
+      auto* hc = qk;
       const int items = n_seq * NH;
       const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
       prof::begin(prof::K_ATTENTION, st);
@@ -917,14 +1044,33 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       }
       prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
       CHM_LAUNCH_CHECK();
-      rc = gemm_bf16(ctx_c, w.w_o[l], xc, w.b_o[l], x, n_seq, H, H, 5, st, nullptr, 0, 0,
-                     w.ln1_g[l], w.ln1_b[l], cfg.ln_eps, (long long)S * H);
+      prof::begin(prof::K_ROWWISE, st);
+      ln_rows_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(x, S, n_seq, st_in, P,
+                                                                       g_prev, b_prev, eps, hc);
+      prof::end(prof::K_ROWWISE, st, (double)n_seq * (4.0 * H + 8.0 * P));
+      CHM_LAUNCH_CHECK();
+      GemmArgs go;
+      go.epilogue = 5;
+      go.bias = w.b_o[l];
+      go.residual = hc;
+      go.gamma = w.ln1_g[l];
+      go.beta = w.ln1_b[l];
+      go.eps = eps;
+      rc = gemm_run(ctx_c, w.w_o[l], xc, n_seq, H, H, go, st);
       if (rc != CHM_OK) return rc;
-      rc = gemm_bf16(xc, w.w_1[l], ffn, w.b_1[l], nullptr, n_seq, F, H, 2, st, nullptr, 0, 0,
-                     nullptr, nullptr, 0.f, 0);
+      GemmArgs g1;
+      g1.epilogue = 2;
+      g1.bias = w.b_1[l];
+      rc = gemm_run(xc, w.w_1[l], ffn, n_seq, F, H, g1, st);
       if (rc != CHM_OK) return rc;
-      rc = gemm_bf16(ffn, w.w_2[l], xc, w.b_2[l], xc, n_seq, H, F, 5, st, nullptr, 0, 0,
-                     w.ln2_g[l], w.ln2_b[l], cfg.ln_eps, 0);
+      GemmArgs g2;
+      g2.epilogue = 5;
+      g2.bias = w.b_2[l];
+      g2.residual = xc;
+      g2.gamma = w.ln2_g[l];
+      g2.beta = w.ln2_b[l];
+      g2.eps = eps;
+      rc = gemm_run(ffn, w.w_2[l], xc, n_seq, H, F, g2, st);
       if (rc != CHM_OK) return rc;
       break;
     }
@@ -932,16 +1078,67 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       rc = run_attention(qk, ctx, n_seq, S, H, st);
       if (rc != CHM_OK) return rc;
     }
-    // out-projection + residual + LayerNorm fused (x updated in place)
-    rc = gemm_bf16(ctx, w.w_o[l], x, w.b_o[l], x, (int)T, H, H, 5, st, nullptr, 0, 0,
-                   w.ln1_g[l], w.ln1_b[l], cfg.ln_eps);
+    if (cluster_ln) {
+      GemmArgs go;
+      go.epilogue = 5;
+      go.bias = w.b_o[l];
+      go.residual = x;
+      go.gamma = w.ln1_g[l];
+      go.beta = w.ln1_b[l];
+      go.eps = eps;
+      rc = gemm_run(ctx, w.w_o[l], x, (int)T, H, H, go, st);
+      if (rc != CHM_OK) return rc;
+      GemmArgs g1;
+      g1.epilogue = 2;
+      g1.bias = w.b_1[l];
+      rc = gemm_run(x, w.w_1[l], ffn, (int)T, F, H, g1, st);
+      if (rc != CHM_OK) return rc;
+      GemmArgs g2;
+      g2.epilogue = 5;
+      g2.bias = w.b_2[l];
+      g2.residual = x;
+      g2.gamma = w.ln2_g[l];
+      g2.beta = w.ln2_b[l];
+      g2.eps = eps;
+      rc = gemm_run(ffn, w.w_2[l], x, (int)T, H, F, g2, st);
+      if (rc != CHM_OK) return rc;
+      continue;
+    }
+    // out-projection: v = ctx.Wo^T + b_o + LN2_{l-1}(u_l) -> tmp, statistics -> st_v
+    GemmArgs go;
+    go.epilogue = 6;
+    go.bias = w.b_o[l];
+    go.residual = x;
+    go.gamma = g_prev;
+    go.beta = b_prev;
+    go.stats_in = st_in;
+    go.n_part = P;
+    go.stats_out = st_v;
+    go.eps = eps;
+    rc = gemm_run(ctx, w.w_o[l], tmp, (int)T, H, H, go, st);
     if (rc != CHM_OK) return rc;
-    rc = gemm_bf16(x, w.w_1[l], ffn, w.b_1[l], nullptr, (int)T, F, H, 2, st, nullptr, 0, 0,
-                   nullptr, nullptr, 0.f);
+    // FFN1 on LN1(v), folded: W1' = W1 diag(ln1_g), b1' = b1 + W1 ln1_b
+    GemmArgs g1;
+    g1.epilogue = 2;
+    g1.bias = reinterpret_cast<const float*>(fb + FL.b1);
+    g1.colsum = reinterpret_cast<const float*>(fb + FL.c1);
+    g1.stats_in = st_v;
+    g1.n_part = P;
+    g1.eps = eps;
+    rc = gemm_run(tmp, fb + FL.w1, ffn, (int)T, F, H, g1, st);
     if (rc != CHM_OK) return rc;
-    // FFN2 + residual + LayerNorm fused (x updated in place)
-    rc = gemm_bf16(ffn, w.w_2[l], x, w.b_2[l], x, (int)T, H, F, 5, st, nullptr, 0, 0,
-                   w.ln2_g[l], w.ln2_b[l], cfg.ln_eps);
+    // FFN2: u_{l+1} = f.W2^T + b_2 + LN1(v) -> x, statistics -> st_u
+    GemmArgs g2;
+    g2.epilogue = 6;
+    g2.bias = w.b_2[l];
+    g2.residual = tmp;
+    g2.gamma = w.ln1_g[l];
+    g2.beta = w.ln1_b[l];
+    g2.stats_in = st_v;
+    g2.n_part = P;
+    g2.stats_out = st_u;
+    g2.eps = eps;
+    rc = gemm_run(ffn, w.w_2[l], x, (int)T, H, F, g2, st);
     if (rc != CHM_OK) return rc;
   }
   prof::begin(prof::K_ROWWISE, st);
@@ -954,6 +1151,43 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
 
 }  // namespace enc
 }  // namespace chm
+
+extern "C" uint64_t chm_encoder_folded_bytes(const chm_encoder_cfg* cfg) {
+  if (!cfg || cfg->n_layers < 1 || cfg->hidden <= 0 || cfg->ffn <= 0) return 0;
+  return (uint64_t)chm::enc::folded_layout(*cfg).per_layer * (uint64_t)cfg->n_layers;
+}
+
+extern "C" uint64_t chm_encoder_stats_bytes(const chm_encoder_cfg* cfg, int64_t max_tokens) {
+  if (!cfg || cfg->hidden <= 0 || max_tokens < 0) return 0;
+  return 2ull * (uint64_t)max_tokens * (uint64_t)(cfg->hidden / chm::kLnPartCols) * 8ull;
+}
+
+extern "C" chm_status chm_encoder_fold_weights(const chm_encoder_cfg* cfg,
+                                               const chm_encoder_weights* w,
+                                               const chm_encoder_workspace* ws, void* stream) {
+  if (!cfg || !w || !ws || !ws->folded) return CHM_ERR_INVALID_ARG;
+  const int H = cfg->hidden, F = cfg->ffn, L = cfg->n_layers;
+  if (L < 1 || H % chm::kLnPartCols != 0 || H / chm::kLnPartCols > chm::kLnMaxParts ||
+      F % 64 != 0)
+    return CHM_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const chm::enc::FoldedLayout FL = chm::enc::folded_layout(*cfg);
+  for (int l = 0; l < L; ++l) {
+    uint8_t* fb = reinterpret_cast<uint8_t*>(ws->folded) + (size_t)l * FL.per_layer;
+    chm::enc::fold_ln_kernel<<<(unsigned)((3 * H + 7) / 8), 256, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(w->w_qkv[l]), w->b_qkv[l],
+        l ? w->ln2_g[l - 1] : nullptr, l ? w->ln2_b[l - 1] : nullptr, 3 * H, H,
+        reinterpret_cast<__nv_bfloat16*>(fb + FL.wqkv), reinterpret_cast<float*>(fb + FL.cqkv),
+        reinterpret_cast<float*>(fb + FL.bqkv));
+    CHM_LAUNCH_CHECK();
+    chm::enc::fold_ln_kernel<<<(unsigned)((F + 7) / 8), 256, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(w->w_1[l]), w->b_1[l], w->ln1_g[l], w->ln1_b[l],
+        F, H, reinterpret_cast<__nv_bfloat16*>(fb + FL.w1), reinterpret_cast<float*>(fb + FL.c1),
+        reinterpret_cast<float*>(fb + FL.b1));
+    CHM_LAUNCH_CHECK();
+  }
+  return CHM_OK;
+}
 
 extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
                                           const chm_encoder_weights* w,
@@ -970,6 +1204,7 @@ extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
       cfg->n_models > CHM_MAX_MODELS || cfg->ffn % 64 != 0)
     return CHM_ERR_INVALID_ARG;
   if ((long long)n_seq * seq_len > ws->max_tokens) return CHM_ERR_INVALID_ARG;
+  if (!ws->stats || !ws->folded) return CHM_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   switch (cfg->hidden) {
     case 256:

@@ -34,6 +34,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include "common.cuh"
+#include "deferred_ln.cuh"
+#include "gemm.cuh"
 #include "prof.cuh"
 #include "sm100.cuh"
 
@@ -42,7 +44,6 @@ namespace gemm {
 
 constexpr int BM = 256, BN = 256, BK = 64;  // pair tile
 constexpr int CM = 128, CN = 128;           // per-CTA operand rows (A half, B half)
-constexpr int kStages = 4;
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 constexpr uint32_t kTileABytes = CM * BK * 2;  // 16 KB
@@ -61,32 +62,50 @@ enum Epilogue : int {
   EPI_QKV = 4,
   // C = LayerNorm(A.B^T + bias + residual) * gamma + beta, N = 256 g.
   EPI_RESIDUAL_LN = 5,
+  // Deferred LayerNorm (post-LN sublayer without whole-row ownership):
+  //   C = A.B^T + bias + LN(residual)   (LN(residual) = residual when no
+  //   statistics are given), plus per-row partial statistics (mean, M2) of C
+  //   over every 128-column chunk -> stats_out[M][N/128]. The consumer
+  //   applies the LayerNorm: the next GEMM folds it into its epilogue
+  //   (EPI_BIAS / EPI_BIAS_GELU / EPI_QKV with stats_in + colsum, weights
+  //   pre-scaled by gamma: LN(x).W^T = rstd (x.W'^T) - rstd mean c + W.beta),
+  //   the next residual sublayer normalises its residual box here.
+  EPI_RESLN_STATS = 6,
 };
 
 struct EpiParams {
-  __nv_bfloat16* vt;   // QKV: [n_seq, n_heads, 64, seq_len]
   int hidden;          // QKV: H
-  int seq_len;         // QKV: S (multiple of 128)
   const float* gamma;  // LN
   const float* beta;   // LN
   float eps;           // LN
   long long res_ld;    // residual row pitch in elements (0 = N)
+  const float2* stats_in;  // deferred LN of the A rows (fold) / residual rows (EPI 6):
+  int n_part;              //   [M][n_part] partial (mean, M2) over 128 columns each
+  const float* colsum;     // fold: c_n = sum_k B'[n][k]
+  float2* stats_out;       // EPI 6: [M][N/128]
+  int dbg;             // measurement only: 1 = epilogue drains TMEM without math/stores,
+                       // 2 = also no operand loads (MMAs on stale shared memory)
 };
 
-struct __align__(1024) Smem {
-  uint8_t tiles[kStages][kStageBytes];          // A (16 KB) then B (16 KB) per stage
-  uint8_t stage_out[kEpiWarps][2][kBoxBytes];   // epilogue boxes (SW128)
-  float2 stats[2][kMaxLnGroups][2][CM];         // LN partials [buf][src pair][half][row]
-  float ln_vec[3][BN];                          // LN: bias, gamma, beta of this CTA's columns
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+// STAGES-deep operand ring; NBOX epilogue staging boxes per warp (2 lets a
+// warp fill one box while the TMA store of the other drains); the LN
+// statistics exchange exists only in the LN variant.
+template <int STAGES, int NBOX, bool LN>
+struct __align__(1024) SmemT {
+  uint8_t tiles[STAGES][kStageBytes];                // A (16 KB) then B (16 KB) per stage
+  uint8_t stage_out[kEpiWarps][NBOX][kBoxBytes];     // epilogue boxes (SW128)
+  float2 stats[LN ? 2 : 1][LN ? kMaxLnGroups : 1][LN ? 2 : 1][LN ? CM : 1];  // [buf][pair][half][row]
+  float ln_vec[LN ? 3 : 1][LN ? BN : 1];             // LN: bias, gamma, beta of this CTA's columns
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint64_t res_bar[kEpiWarps][2];
   uint64_t stats_bar[2];
   uint32_t tmem_base;
 };
-constexpr size_t kSmemBytes = sizeof(Smem) + 1024;  // + alignment slack
+template <int STAGES, int NBOX, bool LN>
+constexpr size_t smem_bytes() { return sizeof(SmemT<STAGES, NBOX, LN>) + 1024; }  // + alignment slack
 
 // GELU, tanh form: 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))), with the
 // hardware tanh (MUFU). oracle/encoder_ref.py uses the same definition.
@@ -119,6 +138,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
+__device__ __forceinline__ void ld8(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
 // v[0..63] = acc + bias + residual for this thread's row and a 64-column chunk.
 // `bias_s` points at the chunk's first column in the staged shared-memory copy.
 __device__ __forceinline__ void load_chunk_ln(const uint32_t (&r0)[32], const uint32_t (&r1)[32],
@@ -140,7 +166,7 @@ __device__ __forceinline__ void load_chunk_ln(const uint32_t (&r0)[32], const ui
   }
 }
 
-template <int EPI>
+template <int EPI, int kStages>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                 const __grid_constant__ CUtensorMap tmap_b,
@@ -148,6 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __grid_constant__ CUtensorMap tmap_r, const float* __restrict__ bias,
                 int M, int N, int K, EpiParams ep) {
   constexpr bool kLN = EPI == EPI_RESIDUAL_LN;
+  constexpr int kBoxes = kStages > 4 ? 1 : 2;
+  using Smem = SmemT<kStages, kBoxes, kLN>;
   const int ln_groups = kLN ? N / BN : 1;
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -171,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::tma_prefetch(&tmap_a);
     sm100::tma_prefetch(&tmap_b);
     sm100::tma_prefetch(&tmap_c);
-    if (EPI == EPI_BIAS_RESIDUAL || kLN) sm100::tma_prefetch(&tmap_r);
+    if (EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESLN_STATS || kLN) sm100::tma_prefetch(&tmap_r);
     for (int i = 0; i < kStages; ++i) {
       sm100::mbar_init(&s.full[i], 1);
       sm100::mbar_init(&s.empty[i], 1);
@@ -203,6 +231,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
           const uint32_t full_leader =
               sm100::mapa(sm100::smem_u32(&s.full[stage]), leader_rank);
+          if (ep.dbg == 2) {
+            if (leader) sm100::mbar_arrive(&s.full[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (leader) sm100::mbar_arrive_expect_tx(&s.full[stage], 2 * kStageBytes);
           uint8_t* base = s.tiles[stage];
           sm100::tma_load_2d_cg2(base, &tmap_a, full_leader, kb * BK, m0);
@@ -271,6 +304,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n_tile0 = (kLN ? (int)pair : (t % n_tiles_n)) * BN + half * 128;
       const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN +
                                  half * 128;
+      if (ep.dbg != 0) {
+        sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
+        sm100::tc_fence_after();
+        sm100::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive_remote(acc ? empty_leader1 : empty_leader0);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       if constexpr (kLN) {
         // ---- residual + LayerNorm epilogue ----
         if (lane == 0) {
@@ -385,19 +427,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         // ---- pointwise epilogues ----
+        constexpr bool kRes = EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESLN_STATS;
+        constexpr bool kFold = EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_QKV;
+        const int row = mrow0 + lane;
+        // Deferred LayerNorm of this thread's row (statistics from the producer
+        // GEMM's partials; loaded before the accumulator wait so the L2
+        // latency overlaps the MMAs). fold: v = rs_a acc + (rs_b c_n + b_n);
+        // EPI_RESLN_STATS: LN(r) = (rs_a r + rs_b) gamma_n + beta_n.
+        float rs_a = 1.f, rs_b = 0.f;
+        const bool have_stats = ep.stats_in != nullptr;
+        if (have_stats && row < M) row_affine(ep.stats_in + (size_t)row * ep.n_part, ep.n_part,
+                                              ep.eps, rs_a, rs_b);
+        float sh = 0.f, s1 = 0.f, s2 = 0.f;  // EPI_RESLN_STATS: shifted sums of the output row
+        if constexpr (kRes) {
+          // residual boxes of both chunks requested before the accumulator
+          // wait: their HBM latency overlaps the MMAs instead of the epilogue
+          // (box c <- chunk c; both boxes are free once the previous tile's
+          // stores have read them)
+          static_assert(kBoxes == 2, "residual epilogues stage both chunks");
+          if (lane == 0) {
+            sm100::bulk_wait_read<0>();
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              if (n_tile0 + c * 64 < N) {
+                sm100::mbar_arrive_expect_tx(&s.res_bar[ew][c], kBoxBytes);
+                sm100::tma_load_2d(s.stage_out[ew][c], &tmap_r, &s.res_bar[ew][c],
+                                   n_tile0 + c * 64, mrow0);
+              }
+            }
+          }
+          __syncwarp();
+        }
         sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
         sm100::tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
           const int col0 = n_tile0 + c * 64;
+          if (kRes) box = c;
           uint8_t* sb = s.stage_out[ew][box];
           // the box is free once the TMA store issued from it two chunks ago
           // has finished reading shared memory
-          if (lane == 0) sm100::bulk_wait_read<1>();
-          __syncwarp();
-          if (EPI == EPI_BIAS_RESIDUAL && lane == 0 && col0 < N) {
-            sm100::mbar_arrive_expect_tx(&s.res_bar[ew][box], kBoxBytes);
-            sm100::tma_load_2d(sb, &tmap_r, &s.res_bar[ew][box], col0, mrow0);
+          if (!kRes) {
+            if (lane == 0) sm100::bulk_wait_read<kBoxes - 1>();
+            __syncwarp();
           }
           uint32_t r0[32], r1[32];
           sm100::tmem_ld_32x32b_x32(lane_base + c * 64, r0);
@@ -410,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) sm100::mbar_arrive_remote(acc ? empty_leader1 : empty_leader0);
           }
           if (col0 >= N) continue;
-          if (EPI == EPI_BIAS_RESIDUAL) {
+          if (kRes) {
             sm100::mbar_wait(&s.res_bar[ew][box], (res_phase >> box) & 1);
             res_phase ^= 1u << box;
           }
@@ -423,25 +495,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 8; ++e)
               v[e] = __uint_as_float(j < 4 ? r0[j * 8 + e] : r1[(j - 4) * 8 + e]);
             if (EPI != EPI_NONE) {
-              const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + col0 + j * 8));
-              const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + col0 + j * 8 + 4));
-              v[0] += b0.x; v[1] += b0.y; v[2] += b0.z; v[3] += b0.w;
-              v[4] += b1.x; v[5] += b1.y; v[6] += b1.z; v[7] += b1.w;
+              float bb[8];
+              ld8(bias + col0 + j * 8, bb);
+              if (kFold && have_stats) {
+                float cc[8];
+                ld8(ep.colsum + col0 + j * 8, cc);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = fmaf(rs_a, v[e], fmaf(rs_b, cc[e], bb[e]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] += bb[e];
+              }
             }
             uint4* slot = reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4));
-            if (EPI == EPI_BIAS_RESIDUAL) {
+            if (kRes) {
               const uint4 u = *slot;
               const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+              float r[8];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 f = __bfloat1622float2(h[e]);
-                v[2 * e] += f.x;
-                v[2 * e + 1] += f.y;
+                r[2 * e] = f.x;
+                r[2 * e + 1] = f.y;
               }
+              if (EPI == EPI_RESLN_STATS && have_stats) {
+                float gg[8], be[8];
+                ld8(ep.gamma + col0 + j * 8, gg);
+                ld8(ep.beta + col0 + j * 8, be);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) r[e] = fmaf(fmaf(rs_a, r[e], rs_b), gg[e], be[e]);
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] += r[e];
             }
             if (EPI == EPI_BIAS_GELU) {
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[e] = gelu_tanh(v[e]);
+            }
+            if (EPI == EPI_RESLN_STATS) {
+              if (c == 0 && j == 0) sh = v[0];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float d = v[e] - sh;
+                s1 += d;
+                s2 = fmaf(d, d, s2);
+              }
             }
             uint4 o;
             o.x = pack_bf16(v[0] * qscale, v[1] * qscale);
@@ -456,7 +554,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tma_store_2d(&tmap_c, sb, col0, mrow0);
             sm100::bulk_commit();
           }
-          box ^= 1;
+          if (kBoxes == 2 && !kRes) box ^= 1;
+        }
+        if (EPI == EPI_RESLN_STATS && row < M) {
+          // (mean, M2) of the fp32 (pre-rounding) output over this thread's
+          // 128 columns: partial n_tile0 / 128 of the row
+          const float mean = sh + s1 * (1.0f / 128.0f);
+          const float m2 = fmaxf(fmaf(-s1, s1 * (1.0f / 128.0f), s2), 0.0f);
+          ep.stats_out[(size_t)row * (N / 128) + n_tile0 / 128] = make_float2(mean, m2);
         }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -513,7 +618,7 @@ static int num_sms() {
   return n;
 }
 
-template <int EPI>
+template <int EPI, int kStages>
 static chm_status launch(const void* A, const void* B, void* C, const float* bias,
                          const void* residual, int M, int N, int K, EpiParams ep,
                          cudaStream_t s) {
@@ -521,15 +626,17 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   if (!make_tmap_bf16(&ta, A, (uint64_t)M, (uint64_t)K, CM, BK, 0)) return CHM_ERR_CUDA;
   if (!make_tmap_bf16(&tb, B, (uint64_t)N, (uint64_t)K, CN, BK, 0)) return CHM_ERR_CUDA;
   if (!make_tmap_bf16(&tc, C, (uint64_t)M, (uint64_t)N, 32, 64, 0)) return CHM_ERR_CUDA;
-  if (EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESIDUAL_LN) {
+  if (EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESIDUAL_LN || EPI == EPI_RESLN_STATS) {
     if (!make_tmap_bf16(&tr, residual, (uint64_t)M, (uint64_t)N, 32, 64, (uint64_t)ep.res_ld))
       return CHM_ERR_CUDA;
   } else {
     tr = tc;
   }
+  constexpr size_t kSmemBytes =
+      smem_bytes<kStages, (kStages > 4 ? 1 : 2), EPI == EPI_RESIDUAL_LN>();
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_kernel<EPI, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kSmemBytes);
     attr_set = true;
   }
@@ -550,11 +657,11 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   // Persistent grid: only as many clusters as can be co-resident (clusters
   // must fit inside a GPC, so e.g. 6-CTA clusters cannot use every SM); a
   // second partial wave would double the kernel time.
-  static int max_active[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  static int max_active[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // per template instance
   if (!max_active[cluster - 1]) {
     cfg.gridDim = dim3(cluster * (num_sms() / cluster), 1, 1);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI>, &cfg) != cudaSuccess || n < 1)
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI, kStages>, &cfg) != cudaSuccess || n < 1)
       n = num_sms() / cluster;
     max_active[cluster - 1] = n;
   }
@@ -562,7 +669,7 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   const int n_clusters = tiles < max_clusters ? tiles : max_clusters;
   cfg.gridDim = dim3(cluster * n_clusters, 1, 1);
   prof::begin(prof::K_GEMM, s);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<EPI>, ta, tb, tc, tr, bias, M, N, K, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, kStages>, ta, tb, tc, tr, bias, M, N, K, ep);
   prof::end(prof::K_GEMM, s, 2.0 * M * N * K);
   if (e != cudaSuccess) return CHM_ERR_CUDA;
   CHM_LAUNCH_CHECK();
@@ -571,40 +678,64 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
 
 }  // namespace gemm
 
-// Internal entry (also used by the encoder). Epilogue 4 = QKV split with V^T
-// (vt/hidden/seq_len), 5 = residual + LayerNorm (gamma/beta/eps, N = 256 g, g <= 4).
-chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
-                     const void* residual, int M, int N, int K, int epilogue, cudaStream_t s,
-                     void* vt, int hidden, int seq_len, const float* gamma, const float* beta,
-                     float eps, long long res_ld) {
+// Internal entry (gemm.cuh), used by the encoder and the C-ABI wrappers.
+chm_status gemm_run(const void* A, const void* B, void* C, int M, int N, int K,
+                    const GemmArgs& g, cudaStream_t s) {
+  const int epilogue = g.epilogue;
   if (M <= 0 || N <= 0 || K <= 0) return M == 0 ? CHM_OK : CHM_ERR_INVALID_ARG;
   if (K % gemm::BK != 0 || N % 64 != 0) return CHM_ERR_INVALID_ARG;
-  if (epilogue != gemm::EPI_NONE && !bias) return CHM_ERR_INVALID_ARG;
-  if ((epilogue == gemm::EPI_BIAS_RESIDUAL || epilogue == gemm::EPI_RESIDUAL_LN) && !residual)
-    return CHM_ERR_INVALID_ARG;
-  if (res_ld != 0 && res_ld < N) return CHM_ERR_INVALID_ARG;
-  gemm::EpiParams ep{reinterpret_cast<__nv_bfloat16*>(vt), hidden, seq_len, gamma,
-                     beta, eps,    res_ld};
-  if (epilogue == gemm::EPI_QKV && (hidden % 64 != 0 || N != 3 * hidden))
+  if (epilogue != gemm::EPI_NONE && !g.bias) return CHM_ERR_INVALID_ARG;
+  const bool res = epilogue == gemm::EPI_BIAS_RESIDUAL || epilogue == gemm::EPI_RESIDUAL_LN ||
+                   epilogue == gemm::EPI_RESLN_STATS;
+  if (res && !g.residual) return CHM_ERR_INVALID_ARG;
+  if (g.res_ld != 0 && g.res_ld < N) return CHM_ERR_INVALID_ARG;
+  if (epilogue == gemm::EPI_QKV && (g.hidden % 64 != 0 || N != 3 * g.hidden))
     return CHM_ERR_INVALID_ARG;
   if (epilogue == gemm::EPI_RESIDUAL_LN &&
-      (N % gemm::BN != 0 || N / gemm::BN > gemm::kMaxLnGroups || !gamma || !beta))
+      (N % gemm::BN != 0 || N / gemm::BN > gemm::kMaxLnGroups || !g.gamma || !g.beta))
     return CHM_ERR_UNSUPPORTED;
+  if (g.stats_in && (g.n_part < 1 || g.n_part > kLnMaxParts)) return CHM_ERR_INVALID_ARG;
+  if (g.stats_in && (epilogue == gemm::EPI_BIAS || epilogue == gemm::EPI_BIAS_GELU ||
+                     epilogue == gemm::EPI_QKV) && !g.colsum)
+    return CHM_ERR_INVALID_ARG;
+  if (epilogue == gemm::EPI_RESLN_STATS &&
+      (N % kLnPartCols != 0 || !g.stats_out || (g.stats_in && (!g.gamma || !g.beta))))
+    return CHM_ERR_INVALID_ARG;
+  gemm::EpiParams ep{};
+  ep.hidden = g.hidden;
+  ep.gamma = g.gamma;
+  ep.beta = g.beta;
+  ep.eps = g.eps;
+  ep.res_ld = g.res_ld;
+  ep.stats_in = g.stats_in;
+  ep.n_part = g.n_part;
+  ep.colsum = g.colsum;
+  ep.stats_out = g.stats_out;
+  const float* bias = g.bias;
+  const void* residual = g.residual;
+  // measurement overrides: CHM_GEMM_STAGES (4 or 6 operand stages for the
+  // pointwise epilogues), CHM_GEMM_DEBUG (EpiParams::dbg)
+  static const int stages = getenv("CHM_GEMM_STAGES") ? atoi(getenv("CHM_GEMM_STAGES")) : 4;
+  static const int dbg = getenv("CHM_GEMM_DEBUG") ? atoi(getenv("CHM_GEMM_DEBUG")) : 0;
+  ep.dbg = dbg;
+#define CHM_GEMM_CASE(E)                                                              \
+  case E:                                                                              \
+    return stages == 6 ? gemm::launch<E, 6>(A, B, C, bias, residual, M, N, K, ep, s)   \
+                       : gemm::launch<E, 4>(A, B, C, bias, residual, M, N, K, ep, s);
   switch (epilogue) {
-    case gemm::EPI_NONE:
-      return gemm::launch<gemm::EPI_NONE>(A, B, C, bias, residual, M, N, K, ep, s);
-    case gemm::EPI_BIAS:
-      return gemm::launch<gemm::EPI_BIAS>(A, B, C, bias, residual, M, N, K, ep, s);
-    case gemm::EPI_BIAS_GELU:
-      return gemm::launch<gemm::EPI_BIAS_GELU>(A, B, C, bias, residual, M, N, K, ep, s);
+    CHM_GEMM_CASE(gemm::EPI_NONE)
+    CHM_GEMM_CASE(gemm::EPI_BIAS)
+    CHM_GEMM_CASE(gemm::EPI_BIAS_GELU)
+    CHM_GEMM_CASE(gemm::EPI_QKV)
     case gemm::EPI_BIAS_RESIDUAL:
-      return gemm::launch<gemm::EPI_BIAS_RESIDUAL>(A, B, C, bias, residual, M, N, K, ep, s);
-    case gemm::EPI_QKV:
-      return gemm::launch<gemm::EPI_QKV>(A, B, C, bias, residual, M, N, K, ep, s);
+      return gemm::launch<gemm::EPI_BIAS_RESIDUAL, 4>(A, B, C, bias, residual, M, N, K, ep, s);
+    case gemm::EPI_RESLN_STATS:
+      return gemm::launch<gemm::EPI_RESLN_STATS, 4>(A, B, C, bias, residual, M, N, K, ep, s);
     case gemm::EPI_RESIDUAL_LN:
-      return gemm::launch<gemm::EPI_RESIDUAL_LN>(A, B, C, bias, residual, M, N, K, ep, s);
+      return gemm::launch<gemm::EPI_RESIDUAL_LN, 4>(A, B, C, bias, residual, M, N, K, ep, s);
     default: return CHM_ERR_INVALID_ARG;
   }
+#undef CHM_GEMM_CASE
 }
 
 }  // namespace chm
@@ -612,16 +743,49 @@ chm_status gemm_bf16(const void* A, const void* B, void* C, const float* bias,
 extern "C" chm_status chm_gemm_bf16(const void* A, const void* B, void* C, const float* bias,
                                     const void* residual, int32_t M, int32_t N, int32_t K,
                                     int32_t epilogue, void* stream) {
-  if (epilogue == chm::gemm::EPI_QKV || epilogue == chm::gemm::EPI_RESIDUAL_LN)
+  if (epilogue < chm::gemm::EPI_NONE || epilogue > chm::gemm::EPI_BIAS_RESIDUAL)
     return CHM_ERR_INVALID_ARG;
-  return chm::gemm_bf16(A, B, C, bias, residual, M, N, K, epilogue, (cudaStream_t)stream,
-                        nullptr, 0, 0, nullptr, nullptr, 0.f, 0);
+  chm::GemmArgs g;
+  g.epilogue = epilogue;
+  g.bias = bias;
+  g.residual = residual;
+  return chm::gemm_run(A, B, C, M, N, K, g, (cudaStream_t)stream);
 }
 
 extern "C" chm_status chm_gemm_bf16_ln(const void* A, const void* B, void* C, const float* bias,
                                        const void* residual, const float* gamma,
                                        const float* beta, float eps, int32_t M, int32_t N,
                                        int32_t K, void* stream) {
-  return chm::gemm_bf16(A, B, C, bias, residual, M, N, K, chm::gemm::EPI_RESIDUAL_LN,
-                        (cudaStream_t)stream, nullptr, 0, 0, gamma, beta, eps, 0);
+  chm::GemmArgs g;
+  g.epilogue = chm::gemm::EPI_RESIDUAL_LN;
+  g.bias = bias;
+  g.residual = residual;
+  g.gamma = gamma;
+  g.beta = beta;
+  g.eps = eps;
+  return chm::gemm_run(A, B, C, M, N, K, g, (cudaStream_t)stream);
+}
+
+extern "C" chm_status chm_gemm_bf16_deferred_ln(const void* A, const void* B, void* C,
+                                                const float* bias, int32_t epilogue,
+                                                const void* residual, const float* gamma,
+                                                const float* beta, const void* stats_in,
+                                                int32_t n_part, const float* colsum,
+                                                void* stats_out, float eps, int32_t M,
+                                                int32_t N, int32_t K, void* stream) {
+  if (epilogue != chm::gemm::EPI_BIAS && epilogue != chm::gemm::EPI_BIAS_GELU &&
+      epilogue != chm::gemm::EPI_RESLN_STATS)
+    return CHM_ERR_INVALID_ARG;
+  chm::GemmArgs g;
+  g.epilogue = epilogue;
+  g.bias = bias;
+  g.residual = residual;
+  g.gamma = gamma;
+  g.beta = beta;
+  g.eps = eps;
+  g.stats_in = reinterpret_cast<const float2*>(stats_in);
+  g.n_part = n_part;
+  g.colsum = colsum;
+  g.stats_out = reinterpret_cast<float2*>(stats_out);
+  return chm::gemm_run(A, B, C, M, N, K, g, (cudaStream_t)stream);
 }

@@ -36,6 +36,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include "common.cuh"
+#include "deferred_ln.cuh"
 #include "prof.cuh"
 #include "sm100.cuh"
 
@@ -86,8 +87,10 @@ template <int CS, int CH>
 __global__ void __launch_bounds__(kThreads, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tm_x,
                          const __grid_constant__ CUtensorMap tm_w,
-                         const float* __restrict__ b_qkv, int n_seq, int n_heads, int hidden,
-                         __nv_bfloat16* __restrict__ ctx, int lag, int dbg) {
+                         const float* __restrict__ b_qkv, const float* __restrict__ c_qkv,
+                         const float2* __restrict__ stats_in, int n_part, float eps, int n_seq,
+                         int n_heads, int hidden, __nv_bfloat16* __restrict__ ctx, int lag,
+                         int dbg) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
@@ -102,9 +105,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int head_groups = n_heads / CH;
   const int n_citems = ((n_seq + CS - 1) / CS) * head_groups;
   const int cl = (int)sm100::cluster_id_x(), n_cl = (int)sm100::n_clusters_x();
-  const int n_my = cl < n_citems ? (n_citems - 1 - cl) / n_cl + 1 : 0;
+  // Each cluster owns a contiguous range of cluster items (head-group minor),
+  // so consecutive items of a CTA share a sequence: the deferred-LayerNorm
+  // row affine is computed once per sequence, and the x tile is re-read from
+  // L2 while hot.
+  const int per = (n_citems + n_cl - 1) / n_cl;
+  const int c_lo = cl * per;
+  const int n_my = c_lo < n_citems ? min(per, n_citems - c_lo) : 0;
   auto item_of = [&](int it, int& seq, int& h) {
-    const int c = cl + it * n_cl;
+    const int c = c_lo + it;
     const int sg = c / head_groups, hg = c - sg * head_groups;
     seq = sg * CS + ci;
     h = hg * CH + cj;
@@ -257,11 +266,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = quarter * 32 + lane;  // token row of the item
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     constexpr float kLog2e = 1.4426950408889634f;
+    int aff_seq = -1;           // sequence the cached row affine belongs to
+    float rs_a = 1.f, rs_b = 0.f;
     for (int it = 0; it < n_my; ++it) {
       int seq, h;
       item_of(it, seq, h);
       const uint32_t par = it & 1;
       const int a = it & 1;
+      // deferred LayerNorm of the input row (folded: x' = rs_a x + rs_b per
+      // row, gamma inside the weights, W.beta inside the bias)
+      if (stats_in != nullptr && seq != aff_seq && seq < n_seq) {
+        row_affine(stats_in + ((size_t)seq * kS + r) * n_part, n_part, eps, rs_a, rs_b);
+        aff_seq = seq;
+      }
       // (1) acc + bias -> bf16 Q/K/V tiles. Chunk c (32 columns) of the 192:
       // part t = c/2 (Q, K, V), columns (c&1)*32.. of that part.
       sm100::mbar_wait(&s.acc_full[a], (it >> 1) & 1);
@@ -279,16 +296,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tmem_ld_32x32b_x32(lane_base + (uint32_t)a * kAccCols + c * 32, raw);
         sm100::tmem_ld_wait();
         const float* bp = b_qkv + t * hidden + h * 64 + c32 * 32;
+        const float* cp = c_qkv + t * hidden + h * 64 + c32 * 32;
         const float scale = t == 0 ? 0.125f : 1.0f;
         uint8_t* rowp = s.qkv[t] + r * 128;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + q4 * 8));
           const float4 b1 = __ldg(reinterpret_cast<const float4*>(bp + q4 * 8 + 4));
-          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+          float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+          if (stats_in != nullptr) {
+            const float4 c0 = __ldg(reinterpret_cast<const float4*>(cp + q4 * 8));
+            const float4 c1 = __ldg(reinterpret_cast<const float4*>(cp + q4 * 8 + 4));
+            const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) bb[e] = fmaf(rs_b, cc[e], bb[e]);
+          }
           float v[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = (__uint_as_float(raw[q4 * 8 + e]) + bb[e]) * scale;
+          for (int e = 0; e < 8; ++e) v[e] = fmaf(rs_a, __uint_as_float(raw[q4 * 8 + e]), bb[e]) * scale;
           uint4 u;
           u.x = pack_bf16(v[0], v[1]);
           u.y = pack_bf16(v[2], v[3]);
@@ -390,8 +415,9 @@ static int env_int(const char* name, int dflt) {
 }
 
 template <int CS, int CH>
-static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv, void* ctx,
-                         int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
+static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
+                         const float* c_qkv, const float2* stats_in, int n_part, float eps,
+                         void* ctx, int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
   const int n_heads = hidden / 64;
   if (n_heads % CH != 0) return CHM_ERR_UNSUPPORTED;
   constexpr int kCluster = CS * CH;
@@ -427,7 +453,8 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv, v
   const int n_cl = citems < max_clusters ? citems : max_clusters;
   cfg.gridDim = dim3(kCluster * n_cl, 1, 1);
   prof::begin(prof::K_QKV_ATTENTION, st);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, n_seq, n_heads, hidden,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, c_qkv, stats_in, n_part, eps,
+                                     n_seq, n_heads, hidden,
                                      reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg);
   // tensor work: the projection (2 T 3H H) + S and O (4 S^2 64 per item)
   prof::end(prof::K_QKV_ATTENTION, st,
@@ -437,18 +464,22 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv, v
   return CHM_OK;
 }
 
-// ctx = attention(x . w_qkv^T + b_qkv) for n_seq sequences of 128 tokens.
-chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv, void* ctx,
-                         int n_seq, int hidden, cudaStream_t st) {
+// ctx = attention(x' . w_qkv^T + b_qkv) for n_seq sequences of 128 tokens,
+// x' = x, or with stats_in the deferred LayerNorm of x folded in (w_qkv
+// pre-scaled by gamma, b_qkv including W.beta, c_qkv = row sums of w_qkv).
+chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
+                         const float* c_qkv, const float2* stats_in, int n_part, float eps,
+                         void* ctx, int n_seq, int hidden, cudaStream_t st) {
+  if (stats_in && (!c_qkv || n_part < 1 || n_part > kLnMaxParts)) return CHM_ERR_INVALID_ARG;
   static const int cluster = env_int("CHM_QA_CLUSTER", 21);
   static const int lag = env_int("CHM_QA_LAG", 0);
   static const int dbg = env_int("CHM_QA_DEBUG", 0);
   switch (cluster) {
-    case 11: return launch<1, 1>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
-    case 12: return launch<1, 2>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
-    case 21: return launch<2, 1>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
-    case 24: return launch<2, 4>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
-    default: return launch<2, 2>(x, w_qkv, b_qkv, ctx, n_seq, hidden, lag, dbg, st);
+    case 11: return launch<1, 1>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 12: return launch<1, 2>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 21: return launch<2, 1>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 24: return launch<2, 4>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    default: return launch<2, 2>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
   }
 }
 
@@ -460,5 +491,6 @@ extern "C" chm_status chm_qkv_attention_bf16(const void* x, const void* w_qkv,
   if (!x || !w_qkv || !b_qkv || !ctx || n_seq < 0) return CHM_ERR_INVALID_ARG;
   if (hidden <= 0 || hidden % 64 != 0) return CHM_ERR_INVALID_ARG;
   if (n_seq == 0) return CHM_OK;
-  return chm::qkv_attention(x, w_qkv, b_qkv, ctx, n_seq, hidden, (cudaStream_t)stream);
+  return chm::qkv_attention(x, w_qkv, b_qkv, nullptr, nullptr, 0, 0.f, ctx, n_seq, hidden,
+                            (cudaStream_t)stream);
 }

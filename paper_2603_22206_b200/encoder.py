@@ -5,7 +5,8 @@ BERT-style post-LN encoder (embedding + LN, L x [QKV -> attention -> out-proj
 q[m] = sigmoid(Linear(h_[CLS]))[m]. Weights are bf16 in
 nn.Linear layout [out, in]; LN/bias/head parameters fp32. The forward runs
 entirely in libchimera_sm100a.so (chm_encoder_forward): tcgen05 GEMMs with
-fused epilogues, tcgen05 attention, warp-per-row LayerNorm.
+fused epilogues, tcgen05 attention, LayerNorms deferred into the consuming
+GEMM's epilogue (weights folded once by chm_encoder_fold_weights).
 
 FLOPs per routed request (S tokens):
   L * (8*S*H^2 + 4*S^2*H + 4*S*H*F) + 2*H*K
@@ -147,8 +148,24 @@ class GpuEncoderRouter:
             "tmp": torch.empty(T, H, dtype=bf, device=self.device),
             "ffn": torch.empty(T, F, dtype=bf, device=self.device),
         }
+        # deferred-LayerNorm statistics and the LayerNorm-folded QKV / FFN1
+        # weights (chm_encoder_fold_weights; recomputed by refold())
+        self.ws["stats"] = torch.empty(
+            int(self.lib.chm_encoder_stats_bytes(self.cfg_c, T)), dtype=torch.uint8,
+            device=self.device)
+        self.ws["folded"] = torch.empty(
+            int(self.lib.chm_encoder_folded_bytes(self.cfg_c)), dtype=torch.uint8,
+            device=self.device)
         self.ws_c = _lib.EncoderWorkspace(T, *(self.ws[k].data_ptr()
-                                               for k in ("x", "qkv", "ctx", "tmp", "ffn")))
+                                               for k in ("x", "qkv", "ctx", "tmp", "ffn",
+                                                         "stats", "folded")))
+        self.refold()
+
+    def refold(self, stream=None) -> None:
+        """Recompute the LayerNorm-folded weights after a weight change."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(self.lib.chm_encoder_fold_weights(self.cfg_c, self.w_c, self.ws_c,
+                                                     s.cuda_stream), "chm_encoder_fold_weights")
 
     def forward(self, token_ids: torch.Tensor, q_out: torch.Tensor, rows=None, n_rows=None,
                 n_seq: int | None = None, stream=None) -> None:

@@ -131,3 +131,100 @@ def test_encoder_routed_rows_only():
             assert np.abs(got[i] - want[i]).max() <= Q_TOL
         else:
             assert np.all(got[i] == -1.0)
+
+
+def _partials(x):
+    """(mean, M2) per 128-column chunk of every row, fp32 (deferred_ln.cuh)."""
+    M, N = x.shape
+    c = x.float().view(M, N // 128, 128)
+    mean = c.mean(-1)
+    m2 = ((c - mean[..., None]) ** 2).sum(-1)
+    return torch.stack([mean, m2], -1).contiguous()
+
+
+def _deferred(A, B, bias, epilogue, residual=None, gamma=None, beta=None, stats_in=None,
+              colsum=None, eps=1e-12):
+    M, K = A.shape
+    N = B.shape[0]
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    st_out = torch.full((M, N // 128, 2), float("nan"), device="cuda")
+    n_part = 0 if stats_in is None else stats_in.shape[1]
+    ptr = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    _lib.check(_lib.load().chm_gemm_bf16_deferred_ln(
+        A.data_ptr(), B.data_ptr(), C.data_ptr(), bias.data_ptr(), epilogue, ptr(residual),
+        ptr(gamma), ptr(beta), ptr(stats_in), n_part, ptr(colsum), st_out.data_ptr(), eps,
+        M, N, K, torch.cuda.current_stream().cuda_stream), "deferred_ln")
+    torch.cuda.synchronize()
+    return C, st_out
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 768, 768), (1000, 768, 3072), (777, 256, 128),
+                                   (2048, 1024, 256)])
+@pytest.mark.parametrize("with_ln", [False, True])
+def test_gemm_resln_stats(M, N, K, with_ln):
+    """Epilogue 6: C = A.B^T + bias + LN(residual) (statistics of the residual
+    from its own partials) and the (mean, M2) partials of C per 128 columns."""
+    g = torch.Generator(device="cuda").manual_seed(M + 3 * N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    bias = 0.1 * torch.randn(N, device="cuda", generator=g)
+    res = (2 * torch.randn(M, N, device="cuda", generator=g) + 0.7).to(torch.bfloat16)
+    gamma = 1 + 0.2 * torch.randn(N, device="cuda", generator=g)
+    beta = 0.1 * torch.randn(N, device="cuda", generator=g)
+    if with_ln:
+        st = _partials(res)
+        C, st_out = _deferred(A, B, bias, 6, res, gamma, beta, st)
+        r = F.layer_norm(res.float(), (N,), gamma, beta, 1e-12)
+    else:
+        C, st_out = _deferred(A, B, bias, 6, res)
+        r = res.float()
+    ref = A.float() @ B.float().T + bias + r
+    torch.testing.assert_close(C.float(), ref, rtol=GEMM_RTOL, atol=GEMM_ATOL)
+    want = _partials(ref)
+    torch.testing.assert_close(st_out[..., 0], want[..., 0], rtol=1e-3, atol=2e-3)
+    torch.testing.assert_close(st_out[..., 1], want[..., 1], rtol=1e-2, atol=1e-1)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 3072, 768), (1000, 2304, 768), (300, 512, 256)])
+@pytest.mark.parametrize("epilogue", [1, 2])
+def test_gemm_folded_layernorm(M, N, K, epilogue):
+    """Epilogues 1/2 with stats_in: the LayerNorm of A's rows folded into the
+    epilogue with chm_encoder_fold_weights' rule equals GEMM(LN(A))."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + 5 * K + epilogue)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 1.5 + 0.3).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    b = 0.1 * torch.randn(N, device="cuda", generator=g)
+    gamma = 1 + 0.2 * torch.randn(K, device="cuda", generator=g)
+    beta = 0.1 * torch.randn(K, device="cuda", generator=g)
+    Wf = (W.float() * gamma).to(torch.bfloat16)
+    colsum = Wf.float().sum(1)
+    bf = b + W.float() @ beta
+    C, _ = _deferred(A, Wf, bf, epilogue, stats_in=_partials(A), colsum=colsum)
+    ref = F.layer_norm(A.float(), (K,), gamma, beta, 1e-12) @ W.float().T + b
+    if epilogue == 2:
+        ref = F.gelu(ref, approximate="tanh")
+    torch.testing.assert_close(C.float(), ref, rtol=GEMM_RTOL, atol=3e-2)
+
+
+@pytest.mark.parametrize("cfg,S", [(SMALL, 128), (EncoderConfig(n_layers=3), 128), (SMALL, 256)])
+def test_encoder_random_layernorm_params(cfg, S):
+    """Non-trivial LayerNorm gamma/beta (BERT init has 1/0): exercises the
+    folded weights and the residual-side LayerNorm of the deferred path."""
+    from dataclasses import replace
+    cfg = replace(cfg, seq_len=S)
+    K, B = 5, 8
+    r = GpuEncoderRouter(cfg, K, max_rows=B, seed=6, head_std=2 / math.sqrt(cfg.hidden))
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    for name, t in r.weights.items():
+        if name.startswith(("ln1_", "ln2_", "emb_ln_")):
+            if "_g" in name:
+                t.copy_(1 + 0.3 * torch.randn(t.shape, device="cuda", generator=gen))
+            else:
+                t.copy_(0.2 * torch.randn(t.shape, device="cuda", generator=gen))
+    r.refold()
+    ids = torch.as_tensor(synthetic_token_ids(B, S, seed=31), device="cuda")
+    q = torch.zeros(B * K, dtype=torch.float32, device="cuda")
+    r.forward(ids, q)
+    torch.cuda.synchronize()
+    err = np.abs(q.view(B, K).cpu().numpy() - _ref_q(r, ids)).max()
+    assert err <= Q_TOL, err
