@@ -11,6 +11,8 @@
  * /root/reference/pkg/src/hetsched):
  *   chm_prepare_rows       balancer.py:100-103   (assignment lookup `monitor.assignment`)
  *   chm_encoder_forward    router.py:39-42       (Router.score -> ConfidenceVector)
+ *   chm_trace_*            workload.py:125-253, 454-495 (TraceRecord columns,
+ *                          remaining_tokens, first/next_stage_request)
  *   chm_predict_*          predictor.py:22-27    (Predictor.predict) and the concrete
  *                          predictors at predictor.py:30-45, 65-108
  *   chm_schedule_rows      balancer.py:89-129    (schedule_request = Alg. 1), with
@@ -167,6 +169,23 @@ typedef struct chm_queue_state {
  * compaction): ~68/entry. */
 uint64_t chm_queue_scratch_bytes(int32_t capacity);
 
+/* ---- columnar trace store (TraceRecord, workload.py:111-253) ------------ */
+
+/* Dense SoA columns of a trace: program p (dense index), 0-based stage s
+ * (padded to max_stages), model m in pool order. The caller fills the input
+ * columns (n_stages .. carried); chm_trace_derive fills the two derived ones. */
+typedef struct chm_trace {
+  int32_t n_programs, max_stages, n_models;
+  const int32_t* n_stages;     /* [NP] number of stages                          */
+  const int32_t* workflow;     /* [NP] predictor workflow index (-1: unknown)    */
+  const double* user_arrival;  /* [NP] user_arrival_time_ms                      */
+  const int32_t* base_input;   /* [NP*S] base_input_tokens                       */
+  const int32_t* out_tokens;   /* [NP*S*K] out_tokens                            */
+  const int32_t* carried;      /* [NP*S*K] carried_context_tokens                */
+  int64_t* remaining;          /* [NP*S*K] derived: sum_{j>=s} out_tokens        */
+  int64_t* carried_prefix;     /* [NP*S*K] derived: sum_{j<s} carried            */
+} chm_trace;
+
 /* ---- router encoder (BERT-style post-LN, CLS -> Linear(H,K) -> sigmoid) --- */
 
 typedef struct chm_encoder_cfg {
@@ -289,6 +308,43 @@ chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* aging,
                           const chm_monitor_state* mon, const chm_queue_state* q,
                           const chm_rows* rows, const chm_decisions* dec,
                           int32_t n_iterations, int32_t* error, void* stream);
+
+/* Trace store. chm_trace_derive: remaining (the suffix
+ * sums TraceRecord.remaining_tokens returns, workload.py:160-165) and
+ * carried_prefix (next_stage_request's carried context, workload.py:484-486),
+ * validating n_stages in 1..max_stages, token counts >= 0 and base >= 1
+ * (TraceRecord.validate, workload.py:170-200): CHM_ERR_VALIDATION, row =
+ * program. HBM bound: 8 bytes read + 16 written per (program, stage, model). */
+chm_status chm_trace_derive(const chm_trace* t, int32_t* error, void* stream);
+/* Per batch row (program, 1-based stage): out_tokens[B*K]
+ * (rec.out_tokens(stage, m), the EngineSim.enqueue argument), workflow[B],
+ * n_stages[B], oracle_yhat[B*K] (OraclePredictor.predict, predictor.py:30-36).
+ * Any output may be NULL. Stage outside 1..n_stages -> CHM_ERR_UNKNOWN_STAGE
+ * (TraceRecord._stage, workload.py:143-147). */
+chm_status chm_trace_gather_rows(const chm_trace* t, const int32_t* program,
+                                 const int32_t* stage, int32_t n_rows, int32_t* out_tokens,
+                                 int32_t* workflow, int32_t* n_stages, double* oracle_yhat,
+                                 int32_t* error, void* stream);
+/* next_stage_request (workload.py:467-495) for n completions (program,
+ * completed stage, completion time, assigned model index): the requests of
+ * programs with a next stage, compacted in input order into next_* (stage
+ * s+1, arrival = completion time, input = base + carried prefix),
+ * *n_next = their count, source_row = the completion each came from
+ * (next_workflow / source_row may be NULL). Completed stage outside
+ * 1..n_stages -> CHM_ERR_UNKNOWN_STAGE. */
+chm_status chm_trace_next_stage(const chm_trace* t, const int32_t* program,
+                                const int32_t* completed_stage, const double* completion_time,
+                                const int8_t* model, int32_t n, int32_t* next_program,
+                                int32_t* next_stage, double* next_arrival,
+                                int32_t* next_input_tokens, int32_t* next_workflow,
+                                int32_t* source_row, int32_t* n_next, int32_t* error,
+                                void* stream);
+/* first_stage_request (workload.py:454-464): input = base of stage 1,
+ * arrival = arrival_in[i] or the program's user_arrival_time_ms (NULL). */
+chm_status chm_trace_first_stage(const chm_trace* t, const int32_t* program,
+                                 const double* arrival_in, int32_t n, int32_t* input_tokens,
+                                 double* arrival, int32_t* workflow, int32_t* error,
+                                 void* stream);
 
 /* Deferred LayerNorm. The encoder does not normalise a sublayer output where
  * it is produced: out-projection and FFN2 write the pre-LN sum plus per-row

@@ -11,6 +11,8 @@ Contents
                     algorithm and same cost structure (dict re-sum per
                     decision, lazy-deletion heap), each function citing the
                     reference file:line it follows.
+  trace_ref.py      numpy restatement of TraceRecord.remaining_tokens and
+                    first/next_stage_request on dense trace columns.
   encoder_ref.py    torch fp32 restatement of the router encoder (the
                     reference has no neural router: router.py only pins the
                     contract -- one score per pool model in [0,1]).

@@ -135,6 +135,22 @@ class QueueState(ctypes.Structure):
 
 
 
+class Trace(ctypes.Structure):
+    _fields_ = [
+        ("n_programs", c_int32),
+        ("max_stages", c_int32),
+        ("n_models", c_int32),
+        ("n_stages", c_void_p),
+        ("workflow", c_void_p),
+        ("user_arrival", c_void_p),
+        ("base_input", c_void_p),
+        ("out_tokens", c_void_p),
+        ("carried", c_void_p),
+        ("remaining", c_void_p),
+        ("carried_prefix", c_void_p),
+    ]
+
+
 class EncoderCfg(ctypes.Structure):
     _fields_ = [
         ("n_layers", c_int32),
@@ -228,6 +244,16 @@ _SIGNATURES = [
     ("chm_encoder_fold_weights", c_int32,
      [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p]),
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
+    ("chm_trace_derive", c_int32, [POINTER(Trace), c_void_p, c_void_p]),
+    ("chm_trace_gather_rows", c_int32,
+     [POINTER(Trace), c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p, c_void_p]),
+    ("chm_trace_next_stage", c_int32,
+     [POINTER(Trace), c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("chm_trace_first_stage", c_int32,
+     [POINTER(Trace), c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+      c_void_p]),
     ("chm_monitor_complete", c_int32,
      [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_int32, c_void_p, c_void_p,
       c_void_p]),
@@ -240,7 +266,7 @@ _SIGNATURES = [
 ]
 
 PROFILE_KINDS = ["gemm", "attention", "rowwise", "predict", "prepare", "select", "queue",
-                 "qkv_attention"]
+                 "qkv_attention", "trace"]
 
 
 def profile_enable(on: bool) -> None:

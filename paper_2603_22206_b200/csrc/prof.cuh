@@ -17,7 +17,8 @@ enum Kind : int {
   K_SELECT = 5,
   K_QUEUE = 6,
   K_QKV_ATTENTION = 7,  // fused QKV projection + attention (qkv_attn.cu)
-  K_NUM = 8
+  K_TRACE = 8,          // columnar trace store derivation (trace.cu)
+  K_NUM = 9
 };
 
 // Call around one kernel launch on `s`. `work` is the algorithmic FLOPs

@@ -93,10 +93,15 @@ class GpuQuantilePredictor:
 
 
 class GpuOraclePredictor:
+    """With a TraceStore (trace.py) the prediction is gathered on the device
+    from the derived suffix sums by (program, stage) alone; without one the
+    batch carries per-row stage outputs (n_stages / stage_out columns)."""
+
     name = "oracle"
 
-    def __init__(self, max_stages: int = 8):
+    def __init__(self, max_stages: int = 8, trace=None):
         self.max_stages = max_stages
+        self.trace = trace
 
     def predict(self, req, rec, model_id) -> float:
         return float(rec.remaining_tokens(req.stage_index, model_id))
@@ -114,6 +119,13 @@ class GpuOraclePredictor:
         return {"n_stages": n_st, "stage_out": so}
 
     def predict_rows(self, batch, K, yhat, error, stream) -> None:
+        if self.trace is not None:
+            if K != self.trace.K:
+                raise ValidationError(f"trace has {self.trace.K} models, pool has {K}")
+            _lib.check(_lib.load().chm_trace_gather_rows(
+                self.trace.t, _p(batch.program), _p(batch.stage), batch.n_rows, None, None, None,
+                _p(yhat), _p(error), stream.cuda_stream), "chm_trace_gather_rows")
+            return
         _lib.check(_lib.load().chm_predict_oracle(
             _p(batch.stage_out), _p(batch.n_stages), _p(batch.stage), self.max_stages, K,
             batch.n_rows, _p(yhat), _p(error), stream.cuda_stream), "chm_predict_oracle")

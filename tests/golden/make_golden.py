@@ -23,6 +23,11 @@ Fixtures
   quantile.npz        EmpiricalQuantilePredictor on synthesize_trace(2000, 1)
                       (predictor.py:65-108) over a (wf, stage, model) grid
   synth.json          fingerprints of synthesize_trace outputs (workload.py:334-416)
+  trace_small.ndjson  a mixed code/math trace written by save_trace (workload.py:294-297),
+  trace_small.npz     carried context != out tokens for some stages, and the reference's
+                      remaining_tokens / first_stage_request / next_stage_request answers
+                      for every (program, stage, model) (workload.py:160-165, 454-495)
+  trace_errors.json   malformed trace files and the error load_trace raises (256-291)
 """
 
 from __future__ import annotations
@@ -457,6 +462,105 @@ def make_synth():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def make_trace():
+    """A small mixed trace through the reference's own writer and readers."""
+    code_stats = {f"m{i}": workload.LengthStats(300 + 150 * i, 200 + 50 * i) for i in range(3)}
+    succ = {f"m{i}": {"easy": 0.5 + 0.1 * i, "hard": 0.1 + 0.1 * i} for i in range(3)}
+    recs = workload.synthesize_trace(workload.CODE_WORKFLOWS, code_stats, succ, 30, 11)
+    recs += workload.synthesize_trace(workload.MATH_WORKFLOWS, code_stats, succ, 30, 12)
+    rng = np.random.default_rng(13)
+    edited = []
+    for p, rec in enumerate(recs):
+        d = rec.to_json_dict()
+        d["program_id"] = f"t{p:04d}"
+        d["user_arrival_time_ms"] = float(rng.integers(0, 10**6)) / 8.0
+        for st in d["stages"]:
+            for mid, o in st["models"].items():
+                if rng.random() < 0.5:  # carried context differs from the output
+                    o["carried_context_tokens"] = int(rng.integers(0, 3 * o["out_tokens"] + 2))
+        edited.append(workload.TraceRecord.from_json_dict(d))
+    path = os.path.join(OUT, "trace_small.ndjson")
+    workload.save_trace(edited, path)
+    recs = workload.load_trace(path)
+    ids = sorted(recs[0].model_ids)
+    NP, S, K = len(recs), max(r.n_stages for r in recs), len(ids)
+    remaining = np.full((NP, S, K), -1, np.int64)
+    nxt_input = np.full((NP, S, K), -1, np.int64)   # -1: no next stage (final stage)
+    nxt_arrival = np.full((NP, S, K), -1.0)
+    first_input = np.zeros(NP, np.int64)
+    first_arrival = np.zeros(NP)
+    for p, rec in enumerate(recs):
+        req = workload.first_stage_request(rec)
+        first_input[p], first_arrival[p] = req.input_tokens, req.arrival_time
+        for s in range(1, rec.n_stages + 1):
+            for k, m in enumerate(ids):
+                remaining[p, s - 1, k] = rec.remaining_tokens(s, m)
+                nx = workload.next_stage_request(rec, s, 1000.0 + p + 0.25 * s, m)
+                if nx is not None:
+                    assert nx.stage_index == s + 1
+                    nxt_input[p, s - 1, k] = nx.input_tokens
+                    nxt_arrival[p, s - 1, k] = nx.arrival_time
+    unknown = []
+    for s in (0, recs[0].n_stages + 1):
+        try:
+            workload.next_stage_request(recs[0], s, 0.0, ids[0])
+        except SimError as exc:
+            unknown.append([s, type(exc).__name__])
+    np.savez_compressed(os.path.join(OUT, "trace_small.npz"), model_ids=np.array(ids),
+                        program_ids=np.array([r.program_id for r in recs]),
+                        n_stages=np.array([r.n_stages for r in recs], np.int32),
+                        remaining=remaining, next_input=nxt_input, next_arrival=nxt_arrival,
+                        first_input=first_input, first_arrival=first_arrival,
+                        unknown=np.array(unknown, dtype=object).astype(str))
+    # malformed files: (name, content) -> reference exception, line, message
+    good = open(path).read().splitlines()
+    bad_rec = json.loads(good[1])
+    cases = {
+        "bad_json": good[0] + "\n{not json\n",
+        "not_object": good[0] + "\n[1, 2]\n",
+        "missing_field": good[0] + "\n" + json.dumps({k: v for k, v in bad_rec.items()
+                                                       if k != "stages"}) + "\n",
+        "negative_tokens": good[0] + "\n" + json.dumps(_edit(bad_rec, "neg")) + "\n",
+        "bad_stage_index": "\n" + json.dumps(_edit(bad_rec, "idx")) + "\n",
+        "model_mismatch": good[0] + "\n" + json.dumps(_edit(bad_rec, "models")) + "\n",
+        "base_zero": json.dumps(_edit(bad_rec, "base")) + "\n",
+        "blank_lines_ok": "\n" + good[0] + "\n\n" + good[1] + "\n",
+    }
+    out = {}
+    tmp = os.path.join(OUT, "_tmp_trace.ndjson")
+    for name, text in cases.items():
+        with open(tmp, "w") as fh:
+            fh.write(text)
+        try:
+            n = len(workload.load_trace(tmp))
+            out[name] = {"text": text, "error": None, "n": n}
+        except SimError as exc:
+            out[name] = {"text": text, "error": type(exc).__name__,
+                         "line": getattr(exc, "line", None), "message": str(exc)}
+    os.remove(tmp)
+    with open(os.path.join(OUT, "trace_errors.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    return NP
+
+
+def _edit(rec, how):
+    import copy
+    d = copy.deepcopy(rec)
+    if how == "neg":
+        first = sorted(d["stages"][0]["models"])[0]
+        d["stages"][0]["models"][first]["out_tokens"] = -3
+    elif how == "idx":
+        d["stages"][0]["stage_index"] = 2
+    elif how == "models":
+        first = sorted(d["success"])[0]
+        del d["success"][first]
+        for st in d["stages"]:
+            del st["models"][first]
+    elif how == "base":
+        d["stages"][-1]["base_input_tokens"] = 0
+    return d
+
+
 def _reference_rows(sc, ids, state, engines, recs, rt_tab, pr_tab):
     """schedule_request over sc's rows against a live SchedulerState."""
     k = len(ids)
@@ -598,4 +702,5 @@ if __name__ == "__main__":
     make_queues()
     make_quantile()
     make_synth()
+    print("trace programs:", make_trace())
     print("done")

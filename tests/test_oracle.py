@@ -142,4 +142,3 @@ def test_quantile_tables(q):
             sti = st if st <= gp.s_cap else 0
             for m in range(3):
                 assert tab[wi, sti, m] == grid[a, st - 1, m], (wf, st, m)
-
