@@ -55,9 +55,10 @@ def parse_args():
     p.add_argument("--attention", default="fused", choices=["fused", "unfused"],
                    help="S=128 router layers: fused QKV+attention kernel or QKV GEMM + "
                         "attention kernel (A/B measurement)")
-    p.add_argument("--layernorm", default="deferred", choices=["deferred", "cluster"],
-                   help="post-LN sublayers: deferred LayerNorm folded into the next GEMM "
-                        "(default) or normalised in a cluster-row GEMM epilogue (A/B)")
+    p.add_argument("--layernorm", default="auto", choices=["auto", "deferred", "cluster"],
+                   help="post-LN sublayers: deferred LayerNorm folded into the next GEMM or "
+                        "normalised in a cluster-row GEMM epilogue; auto = deferred for "
+                        "H >= 768, cluster below (A/B measurement)")
     p.add_argument("--graph", action="store_true",
                    help="replay the tick as a CUDA graph (1 GPU; per-kernel timing from an "
                         "eager profiled pass)")
@@ -327,6 +328,8 @@ def run_ours(args):
         wl.router.cfg_c.flags |= _lib.ENC_UNFUSED_ATTENTION
     if args.layernorm == "cluster":
         wl.router.cfg_c.flags |= _lib.ENC_CLUSTER_LN
+    elif args.layernorm == "deferred":
+        wl.router.cfg_c.flags |= _lib.ENC_DEFERRED_LN
     B, K = wl.batch_size, len(wl.pool)
     gs = GpuScheduler(wl.pool, wl.balancer, wl.aging, router=wl.router, predictor=wl.predictor,
                       n_programs=wl.n_programs, max_rows=B, device=dev,

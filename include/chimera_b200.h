@@ -200,8 +200,11 @@ typedef struct chm_encoder_cfg {
 #define CHM_ENC_UNFUSED_ATTENTION 1
 /* chm_encoder_cfg.flags: normalise every post-LN sublayer inside its own GEMM
  * epilogue (rows owned by clusters of 2H/256 CTAs exchanging statistics over
- * DSMEM) instead of the deferred LayerNorm. Same math; A/B measurement. */
+ * DSMEM) instead of the deferred LayerNorm, also for H >= 768. Same math. */
 #define CHM_ENC_CLUSTER_LN 2
+/* chm_encoder_cfg.flags: force the deferred LayerNorm (default only for
+ * H >= 768; H <= 512 uses the cluster path, whose clusters tile every SM). */
+#define CHM_ENC_DEFERRED_LN 4
 
 /* bf16 weights, row-major [out_features, in_features] (nn.Linear layout). */
 typedef struct chm_encoder_weights {

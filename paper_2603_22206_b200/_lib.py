@@ -167,6 +167,7 @@ class EncoderCfg(ctypes.Structure):
 
 ENC_UNFUSED_ATTENTION = 1
 ENC_CLUSTER_LN = 2
+ENC_DEFERRED_LN = 4
 
 
 class EncoderWeights(ctypes.Structure):

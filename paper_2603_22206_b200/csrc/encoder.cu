@@ -996,9 +996,13 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   const FoldedLayout FL = folded_layout(cfg);
   chm_status rc;
   const bool fused = S == kAttnS && !(cfg.flags & CHM_ENC_UNFUSED_ATTENTION);
-  // A/B measurement: the cluster-LayerNorm path (each post-LN sublayer
-  // normalised in its own GEMM epilogue, rows owned by 2H/256-CTA clusters)
-  const bool cluster_ln = (cfg.flags & CHM_ENC_CLUSTER_LN) != 0;
+  // Cluster-LayerNorm path (each post-LN sublayer normalised in its own GEMM
+  // epilogue, rows owned by 2H/256-CTA clusters): for H <= 512 the clusters
+  // (2 or 4 CTAs) still tile all 148 SMs and the row statistics never leave
+  // the cluster, so it is the default there; for H >= 768 the 6-CTA clusters
+  // leave SMs idle and the deferred LayerNorm wins (profiles/r1c_gemm_cycles.md).
+  const bool cluster_ln = ((cfg.flags & CHM_ENC_CLUSTER_LN) != 0 || H <= 512) &&
+                          (cfg.flags & CHM_ENC_DEFERRED_LN) == 0;
   for (int l = 0; l < L; ++l) {
     const uint8_t* fb = reinterpret_cast<const uint8_t*>(ws.folded) + (size_t)l * FL.per_layer;
     const void* wq = cluster_ln ? w.w_qkv[l] : fb + FL.wqkv;

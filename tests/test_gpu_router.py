@@ -206,14 +206,19 @@ def test_gemm_folded_layernorm(M, N, K, epilogue):
     torch.testing.assert_close(C.float(), ref, rtol=GEMM_RTOL, atol=3e-2)
 
 
-@pytest.mark.parametrize("cfg,S", [(SMALL, 128), (EncoderConfig(n_layers=3), 128), (SMALL, 256)])
-def test_encoder_random_layernorm_params(cfg, S):
+@pytest.mark.parametrize("cfg,S,flags", [(SMALL, 128, 0), (SMALL, 128, _lib.ENC_DEFERRED_LN),
+                                         (EncoderConfig(n_layers=3), 128, 0),
+                                         (EncoderConfig(n_layers=3), 128, _lib.ENC_CLUSTER_LN),
+                                         (SMALL, 256, _lib.ENC_DEFERRED_LN)])
+def test_encoder_random_layernorm_params(cfg, S, flags):
     """Non-trivial LayerNorm gamma/beta (BERT init has 1/0): exercises the
-    folded weights and the residual-side LayerNorm of the deferred path."""
+    folded weights and the residual-side LayerNorm of the deferred path, and
+    the cluster-LayerNorm path, on both hidden sizes."""
     from dataclasses import replace
     cfg = replace(cfg, seq_len=S)
     K, B = 5, 8
     r = GpuEncoderRouter(cfg, K, max_rows=B, seed=6, head_std=2 / math.sqrt(cfg.hidden))
+    r.cfg_c.flags |= flags
     gen = torch.Generator(device="cuda").manual_seed(17)
     for name, t in r.weights.items():
         if name.startswith(("ln1_", "ln2_", "emb_ln_")):
