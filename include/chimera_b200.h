@@ -105,6 +105,12 @@ typedef struct chm_monitor_state {
   int32_t inflight_capacity;
   int64_t* inflight_key;
   double* inflight_yhat;
+  /* ActivityMonitor(decay_in_flight=True) (monitor.py:40-42, 108-129): the
+   * tokens each live request has already emitted, parallel to the log
+   * (0 on dispatch, set by chm_monitor_note_progress); the in-flight sum is
+   * then the Neumaier sum of max(yhat - progress, 0) in insertion order.
+   * NULL = decay off (the reference default). */
+  double* inflight_progress;
 } chm_monitor_state;
 
 /* ---- one batch of requests, in arrival order ----------------------------- */
@@ -311,6 +317,18 @@ chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* aging,
                           const chm_monitor_state* mon, const chm_queue_state* q,
                           const chm_rows* rows, const chm_decisions* dec,
                           int32_t n_iterations, int32_t* error, void* stream);
+
+/* ActivityMonitor.note_progress (monitor.py:108-111) for n (model index,
+ * request key, emitted tokens) updates, in call order (a later update of the
+ * same request wins); requests not in flight on that model are ignored, as in
+ * the reference. Then the in-flight sums are recomputed with the decayed terms
+ * (in_flight_sum, monitor.py:122-129): the snapshot the next
+ * chm_schedule_rows starts from (simcore._sync_progress before a dispatch,
+ * simcore.py:260-264, 278-279). Requires inflight_progress. */
+chm_status chm_monitor_note_progress(const chm_pool* pool, const chm_monitor_state* mon,
+                                     const int32_t* model, const int64_t* key,
+                                     const double* emitted, int32_t n, int32_t* error,
+                                     void* stream);
 
 /* Trace store. chm_trace_derive: remaining (the suffix
  * sums TraceRecord.remaining_tokens returns, workload.py:160-165) and

@@ -48,10 +48,12 @@ class PortError(Exception):
 # activity monitor (monitor.py:40-140)
 # --------------------------------------------------------------------------
 class PortMonitor:
-    def __init__(self, model_ids):
+    def __init__(self, model_ids, decay_in_flight: bool = False):  # monitor.py:40-48
         self.live: dict[str, dict[str, float]] = {m: {} for m in sorted(model_ids)}
+        self.progress: dict[str, dict[str, float]] = {m: {} for m in self.live}
         self.owner: dict[str, str] = {}
         self.assignments: dict[str, str] = {}
+        self.decay_in_flight = decay_in_flight
 
     def assignment(self, program_id):
         return self.assignments.get(program_id)
@@ -78,11 +80,19 @@ class PortMonitor:
         if self.live[model_id].pop(request_id, None) is None:
             raise PortError("UnknownRequest", request_id)
         del self.owner[request_id]
+        self.progress[model_id].pop(request_id, None)
 
-    def in_flight_sum(self, model_id):  # monitor.py:122-127 (no decay)
+    def note_progress(self, model_id, request_id, emitted):  # monitor.py:108-111
+        if request_id in self.live.get(model_id, {}):
+            self.progress[model_id][request_id] = emitted
+
+    def in_flight_sum(self, model_id):  # monitor.py:122-129
         # builtin sum(): Neumaier-compensated on CPython >= 3.12, re-evaluated
         # over every live entry on every call -- the reference's cost.
-        return sum(self.live[model_id].values())
+        if not self.decay_in_flight:
+            return sum(self.live[model_id].values())
+        prog = self.progress[model_id]
+        return sum(max(y - prog.get(rid, 0.0), 0.0) for rid, y in self.live[model_id].items())
 
 
 # --------------------------------------------------------------------------

@@ -76,6 +76,7 @@ class MonitorState(ctypes.Structure):
         ("inflight_capacity", c_int32),
         ("inflight_key", c_void_p),
         ("inflight_yhat", c_void_p),
+        ("inflight_progress", c_void_p),
     ]
 
 
@@ -246,6 +247,9 @@ _SIGNATURES = [
      [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p]),
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
     ("chm_trace_derive", c_int32, [POINTER(Trace), c_void_p, c_void_p]),
+    ("chm_monitor_note_progress", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
+      c_void_p]),
     ("chm_trace_gather_rows", c_int32,
      [POINTER(Trace), c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
       c_void_p, c_void_p]),

@@ -17,6 +17,9 @@
 //     synthetic workloads);
 //   * otherwise one thread replays the serial Neumaier recurrence in insertion
 //     order (bit-identical to the reference for any values).
+// With decay_in_flight (monitor.inflight_progress != NULL) the recomputed sum
+// is over max(yhat - progress, 0) (monitor.py:122-129), and
+// chm_monitor_note_progress sets the progress column (monitor.py:108-111).
 // A completion naming a request that is not in flight on that model is
 // errors.UnknownRequest (monitor.py:104-105). The (program, stage) in-flight
 // bit is cleared, so the same request id may be dispatched again.
@@ -47,21 +50,76 @@ struct Smem {
   int dy[kThreads / 32];
 };
 
-__global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mon,
-                                                            const int32_t* __restrict__ model,
-                                                            const int64_t* __restrict__ key, int n,
-                                                            int32_t* n_complete, int32_t* err) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
-  const int m = blockIdx.x, K = gridDim.x;
+// The term one live entry contributes to in_flight_sum (monitor.py:122-129):
+// y, or with decay Python's max(y - progress, 0.0) (first argument unless 0.0
+// is strictly greater).
+__device__ __forceinline__ double live_term(double y, const double* prog, size_t at) {
+  if (!prog) return y;
+  const double d = __dsub_rn(y, prog[at]);
+  return (0.0 > d) ? 0.0 : d;
+}
+
+// (sum, comp) of model m's n_live entries in insertion order, as CPython 3.12
+// sum() leaves them (Neumaier):
+//   * exact fast path: every term a multiple of 2^-8 below 2^36 and the total
+//     below 2^44 -> every partial sum is exact in fp64 in any order and the
+//     compensation is exactly 0: a parallel int64 reduction;
+//   * otherwise one thread replays the recurrence in insertion order.
+// Block-wide (all threads call it); writes sum / comp / count of model m.
+__device__ void recompute_sum(const chm_monitor_state& mon, int m, int n_live,
+                              unsigned long long* red, int* dy) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // ---- this model's completions, in call order ----
+  const size_t base = (size_t)m * mon.inflight_capacity;
+  bool dyadic = true;
+  unsigned long long fixed = 0;  // exact sum in units of 2^-8
+  for (int i = tid; i < n_live; i += blockDim.x) {
+    const double y = live_term(mon.inflight_yhat[base + i], mon.inflight_progress, base + i);
+    const double sc = y * 256.0;
+    if (!(y >= 0.0 && y < 68719476736.0 && sc == floor(sc))) dyadic = false;
+    else fixed += (unsigned long long)sc;
+  }
+  for (int o = 16; o; o >>= 1) fixed += __shfl_xor_sync(0xffffffffu, fixed, o);
+  const int dy_all = __all_sync(0xffffffffu, dyadic);
+  if (lane == 0) {
+    red[warp] = fixed;
+    dy[warp] = dy_all;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long tot = 0;
+    int ok = 1;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      tot += red[w];
+      ok &= dy[w];
+    }
+    double sum, comp = 0.0;
+    if (ok && tot < (1ull << 52)) {  // total < 2^44 in units of 2^-8
+      sum = (double)tot * (1.0 / 256.0);
+    } else {
+      sum = 0.0;
+      for (int i = 0; i < n_live; ++i)
+        neumaier_add(sum, comp,
+                     live_term(mon.inflight_yhat[base + i], mon.inflight_progress, base + i));
+    }
+    mon.inflight_sum[m] = sum;
+    mon.inflight_comp[m] = comp;
+    mon.inflight_count[m] = n_live;
+  }
+}
+
+// This model's entries of the call's (model, key) list, sorted by (key, call
+// index) in shared memory (bitonic over the next power of two). Returns the
+// count, or -1 when it exceeds kMaxPerModel (reported).
+__device__ int gather_sorted(Smem& s, int m, int K, const int32_t* __restrict__ model,
+                             const int64_t* __restrict__ key, int n, int32_t* err,
+                             bool unknown_model_is_error) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s.misc[0] = 0;
   __syncthreads();
   for (int b0 = 0; b0 < n; b0 += kThreads) {
     const int j = b0 + tid;
     const int mj = j < n ? model[j] : -1;
-    if (j < n && (mj < 0 || mj >= K) && m == 0)
+    if (unknown_model_is_error && j < n && (mj < 0 || mj >= K) && m == 0)
       report_error(err, CHM_ERR_VALIDATION, j, mj, 0);  // errors.UnknownModel
     const bool mine = j < n && mj == m;
     const unsigned bal = __ballot_sync(0xffffffffu, mine);
@@ -92,16 +150,14 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
   const int nm = s.misc[0];
   if (nm > kMaxPerModel) {
     if (tid == 0) report_error(err, CHM_ERR_UNSUPPORTED, 0, m, nm);
-    return;
+    return -1;
   }
-  if (n_complete && tid == 0) n_complete[m] = nm;
-  if (nm == 0) return;
-  // ---- bitonic sort of (key, idx) by key over the next power of two ----
+  if (nm == 0) return 0;
   int np2 = 1;
   while (np2 < nm) np2 <<= 1;
   for (int i = nm + tid; i < np2; i += kThreads) {
     s.key[i] = LLONG_MAX;
-    s.idx[i] = -1;
+    s.idx[i] = INT_MAX;
   }
   for (int i = tid; i < np2; i += kThreads) s.found[i] = 0;
   __syncthreads();
@@ -112,7 +168,8 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
         if (pr > i) {
           const bool up = (i & size) == 0;
           const long long a = s.key[i], b = s.key[pr];
-          if ((a > b) == up) {
+          const bool gt = a > b || (a == b && s.idx[i] > s.idx[pr]);  // (key, call order)
+          if (gt == up) {
             s.key[i] = b;
             s.key[pr] = a;
             const int t = s.idx[i];
@@ -124,6 +181,32 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
       __syncthreads();
     }
   }
+  return nm;
+}
+
+__device__ __forceinline__ int find_key(const Smem& s, int nm, long long kk) {
+  int lo = 0, hi = nm - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const long long v = s.key[mid];
+    if (v == kk) return mid;
+    if (v < kk) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mon,
+                                                            const int32_t* __restrict__ model,
+                                                            const int64_t* __restrict__ key, int n,
+                                                            int32_t* n_complete, int32_t* err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int m = blockIdx.x, K = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nm = gather_sorted(s, m, K, model, key, n, err, true);
+  if (nm < 0) return;
+  if (n_complete && tid == 0) n_complete[m] = nm;
+  if (nm == 0) return;
   // duplicate completions of one request: the second is unknown by then
   for (int i = tid + 1; i < nm; i += kThreads)
     if (s.key[i] == s.key[i - 1]) report_error(err, CHM_ERR_UNKNOWN_REQUEST, s.idx[i], m, 0);
@@ -131,23 +214,17 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
   const size_t base = (size_t)m * mon.inflight_capacity;
   const int live = (int)mon.inflight_count[m];
   int out = 0;
-  bool dyadic = true;
-  unsigned long long fixed = 0;  // exact sum in units of 2^-8 (fast path)
+  double* prog = mon.inflight_progress;
   for (int b0 = 0; b0 < live; b0 += kThreads) {
     const int i = b0 + tid;
     long long kk = 0;
-    double y = 0.0;
+    double y = 0.0, pg = 0.0;
     bool keep = false;
     if (i < live) {
       kk = mon.inflight_key[base + i];
       y = mon.inflight_yhat[base + i];
-      int lo = 0, hi = nm - 1, hit = -1;
-      while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const long long v = s.key[mid];
-        if (v == kk) { hit = mid; break; }
-        if (v < kk) lo = mid + 1; else hi = mid - 1;
-      }
+      if (prog) pg = prog[base + i];
+      int hit = find_key(s, nm, kk);
       if (hit >= 0) {
         // first occurrence among duplicates
         while (hit > 0 && s.key[hit - 1] == kk) --hit;
@@ -156,9 +233,6 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
           atomicAnd(mon.stage_bits + kk / 32, ~(1u << (int)(kk & 31)));
       } else {
         keep = true;
-        const double sc = y * 256.0;
-        if (!(y >= 0.0 && y < 68719476736.0 && sc == floor(sc))) dyadic = false;
-        else fixed += (unsigned long long)sc;
       }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -175,10 +249,13 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
       if (lane == 31) s.misc[1] = incl;
     }
     __syncthreads();
+    // (all reads of this block of entries precede the writes: the barrier
+    // above; writes go to positions <= the read positions, stable order)
     if (keep) {
       const size_t pos = base + out + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
       mon.inflight_key[pos] = kk;
       mon.inflight_yhat[pos] = y;
+      if (prog) prog[pos] = pg;
     }
     out += s.misc[1];
     __syncthreads();
@@ -187,32 +264,36 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
   for (int i = tid; i < nm; i += kThreads)
     if (!s.found[i] && (i == 0 || s.key[i] != s.key[i - 1]))
       report_error(err, CHM_ERR_UNKNOWN_REQUEST, s.idx[i], m, 0);
-  // ---- recompute (sum, comp) over the survivors ----
-  for (int o = 16; o; o >>= 1) fixed += __shfl_xor_sync(0xffffffffu, fixed, o);
-  const int dy_all = __all_sync(0xffffffffu, dyadic);
-  if (lane == 0) {
-    s.red[warp] = fixed;
-    s.dy[warp] = dy_all;
+  __syncthreads();
+  recompute_sum(mon, m, out, s.red, s.dy);
+}
+
+// ActivityMonitor.note_progress for this model's updates, then the decayed sum.
+__global__ void __launch_bounds__(kThreads) progress_kernel(chm_monitor_state mon,
+                                                            const int32_t* __restrict__ model,
+                                                            const int64_t* __restrict__ key,
+                                                            const double* __restrict__ emitted,
+                                                            int n, int32_t* err) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  const int m = blockIdx.x, K = gridDim.x;
+  // note_progress ignores unknown models and requests not in flight
+  const int nm = gather_sorted(s, m, K, model, key, n, err, false);
+  if (nm < 0) return;
+  const size_t base = (size_t)m * mon.inflight_capacity;
+  const int live = (int)mon.inflight_count[m];
+  if (nm > 0) {
+    for (int i = threadIdx.x; i < live; i += kThreads) {
+      const long long kk = mon.inflight_key[base + i];
+      int hit = find_key(s, nm, kk);
+      if (hit >= 0) {
+        while (hit + 1 < nm && s.key[hit + 1] == kk) ++hit;  // the last call wins
+        mon.inflight_progress[base + i] = emitted[s.idx[hit]];
+      }
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    unsigned long long tot = 0;
-    int ok = 1;
-    for (int w = 0; w < kThreads / 32; ++w) {
-      tot += s.red[w];
-      ok &= s.dy[w];
-    }
-    double sum, comp = 0.0;
-    if (ok && tot < (1ull << 52)) {  // total < 2^44 in units of 2^-8
-      sum = (double)tot * (1.0 / 256.0);
-    } else {
-      sum = 0.0;
-      for (int i = 0; i < out; ++i) neumaier_add(sum, comp, mon.inflight_yhat[base + i]);
-    }
-    mon.inflight_sum[m] = sum;
-    mon.inflight_comp[m] = comp;
-    mon.inflight_count[m] = out;
-  }
+  recompute_sum(mon, m, live, s.red, s.dy);
 }
 
 }  // namespace mon
@@ -235,6 +316,30 @@ extern "C" chm_status chm_monitor_complete(const chm_pool* pool, const chm_monit
                                                                  error);
   // bytes: the completion list per model + live log read + survivors written
   chm::prof::end(chm::prof::K_PREPARE, s, (double)n * 12.0 * K);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_monitor_note_progress(const chm_pool* pool,
+                                                const chm_monitor_state* mon,
+                                                const int32_t* model, const int64_t* key,
+                                                const double* emitted, int32_t n,
+                                                int32_t* error, void* stream) {
+  if (!pool || !mon || n < 0 || (n > 0 && (!model || !key || !emitted)))
+    return CHM_ERR_INVALID_ARG;
+  if (!mon->inflight_key || !mon->inflight_yhat || !mon->inflight_progress ||
+      mon->inflight_capacity < 1)
+    return CHM_ERR_UNSUPPORTED;
+  const int K = pool->n_models;
+  if (K < 1 || K > CHM_MAX_MODELS) return CHM_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = sizeof(chm::mon::Smem);
+  cudaFuncSetAttribute(chm::mon::progress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  chm::prof::begin(chm::prof::K_PREPARE, s);
+  chm::mon::progress_kernel<<<K, chm::mon::kThreads, smem, s>>>(*mon, model, key, emitted, n,
+                                                                 error);
+  chm::prof::end(chm::prof::K_PREPARE, s, (double)n * 20.0 * K);
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }

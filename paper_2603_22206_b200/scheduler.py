@@ -158,7 +158,8 @@ class GpuScheduler:
     def __init__(self, pool: Pool, balancer: BalancerConfig = BalancerConfig(),
                  aging: AgingConfig = AgingConfig(), *, router=None, predictor=None,
                  n_programs: int = 1 << 20, max_rows: int = 16384,
-                 queue_capacity: int = 10240, device="cuda", inflight_capacity=None):
+                 queue_capacity: int = 10240, device="cuda", inflight_capacity=None,
+                 decay_in_flight: bool = False):
         self.lib = _lib.load()
         self.pool = pool
         self.ids = pool.model_ids
@@ -169,7 +170,8 @@ class GpuScheduler:
         self.predictor = predictor
         self.device = torch.device(device)
         self.state = DeviceState(pool, n_programs, queue_capacity, self.device,
-                                 inflight_capacity=inflight_capacity)
+                                 inflight_capacity=inflight_capacity,
+                                 decay_in_flight=decay_in_flight)
         self.buf = BatchBuffers(self.K, max_rows, self.device)
         self.bal_c = balancer_struct(balancer)
         self.aging_c = aging_struct(aging)
@@ -226,6 +228,24 @@ class GpuScheduler:
             _lib.check(lib.chm_queue_tick(st.pool_c, self.aging_c, st.monitor_c, st.queue_c,
                                           rows_c, dec_c, int(n_iterations), _p(buf.error), sh),
                        "chm_queue_tick")
+
+    def note_progress(self, models, keys, emitted, stream=None) -> None:
+        """ActivityMonitor.note_progress (monitor.py:108-111) for a batch of
+        (model index, request key, emitted tokens) updates, then the decayed
+        in-flight sums (decay_in_flight=True schedulers only). Keys are
+        `state.request_key(program, stage)` (negative for seeded entries)."""
+        if not self.state.decay_in_flight:
+            raise ValueError("note_progress needs GpuScheduler(decay_in_flight=True)")
+        d = self.device
+        m = torch.as_tensor(np.asarray(models, np.int32), device=d)
+        k = torch.as_tensor(np.asarray(keys, np.int64), device=d)
+        e = torch.as_tensor(np.asarray(emitted, np.float64), device=d)
+        s = stream if stream is not None else torch.cuda.current_stream(d)
+        self.buf.error.copy_(self.buf.error_init)
+        _lib.check(self.lib.chm_monitor_note_progress(
+            self.state.pool_c, self.state.monitor_c, _p(m), _p(k), _p(e), int(m.numel()),
+            _p(self.buf.error), s.cuda_stream), "chm_monitor_note_progress")
+        self._keep = (m, k, e)  # alive until the stream has consumed them
 
     def check_errors(self, context: str = "") -> None:
         _lib.raise_device_error(self.buf.error.cpu().tolist(), context)

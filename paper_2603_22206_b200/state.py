@@ -56,7 +56,8 @@ class DeviceState:
     """Monitor + engine + queue state for one pool on one device."""
 
     def __init__(self, pool: Pool, n_programs: int, queue_capacity: int = 10240,
-                 device: str | torch.device = "cuda", inflight_capacity: int | None = None):
+                 device: str | torch.device = "cuda", inflight_capacity: int | None = None,
+                 decay_in_flight: bool = False):
         self.pool = pool
         self.ids = pool.model_ids
         self.K = len(self.ids)
@@ -84,6 +85,10 @@ class DeviceState:
                                      else min(max(NP, 65536), 1 << 22))
         self.inflight_key = torch.zeros(K * self.inflight_capacity, dtype=i64, device=d)
         self.inflight_yhat = torch.zeros(K * self.inflight_capacity, dtype=f64, device=d)
+        # ActivityMonitor(decay_in_flight=True): emitted tokens per live entry
+        self.decay_in_flight = bool(decay_in_flight)
+        self.inflight_progress = (torch.zeros(K * self.inflight_capacity, dtype=f64, device=d)
+                                  if self.decay_in_flight else None)
         n = K * C
         self.q_priority = torch.zeros(n, dtype=f64, device=d)
         self.q_arrival = torch.zeros(n, dtype=f64, device=d)
@@ -112,7 +117,7 @@ class DeviceState:
             _ptr(self.assignment), _ptr(self.stage_bits), _ptr(self.batch_stamp),
             _ptr(self.engine_clock), _ptr(self.engine_seq), _ptr(self.engine_running),
             _ptr(self.engine_queued), _ptr(self.engine_iterations), self.inflight_capacity,
-            _ptr(self.inflight_key), _ptr(self.inflight_yhat))
+            _ptr(self.inflight_key), _ptr(self.inflight_yhat), _ptr(self.inflight_progress))
         self.queue_c = _lib.QueueState(
             C, _ptr(self.q_priority), _ptr(self.q_arrival), _ptr(self.q_seq),
             _ptr(self.q_handle), _ptr(self.q_out_tokens), _ptr(self.q_level),
@@ -185,11 +190,14 @@ class DeviceState:
                 "engine_iterations", "q_priority", "q_arrival", "q_seq", "q_handle",
                 "q_out_tokens", "q_level", "q_count", "q_quantum")
 
+    def _mutable(self):
+        return self._MUTABLE + (("inflight_progress",) if self.decay_in_flight else ())
+
     def snapshot(self) -> dict:
-        return {k: getattr(self, k).clone() for k in self._MUTABLE}
+        return {k: getattr(self, k).clone() for k in self._mutable()}
 
     def restore(self, snap: dict) -> None:
-        for k in self._MUTABLE:
+        for k in self._mutable():
             getattr(self, k).copy_(snap[k], non_blocking=True)
 
     # -- views ---------------------------------------------------------------

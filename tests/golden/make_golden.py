@@ -603,19 +603,29 @@ def _reference_rows(sc, ids, state, engines, recs, rt_tab, pr_tab):
     return dict(model=model, priority=prio, cached=cached, loads=loads), err
 
 
-def make_completions():
+COMPLETION_SPECS = {
+    "c5_dyadic": dict(seed=21, k=5, n1=1500, n2=1500, p0=800, dyadic=True, frac=0.4),
+    "c3_nondyadic": dict(seed=22, k=3, n1=1000, n2=800, p0=200, dyadic=False, frac=0.5),
+    "c8_mixed": dict(seed=23, k=8, n1=2000, n2=1500, p0=300, dyadic=False, frac=0.3),
+    "c4_all": dict(seed=24, k=4, n1=600, n2=600, p0=100, dyadic=True, frac=1.0),
+    # ActivityMonitor(decay_in_flight=True) + note_progress before the completions
+    "c5_decay": dict(seed=25, k=5, n1=1200, n2=1000, p0=300, dyadic=True, frac=0.3, decay=True),
+    "c3_decay_nondyadic": dict(seed=26, k=3, n1=800, n2=700, p0=150, dyadic=False, frac=0.4,
+                               decay=True),
+}
+
+
+def make_completions(only=None):
     """Completion path (monitor.py:98-129): batch 1 through schedule_request,
-    then record_completion for a random subset of the live requests (batch-1
-    rows and pre-seeded entries, shuffled), then batch 2 -- fresh programs and
-    later stages of batch-1 programs -- against the reduced in-flight sums."""
-    specs = {
-        "c5_dyadic": dict(seed=21, k=5, n1=1500, n2=1500, p0=800, dyadic=True, frac=0.4),
-        "c3_nondyadic": dict(seed=22, k=3, n1=1000, n2=800, p0=200, dyadic=False, frac=0.5),
-        "c8_mixed": dict(seed=23, k=8, n1=2000, n2=1500, p0=300, dyadic=False, frac=0.3),
-        "c4_all": dict(seed=24, k=4, n1=600, n2=600, p0=100, dyadic=True, frac=1.0),
-    }
+    then (decay specs) note_progress for a random subset of live requests plus
+    unknown ids and repeats, then record_completion for a random subset of the
+    live requests (batch-1 rows and pre-seeded entries, shuffled), then batch 2
+    -- fresh programs and later stages of batch-1 programs -- against the
+    reduced (decayed) in-flight sums."""
     out = {}
-    for name, sp in specs.items():
+    for name, sp in COMPLETION_SPECS.items():
+        if only is not None and name not in only:
+            continue
         rng = np.random.default_rng(sp["seed"] + 1000)
         k, n1, n2 = sp["k"], sp["n1"], sp["n2"]
         sc1 = build_scenario(sp["seed"], k, n1, dyadic=sp["dyadic"], p0_entries=sp["p0"],
@@ -645,7 +655,8 @@ def make_completions():
         ids = sc1["ids"]
         pool = profiles.Pool(tuple(profiles.ModelProfile(ids[i], sc1["decode"][i],
                                                          sc1["batch"][i]) for i in range(k)))
-        mon = monitor.ActivityMonitor(ids)
+        decay = bool(sp.get("decay", False))
+        mon = monitor.ActivityMonitor(ids, decay_in_flight=decay)
         seed_pos = {m: 0 for m in range(k)}
         seed_keys = []
         for j, (m, v) in enumerate(sc1["p0"]):
@@ -662,6 +673,25 @@ def make_completions():
         live = [(int(res1["model"][i]), int(sc1["prog"][i]) * 32 + int(sc1["stage"][i]) - 1,
                  f"p{int(sc1['prog'][i]):06d}:{int(sc1['stage'][i])}") for i in range(n1)]
         live += seed_keys
+        prog_upd = []  # (model, key, emitted) in call order
+        if decay:
+            for m, kk, rid in live:
+                if rng.random() < 0.5:
+                    y = mon._in_flight[ids[m]][rid]
+                    e = float(rng.integers(0, int(2 * y) + 2)) / (2 if sp["dyadic"] else 3)
+                    mon.note_progress(ids[m], rid, e)
+                    prog_upd.append((m, kk, e))
+            rows = [c for c in live if c[1] >= 0]  # program keys are unique across models
+            for _ in range(20):  # not in flight on that model: ignored
+                m, kk, rid = rows[int(rng.integers(0, len(rows)))]
+                mon.note_progress(ids[(m + 1) % k], rid, 5.0)
+                prog_upd.append(((m + 1) % k, kk, 5.0))
+            for _ in range(30):  # repeats: the last call wins
+                m, kk, rid = live[int(rng.integers(0, len(live)))]
+                e = float(rng.integers(0, 50))
+                mon.note_progress(ids[m], rid, e)
+                prog_upd.append((m, kk, e))
+        prog_p = np.array([mon.in_flight_sum(mid) for mid in ids], dtype=np.float64)
         pick = [c for c in live if rng.random() < sp["frac"]]
         rng.shuffle(pick)
         for m, _, rid in pick:
@@ -681,6 +711,10 @@ def make_completions():
             out_tok1=sc1["out_tok"], arrival1=sc1["arrival"],
             prog2=sc2["prog"], stage2=sc2["stage"], q2=sc2["q"], yhat2=sc2["yhat"],
             out_tok2=sc2["out_tok"], arrival2=sc2["arrival"],
+            decay=int(decay), prog_p=prog_p,
+            p_model=np.array([u[0] for u in prog_upd], dtype=np.int32),
+            p_key=np.array([u[1] for u in prog_upd], dtype=np.int64),
+            p_emitted=np.array([u[2] for u in prog_upd], dtype=np.float64),
             c_model=np.array([c[0] for c in pick], dtype=np.int32),
             c_key=np.array([c[1] for c in pick], dtype=np.int64),
             mid_p=mid_p, mid_cnt=mid_cnt, final_p=final_p, final_cnt=final_cnt,

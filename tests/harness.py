@@ -134,6 +134,9 @@ def load_complete(name):
     b2 = dict(common, prog=d["prog2"], stage=d["stage2"], q=d["q2"], yhat=d["yhat2"],
               out_tok=d["out_tok2"], arrival=d["arrival2"], p0=np.zeros((0, 2)),
               pre=np.zeros((0, 2), np.int64))
+    d.setdefault("decay", np.array(0))
+    for key, dt in (("p_model", np.int32), ("p_key", np.int64), ("p_emitted", np.float64)):
+        d.setdefault(key, np.zeros(0, dt))
     return d, b1, b2
 
 
@@ -154,13 +157,16 @@ def run_port_complete(name):
     d, b1, b2 = load_complete(name)
     ids, k = b1["ids"], b1["k"]
     pool = pool_of(b1)
-    mon = hp.PortMonitor(ids)
+    mon = hp.PortMonitor(ids, decay_in_flight=bool(int(d["decay"])))
     for j, (m, v) in enumerate(b1["p0"]):
         mon.record_dispatch(ids[int(m)], f"seed:{j}", float(v))
     for p, m in b1["pre"]:
         mon.assign(f"p{int(p):06d}", ids[int(m)])
     engines = {mid: hp.PortEngine(pool[mid].max_batch_size) for mid in ids}
     seeds = seed_request_ids(b1["p0"], k)
+
+    def rid_of(m, key):
+        return seeds[(m, key)] if key < 0 else f"p{key // 32:06d}:{key % 32 + 1}"
 
     def run(sc):
         reqs, recs = requests_of(sc)
@@ -184,9 +190,13 @@ def run_port_complete(name):
         return res
 
     r1 = run(b1)
+    for m, key, e in zip(d["p_model"].tolist(), d["p_key"].tolist(), d["p_emitted"].tolist()):
+        # (updates naming another model use program keys, unique across models)
+        mon.note_progress(ids[m], rid_of(m, key) if key >= 0 else seeds[(m, key)], e)
+    if len(d["p_model"]):
+        assert np.array([mon.in_flight_sum(m) for m in ids]).tobytes() == d["prog_p"].tobytes()
     for m, key in zip(d["c_model"].tolist(), d["c_key"].tolist()):
-        rid = seeds[(m, key)] if key < 0 else f"p{key // 32:06d}:{key % 32 + 1}"
-        mon.record_completion(ids[m], rid)
+        mon.record_completion(ids[m], rid_of(m, key))
     mid_p = np.array([mon.in_flight_sum(m) for m in ids], dtype=np.float64)
     mid_cnt = np.array([len(mon.live[m]) for m in ids], dtype=np.int64)
     r2 = run(b2)

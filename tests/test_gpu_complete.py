@@ -49,10 +49,17 @@ def _complete(gs, models, keys):
 @pytest.mark.parametrize("name", H.complete_names())
 def test_completion_matches_reference(name):
     d, b1, b2 = H.load_complete(name)
-    gs, rt, pr = make_scheduler(b1, max_rows=max(len(b1["prog"]), len(b2["prog"])))
+    decay = bool(int(d["decay"]))
+    gs, rt, pr = make_scheduler(b1, max_rows=max(len(b1["prog"]), len(b2["prog"])),
+                                decay_in_flight=decay)
     r1 = _batch(gs, rt, pr, b1)
     for key in ("model", "priority", "cached"):
         np.testing.assert_array_equal(r1[key], d[f"out1_{key}"], err_msg=key)
+    if decay:  # note_progress (monitor.py:108-111), then the decayed sums (122-129)
+        gs.note_progress(d["p_model"], d["p_key"], d["p_emitted"])
+        torch.cuda.synchronize()
+        gs.check_errors("progress")
+        assert np.array(gs.state.in_flight_sums()).tobytes() == d["prog_p"].tobytes()
     _complete(gs, d["c_model"], d["c_key"])
     gs.check_errors("completions")
     st = gs.state

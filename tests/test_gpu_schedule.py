@@ -20,13 +20,13 @@ ERR_CLASS = {"ValidationError": E.ValidationError, "ValueError": ValueError,
              "DuplicateRequest": E.DuplicateRequest}
 
 
-def make_scheduler(sc, max_rows=None, aging=AgingConfig()):
+def make_scheduler(sc, max_rows=None, aging=AgingConfig(), decay_in_flight=False):
     pool = H.pool_of(sc)
     rt, pr = ScoreTableRouter(), PrecomputedPredictor()
     n = len(sc["prog"])
     gs = GpuScheduler(pool, BalancerConfig(sc["tau"], sc["margin"]), aging, router=rt,
                       predictor=pr, n_programs=sc["n_prog"], max_rows=max_rows or max(n, 1),
-                      queue_capacity=10240)
+                      queue_capacity=10240, decay_in_flight=decay_in_flight)
     st = gs.state
     per_model = {m: [] for m in sc["ids"]}
     for m, v in sc["p0"]:
