@@ -13,6 +13,8 @@
  *   chm_encoder_forward    router.py:39-42       (Router.score -> ConfidenceVector)
  *   chm_trace_*            workload.py:125-253, 454-495 (TraceRecord columns,
  *                          remaining_tokens, first/next_stage_request)
+ *   chm_kendall_tau_*      predictor.py:132-251 (kendall_tau_distance,
+ *                          evaluate_predictor, arrival_order_distance)
  *   chm_predict_*          predictor.py:22-27    (Predictor.predict) and the concrete
  *                          predictors at predictor.py:30-45, 65-108
  *   chm_schedule_rows      balancer.py:89-129    (schedule_request = Alg. 1), with
@@ -366,6 +368,19 @@ chm_status chm_trace_first_stage(const chm_trace* t, const int32_t* program,
                                  const double* arrival_in, int32_t n, int32_t* input_tokens,
                                  double* arrival, int32_t* workflow, int32_t* error,
                                  void* stream);
+
+/* Predictor evaluation: kendall_tau_distance
+ * (predictor.py:182-214) of n >= 2 (predicted, truth) pairs on the device --
+ * merge-sort strict-inversion count after sorting by (predicted, truth), tied
+ * pairs by binary search -- exact int64 counts, *result = (discordant + 0.5 *
+ * half) / (n(n-1)/2) in fp64 like the reference. counts_out (may be NULL) =
+ * {discordant, ties_predicted, ties_truth, ties_both}. Scratch:
+ * chm_kendall_tau_scratch_bytes(n). NaN inputs are not supported (the
+ * reference's sorted() order is undefined for them). */
+uint64_t chm_kendall_tau_scratch_bytes(int64_t n);
+chm_status chm_kendall_tau_distance(const double* predicted, const double* truth, int64_t n,
+                                    void* scratch, uint64_t scratch_bytes, double* result,
+                                    int64_t* counts_out, void* stream);
 
 /* Deferred LayerNorm. The encoder does not normalise a sublayer output where
  * it is produced: out-projection and FFN2 write the pre-LN sum plus per-row

@@ -247,6 +247,10 @@ _SIGNATURES = [
      [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p]),
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
     ("chm_trace_derive", c_int32, [POINTER(Trace), c_void_p, c_void_p]),
+    ("chm_kendall_tau_scratch_bytes", ctypes.c_uint64, [ctypes.c_int64]),
+    ("chm_kendall_tau_distance", c_int32,
+     [c_void_p, c_void_p, ctypes.c_int64, c_void_p, ctypes.c_uint64, c_void_p, c_void_p,
+      c_void_p]),
     ("chm_monitor_note_progress", c_int32,
      [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
       c_void_p]),
@@ -271,7 +275,7 @@ _SIGNATURES = [
 ]
 
 PROFILE_KINDS = ["gemm", "attention", "rowwise", "predict", "prepare", "select", "queue",
-                 "qkv_attention", "trace"]
+                 "qkv_attention", "trace", "eval"]
 
 
 def profile_enable(on: bool) -> None:

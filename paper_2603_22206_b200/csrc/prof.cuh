@@ -18,7 +18,8 @@ enum Kind : int {
   K_QUEUE = 6,
   K_QKV_ATTENTION = 7,  // fused QKV projection + attention (qkv_attn.cu)
   K_TRACE = 8,          // columnar trace store derivation (trace.cu)
-  K_NUM = 9
+  K_EVAL = 9,           // predictor evaluation (evaluate.cu)
+  K_NUM = 10
 };
 
 // Call around one kernel launch on `s`. `work` is the algorithmic FLOPs

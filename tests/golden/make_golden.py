@@ -28,6 +28,8 @@ Fixtures
                       remaining_tokens / first_stage_request / next_stage_request answers
                       for every (program, stage, model) (workload.py:160-165, 454-495)
   trace_errors.json   malformed trace files and the error load_trace raises (256-291)
+  kendall.npz         kendall_tau_distance cases + evaluate_predictor / arrival_order_distance
+  kendall_training.ndjson  on trace_small per model and predictor (predictor.py:182-261)
 """
 
 from __future__ import annotations
@@ -543,6 +545,52 @@ def make_trace():
     return NP
 
 
+def make_kendall():
+    """kendall_tau_distance on hand-made and random sequences (ties in one,
+    the other and both; -0.0; identical and reversed), and evaluate_predictor /
+    arrival_order_distance on trace_small with every predictor kind
+    (predictor.py:182-261)."""
+    rng = np.random.default_rng(31)
+    cases = {
+        "identical": ([1.0, 2.0, 3.0, 4.0], [1.0, 2.0, 3.0, 4.0]),
+        "reversed": ([1.0, 2.0, 3.0, 4.0], [4.0, 3.0, 2.0, 1.0]),
+        "pair": ([0.0, 1.0], [1.0, 0.0]),
+        "ties_pred": ([1.0, 1.0, 2.0, 2.0, 3.0], [5.0, 3.0, 2.0, 9.0, 1.0]),
+        "ties_both": ([1.0, 1.0, 1.0, 2.0, 2.0], [3.0, 3.0, 1.0, 0.5, 0.5]),
+        "neg_zero": ([-0.0, 0.0, 1.0, -1.0], [0.0, -0.0, 2.0, 2.0]),
+        "constant": ([7.0] * 6, [1.0, 2.0, 3.0, 4.0, 5.0, 6.0]),
+    }
+    for n in (17, 1000, 20000):
+        cases[f"rand_{n}"] = (rng.normal(size=n).tolist(), rng.normal(size=n).tolist())
+        cases[f"tied_{n}"] = (rng.integers(0, 20, n).astype(float).tolist(),
+                              rng.integers(0, 50, n).astype(float).tolist())
+    out = {}
+    for name, (p, t) in cases.items():
+        out[f"{name}_p"] = np.array(p)
+        out[f"{name}_t"] = np.array(t)
+        out[f"{name}_d"] = np.array(predictor.kendall_tau_distance(p, t))
+    for bad, (p, t) in {"len": ([1.0, 2.0], [1.0]), "short": ([1.0], [1.0])}.items():
+        try:
+            predictor.kendall_tau_distance(p, t)
+        except SimError as exc:
+            out[f"err_{bad}"] = np.array(type(exc).__name__)
+    recs = workload.load_trace(os.path.join(OUT, "trace_small.ndjson"))
+    ids = sorted(recs[0].model_ids)
+    stats = {m: workload.LengthStats(300 + 150 * i, 200 + 50 * i) for i, m in enumerate(ids)}
+    succ = {m: {"easy": 0.6, "hard": 0.2} for m in ids}
+    training = workload.synthesize_trace(workload.CODE_WORKFLOWS, stats, succ, 400, 41)
+    training += workload.synthesize_trace(workload.MATH_WORKFLOWS, stats, succ, 400, 42)
+    preds = {"oracle": predictor.OraclePredictor(), "input-length": predictor.InputLengthPredictor(),
+             "quantile": predictor.EmpiricalQuantilePredictor(training, 0.5),
+             "quantile90": predictor.EmpiricalQuantilePredictor(training, 0.9)}
+    for pname, pr in preds.items():
+        out[f"eval_{pname}"] = np.array([predictor.evaluate_predictor(pr, recs, m) for m in ids])
+    out["eval_arrival"] = np.array([predictor.arrival_order_distance(recs, m) for m in ids])
+    np.savez_compressed(os.path.join(OUT, "kendall.npz"), cases=np.array(sorted(cases)), **out)
+    workload.save_trace(training, os.path.join(OUT, "kendall_training.ndjson"))
+    return len(cases)
+
+
 def _edit(rec, how):
     import copy
     d = copy.deepcopy(rec)
@@ -737,4 +785,5 @@ if __name__ == "__main__":
     make_quantile()
     make_synth()
     print("trace programs:", make_trace())
+    print("kendall cases:", make_kendall())
     print("done")
