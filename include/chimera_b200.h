@@ -382,6 +382,21 @@ chm_status chm_kendall_tau_distance(const double* predicted, const double* truth
                                     void* scratch, uint64_t scratch_bytes, double* result,
                                     int64_t* counts_out, void* stream);
 
+/* EmpiricalQuantilePredictor training (predictor.py:78-98) on the device:
+ * the table chm_predict_quantile reads, [n_wf + 1, s_cap + 1, K] fp64, from
+ * the derived `remaining` column of a training trace (chm_trace_derive) and a
+ * per-program workflow index in 0..n_wf-1 (sorted workflow ids). Values per
+ * group = remaining tokens of every training (program, stage, model); numpy's
+ * 'linear' quantile with its exact arithmetic; the (workflow, stage, model)
+ * -> (stage, model) -> (model) -> global fallback resolved into the table
+ * (row n_wf: unseen workflow, column 0: stage outside 1..s_cap). n_entries =
+ * sum of n_stages * K. Scratch: chm_quantile_train_scratch_bytes. */
+uint64_t chm_quantile_train_scratch_bytes(int64_t n_entries, int32_t n_wf, int32_t s_cap,
+                                          int32_t n_models);
+chm_status chm_quantile_train(const chm_trace* t, const int32_t* workflow, int32_t n_wf,
+                              int32_t s_cap, double quantile, int64_t n_entries, void* scratch,
+                              uint64_t scratch_bytes, double* table, void* stream);
+
 /* Deferred LayerNorm. The encoder does not normalise a sublayer output where
  * it is produced: out-projection and FFN2 write the pre-LN sum plus per-row
  * partial statistics, and the next projection folds the LayerNorm in

@@ -248,6 +248,11 @@ _SIGNATURES = [
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
     ("chm_trace_derive", c_int32, [POINTER(Trace), c_void_p, c_void_p]),
     ("chm_kendall_tau_scratch_bytes", ctypes.c_uint64, [ctypes.c_int64]),
+    ("chm_quantile_train_scratch_bytes", ctypes.c_uint64,
+     [ctypes.c_int64, c_int32, c_int32, c_int32]),
+    ("chm_quantile_train", c_int32,
+     [POINTER(Trace), c_void_p, c_int32, c_int32, ctypes.c_double, ctypes.c_int64, c_void_p,
+      ctypes.c_uint64, c_void_p, c_void_p]),
     ("chm_kendall_tau_distance", c_int32,
      [c_void_p, c_void_p, ctypes.c_int64, c_void_p, ctypes.c_uint64, c_void_p, c_void_p,
       c_void_p]),

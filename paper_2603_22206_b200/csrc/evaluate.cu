@@ -21,6 +21,9 @@
 // All counts are exact int64; the distance is formed exactly as the
 // reference does: (discordant + 0.5 * half) / total in fp64.
 //
+// The same merge machinery trains EmpiricalQuantilePredictor's tables
+// (chm_quantile_train, below).
+//
 // Work: O(n log^2 n) key reads (binary searches hit L2), O(n log n) key
 // writes. Scratch: 6 * 8 bytes per element (chm_kendall_tau_scratch_bytes).
 #include <utility>
@@ -141,8 +144,156 @@ __global__ void finish_kernel(const unsigned long long* __restrict__ counts, int
 
 static unsigned grid_of(int64_t n) { return (unsigned)((n + 255) / 256); }
 
+// ---------------------------------------------------------------------------
+// EmpiricalQuantilePredictor training (predictor.py:78-98): per group the
+// np.quantile(values, q) of the remaining-token values y = remaining[p, s, m]
+// of every training (program, stage, model), at four levels:
+//   L0 (workflow, stage, model), L1 (stage, model), L2 (model), L3 global.
+// Each level: one sort of (group id, value key) pairs (the merge levels
+// above), then per group id its [start, end) by binary search and numpy's
+// 'linear' quantile (method 7) with numpy's exact arithmetic:
+//   v = (n - 1) * q; v >= n - 1 -> last; else i = floor(v), g = v - i,
+//   d = x[i+1] - x[i]; g >= 0.5 ? x[i+1] - d * (1 - g) : x[i] + d * g   (_lerp)
+// The table [n_wf + 1, s_cap + 1, K] resolves the fallback chain
+// (predictor.py:100-108) exactly like the host build.
+__device__ __forceinline__ double okey_inv(uint64_t k) {
+  const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// level ids: L0 (wf * (s_cap+1) + st) * K + m, L1 st * K + m, L2 m, L3 0
+__global__ void train_entries_kernel(chm_trace t, const int32_t* __restrict__ workflow,
+                                     int s_cap, int level, uint64_t* __restrict__ id,
+                                     uint64_t* __restrict__ val,
+                                     unsigned long long* __restrict__ cursor) {
+  const int S = t.max_stages, K = t.n_models;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)t.n_programs * S * K) return;
+  const long long p = idx / ((long long)S * K);
+  const int r = (int)(idx - p * S * K), s = r / K, m = r - s * K;
+  if (s >= t.n_stages[p]) return;
+  const int st = s + 1, wf = workflow[p];
+  uint64_t g;
+  switch (level) {
+    case 0: g = ((uint64_t)wf * (s_cap + 1) + st) * K + m; break;
+    case 1: g = (uint64_t)st * K + m; break;
+    case 2: g = (uint64_t)m; break;
+    default: g = 0; break;
+  }
+  const unsigned long long at = atomicAdd(cursor, 1ull);
+  id[at] = g;
+  val[at] = okey((double)t.remaining[idx]);
+}
+
+__device__ __forceinline__ int64_t lower_id(const uint64_t* id, int64_t n, uint64_t g) {
+  int64_t l = 0, h = n;
+  while (l < h) {
+    const int64_t m = (l + h) >> 1;
+    if (id[m] < g) l = m + 1; else h = m;
+  }
+  return l;
+}
+
+// One thread per group id of the level: quantile of its sorted values.
+__global__ void group_quantile_kernel(const uint64_t* __restrict__ id,
+                                      const uint64_t* __restrict__ val, int64_t n, int n_groups,
+                                      double q, double* __restrict__ out,
+                                      uint8_t* __restrict__ present) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const int64_t a = lower_id(id, n, (uint64_t)g), b = lower_id(id, n, (uint64_t)g + 1);
+  const int64_t cnt = b - a;
+  present[g] = cnt > 0;
+  if (cnt <= 0) return;
+  const double v = __dmul_rn((double)(cnt - 1), q);  // (n - 1) * quantiles
+  double r;
+  if (v >= (double)(cnt - 1)) {
+    r = okey_inv(val[b - 1]);
+  } else if (v < 0.0) {
+    r = okey_inv(val[a]);
+  } else {
+    const double fl = floor(v);
+    const int64_t i = (int64_t)fl;
+    const double gam = __dsub_rn(v, fl);
+    const double x0 = okey_inv(val[a + i]), x1 = okey_inv(val[a + i + 1]);
+    const double d = __dsub_rn(x1, x0);
+    r = gam >= 0.5 ? __dsub_rn(x1, __dmul_rn(d, __dsub_rn(1.0, gam)))
+                   : __dadd_rn(x0, __dmul_rn(d, gam));
+  }
+  out[g] = r;
+}
+
+// table[a, st, m] with the fallback chain; a == n_wf: unknown workflow,
+// st == 0: stage outside 1..s_cap (no L0 / L1 entry can match).
+__global__ void table_kernel(const double* __restrict__ q0, const uint8_t* __restrict__ h0,
+                             const double* __restrict__ q1, const uint8_t* __restrict__ h1,
+                             const double* __restrict__ q2, const uint8_t* __restrict__ h2,
+                             const double* __restrict__ q3, int n_wf, int s_cap, int K,
+                             double* __restrict__ table) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (n_wf + 1) * (s_cap + 1) * K) return;
+  const int m = e % K, st = (e / K) % (s_cap + 1), a = e / (K * (s_cap + 1));
+  double v = q3[0];
+  if (h2[m]) v = q2[m];
+  if (st >= 1 && h1[st * K + m]) v = q1[st * K + m];
+  if (a < n_wf && st >= 1 && h0[(a * (s_cap + 1) + st) * K + m]) v = q0[(a * (s_cap + 1) + st) * K + m];
+  table[e] = v;
+}
+
 }  // namespace eval
 }  // namespace chm
+
+extern "C" uint64_t chm_quantile_train_scratch_bytes(int64_t n_entries, int32_t n_wf,
+                                                     int32_t s_cap, int32_t n_models) {
+  if (n_entries < 0 || n_wf < 0 || s_cap < 1 || n_models < 1) return 0;
+  const uint64_t groups = (uint64_t)(n_wf * (s_cap + 1) + (s_cap + 1) + 2) * n_models + 1;
+  return (uint64_t)n_entries * 4 * 8 + groups * 9 + 256;
+}
+
+extern "C" chm_status chm_quantile_train(const chm_trace* t, const int32_t* workflow,
+                                         int32_t n_wf, int32_t s_cap, double quantile,
+                                         int64_t n_entries, void* scratch,
+                                         uint64_t scratch_bytes, double* table, void* stream) {
+  using namespace chm::eval;
+  if (!t || !workflow || !t->remaining || !t->n_stages || !scratch || !table || n_wf < 1 ||
+      s_cap < 1 || n_entries < 1 || !(quantile > 0.0 && quantile < 1.0))
+    return CHM_ERR_INVALID_ARG;
+  if (scratch_bytes < chm_quantile_train_scratch_bytes(n_entries, n_wf, s_cap, t->n_models))
+    return CHM_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int K = t->n_models;
+  const int64_t n = n_entries;
+  char* sp = reinterpret_cast<char*>(scratch);
+  unsigned long long* cursor = reinterpret_cast<unsigned long long*>(sp);
+  uint64_t* id0 = reinterpret_cast<uint64_t*>(sp + 256);
+  uint64_t *v0 = id0 + n, *id1 = id0 + 2 * n, *v1 = id0 + 3 * n;
+  const int ng[4] = {n_wf * (s_cap + 1) * K, (s_cap + 1) * K, K, 1};
+  double* qv = reinterpret_cast<double*>(id0 + 4 * n);
+  double* qs[4] = {qv, qv + ng[0], qv + ng[0] + ng[1], qv + ng[0] + ng[1] + ng[2]};
+  uint8_t* hv = reinterpret_cast<uint8_t*>(qv + ng[0] + ng[1] + ng[2] + ng[3]);
+  uint8_t* hs[4] = {hv, hv + ng[0], hv + ng[0] + ng[1], hv + ng[0] + ng[1] + ng[2]};
+  const long long cells = (long long)t->n_programs * t->max_stages * K;
+  chm::prof::begin(chm::prof::K_EVAL, st);
+  for (int level = 0; level < 4; ++level) {
+    if (cudaMemsetAsync(cursor, 0, 8, st) != cudaSuccess) return CHM_ERR_CUDA;
+    train_entries_kernel<<<grid_of(cells), 256, 0, st>>>(*t, workflow, s_cap, level, id0, v0,
+                                                           cursor);
+    uint64_t *a1 = id0, *a2 = v0, *b1 = id1, *b2 = v1;
+    for (int64_t w = 1; w < n; w *= 2) {
+      merge_level<true, false><<<grid_of(n), 256, 0, st>>>(a1, a2, b1, b2, n, w, nullptr);
+      std::swap(a1, b1);
+      std::swap(a2, b2);
+    }
+    group_quantile_kernel<<<(unsigned)((ng[level] + 255) / 256), 256, 0, st>>>(
+        a1, a2, n, ng[level], quantile, qs[level], hs[level]);
+  }
+  const int cells_t = (n_wf + 1) * (s_cap + 1) * K;
+  table_kernel<<<(unsigned)((cells_t + 255) / 256), 256, 0, st>>>(
+      qs[0], hs[0], qs[1], hs[1], qs[2], hs[2], qs[3], n_wf, s_cap, K, table);
+  chm::prof::end(chm::prof::K_EVAL, st, (double)n * 4 * 16.0);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
 
 extern "C" uint64_t chm_kendall_tau_scratch_bytes(int64_t n) {
   if (n < 0) return 0;

@@ -67,8 +67,46 @@ class GpuQuantilePredictor:
         self.table = torch.as_tensor(table.ravel(), device=device)
         self.n_wf = len(wfs)
 
+    @classmethod
+    def from_trace(cls, store, quantile: float = 0.5, extra_workflows=()):
+        """Train on the device from a TraceStore (chm_quantile_train): the same
+        table as the host build from the same trace, bit for bit."""
+        if not 0.0 < quantile < 1.0:
+            raise ValidationError(f"quantile must be in (0,1), got {quantile}")
+        cols = store.cols
+        n_entries = int(cols.n_stages.sum()) * store.K
+        if n_entries == 0:
+            raise EmptyTrainingSet("no training values at any fallback level")
+        self = cls.__new__(cls)
+        self.quantile = quantile
+        self.model_ids = list(store.model_ids)
+        wfs = sorted(set(cols.workflow_ids) | set(extra_workflows))
+        self.workflow_index = {w: i for i, w in enumerate(wfs)}
+        self.n_wf = len(wfs)
+        self.s_cap = int(cols.n_stages.max())
+        d = store.device
+        wf = torch.as_tensor(np.array([self.workflow_index[w] for w in cols.workflow_ids],
+                                      np.int32), device=d)
+        lib = _lib.load()
+        nbytes = int(lib.chm_quantile_train_scratch_bytes(n_entries, self.n_wf, self.s_cap,
+                                                          store.K))
+        scratch = torch.empty(nbytes, dtype=torch.uint8, device=d)
+        self.table = torch.empty((self.n_wf + 1) * (self.s_cap + 1) * store.K,
+                                 dtype=torch.float64, device=d)
+        _lib.check(lib.chm_quantile_train(store.t, _p(wf), self.n_wf, self.s_cap, quantile,
+                                          n_entries, _p(scratch), nbytes, _p(self.table),
+                                          torch.cuda.current_stream(d).cuda_stream),
+                   "chm_quantile_train")
+        self.table_host = self.table.cpu().numpy().reshape(self.n_wf + 1, self.s_cap + 1, store.K)
+        self._by_key = None  # lookups read the resolved table
+        return self
+
     def lookup(self, workflow_id, stage_index, model_id) -> float:
         """The reference fallback chain (predictor.py:100-108)."""
+        if self._by_key is None:  # device-trained: the table holds the resolved chain
+            a = self.workflow_index.get(workflow_id, self.n_wf)
+            st = stage_index if 1 <= stage_index <= self.s_cap else 0
+            return float(self.table_host[a, st, self.model_ids.index(model_id)])
         v = self._by_key.get((workflow_id, stage_index, model_id))
         if v is None:
             v = self._by_sm.get((stage_index, model_id))

@@ -84,3 +84,27 @@ def test_evaluate_predictor_on_trace(gold):
     got = [arrival_order_distance(store, m) for m in ids]
     np.testing.assert_array_equal(got, gold["eval_arrival"])
     _ = columns_from_records  # (records path covered in test_gpu_trace)
+
+
+@pytest.mark.parametrize("q", [0.5, 0.9, 0.37])
+def test_quantile_training_on_device(q):
+    """chm_quantile_train from a trace store == the host np.quantile build and
+    the reference's EmpiricalQuantilePredictor (tests/golden/quantile.npz grid)."""
+    from paper_2603_22206_b200.predictor import GpuQuantilePredictor
+    from paper_2603_22206_b200.trace import TraceStore
+    from paper_2603_22206_b200.workload import MATH_WORKFLOWS, LengthStats, synthesize_trace
+    from tests.test_oracle import MATH_STATS, MATH_SUCCESS  # the golden generator's inputs
+
+    stats = {m: LengthStats(*v) for m, v in MATH_STATS.items()}
+    tr = synthesize_trace(MATH_WORKFLOWS, stats, MATH_SUCCESS, 2000, 1)
+    ids = ["m0", "m1", "m2"]
+    host = GpuQuantilePredictor(tr, ids, q)
+    dev = GpuQuantilePredictor.from_trace(TraceStore.from_records(tr, ids, "cuda"), q)
+    assert dev.workflow_index == host.workflow_index and dev.s_cap == host.s_cap
+    assert dev.table_host.tobytes() == host.table_host.tobytes()
+    z = np.load(os.path.join(GOLD, "quantile.npz"))
+    grid = z[f"q{q}"]
+    for a, wf in enumerate(z["wfs"]):
+        for st in range(1, 8):
+            for m in range(3):
+                assert dev.lookup(str(wf), st, f"m{m}") == grid[a, st - 1, m]
