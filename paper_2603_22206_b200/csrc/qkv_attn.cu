@@ -467,10 +467,19 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
 // ctx = attention(x' . w_qkv^T + b_qkv) for n_seq sequences of 128 tokens,
 // x' = x, or with stats_in the deferred LayerNorm of x folded in (w_qkv
 // pre-scaled by gamma, b_qkv including W.beta, c_qkv = row sums of w_qkv).
+chm_status qkv_attention_pair(const void* x, const void* w_qkv, const float* b_qkv,
+                              const float* c_qkv, const float2* stats_in, int n_part, float eps,
+                              void* ctx, int n_seq, int hidden, cudaStream_t st);
+
 chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
                          void* ctx, int n_seq, int hidden, cudaStream_t st) {
   if (stats_in && (!c_qkv || n_part < 1 || n_part > kLnMaxParts)) return CHM_ERR_INVALID_ARG;
+  // CHM_QA_PAIR=1: the cta_group::2 kernel (qkv_attn_pair.cu)
+  static const int pair = env_int("CHM_QA_PAIR", 0);
+  if (pair)
+    return qkv_attention_pair(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden,
+                              st);
   static const int cluster = env_int("CHM_QA_CLUSTER", 21);
   static const int lag = env_int("CHM_QA_LAG", 0);
   static const int dbg = env_int("CHM_QA_DEBUG", 0);
