@@ -55,10 +55,9 @@ def parse_args():
     p.add_argument("--attention", default="fused", choices=["fused", "unfused"],
                    help="S=128 router layers: fused QKV+attention kernel or QKV GEMM + "
                         "attention kernel (A/B measurement)")
-    p.add_argument("--layernorm", default="auto", choices=["auto", "deferred", "cluster"],
-                   help="post-LN sublayers: deferred LayerNorm folded into the next GEMM or "
-                        "normalised in a cluster-row GEMM epilogue; auto = deferred for "
-                        "H >= 768, cluster below (A/B measurement)")
+    p.add_argument("--layernorm", default="cluster", choices=["deferred", "cluster"],
+                   help="post-LN sublayers: normalised in a cluster-row GEMM epilogue "
+                        "(default) or deferred and folded into the next GEMM (A/B)")
     p.add_argument("--graph", action="store_true",
                    help="replay the tick as a CUDA graph (1 GPU; per-kernel timing from an "
                         "eager profiled pass)")

@@ -208,10 +208,11 @@ typedef struct chm_encoder_cfg {
 #define CHM_ENC_UNFUSED_ATTENTION 1
 /* chm_encoder_cfg.flags: normalise every post-LN sublayer inside its own GEMM
  * epilogue (rows owned by clusters of 2H/256 CTAs exchanging statistics over
- * DSMEM) instead of the deferred LayerNorm, also for H >= 768. Same math. */
+ * DSMEM). This is the default; the flag is kept for explicitness. */
 #define CHM_ENC_CLUSTER_LN 2
-/* chm_encoder_cfg.flags: force the deferred LayerNorm (default only for
- * H >= 768; H <= 512 uses the cluster path, whose clusters tile every SM). */
+/* chm_encoder_cfg.flags: deferred LayerNorm (out-projection / FFN2 write the
+ * pre-LN sum + row statistics on pair tiles; QKV and FFN1 fold the LayerNorm
+ * into their epilogues). Same math; measured slower in the power-capped tick. */
 #define CHM_ENC_DEFERRED_LN 4
 
 /* bf16 weights, row-major [out_features, in_features] (nn.Linear layout). */

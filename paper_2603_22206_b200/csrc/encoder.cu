@@ -996,13 +996,14 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   const FoldedLayout FL = folded_layout(cfg);
   chm_status rc;
   const bool fused = S == kAttnS && !(cfg.flags & CHM_ENC_UNFUSED_ATTENTION);
-  // Cluster-LayerNorm path (each post-LN sublayer normalised in its own GEMM
-  // epilogue, rows owned by 2H/256-CTA clusters): for H <= 512 the clusters
-  // (2 or 4 CTAs) still tile all 148 SMs and the row statistics never leave
-  // the cluster, so it is the default there; for H >= 768 the 6-CTA clusters
-  // leave SMs idle and the deferred LayerNorm wins (profiles/r1c_gemm_cycles.md).
-  const bool cluster_ln = ((cfg.flags & CHM_ENC_CLUSTER_LN) != 0 || H <= 512) &&
-                          (cfg.flags & CHM_ENC_DEFERRED_LN) == 0;
+  // LayerNorm path. Cluster LN (default): each post-LN sublayer is normalised
+  // in its own GEMM epilogue (rows owned by 2H/256-CTA clusters, DSMEM
+  // statistics), so the fused QKV+attention kernel reads a normalised stream
+  // and runs its lean instantiation. Deferred LN (CHM_ENC_DEFERRED_LN): pair
+  // tiles on all SMs for out-proj / FFN2 (faster GEMMs), but the fold costs
+  // the fused kernel more than the GEMMs gain in the power-capped tick
+  // (same-box A/B, profiles/r1c_gemm_cycles.md).
+  const bool cluster_ln = (cfg.flags & CHM_ENC_DEFERRED_LN) == 0;
   for (int l = 0; l < L; ++l) {
     const uint8_t* fb = reinterpret_cast<const uint8_t*>(ws.folded) + (size_t)l * FL.per_layer;
     const void* wq = cluster_ln ? w.w_qkv[l] : fb + FL.wqkv;

@@ -166,7 +166,7 @@ __device__ __forceinline__ void load_chunk_ln(const uint32_t (&r0)[32], const ui
   }
 }
 
-template <int EPI, int kStages>
+template <int EPI, int kStages, bool FOLD>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                 const __grid_constant__ CUtensorMap tmap_b,
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
           const uint32_t full_leader =
               sm100::mapa(sm100::smem_u32(&s.full[stage]), leader_rank);
-          if (ep.dbg == 2) {
+          if (!kLN && ep.dbg == 2) {
             if (leader) sm100::mbar_arrive(&s.full[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1; }
             continue;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n_tile0 = (kLN ? (int)pair : (t % n_tiles_n)) * BN + half * 128;
       const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN +
                                  half * 128;
-      if (ep.dbg != 0) {
+      if (!kLN && ep.dbg != 0) {  // (not in the LN variant: keeps it spill-free)
         sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
         sm100::tc_fence_after();
         sm100::tc_fence_before();
@@ -428,14 +428,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         // ---- pointwise epilogues ----
         constexpr bool kRes = EPI == EPI_BIAS_RESIDUAL || EPI == EPI_RESLN_STATS;
-        constexpr bool kFold = EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_QKV;
+        // FOLD instantiations carry the folded-LayerNorm arithmetic; the plain
+        // ones compile without it
+        constexpr bool kFold = FOLD && (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_QKV);
         const int row = mrow0 + lane;
         // Deferred LayerNorm of this thread's row (statistics from the producer
         // GEMM's partials; loaded before the accumulator wait so the L2
         // latency overlaps the MMAs). fold: v = rs_a acc + (rs_b c_n + b_n);
         // EPI_RESLN_STATS: LN(r) = (rs_a r + rs_b) gamma_n + beta_n.
         float rs_a = 1.f, rs_b = 0.f;
-        const bool have_stats = ep.stats_in != nullptr;
+        const bool have_stats = (kFold || EPI == EPI_RESLN_STATS) && ep.stats_in != nullptr;
         if (have_stats && row < M) row_affine(ep.stats_in + (size_t)row * ep.n_part, ep.n_part,
                                               ep.eps, rs_a, rs_b);
         float sh = 0.f, s1 = 0.f, s2 = 0.f;  // EPI_RESLN_STATS: shifted sums of the output row
@@ -618,7 +620,7 @@ static int num_sms() {
   return n;
 }
 
-template <int EPI, int kStages>
+template <int EPI, int kStages, bool FOLD = false>
 static chm_status launch(const void* A, const void* B, void* C, const float* bias,
                          const void* residual, int M, int N, int K, EpiParams ep,
                          cudaStream_t s) {
@@ -636,7 +638,7 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
       smem_bytes<kStages, (kStages > 4 ? 1 : 2), EPI == EPI_RESIDUAL_LN>();
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<EPI, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_kernel<EPI, kStages, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kSmemBytes);
     attr_set = true;
   }
@@ -661,7 +663,7 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   if (!max_active[cluster - 1]) {
     cfg.gridDim = dim3(cluster * (num_sms() / cluster), 1, 1);
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI, kStages>, &cfg) != cudaSuccess || n < 1)
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<EPI, kStages, FOLD>, &cfg) != cudaSuccess || n < 1)
       n = num_sms() / cluster;
     max_active[cluster - 1] = n;
   }
@@ -669,7 +671,7 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   const int n_clusters = tiles < max_clusters ? tiles : max_clusters;
   cfg.gridDim = dim3(cluster * n_clusters, 1, 1);
   prof::begin(prof::K_GEMM, s);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, kStages>, ta, tb, tc, tr, bias, M, N, K, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, kStages, FOLD>, ta, tb, tc, tr, bias, M, N, K, ep);
   prof::end(prof::K_GEMM, s, 2.0 * M * N * K);
   if (e != cudaSuccess) return CHM_ERR_CUDA;
   CHM_LAUNCH_CHECK();
@@ -718,12 +720,16 @@ chm_status gemm_run(const void* A, const void* B, void* C, int M, int N, int K,
   static const int stages = getenv("CHM_GEMM_STAGES") ? atoi(getenv("CHM_GEMM_STAGES")) : 4;
   static const int dbg = getenv("CHM_GEMM_DEBUG") ? atoi(getenv("CHM_GEMM_DEBUG")) : 0;
   ep.dbg = dbg;
-#define CHM_GEMM_CASE(E)                                                              \
-  case E:                                                                              \
-    return stages == 6 ? gemm::launch<E, 6>(A, B, C, bias, residual, M, N, K, ep, s)   \
+#define CHM_GEMM_CASE(E)                                                                    \
+  case E:                                                                                    \
+    if (g.stats_in)                                                                          \
+      return gemm::launch<E, 4, true>(A, B, C, bias, residual, M, N, K, ep, s);              \
+    return stages == 6 ? gemm::launch<E, 6>(A, B, C, bias, residual, M, N, K, ep, s)         \
                        : gemm::launch<E, 4>(A, B, C, bias, residual, M, N, K, ep, s);
   switch (epilogue) {
-    CHM_GEMM_CASE(gemm::EPI_NONE)
+    case gemm::EPI_NONE:
+      return stages == 6 ? gemm::launch<gemm::EPI_NONE, 6>(A, B, C, bias, residual, M, N, K, ep, s)
+                         : gemm::launch<gemm::EPI_NONE, 4>(A, B, C, bias, residual, M, N, K, ep, s);
     CHM_GEMM_CASE(gemm::EPI_BIAS)
     CHM_GEMM_CASE(gemm::EPI_BIAS_GELU)
     CHM_GEMM_CASE(gemm::EPI_QKV)

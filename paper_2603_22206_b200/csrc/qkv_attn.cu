@@ -83,14 +83,16 @@ __device__ __forceinline__ void epi_sync() {
 // the cluster (rank = i*CH + j) owns sequence sg*CS + i, head hg*CH + j.
 // lag > 0: the MMA issuer keeps at most `lag` projection k-blocks queued on
 // the tensor pipe, so S(i) / O(i) slotted between them start soon.
-template <int CS, int CH>
+// FOLD: the deferred-LayerNorm instantiation (row affine + column sums); the
+// plain one compiles without it.
+template <int CS, int CH, bool FOLD>
 __global__ void __launch_bounds__(kThreads, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tm_x,
                          const __grid_constant__ CUtensorMap tm_w,
                          const float* __restrict__ b_qkv, const float* __restrict__ c_qkv,
                          const float2* __restrict__ stats_in, int n_part, float eps, int n_seq,
                          int n_heads, int hidden, __nv_bfloat16* __restrict__ ctx, int lag,
-                         int dbg) {
+                         int dbg, int contiguous) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
@@ -105,15 +107,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int head_groups = n_heads / CH;
   const int n_citems = ((n_seq + CS - 1) / CS) * head_groups;
   const int cl = (int)sm100::cluster_id_x(), n_cl = (int)sm100::n_clusters_x();
-  // Each cluster owns a contiguous range of cluster items (head-group minor),
-  // so consecutive items of a CTA share a sequence: the deferred-LayerNorm
-  // row affine is computed once per sequence, and the x tile is re-read from
-  // L2 while hot.
-  const int per = (n_citems + n_cl - 1) / n_cl;
-  const int c_lo = cl * per;
-  const int n_my = c_lo < n_citems ? min(per, n_citems - c_lo) : 0;
+  // Item order: interleaved (cluster cl takes items cl, cl + n_cl, ...: the
+  // clusters sweep the items together) or contiguous (a range per cluster, so
+  // consecutive items of a CTA share a sequence and its cached LayerNorm row
+  // affine). `contiguous` is chosen on the host.
+  const int per = contiguous ? (n_citems + n_cl - 1) / n_cl : 0;
+  const int c_lo = contiguous ? cl * per : cl;
+  const int n_my = contiguous ? (c_lo < n_citems ? min(per, n_citems - c_lo) : 0)
+                              : (cl < n_citems ? (n_citems - 1 - cl) / n_cl + 1 : 0);
+  const int c_step = contiguous ? 1 : n_cl;
   auto item_of = [&](int it, int& seq, int& h) {
-    const int c = c_lo + it;
+    const int c = c_lo + it * c_step;
     const int sg = c / head_groups, hg = c - sg * head_groups;
     seq = sg * CS + ci;
     h = hg * CH + cj;
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int a = it & 1;
       // deferred LayerNorm of the input row (folded: x' = rs_a x + rs_b per
       // row, gamma inside the weights, W.beta inside the bias)
-      if (stats_in != nullptr && seq != aff_seq && seq < n_seq) {
+      if (FOLD && seq != aff_seq && seq < n_seq) {
         row_affine(stats_in + ((size_t)seq * kS + r) * n_part, n_part, eps, rs_a, rs_b);
         aff_seq = seq;
       }
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float4 b0 = __ldg(reinterpret_cast<const float4*>(bp + q4 * 8));
           const float4 b1 = __ldg(reinterpret_cast<const float4*>(bp + q4 * 8 + 4));
           float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-          if (stats_in != nullptr) {
+          if (FOLD) {
             const float4 c0 = __ldg(reinterpret_cast<const float4*>(cp + q4 * 8));
             const float4 c1 = __ldg(reinterpret_cast<const float4*>(cp + q4 * 8 + 4));
             const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -414,10 +418,13 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <int CS, int CH>
+template <int CS, int CH, bool FOLD>
 static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
                          void* ctx, int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
+  // CHM_QA_ORDER: 0 interleaved, 1 contiguous (measurement override)
+  static const int order_env = env_int("CHM_QA_ORDER", -1);
+  const int order = order_env >= 0 ? order_env : 0;
   const int n_heads = hidden / 64;
   if (n_heads % CH != 0) return CHM_ERR_UNSUPPORTED;
   constexpr int kCluster = CS * CH;
@@ -428,7 +435,7 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   if (!gemm::make_tmap_bf16(&tm_w, w_qkv, (uint64_t)3 * hidden, (uint64_t)hidden, qa::kWBox, 64,
                             0))
     return CHM_ERR_CUDA;
-  auto kern = qa::qkv_attention_kernel<CS, CH>;
+  auto kern = qa::qkv_attention_kernel<CS, CH, FOLD>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(qa::kThreads, 1, 1);
   cfg.dynamicSmemBytes = qa::kSmemBytes;
@@ -455,7 +462,7 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   prof::begin(prof::K_QKV_ATTENTION, st);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, c_qkv, stats_in, n_part, eps,
                                      n_seq, n_heads, hidden,
-                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg);
+                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg, order);
   // tensor work: the projection (2 T 3H H) + S and O (4 S^2 64 per item)
   prof::end(prof::K_QKV_ATTENTION, st,
             2.0 * T * 3.0 * hidden * hidden + 4.0 * qa::kS * qa::kS * 64.0 * n_seq * n_heads);
@@ -484,11 +491,11 @@ chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
   static const int lag = env_int("CHM_QA_LAG", 0);
   static const int dbg = env_int("CHM_QA_DEBUG", 0);
   switch (cluster) {
-    case 11: return launch<1, 1>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
-    case 12: return launch<1, 2>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
-    case 21: return launch<2, 1>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
-    case 24: return launch<2, 4>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
-    default: return launch<2, 2>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 11: return stats_in ? launch<1, 1, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<1, 1, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 12: return stats_in ? launch<1, 2, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<1, 2, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 21: return stats_in ? launch<2, 1, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 1, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 24: return stats_in ? launch<2, 4, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 4, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    default: return stats_in ? launch<2, 2, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 2, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
   }
 }
 
