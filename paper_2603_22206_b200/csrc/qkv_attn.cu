@@ -488,7 +488,9 @@ chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
     return qkv_attention_pair(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden,
                               st);
   static const int cluster = env_int("CHM_QA_CLUSTER", 21);
-  static const int lag = env_int("CHM_QA_LAG", 0);
+  // (the kdone ring has kStages slots: larger lags would alias its phases)
+  static const int lag = env_int("CHM_QA_LAG", 0) < qa::kStages ? env_int("CHM_QA_LAG", 0)
+                                                                  : qa::kStages - 1;
   static const int dbg = env_int("CHM_QA_DEBUG", 0);
   switch (cluster) {
     case 11: return stats_in ? launch<1, 1, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<1, 1, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
