@@ -89,7 +89,10 @@ class ClockSampler:
     def __init__(self, index: int, enabled: bool):
         self.proc = None
         self.path = None
+        self.index = index
         self.t0 = self.t1 = None
+        self.e0 = self.e1 = None
+        self.steps = 0
         if not enabled:
             return
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -104,11 +107,23 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def _energy_mj(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            return pynvml.nvmlDeviceGetTotalEnergyConsumption(
+                pynvml.nvmlDeviceGetHandleByIndex(self.index))
+        except Exception:  # noqa: BLE001
+            return None
+
     def mark_start(self):
+        self.e0 = self._energy_mj() if self.proc is not None else None
         self.t0 = time.time()
 
-    def mark_end(self):
+    def mark_end(self, steps: int = 0):
         self.t1 = time.time()
+        self.e1 = self._energy_mj() if self.proc is not None else None
+        self.steps = steps
         if self.proc is not None and self.t1 - self.t0 < 0.25:
             time.sleep(0.25)  # let the sample after the window land
 
@@ -128,7 +143,8 @@ class ClockSampler:
                 continue
             try:
                 ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                rows.append((ts, float(parts[1]), float(parts[2]), int(parts[4], 16)))
+                rows.append((ts, float(parts[1]), float(parts[2]), int(parts[4], 16),
+                             float(parts[3])))
             except ValueError:
                 continue
         if not rows:
@@ -145,9 +161,13 @@ class ClockSampler:
             for b, name in REASON_BITS.items():
                 if r[3] & b and name != "gpu_idle":
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(r[1] for r in sel),
-                "sm_max_mhz": max(r[2] for r in sel), "samples": len(sel), "window": window,
-                "reasons": sorted(reasons)}
+        out = {"sm_mhz": statistics.median(r[1] for r in sel),
+               "sm_max_mhz": max(r[2] for r in sel), "samples": len(sel), "window": window,
+               "reasons": sorted(reasons), "power_w": statistics.median(r[4] for r in sel)}
+        if self.e0 is not None and self.e1 is not None and self.steps:
+            # NVML cumulative energy counter across the timed region
+            out["energy_j_per_step"] = (self.e1 - self.e0) * 1e-3 / self.steps
+        return out
 
 
 # ---------------------------------------------------------------- CPU reference path
@@ -396,7 +416,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.mark_end()
+    clocks.mark_end(args.steps)
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     clk = clocks.stop()

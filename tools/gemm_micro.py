@@ -55,6 +55,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=4096 * 128)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--seconds", type=float, default=0.0,
+                    help="> 0: repeat each case for about this long (energy per launch from NVML)")
     ap.add_argument("--only", default="")
     a = ap.parse_args()
     lib = _lib.load()
@@ -117,6 +119,13 @@ def main():
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
+        reps = a.reps
+        if a.seconds > 0:
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            reps = max(a.reps, int(a.seconds / max(time.perf_counter() - t0, 1e-6)))
+        a_reps, a.reps = a.reps, reps
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clk.start()
         mj0 = clk.energy_mj()
@@ -126,8 +135,9 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         mhz = clk.stop()
-        joules = (clk.energy_mj() - mj0) * 1e-3 / a.reps
+        joules = (clk.energy_mj() - mj0) * 1e-3 / reps
         ms = e0.elapsed_time(e1) / a.reps
+        a.reps = a_reps
         # per-clock efficiency: FLOPs / (cycles x 148 SMs x 8192 dense bf16 FLOP/clk/SM)
         eff = fl / (ms * 1e-3 * mhz * 1e6 * 148 * 8192) if mhz else float("nan")
         print(f"{name:10s} {ms:8.3f} ms  {fl / ms / 1e9:8.1f} TFLOP/s  sm {mhz:6.0f} MHz  "
