@@ -83,7 +83,11 @@ def _ref_q(router, ids):
 
 
 @pytest.mark.parametrize("cfg,head_std", [(SMALL, 0.02), (SMALL, 2 / math.sqrt(256)),
-                                          (EncoderConfig(n_layers=2), 2 / math.sqrt(768))])
+                                          (EncoderConfig(n_layers=2), 2 / math.sqrt(768)),
+                                          (EncoderConfig(n_layers=2, hidden=512, n_heads=8,
+                                                         ffn=2048), 2 / math.sqrt(512)),
+                                          (EncoderConfig(n_layers=2, hidden=1024, n_heads=16,
+                                                         ffn=4096), 2 / math.sqrt(1024))])
 def test_encoder_matches_fp32(cfg, head_std):
     K, B = 5, 24
     r = GpuEncoderRouter(cfg, K, max_rows=B, seed=3, head_std=head_std)
