@@ -85,7 +85,11 @@ __device__ __forceinline__ void epi_sync() {
 // the tensor pipe, so S(i) / O(i) slotted between them start soon.
 // FOLD: the deferred-LayerNorm instantiation (row affine + column sums); the
 // plain one compiles without it.
-template <int CS, int CH, bool FOLD>
+// TS: Q and P stay in tensor memory as bf16 (FlashAttention-4 style): the
+// S = Q K^T and O = P V MMAs read their A operand from TMEM (tcgen05.mma
+// [d], [a_tmem], b_desc), saving the Q and P shared-memory round trips
+// (96 KB per item) of a kernel bound by shared-memory traffic.
+template <int CS, int CH, bool FOLD, bool TS>
 __global__ void __launch_bounds__(kThreads, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tm_x,
                          const __grid_constant__ CUtensorMap tm_w,
@@ -212,21 +216,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_wait(&s.acc_empty[it & 1], ((it >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
       };
-      auto issue_s = [&]() {
+      auto issue_s = [&](int it) {
         sm100::tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
-                          sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+        for (int k = 0; k < 4; ++k) {
+          if constexpr (TS)  // Q bf16 in the drained accumulator's first 32 columns
+            sm100::mma_bf16_ts(tmem + kSCol, tmem + (uint32_t)(it & 1) * kAccCols + k * 8,
+                               sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+          else
+            sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
+                            sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+        }
         sm100::mma_commit(&s.s_full);
       };
       auto issue_o = [&]() {
         sm100::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t pa = ((kk >> 2) ? k_addr : q_addr) + (kk & 3) * 32;
-          sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(pa),
-                          sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+          if constexpr (TS) {  // P bf16 over S's first 64 columns, O in its last 64
+            sm100::mma_bf16_ts(tmem + kSCol + 64, tmem + kSCol + kk * 8,
+                               sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+          } else {
+            const uint32_t pa = ((kk >> 2) ? k_addr : q_addr) + (kk & 3) * 32;
+            sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(pa),
+                            sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+          }
         }
         sm100::mma_commit(&s.o_full);
       };
@@ -243,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             gemm_kb(it + 1, kb);
             if (!s_done) {
               if (sm100::mbar_test(&s.qkv_ready, par)) {
-                issue_s();
+                issue_s(it);
                 s_done = true;
               }
             } else if (!o_done && sm100::mbar_test(&s.p_ready, par)) {
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!s_done) {
           sm100::mbar_wait(&s.qkv_ready, par);
-          issue_s();
+          issue_s(it);
         }
         if (!o_done) {
           sm100::mbar_wait(&s.p_ready, par);
@@ -292,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::mbar_arrive(&s.acc_empty[a]);
         continue;
       }
+      uint32_t qp[32];  // TS: this row's Q in bf16 pairs (hf == 0 threads)
 #pragma unroll 1
       for (int cc = 0; cc < 3; ++cc) {
         const int c = hf * 3 + cc;
@@ -324,8 +339,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           u.z = pack_bf16(v[4], v[5]);
           u.w = pack_bf16(v[6], v[7]);
           const int piece = c32 * 4 + q4;
-          *reinterpret_cast<uint4*>(rowp + ((piece ^ (r & 7)) << 4)) = u;
+          if (TS && t == 0) {
+            // (unrolled: cc is 0 or 1 here, so the indices are compile-time per branch)
+            if (c32 == 0) {
+              qp[q4 * 4 + 0] = u.x; qp[q4 * 4 + 1] = u.y; qp[q4 * 4 + 2] = u.z; qp[q4 * 4 + 3] = u.w;
+            } else {
+              qp[16 + q4 * 4 + 0] = u.x; qp[16 + q4 * 4 + 1] = u.y;
+              qp[16 + q4 * 4 + 2] = u.z; qp[16 + q4 * 4 + 3] = u.w;
+            }
+          } else {
+            *reinterpret_cast<uint4*>(rowp + ((piece ^ (r & 7)) << 4)) = u;
+          }
         }
+      }
+      if (TS && hf == 0) {
+        // Q (bf16, 64 per row = 32 columns) over the consumed Q accumulator
+        sm100::tmem_st_32x32b_x32(lane_base + (uint32_t)a * kAccCols, qp);
+        sm100::tmem_st_wait();
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive(&s.acc_empty[a]);
@@ -349,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float mxl = mx * kLog2e;
       float sum = 0.f;
       uint8_t* prow = s.qkv[hf] + r * 128;  // P keys [64 hf, +64) over the Q (hf 0) / K tile
+      uint32_t pp[32];  // TS: P in bf16 pairs, to TMEM over S (all S reads are done: epi_sync)
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         __align__(16) __nv_bfloat162 pv[4];
@@ -361,7 +392,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float2 back = __bfloat1622float2(pv[e]);
           sum += back.x + back.y;
         }
-        *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) = *reinterpret_cast<uint4*>(pv);
+        if (TS) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pp[q * 4 + e] = *reinterpret_cast<uint32_t*>(&pv[e]);
+        } else {
+          *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) << 4)) = *reinterpret_cast<uint4*>(pv);
+        }
+      }
+      if (TS) {
+        sm100::tmem_st_32x32b_x32(lane_base + kSCol + hf * 32, pp);
+        sm100::tmem_st_wait();
       }
       s.red_sum[hf][r] = sum;
       sm100::fence_proxy_async_smem();
@@ -371,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_wait(&s.o_full, par);
       sm100::tc_fence_after();
       uint32_t ov[32];
-      sm100::tmem_ld_32x32b_x32(lane_base + kSCol + hf * 32, ov);
+      sm100::tmem_ld_32x32b_x32(lane_base + kSCol + (TS ? 64 : 0) + hf * 32, ov);
       sm100::tmem_ld_wait();
       epi_sync();
       const float inv = 1.0f / (sum + s.red_sum[hf ^ 1][r]);
@@ -418,7 +458,7 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <int CS, int CH, bool FOLD>
+template <int CS, int CH, bool FOLD, bool TS = false>
 static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
                          void* ctx, int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
@@ -435,7 +475,7 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   if (!gemm::make_tmap_bf16(&tm_w, w_qkv, (uint64_t)3 * hidden, (uint64_t)hidden, qa::kWBox, 64,
                             0))
     return CHM_ERR_CUDA;
-  auto kern = qa::qkv_attention_kernel<CS, CH, FOLD>;
+  auto kern = qa::qkv_attention_kernel<CS, CH, FOLD, TS>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(qa::kThreads, 1, 1);
   cfg.dynamicSmemBytes = qa::kSmemBytes;
@@ -492,10 +532,16 @@ chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
   static const int lag = env_int("CHM_QA_LAG", 0) < qa::kStages ? env_int("CHM_QA_LAG", 0)
                                                                   : qa::kStages - 1;
   static const int dbg = env_int("CHM_QA_DEBUG", 0);
+  // CHM_QA_TS: Q / P operands from tensor memory (cluster config 21 only)
+  static const int ts = env_int("CHM_QA_TS", 0);
   switch (cluster) {
     case 11: return stats_in ? launch<1, 1, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<1, 1, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
     case 12: return stats_in ? launch<1, 2, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<1, 2, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
-    case 21: return stats_in ? launch<2, 1, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 1, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+    case 21:
+      if (ts)
+        return stats_in ? launch<2, 1, true, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st)
+                        : launch<2, 1, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
+      return stats_in ? launch<2, 1, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 1, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
     case 24: return stats_in ? launch<2, 4, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 4, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
     default: return stats_in ? launch<2, 2, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st) : launch<2, 2, false>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden, lag, dbg, st);
   }
