@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(160, 4)
   extern __shared__ uint8_t smem_raw[];
   AttnSmem& s = *reinterpret_cast<AttnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int item = blockIdx.x;
   const int seq = item / n_heads, h = item - seq * n_heads;
   if (warp == 4 && lane == 0) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(160, 4)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const uint32_t tmem = s.tmem_base;
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
 
   if (warp == 4) {
     if (lane == 0) {
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(160, 1)
   extern __shared__ uint8_t smem_raw[];
   AttnLongSmem& s = *reinterpret_cast<AttnLongSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int n_qb = S / kAttnS, n_kb = S / kAttnS;
   const int item = blockIdx.x;
   const int qb = item % n_qb;
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(160, 1)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const uint32_t tmem = s.tmem_base;
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
   constexpr uint32_t kTile = kAttnS * 64 * 2;
 
   if (warp == 4) {
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   FlashSmem& s = *reinterpret_cast<FlashSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int n_kb = S / kAttnS;
   const int n_qp = S / (2 * kAttnS);
   constexpr uint32_t kTile = kAttnS * 64 * 2;
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  const uint32_t tmem = s.tmem_base;
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
   const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (warp == 0) {
@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (warp-uniform loop, *_w helpers elect the lane) ----------------
+    {
       constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
       constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
       const int J = n_my * n_kb;
@@ -565,10 +565,10 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
         const uint32_t qa = sm100::smem_u32(s.q[qb][g]), ka = sm100::smem_u32(s.kv[stage][0]);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16(tmem + 128 * g, sm100::umma_desc_sw128(qa + k * 32),
-                          sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
-        sm100::mma_commit(&s.s_full[g]);
-        if (g == 1 && kb == n_kb - 1) sm100::mma_commit(&s.q_empty[qb]);
+          sm100::mma_bf16_w(tmem + 128 * g, sm100::umma_desc_sw128(qa + k * 32),
+                            sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+        sm100::mma_commit_w(&s.s_full[g]);
+        if (g == 1 && kb == n_kb - 1) sm100::mma_commit_w(&s.q_empty[qb]);
       };
       auto issue_o = [&](int g, int j) {
         const int stage = j & 1;
@@ -578,11 +578,11 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t pa = sm100::smem_u32(s.p[g][kk >> 2]) + (kk & 3) * 32;
-          sm100::mma_bf16(tmem + 256 + 64 * g, sm100::umma_desc_sw128(pa),
-                          sm100::umma_desc_sw128(va + kk * 2048), idesc_o, kk);
+          sm100::mma_bf16_w(tmem + 256 + 64 * g, sm100::umma_desc_sw128(pa),
+                            sm100::umma_desc_sw128(va + kk * 2048), idesc_o, kk);
         }
-        sm100::mma_commit(&s.o_full[g]);
-        if (g == 1) sm100::mma_commit(&s.kv_empty[stage]);
+        sm100::mma_commit_w(&s.o_full[g]);
+        if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
       };
       if (J > 0) {
         issue_s(0, 0);

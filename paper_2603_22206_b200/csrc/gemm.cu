@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
   const uint32_t px = rank & 1;          // position in the pair (M half)
   const uint32_t pair = rank >> 1;       // pair index in the cluster (LN: N tile)
@@ -217,11 +217,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_before();
   sm100::cluster_sync();
   sm100::tc_fence_after();
-  const uint32_t tmem_base = s.tmem_base;
+  const uint32_t tmem_base = sm100::uniform(s.tmem_base);
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
-    if (lane == 0) {
+    // warp-uniform loop, one elected lane issues (see sm100::elect_one)
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster; t < n_tiles; t += n_cl) {
@@ -232,14 +233,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t full_leader =
               sm100::mapa(sm100::smem_u32(&s.full[stage]), leader_rank);
           if (!kLN && ep.dbg == 2) {
-            if (leader) sm100::mbar_arrive(&s.full[stage]);
+            if (leader && lane == 0) sm100::mbar_arrive(&s.full[stage]);
+            __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (leader) sm100::mbar_arrive_expect_tx(&s.full[stage], 2 * kStageBytes);
-          uint8_t* base = s.tiles[stage];
-          sm100::tma_load_2d_cg2(base, &tmap_a, full_leader, kb * BK, m0);
-          sm100::tma_load_2d_cg2(base + kTileABytes, &tmap_b, full_leader, kb * BK, n0);
+          if (sm100::elect_one()) {
+            if (leader) sm100::mbar_arrive_expect_tx(&s.full[stage], 2 * kStageBytes);
+            uint8_t* base = s.tiles[stage];
+            sm100::tma_load_2d_cg2(base, &tmap_a, full_leader, kb * BK, m0);
+            sm100::tma_load_2d_cg2(base + kTileABytes, &tmap_b, full_leader, kb * BK, n0);
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -259,19 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&s.full[stage], phase);
           sm100::tc_fence_after();
-          if (lane == 0) {
+          {
             const uint32_t a_addr = sm100::smem_u32(s.tiles[stage]);
             const uint32_t b_addr = a_addr + kTileABytes;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = sm100::umma_desc_sw128(a_addr + k * 32);
               const uint64_t bd = sm100::umma_desc_sw128(b_addr + k * 32);
-              sm100::mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              sm100::mma_bf16_cg2_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
             }
-            sm100::mma_commit_cg2_mc(&s.empty[stage], pair_mask);
-            if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc(&s.tmem_full[acc], pair_mask);
+            sm100::mma_commit_cg2_mc_w(&s.empty[stage], pair_mask);
+            if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc_w(&s.tmem_full[acc], pair_mask);
           }
-          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -605,6 +609,22 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// W_qkv [3 * H, H] viewed as [3 parts][H rows][H cols]: one box = `box_rows`
+// rows of each of the 3 parts (Q, K, V of a head), 64 columns, 128B swizzle;
+// the box lands in shared memory as 3 * box_rows contiguous 128-byte rows.
+bool make_tmap_qkv3(CUtensorMap* map, const void* ptr, uint64_t hidden, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {hidden, hidden, 3};
+  cuuint64_t strides[2] = {hidden * 2, hidden * hidden * 2};
+  cuuint32_t box[3] = {64, box_rows, 3};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;

@@ -44,6 +44,7 @@ namespace chm {
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, uint64_t ld);
+bool make_tmap_qkv3(CUtensorMap* map, const void* ptr, uint64_t hidden, uint32_t box_rows);
 }
 namespace qa {
 
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int k_blocks = hidden / 64;
   const uint32_t rank = sm100::cluster_ctarank();
   const int ci = (int)rank / CH, cj = (int)rank % CH;
@@ -149,40 +150,64 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_before();
   sm100::cluster_sync();
   sm100::tc_fence_after();
-  const uint32_t tmem = s.tmem_base;
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
 
   if (warp == 0) {
     // ---------------- TMA producer: this CTA's slices, multicast ----------------
-    if (lane == 0) {
+    // (warp-uniform loop like the MMA issuer; one elected lane issues the copies)
+    {
       constexpr int kARows = kS / CH;        // x rows this CTA loads
       constexpr int kBoxes = 6 / CS;         // 32-row W boxes this CTA loads
       int stage = 0;
       uint32_t phase = 0;
-      for (int it = 0; it < n_my; ++it) {
+      for (int it = 0; it < (dbg >= 7 ? 0 : n_my); ++it) {
         int seq, h;
         item_of(it, seq, h);
         const int a_row = seq * kS + cj * kARows;
         for (int kb = 0; kb < k_blocks; ++kb) {
           // every sharer of this stage has consumed its previous contents
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
+          if (dbg >= 4) {  // measurement: no operand loads (MMAs on stale smem)
+            if (lane == 0) sm100::mbar_arrive(&s.full[stage]);
+            __syncwarp();
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          if (sm100::elect_one()) {
           sm100::mbar_arrive_expect_tx(&s.full[stage], kStageBytes);
           uint8_t* st = s.stages[stage];
           sm100::tma_load_2d_mc(st + cj * kARows * 128, &tm_x, &s.full[stage], kb * 64, a_row,
                                 row_mask);
+          if constexpr (TS || CS != 2) {
 #pragma unroll
-          for (int bb = 0; bb < kBoxes; ++bb) {
-            const int b = ci * kBoxes + bb;  // box of the head's 6: part b/2, half b%2
-            sm100::tma_load_2d_mc(st + kATile + b * kWBox * 128, &tm_w, &s.full[stage], kb * 64,
-                                  (b >> 1) * hidden + h * 64 + (b & 1) * kWBox, col_mask);
+            for (int bb = 0; bb < kBoxes; ++bb) {
+              const int b = ci * kBoxes + bb;  // box of the head's 6: part b/2, half b%2
+              sm100::tma_load_2d_mc(st + kATile + b * kWBox * 128, &tm_w, &s.full[stage], kb * 64,
+                                    (b >> 1) * hidden + h * 64 + (b & 1) * kWBox, col_mask);
+            }
+          } else {
+            // one op: rows [64/CS * ci, +64/CS) of the head's Q, K and V parts
+            // (tm_w is the 3-part view); B rows -- and accumulator columns --
+            // are ordered (half, part, row)
+            constexpr int kRowsPer = 64 / CS;
+            sm100::tma_load_3d_mc(st + kATile + ci * 3 * kRowsPer * 128, &tm_w, &s.full[stage],
+                                  kb * 64, h * 64 + ci * kRowsPer, 0, col_mask);
           }
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      constexpr uint32_t idesc_g = sm100::umma_idesc_bf16(128, 192);
+    // The whole warp runs the loop (waits, descriptors and counters stay
+    // warp-uniform); the *_w helpers elect the issuing lane inside their asm.
+    {
+      // (dbg 5 / 6: N = 256 / 128 projection MMAs on stale shared memory -- an MMA-shape probe)
+      const uint32_t idesc_g = dbg == 5   ? sm100::umma_idesc_bf16(128, 256)
+                               : dbg == 6 ? sm100::umma_idesc_bf16(128, 128)
+                                          : sm100::umma_idesc_bf16(128, 192);
       constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
       constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
       const uint16_t share_mask = row_mask | col_mask;
@@ -197,23 +222,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int d = g - lag;
           sm100::mbar_wait(&s.kdone[d % kStages], (d / kStages) & 1);
         }
-        sm100::mbar_wait(&s.full[stage], phase);
+        // (dbg >= 7: no producer at all -- the issue loop alone, as
+        // tools/mma_probe.cu; 8: + accumulators 256 apart, 9: + local commit
+        // instead of the multicast one, 10: + no accumulator handshake)
+        if (dbg < 7) sm100::mbar_wait(&s.full[stage], phase);
         sm100::tc_fence_after();
         const uint32_t a = sm100::smem_u32(s.stages[stage]);
         const uint32_t b = a + kATile;
-        const uint32_t d = tmem + (uint32_t)(it & 1) * kAccCols;
+        // (dbg == 3: projection only, accumulators 256 columns apart -- an
+        // alignment probe; S is unused then)
+        const uint32_t d = tmem + (uint32_t)(it & 1) * (dbg == 3 || dbg == 8 ? 256u : kAccCols);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16(d, sm100::umma_desc_sw128(a + k * 32), sm100::umma_desc_sw128(b + k * 32),
-                          idesc_g, (kb | k) != 0);
-        sm100::mma_commit_mc(&s.empty[stage], share_mask);
-        if (lag > 0) sm100::mma_commit(&s.kdone[stage]);
+          sm100::mma_bf16_w(d, sm100::umma_desc_sw128(a + k * 32), sm100::umma_desc_sw128(b + k * 32),
+                            idesc_g, (kb | k) != 0);
+        if (dbg >= 9)
+          sm100::mma_commit_w(&s.empty[stage]);
+        else
+          sm100::mma_commit_mc_w(&s.empty[stage], share_mask);
+        if (lag > 0) sm100::mma_commit_w(&s.kdone[stage]);
+        if (kb == k_blocks - 1 && dbg != 10) sm100::mma_commit_w(&s.acc_full[it & 1]);
         ++g;
-        if (kb == k_blocks - 1) sm100::mma_commit(&s.acc_full[it & 1]);
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       };
       auto acc_wait = [&](int it) {
-        sm100::mbar_wait(&s.acc_empty[it & 1], ((it >> 1) & 1) ^ 1);
+        if (dbg != 10) sm100::mbar_wait(&s.acc_empty[it & 1], ((it >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
       };
       auto issue_s = [&](int it) {
@@ -221,28 +254,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if constexpr (TS)  // Q bf16 in the drained accumulator's first 32 columns
-            sm100::mma_bf16_ts(tmem + kSCol, tmem + (uint32_t)(it & 1) * kAccCols + k * 8,
-                               sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+            sm100::mma_bf16_ts_w(tmem + kSCol, tmem + (uint32_t)(it & 1) * kAccCols + k * 8,
+                                 sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
           else
-            sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
-                            sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+            sm100::mma_bf16_w(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
+                              sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
         }
-        sm100::mma_commit(&s.s_full);
+        sm100::mma_commit_w(&s.s_full);
       };
       auto issue_o = [&]() {
         sm100::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if constexpr (TS) {  // P bf16 over S's first 64 columns, O in its last 64
-            sm100::mma_bf16_ts(tmem + kSCol + 64, tmem + kSCol + kk * 8,
-                               sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+            sm100::mma_bf16_ts_w(tmem + kSCol + 64, tmem + kSCol + kk * 8,
+                                 sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
           } else {
             const uint32_t pa = ((kk >> 2) ? k_addr : q_addr) + (kk & 3) * 32;
-            sm100::mma_bf16(tmem + kSCol, sm100::umma_desc_sw128(pa),
-                            sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+            sm100::mma_bf16_w(tmem + kSCol, sm100::umma_desc_sw128(pa),
+                              sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
           }
         }
-        sm100::mma_commit(&s.o_full);
+        sm100::mma_commit_w(&s.o_full);
       };
       if (n_my > 0) {
         acc_wait(0);
@@ -250,17 +283,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int it = 0; it < n_my; ++it) {
         const uint32_t par = it & 1;
-        bool s_done = dbg != 0, o_done = dbg != 0;
+        bool s_done = dbg != 0, o_done = dbg != 0;  // dbg 1 / 3: projection only
         if (it + 1 < n_my) {
           acc_wait(it + 1);
           for (int kb = 0; kb < k_blocks; ++kb) {
             gemm_kb(it + 1, kb);
             if (!s_done) {
-              if (sm100::mbar_test(&s.qkv_ready, par)) {
+              if (__shfl_sync(0xffffffffu, sm100::mbar_test(&s.qkv_ready, par), 0)) {
                 issue_s(it);
                 s_done = true;
               }
-            } else if (!o_done && sm100::mbar_test(&s.p_ready, par)) {
+            } else if (!o_done && __shfl_sync(0xffffffffu, sm100::mbar_test(&s.p_ready, par), 0)) {
               issue_o();
               o_done = true;
             }
@@ -286,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr float kLog2e = 1.4426950408889634f;
     int aff_seq = -1;           // sequence the cached row affine belongs to
     float rs_a = 1.f, rs_b = 0.f;
-    for (int it = 0; it < n_my; ++it) {
+    for (int it = 0; it < (dbg == 10 ? 0 : n_my); ++it) {
       int seq, h;
       item_of(it, seq, h);
       const uint32_t par = it & 1;
@@ -301,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // part t = c/2 (Q, K, V), columns (c&1)*32.. of that part.
       sm100::mbar_wait(&s.acc_full[a], (it >> 1) & 1);
       sm100::tc_fence_after();
-      if (dbg == 1) {
+      if (dbg == 1 || dbg >= 3) {
         sm100::tc_fence_before();
         sm100::mbar_arrive(&s.acc_empty[a]);
         continue;
@@ -310,7 +343,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int cc = 0; cc < 3; ++cc) {
         const int c = hf * 3 + cc;
-        const int t = c >> 1, c32 = c & 1;
+        // accumulator chunk c (32 columns) -> (part t, 32-column half c32):
+        // TS loads 6 boxes (Q0 Q1 K0 K1 V0 V1), otherwise one 3-part box per
+        // CTA (Q0 K0 V0 Q1 K1 V1 for 2 sequences per cluster)
+        constexpr bool kOneBox = !TS && CS == 2;
+        const int t = kOneBox ? c % 3 : (c >> 1);
+        const int c32 = kOneBox ? c / 3 : (c & 1);
         uint32_t raw[32];
         sm100::tmem_ld_32x32b_x32(lane_base + (uint32_t)a * kAccCols + c * 32, raw);
         sm100::tmem_ld_wait();
@@ -472,9 +510,13 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   CUtensorMap tm_x, tm_w;
   if (!gemm::make_tmap_bf16(&tm_x, x, (uint64_t)T, (uint64_t)hidden, qa::kS / CH, 64, 0))
     return CHM_ERR_CUDA;
-  if (!gemm::make_tmap_bf16(&tm_w, w_qkv, (uint64_t)3 * hidden, (uint64_t)hidden, qa::kWBox, 64,
-                            0))
+  if (TS || CS != 2) {
+    if (!gemm::make_tmap_bf16(&tm_w, w_qkv, (uint64_t)3 * hidden, (uint64_t)hidden, qa::kWBox, 64,
+                              0))
+      return CHM_ERR_CUDA;
+  } else if (!gemm::make_tmap_qkv3(&tm_w, w_qkv, (uint64_t)hidden, 64 / CS)) {
     return CHM_ERR_CUDA;
+  }
   auto kern = qa::qkv_attention_kernel<CS, CH, FOLD, TS>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(qa::kThreads, 1, 1);

@@ -100,11 +100,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                               const float* __restrict__ b_qkv, const float* __restrict__ c_qkv,
                               const float2* __restrict__ stats_in, int n_part, float eps,
                               int n_seq, int n_heads, int hidden,
-                              __nv_bfloat16* __restrict__ ctx, int lag) {
+                              __nv_bfloat16* __restrict__ ctx, int lag, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int k_blocks = hidden / 64;
   const uint32_t px = sm100::cluster_ctarank() & 1;
   const bool leader = px == 0;
@@ -151,11 +151,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_before();
   sm100::cluster_sync();
   sm100::tc_fence_after();
-  const uint32_t tmem = s.tmem_base;
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
 
   if (warp == 0) {
-    // ---------------- TMA producer (both CTAs) ----------------
-    if (lane == 0) {
+    // ---------------- TMA producer (both CTAs; warp-uniform loop) ----------------
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0; it < n_my; ++it) {
@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < k_blocks; ++kb) {
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
           const uint32_t full_leader = sm100::mapa(sm100::smem_u32(&s.full[stage]), 0);
+          if (sm100::elect_one()) {
           if (leader) sm100::mbar_arrive_expect_tx(&s.full[stage], 2 * kStageBytes);
           uint8_t* st = s.stages[stage];
           sm100::tma_load_2d_cg2(st, &tm_x, full_leader, kb * 64, seq * kS);
@@ -173,13 +174,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tma_load_2d_cg2(st + kXTile + bb * 32 * 128, &tm_w, full_leader, kb * 64,
                                    (b >> 1) * hidden + h * 64 + (b & 1) * 32);
           }
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (leader) ----------------
-    if (leader && lane == 0) {
+    // ---------------- MMA issuer (leader; warp-uniform loop, elected lane issues) ----------------
+    if (leader) {
       constexpr uint32_t idesc_g = sm100::umma_idesc_bf16(256, kAccCols);
       constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(256, 256);
       constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(256, 128) | (1u << 16);  // V' MN-major
@@ -201,11 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b = a + kXTile;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16_cg2(tmem, sm100::umma_desc_sw128(a + k * 32),
-                              sm100::umma_desc_sw128(b + k * 32), idesc_g, (kb | k) != 0);
-        sm100::mma_commit_cg2_mc(&s.empty[stage], 0x3);
-        sm100::mma_commit_cg2_mc(&s.kdone[stage], 0x1);
-        if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc(&s.acc_full, 0x3);
+          sm100::mma_bf16_cg2_w(tmem, sm100::umma_desc_sw128(a + k * 32),
+                                sm100::umma_desc_sw128(b + k * 32), idesc_g, (kb | k) != 0);
+        sm100::mma_commit_cg2_mc_w(&s.empty[stage], 0x3);
+        sm100::mma_commit_cg2_mc_w(&s.kdone[stage], 0x1);
+        if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc_w(&s.acc_full, 0x3);
         ++g;
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       };
@@ -213,18 +216,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          sm100::mma_bf16_cg2(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
-                              sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
-        sm100::mma_commit_cg2_mc(&s.s_full, 0x3);
+          sm100::mma_bf16_cg2_w(tmem + kSCol, sm100::umma_desc_sw128(q_addr + k * 32),
+                                sm100::umma_desc_sw128(k_addr + k * 32), idesc_s, k);
+        sm100::mma_commit_cg2_mc_w(&s.s_full, 0x3);
       };
       auto issue_o = [&]() {
         sm100::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
-          sm100::mma_bf16_cg2(tmem + kSCol,
-                              sm100::umma_desc_sw128(p_addr + (kk >> 2) * kTile + (kk & 3) * 32),
-                              sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
-        sm100::mma_commit_cg2_mc(&s.o_full, 0x3);
+          sm100::mma_bf16_cg2_w(tmem + kSCol,
+                                sm100::umma_desc_sw128(p_addr + (kk >> 2) * kTile + (kk & 3) * 32),
+                                sm100::umma_desc_sw128(v_addr + kk * 2048), idesc_o, kk);
+        sm100::mma_commit_cg2_mc_w(&s.o_full, 0x3);
       };
       if (n_my > 0)
         for (int kb = 0; kb < k_blocks; ++kb) gemm_kb(kb, false);
@@ -232,16 +235,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t par = it & 1;
         // both CTAs drained item it: accumulator free, Q / K / V' staged
         mbar_wait_acq(&s.drained, par);
+        if (dbg) {  // measurement: projections only
+          if (it + 1 < n_my)
+            for (int kb = 0; kb < k_blocks; ++kb) gemm_kb(kb, false);
+          continue;
+        }
         issue_s();
         bool o_done = false;
         if (it + 1 < n_my) {
           for (int kb = 0; kb < k_blocks; ++kb) {
-            if (!o_done && mbar_test_acq(&s.p_ready, par)) {
+            if (!o_done && __shfl_sync(0xffffffffu, mbar_test_acq(&s.p_ready, par), 0)) {
               issue_o();
               o_done = true;
             }
             gemm_kb(kb, !o_done);
-            if (!o_done && mbar_test_acq(&s.p_ready, par)) {
+            if (!o_done && __shfl_sync(0xffffffffu, mbar_test_acq(&s.p_ready, par), 0)) {
               issue_o();
               o_done = true;
             }
@@ -276,6 +284,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (1) accumulator + bias (+ folded LayerNorm) -> bf16 Q (x 1/8), K, V'
       sm100::mbar_wait(&s.acc_full, par);
       sm100::tc_fence_after();
+      if (dbg) {
+        sm100::tc_fence_before();
+        sm100::mbar_arrive_cluster(drained_l);
+        continue;
+      }
 #pragma unroll 1
       for (int cc = 0; cc < 3; ++cc) {
         const int c = hf * 3 + cc;
@@ -431,10 +444,11 @@ chm_status qkv_attention_pair(const void* x, const void* w_qkv, const float* b_q
   const int n_cl = items < max_clusters ? items : max_clusters;
   cfg.gridDim = dim3(2 * n_cl, 1, 1);
   prof::begin(prof::K_QKV_ATTENTION, st);
-  static const int lag = getenv("CHM_QAP_LAG") ? atoi(getenv("CHM_QAP_LAG")) : 2;
+  static const int lag = getenv("CHM_QAP_LAG") ? atoi(getenv("CHM_QAP_LAG")) : 0;
+  static const int dbg = getenv("CHM_QA_DEBUG") ? atoi(getenv("CHM_QA_DEBUG")) : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, c_qkv, stats_in, n_part, eps,
                                      n_seq, n_heads, hidden,
-                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag);
+                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg);
   prof::end(prof::K_QKV_ATTENTION, st,
             2.0 * T * 3.0 * hidden * hidden + 4.0 * qap::kS * qap::kS * 64.0 * n_seq * n_heads);
   if (e != cudaSuccess) return CHM_ERR_CUDA;

@@ -72,6 +72,36 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// One lane of the (fully converged) warp: issue tcgen05 instructions under
+// `if (elect_one())` from a warp-uniform loop. A loop run by a single
+// divergent lane (`if (lane == 0)`) keeps its descriptors in per-thread
+// registers and pays an R2UR move per operand: ~90-260 cycles per MMA issue,
+// which paces N <= 256 MMAs (tools/mma_probe.cu, profiles/r1c_gemm_cycles.md).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// Warp index the compiler can prove warp-uniform (a shuffle from lane 0, as
+// CUTLASS's canonical_warp_idx_sync). With plain threadIdx.x / 32 the role
+// branches (`if (warp == 1)`) are not known to be uniform, loop state stays in
+// per-thread registers and every tcgen05 issue pays an R2UR + reconvergence
+// round trip: ~190 cycles per `if (elect_one())` region, half the tensor rate
+// of an N = 192 MMA (tools/mma_probe.cu `layout`, profiles/r1c_gemm_cycles.md).
+__device__ __forceinline__ int warp_id() {
+  return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+}
+
+// A value every lane holds (e.g. the TMEM base read back from shared memory),
+// made provably warp-uniform so tcgen05 operands derived from it live in
+// uniform registers.
+__device__ __forceinline__ uint32_t uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 // ---- tcgen05 ---------------------------------------------------------------
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -243,6 +273,17 @@ __device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
+// 3D TMA load multicast to the CTAs of `mask` (same offsets in each).
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map,
+                                               uint64_t* bar, int c0, int c1, int c2,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
 // Single-CTA MMA completion arriving on the barrier at the same offset in
 // every CTA of `mask`.
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
@@ -322,6 +363,65 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
          | ((uint32_t)(N >> 3) << 17)     // N >> 3
          | ((uint32_t)(M >> 4) << 24);    // M >> 4
 }
+
+// ---- warp-collective issue ---------------------------------------------------
+// Called by all 32 lanes of a converged warp; one lane (elect.sync inside the
+// same asm block) issues. No C++ branch around the tcgen05 instruction, so the
+// compiler emits it as a uniform-predicated instruction in converged code
+// (VOTEU + @UP UTCHMMA) instead of a BSSY/BSYNC region with R2UR moves, which
+// costs ~190 cycles per region (tools/mma_probe.cu `layout`).
+#define CHM_ELECT_PREFIX "elect.sync _|e, 0xffffffff;\n\t"
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" CHM_ELECT_PREFIX
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" CHM_ELECT_PREFIX
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t" CHM_ELECT_PREFIX
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t" CHM_ELECT_PREFIX
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_cg2_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" CHM_ELECT_PREFIX
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_cg2_mc_w(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t" CHM_ELECT_PREFIX
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+#undef CHM_ELECT_PREFIX
 
 }  // namespace sm100
 }  // namespace chm
