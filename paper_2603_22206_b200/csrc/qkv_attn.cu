@@ -16,11 +16,13 @@
 // barrier of every CTA that writes into its stages (tcgen05.commit multicast).
 //
 //   warp 0      TMA producer: 4-stage ring of x[128 x 64] + W[192 x 64]
-//   warp 1      MMA issuer (one thread). GEMM(i+1) is issued while item i's
-//               attention runs: between k-blocks of GEMM(i+1) it polls
+//   warp 1      MMA issuer (whole warp, warp-uniform; one elected lane issues
+//               inside the asm). GEMM(i+1), GEMM(i+2) are issued while item
+//               i's attention runs: between projection k-blocks it polls
 //               (mbarrier test_wait) for "Q/K/V of item i staged" and
 //               "P of item i written" and slots S(i) = Q K^T and O(i) = P V
-//               into the tensor pipe as soon as they are ready
+//               into the tensor pipe as soon as they are ready; it blocks only
+//               on the accumulator (drain of item i - 2)
 //   warps 2-9   epilogue, 2 threads per token row (column halves hf = 0/1):
 //               (1) acc(i) + bias -> bf16 Q (x 1/8), K, V tiles in smem
 //                   (128B swizzle, the UMMA operand layout), accumulator freed
@@ -74,6 +76,13 @@ constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// dbg 11: per-item timeline of CTA 0, items [8, 16): 16 clock64 stamps per
+// item into ctx (as int64; all ctx output is skipped in this mode).
+__device__ __forceinline__ void stamp(int dbg, void* ctx, int it, int k) {
+  if (dbg >= 11 && blockIdx.x == 0 && it >= 8 && it < 16)
+    reinterpret_cast<long long*>(ctx)[(it - 8) * 16 + k] = clock64();
 }
 
 __device__ __forceinline__ void epi_sync() {
@@ -160,14 +169,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int kBoxes = 6 / CS;         // 32-row W boxes this CTA loads
       int stage = 0;
       uint32_t phase = 0;
-      for (int it = 0; it < (dbg >= 7 ? 0 : n_my); ++it) {
+      for (int it = 0; it < (dbg >= 7 && dbg <= 10 ? 0 : n_my); ++it) {
         int seq, h;
         item_of(it, seq, h);
         const int a_row = seq * kS + cj * kARows;
         for (int kb = 0; kb < k_blocks; ++kb) {
           // every sharer of this stage has consumed its previous contents
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
-          if (dbg >= 4) {  // measurement: no operand loads (MMAs on stale smem)
+          if (dbg >= 4 && dbg <= 10) {  // measurement: no operand loads (MMAs on stale smem)
             if (lane == 0) sm100::mbar_arrive(&s.full[stage]);
             __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -195,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           }
           __syncwarp();
+          if (lane == 0 && (kb == 0 || kb == k_blocks - 1)) stamp(dbg, ctx, it, kb == 0 ? 11 : 12);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (dbg >= 7: no producer at all -- the issue loop alone, as
         // tools/mma_probe.cu; 8: + accumulators 256 apart, 9: + local commit
         // instead of the multicast one, 10: + no accumulator handshake)
-        if (dbg < 7) sm100::mbar_wait(&s.full[stage], phase);
+        if (dbg < 7 || dbg > 10) sm100::mbar_wait(&s.full[stage], phase);
         sm100::tc_fence_after();
         const uint32_t a = sm100::smem_u32(s.stages[stage]);
         const uint32_t b = a + kATile;
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 4; ++k)
           sm100::mma_bf16_w(d, sm100::umma_desc_sw128(a + k * 32), sm100::umma_desc_sw128(b + k * 32),
                             idesc_g, (kb | k) != 0);
-        if (dbg >= 9)
+        if (dbg == 9 || dbg == 10)
           sm100::mma_commit_w(&s.empty[stage]);
         else
           sm100::mma_commit_mc_w(&s.empty[stage], share_mask);
@@ -245,11 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++g;
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       };
-      auto acc_wait = [&](int it) {
-        if (dbg != 10) sm100::mbar_wait(&s.acc_empty[it & 1], ((it >> 1) & 1) ^ 1);
-        sm100::tc_fence_after();
-      };
       auto issue_s = [&](int it) {
+        if (lane == 0) stamp(dbg, ctx, it, 6);
         sm100::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -277,37 +284,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         sm100::mma_commit_w(&s.o_full);
       };
-      if (n_my > 0) {
-        acc_wait(0);
-        for (int kb = 0; kb < k_blocks; ++kb) gemm_kb(0, kb);
-      }
-      for (int it = 0; it < n_my; ++it) {
-        const uint32_t par = it & 1;
-        bool s_done = dbg != 0, o_done = dbg != 0;  // dbg 1 / 3: projection only
-        if (it + 1 < n_my) {
-          acc_wait(it + 1);
-          for (int kb = 0; kb < k_blocks; ++kb) {
-            gemm_kb(it + 1, kb);
-            if (!s_done) {
-              if (__shfl_sync(0xffffffffu, sm100::mbar_test(&s.qkv_ready, par), 0)) {
-                issue_s(it);
-                s_done = true;
-              }
-            } else if (!o_done && __shfl_sync(0xffffffffu, sm100::mbar_test(&s.p_ready, par), 0)) {
-              issue_o();
-              o_done = true;
-            }
-          }
-        }
-        if (!s_done) {
-          sm100::mbar_wait(&s.qkv_ready, par);
-          issue_s(it);
-        }
-        if (!o_done) {
-          sm100::mbar_wait(&s.p_ready, par);
+      // S(j) / O(j) "events": S(j) once Q/K/V(j) are staged (qkv_ready), O(j)
+      // once P(j) is (p_ready). The epilogue produces them strictly in order
+      // S(0) O(0) S(1) O(1) ..., so one counter `ev` (= 2 j + is_o) tracks the
+      // next; the issuer polls it between projection k-blocks and only blocks
+      // on the accumulator (drain of item it - 2), never on attention.
+      // (dbg 1-10, 12, 13: projection only)
+      int ev = (dbg >= 1 && dbg <= 10) || dbg == 12 || dbg == 13 ? 2 * n_my : 0;
+      auto try_event = [&]() {
+        if (ev >= 2 * n_my) return;
+        const int j = ev >> 1;
+        uint64_t* bar = (ev & 1) ? &s.p_ready : &s.qkv_ready;
+        if (!__shfl_sync(0xffffffffu, sm100::mbar_test(bar, j & 1), 0)) return;
+        if (ev & 1) {
+          if (lane == 0) stamp(dbg, ctx, j, 7);
           issue_o();
+        } else {
+          issue_s(j);
+        }
+        ++ev;
+      };
+      // accumulator it & 1 free: item it - 2 drained (and, TS, its S -- which
+      // reads Q from that accumulator -- issued)
+      auto acc_wait = [&](int it) {
+        if (dbg != 10)
+          while (!__shfl_sync(0xffffffffu,
+                              sm100::mbar_test(&s.acc_empty[it & 1], ((it >> 1) & 1) ^ 1), 0) ||
+                 (TS && it >= 2 && ev <= 2 * (it - 2)))
+            try_event();
+        sm100::tc_fence_after();
+      };
+      for (int it = 0; it < n_my; ++it) {
+        acc_wait(it);
+        if (lane == 0) stamp(dbg, ctx, it, 8);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          gemm_kb(it, kb);
+          if (lane == 0 && (kb == 0 || kb == k_blocks - 1)) stamp(dbg, ctx, it, kb == 0 ? 9 : 10);
+          try_event();
         }
       }
+      while (ev < 2 * n_my) try_event();
     }
     __syncwarp();
   } else {
@@ -334,7 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // part t = c/2 (Q, K, V), columns (c&1)*32.. of that part.
       sm100::mbar_wait(&s.acc_full[a], (it >> 1) & 1);
       sm100::tc_fence_after();
-      if (dbg == 1 || dbg >= 3) {
+      const bool tl = warp == 2 && lane == 0;
+      if (tl) stamp(dbg, ctx, it, 0);
+      if (dbg == 1 || (dbg >= 3 && dbg <= 10) || dbg == 12) {
         sm100::tc_fence_before();
         sm100::mbar_arrive(&s.acc_empty[a]);
         continue;
@@ -399,10 +417,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_arrive(&s.acc_empty[a]);
       sm100::fence_proxy_async_smem();
       sm100::mbar_arrive(&s.qkv_ready);
-      if (dbg == 2) continue;
+      if (tl) stamp(dbg, ctx, it, 1);
+      if (dbg == 2 || dbg == 13) continue;
       // (2) softmax over this thread's 64 keys [64 hf, 64 hf + 64)
       sm100::mbar_wait(&s.s_full, par);
       sm100::tc_fence_after();
+      if (tl) stamp(dbg, ctx, it, 2);
       uint32_t sv[2][32];
       sm100::tmem_ld_32x32b_x32(lane_base + kSCol + hf * 64, sv[0]);
       sm100::tmem_ld_32x32b_x32(lane_base + kSCol + hf * 64 + 32, sv[1]);
@@ -445,15 +465,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&s.p_ready);
+      if (tl) stamp(dbg, ctx, it, 3);
       // (3) O / rowsum -> ctx, this thread's 32 of the head's 64 features
       sm100::mbar_wait(&s.o_full, par);
       sm100::tc_fence_after();
+      if (tl) stamp(dbg, ctx, it, 4);
       uint32_t ov[32];
       sm100::tmem_ld_32x32b_x32(lane_base + kSCol + (TS ? 64 : 0) + hf * 32, ov);
       sm100::tmem_ld_wait();
       epi_sync();
       const float inv = 1.0f / (sum + s.red_sum[hf ^ 1][r]);
-      if (seq < n_seq) {  // the last sequence group may be padded
+      if (seq < n_seq && dbg < 11) {  // the last sequence group may be padded
         __nv_bfloat16* dst = ctx + ((size_t)seq * kS + r) * hidden + h * 64 + hf * 32;
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -465,6 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<uint4*>(dst + q4 * 8) = u;
         }
       }
+      if (tl) stamp(dbg, ctx, it, 5);
     }
   }
   sm100::tc_fence_before();
@@ -490,7 +513,7 @@ static int n_sms() {
 }  // namespace qa
 
 // Diagnostic overrides (measurement only): CHM_QA_DEBUG=1 projection alone,
-// 2 + Q/K/V staging; CHM_QA_CLUSTER = "<CS><CH>"; CHM_QA_LAG = issue lag.
+// 2 + Q/K/V staging, 11 per-item timeline (see stamp()), 12 / 13 timeline of 1 / 2; CHM_QA_CLUSTER = "<CS><CH>"; CHM_QA_LAG = issue lag.
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;

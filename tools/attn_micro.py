@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--seq-len", type=int, default=128)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--only", default="")
+    ap.add_argument("--timeline", action="store_true",
+                    help="with CHM_QA_DEBUG=11: print CTA 0's per-item stage stamps (cycles)")
     a = ap.parse_args()
     lib = _lib.load()
     n, H, S = a.n_seq, a.hidden, a.seq_len
@@ -49,6 +51,17 @@ def main():
     flops_a = 4.0 * S * S * 64 * n * (H // 64)
     cases = {"fused": (fused, flops_g + flops_a), "gemm": (gemm, flops_g),
              "attention": (attn, flops_a)}
+    if a.timeline:
+        fused()
+        torch.cuda.synchronize()
+        t = ctx.view(-1).view(torch.int64)[:128].cpu().view(8, 16)[:, :13]
+        base = int(t[0, 0])
+        names = ["acc_full", "staged", "s_full", "p_ready", "o_full", "out_done", "S_issue", "O_issue",
+                 "acc_free", "kb0_mma", "kbN_mma", "kb0_tma", "kbN_tma"]
+        print("item " + " ".join(f"{n:>8s}" for n in names) + "   (cycles from item 8 acc_full)")
+        for i in range(8):
+            print(f"{8 + i:4d} " + " ".join(f"{int(v) - base:8d}" for v in t[i]))
+        return
     for name, (fn, fl) in cases.items():
         if a.only and a.only not in name:
             continue
