@@ -2,7 +2,7 @@
 # reference arm, the cfg3 launch list and a --set full capture of one layer's
 # router kernels (qkv_attention + out-proj / FFN1 / FFN2 GEMMs) inside the tick.
 export PYTHONUNBUFFERED=1
-o=gpurun_out/rm
+o=gpurun_out/${OUT:-rm}
 mkdir -p $o
 nvidia-smi -L > $o/smi.txt
 timeout 900 python -m pytest tests -m gpu -q > $o/pytest_gpu.txt 2>&1; tail -2 $o/pytest_gpu.txt
