@@ -170,6 +170,17 @@ typedef struct chm_queue_state {
                                 L2/HBM instead of shared memory)               */
 } chm_queue_state;
 
+/* One STJF candidate of an engine sub-queue, for the cross-GPU admission
+ * merge: the reference sort key (QueueEntry.sort_key, engine.py:55-69) plus
+ * the entry's handle. level == INT64_MAX marks "no candidate". */
+typedef struct chm_queue_key {
+  int64_t level;             /* starvation_level                               */
+  double priority;
+  double arrival;
+  int64_t seq;               /* global per-engine enqueue counter              */
+  int64_t handle;
+} chm_queue_key;
+
 /* Per-engine scratch bytes chm_queue_* need for a segment capacity: 0 up to
  * 10240 entries (keys in shared memory, one CTA per engine), 20/entry up to
  * 2^18 (keys in global memory, one CTA per engine), above that the
@@ -320,6 +331,33 @@ chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* aging,
                           const chm_monitor_state* mon, const chm_queue_state* q,
                           const chm_rows* rows, const chm_decisions* dec,
                           int32_t n_iterations, int32_t* error, void* stream);
+
+/* Sharded engine queues (global admission). With requests
+ * sharded over G GPUs, engine m's single reference queue (EngineSim._heap,
+ * engine.py:309-326) is split into G sub-queues whose union, ordered by the
+ * global sort key, is the reference queue (seq is the global enqueue counter,
+ * relayed between ranks). One scheduling iteration (engine.py:328-338) then
+ * is:
+ *   chm_queue_candidates    each rank writes its first F = max_batch_size
+ *                           entries per engine in STJF order ([K*F] keys);
+ *   (all-gather of the [G*K*F] keys over NCCL);
+ *   chm_queue_admit_merged  every rank frees release[m] slots (release NULL:
+ *                           none; release[m] < 0: engine m skips this
+ *                           iteration), takes the
+ *                           global top min(free slots, candidates) of the
+ *                           gathered keys, admits its own share of them from
+ *                           its head (in order), adds the GLOBAL admitted
+ *                           count to engine_running, ages the rest of its
+ *                           sub-queue by one iteration and rewrites its order.
+ * Requires capacity <= 2^18 (the huge path returns CHM_ERR_UNSUPPORTED). */
+chm_status chm_queue_candidates(const chm_pool* pool, const chm_monitor_state* mon,
+                                const chm_queue_state* q, int32_t F, chm_queue_key* out,
+                                void* stream);
+chm_status chm_queue_admit_merged(const chm_pool* pool, const chm_aging_cfg* aging,
+                                  const chm_monitor_state* mon, const chm_queue_state* q,
+                                  const chm_queue_key* gathered, int32_t G, int32_t F,
+                                  int32_t rank, const int32_t* release, int32_t* error,
+                                  void* stream);
 
 /* ActivityMonitor.note_progress (monitor.py:108-111) for n (model index,
  * request key, emitted tokens) updates, in call order (a later update of the

@@ -229,6 +229,11 @@ _SIGNATURES = [
     ("chm_queue_tick", c_int32,
      [POINTER(Pool), POINTER(AgingCfg), POINTER(MonitorState), POINTER(QueueState),
       POINTER(Rows), POINTER(Decisions), c_int32, c_void_p, c_void_p]),
+    ("chm_queue_candidates", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), POINTER(QueueState), c_int32, c_void_p, c_void_p]),
+    ("chm_queue_admit_merged", c_int32,
+     [POINTER(Pool), POINTER(AgingCfg), POINTER(MonitorState), POINTER(QueueState), c_void_p,
+      c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("chm_encoder_forward", c_int32,
      [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p,
       c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),

@@ -180,13 +180,84 @@ __device__ void radix_sort(QueueCtl& s, const Keys<Idx>& k, int n, const int* sr
   spare = out;
 }
 
+// Cross-GPU admission merge inputs (mode 2, chm_queue_admit_merged).
+struct MergeArgs {
+  const chm_queue_key* gathered;  // [G][K][F]
+  int G, F, rank;
+  const int32_t* release;         // [K] slots freed before the iteration (nullable)
+};
+
+__device__ __forceinline__ bool cand_less(const chm_queue_key& a, const chm_queue_key& b) {
+  if (a.level != b.level) return a.level < b.level;
+  if (a.priority != b.priority) return a.priority < b.priority;
+  if (a.arrival != b.arrival) return a.arrival < b.arrival;
+  return a.seq < b.seq;
+}
+
+// Engine m's admissions this iteration: a_global = min(free slots, gathered
+// candidates) of the global minimum keys; a_local = how many of them are this
+// rank's (its candidates are its STJF head, so it admits its first a_local).
+__device__ void merge_counts(const MergeArgs& ma, int m, int K, int free_slots, int* misc) {
+  const int n_c = ma.G * ma.F;
+  __shared__ int n_real, n_own;
+  if (threadIdx.x == 0) { n_real = 0; n_own = 0; }
+  __syncthreads();
+  int real = 0;
+  for (int i = threadIdx.x; i < n_c; i += blockDim.x) {
+    const chm_queue_key& c = ma.gathered[((size_t)(i / ma.F) * K + m) * ma.F + i % ma.F];
+    real += c.level != INT64_MAX;
+  }
+  atomicAdd(&n_real, real);
+  __syncthreads();
+  const int a_global = min(free_slots, n_real);
+  int own = 0;
+  for (int j = threadIdx.x; j < ma.F; j += blockDim.x) {
+    const chm_queue_key mine = ma.gathered[((size_t)ma.rank * K + m) * ma.F + j];
+    if (mine.level == INT64_MAX) continue;
+    int rank_j = 0;
+    for (int i = 0; i < n_c && rank_j < a_global; ++i) {
+      const chm_queue_key c = ma.gathered[((size_t)(i / ma.F) * K + m) * ma.F + i % ma.F];
+      if (c.level != INT64_MAX && cand_less(c, mine)) ++rank_j;
+    }
+    own += rank_j < a_global;
+  }
+  atomicAdd(&n_own, own);
+  __syncthreads();
+  if (threadIdx.x == 0) { misc[0] = n_own; misc[1] = a_global; }
+  __syncthreads();
+}
+
+__global__ void candidates_kernel(QueueParams prm, chm_monitor_state mon, chm_queue_state q,
+                                  int F, chm_queue_key* __restrict__ out) {
+  const int m = blockIdx.x;
+  const size_t seg = (size_t)m * q.capacity;
+  const int n = mon.engine_queued[m];
+  const int take = min(n, prm.b[m]);
+  for (int j = threadIdx.x; j < F; j += blockDim.x) {
+    chm_queue_key k;
+    if (j < take) {
+      const int e = q.order[seg + j];
+      k.level = q.level[seg + e];
+      k.priority = q.priority[seg + e];
+      k.arrival = q.arrival[seg + e];
+      k.seq = q.seq[seg + e];
+      k.handle = q.handle[seg + e];
+    } else {
+      k.level = INT64_MAX;
+      k.priority = 0; k.arrival = 0; k.seq = 0; k.handle = -1;
+    }
+    out[(size_t)m * F + j] = k;
+  }
+}
+
 // mode 0: completions (R = n_complete[m], each frees one running slot first)
 // mode 1: tick (append queued rows, then R = n_iterations explicit iterations)
+// mode 2: one iteration with a cross-GPU admission merge (MergeArgs)
 template <typename Idx, bool kBig>
 __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
     QueueParams prm, chm_monitor_state mon, chm_queue_state q, chm_rows rows,
     chm_decisions dec, const int32_t* __restrict__ n_complete, int n_iterations, int mode,
-    int32_t* err) {
+    int32_t* err, MergeArgs ma) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QueueCtl& s = *reinterpret_cast<QueueCtl*>(smem_raw);
   const int m = blockIdx.x;
@@ -255,7 +326,21 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   unsorted = __syncthreads_or(unsorted);
   const bool use_arr = unsorted != 0;
 
-  const int R = (mode == 0) ? n_complete[m] : n_iterations;
+  const int R = (mode == 0) ? n_complete[m] : (mode == 2 ? 1 : n_iterations);
+  // mode 2: this rank's and the global admission counts from the gathered keys
+  // release[m] < 0: engine m runs no iteration this call
+  const int rel = (mode == 2 && ma.release) ? ma.release[m] : 0;
+  int a_local = 0, a_global = 0;
+  if (mode == 2 && rel < 0) {
+    // nothing to do; the order from the previous call stays valid
+    return;
+  }
+  if (mode == 2) {
+    merge_counts(ma, m, prm.K, max(0, bmax - max(run - rel, 0)), &s.misc[0]);
+    a_local = s.misc[0];
+    a_global = s.misc[1];
+    __syncthreads();
+  }
   // Admissions of this call are appended after those already reported since
   // the host last zeroed n_admitted (completions and tick share the list).
   const int n_adm0 = q.n_admitted[m];
@@ -309,7 +394,8 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
       int remaining = n;
       for (int r = 0; r < R; ++r) {
         if (mode == 0) run = max(run - 1, 0);
-        const int a = max(0, min(bmax - run, remaining));
+        if (mode == 2) run = max(run - rel, 0);
+        const int a = mode == 2 ? min(a_local, remaining) : max(0, min(bmax - run, remaining));
         for (int t = 0; t < a; ++t) {
           HeadKey best;
           best.g = -1;
@@ -344,7 +430,7 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
           ++n_adm;
           --remaining;
         }
-        run += a;
+        run += mode == 2 ? a_global : a;
         if (prm.aging_enabled && remaining > 0) {
           for (int g = lane; g < G; g += 32) {
             if (s.g_cur[g] < s.g_end[g]) {
@@ -448,7 +534,7 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
                                const chm_monitor_state* mon, const chm_queue_state* q,
                                const chm_rows* rows, const chm_decisions* dec,
                                const int32_t* n_complete, int n_iterations, int mode,
-                               int32_t* err, cudaStream_t s) {
+                               int32_t* err, cudaStream_t s, MergeArgs ma = MergeArgs{}) {
   if (!pool || !aging || !mon || !q) return CHM_ERR_INVALID_ARG;
   const int K = pool->n_models;
   if (K < 1 || K > CHM_MAX_MODELS || q->capacity < 1) return CHM_ERR_INVALID_ARG;
@@ -469,6 +555,10 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   if (rows) r = *rows;
   if (dec) d = *dec;
   prof::begin(prof::K_QUEUE, s);
+  if (huge && mode == 2) {
+    prof::end(prof::K_QUEUE, s, 0.0);
+    return CHM_ERR_UNSUPPORTED;
+  }
   if (huge) {
     const chm_status rc = launch_queue_huge(prm, *mon, *q, r, d, n_complete, n_iterations, mode,
                                             err, s);
@@ -480,13 +570,13 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
     cudaFuncSetAttribute(queue_kernel<uint32_t, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     queue_kernel<uint32_t, true><<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete,
-                                                             n_iterations, mode, err);
+                                                             n_iterations, mode, err, ma);
   } else {
     const size_t smem = sizeof(QueueCtl) + sizeof(SmallKeysSmem);
     cudaFuncSetAttribute(queue_kernel<uint16_t, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     queue_kernel<uint16_t, false><<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete,
-                                                              n_iterations, mode, err);
+                                                              n_iterations, mode, err, ma);
   }
   prof::end(prof::K_QUEUE, s, 0.0);
   CHM_LAUNCH_CHECK();
@@ -517,4 +607,33 @@ extern "C" chm_status chm_queue_tick(const chm_pool* pool, const chm_aging_cfg* 
   if (!rows || !dec || n_iterations < 0) return CHM_ERR_INVALID_ARG;
   return chm::launch_queue(pool, aging, mon, q, rows, dec, nullptr, n_iterations, 1, error,
                            (cudaStream_t)stream);
+}
+
+extern "C" chm_status chm_queue_candidates(const chm_pool* pool, const chm_monitor_state* mon,
+                                           const chm_queue_state* q, int32_t F,
+                                           chm_queue_key* out, void* stream) {
+  if (!pool || !mon || !q || !out || F < 1) return CHM_ERR_INVALID_ARG;
+  const int K = pool->n_models;
+  if (K < 1 || K > CHM_MAX_MODELS) return CHM_ERR_INVALID_ARG;
+  chm::QueueParams prm{};
+  prm.K = K;
+  for (int m = 0; m < K; ++m) {
+    prm.b[m] = pool->max_batch_size[m];
+    if (prm.b[m] > F) return CHM_ERR_INVALID_ARG;  // F must cover every engine's slots
+  }
+  chm::candidates_kernel<<<K, 256, 0, (cudaStream_t)stream>>>(prm, *mon, *q, F, out);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_queue_admit_merged(const chm_pool* pool, const chm_aging_cfg* aging,
+                                             const chm_monitor_state* mon,
+                                             const chm_queue_state* q,
+                                             const chm_queue_key* gathered, int32_t G,
+                                             int32_t F, int32_t rank, const int32_t* release,
+                                             int32_t* error, void* stream) {
+  if (!gathered || G < 1 || F < 1 || rank < 0 || rank >= G) return CHM_ERR_INVALID_ARG;
+  chm::MergeArgs ma{gathered, G, F, rank, release};
+  return chm::launch_queue(pool, aging, mon, q, nullptr, nullptr, nullptr, 1, 2, error,
+                           (cudaStream_t)stream, ma);
 }

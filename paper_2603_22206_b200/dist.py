@@ -84,25 +84,99 @@ def relay_forward(state: torch.Tensor, group=None) -> None:
         state.copy_(buf)
 
 
+def sharded_iteration(gs, group=None, release=None) -> None:
+    """One scheduling iteration of every engine over the G sub-queues
+    (global admission): each rank's STJF head candidates
+    are all-gathered (NCCL; gloo over host copies), then every rank admits its
+    share of the global top and ages its sub-queue (chm_queue_admit_merged).
+    Equal to one EngineSim._iterate on the union queue (engine.py:328-338)."""
+    cand = gs.queue_candidates()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    send = _p2p_buffer(cand, group)
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send, group=group)
+    gathered = torch.stack(parts).to(cand.device)
+    gs.queue_admit_merged(gathered, rank, release)
+
+
 def _global(rank: int, group) -> int:
     return rank if group is None else dist.get_global_rank(group, rank)
 
 
-class ShardedScheduler:
-    """Wraps a per-rank GpuScheduler with the Mode A / Mode B exchange."""
+# Engine counters relayed with (s, c) under global admission: they make the
+# enqueue-time admission (running < max_batch_size), the seq tie-break and the
+# clock check (engine.py:140-158) see the one reference engine.
+_RELAYED = ("engine_running", "engine_seq", "engine_clock", "engine_iterations")
 
-    def __init__(self, scheduler, mode: str = "B", group=None):
+
+class ShardedScheduler:
+    """Wraps a per-rank GpuScheduler with the Mode A / Mode B exchange.
+
+    global_admission (Mode B only): each engine's queue is the union of the
+    ranks' sub-queues, served in the reference's global STJF order. The relay
+    also carries the engine counters, and every scheduling iteration, whether
+    an explicit one or one per completion, is a `sharded_iteration`. Then the
+    decisions, admissions and queue orders equal one serial replay of the
+    concatenated batch through one EngineSim per model."""
+
+    def __init__(self, scheduler, mode: str = "B", group=None, global_admission: bool = False):
         if mode not in ("A", "B"):
             raise ValueError("mode must be 'A' or 'B'")
+        if global_admission and mode != "B":
+            raise ValueError("global admission needs the Mode B relay")
         self.gs = scheduler
         self.mode = mode
         self.group = group
+        self.global_admission = global_admission
         st = scheduler.state
-        self.packed = torch.empty(2 * st.K, dtype=torch.float64, device=st.device)
+        n = (2 + len(_RELAYED)) * st.K if global_admission else 2 * st.K
+        self.packed = torch.empty(n, dtype=torch.float64, device=st.device)
+
+    def _pack(self) -> None:
+        st, K = self.gs.state, self.gs.state.K
+        self.packed[:K].copy_(st.inflight_sum)
+        self.packed[K:2 * K].copy_(st.inflight_comp)
+        if self.global_admission:
+            for i, name in enumerate(_RELAYED):
+                self.packed[(2 + i) * K:(3 + i) * K].copy_(getattr(st, name))
+
+    def _unpack(self) -> None:
+        st, K = self.gs.state, self.gs.state.K
+        st.inflight_sum.copy_(self.packed[:K])
+        st.inflight_comp.copy_(self.packed[K:2 * K])
+        if self.global_admission:
+            for i, name in enumerate(_RELAYED):
+                getattr(st, name).copy_(self.packed[(2 + i) * K:(3 + i) * K])
+
+    def _run_global(self, batch, n_iterations: int, n_complete, kw) -> None:
+        st = self.gs.state
+        st.q_n_admitted.zero_()
+        st.q_n_promoted.zero_()
+        if n_complete is not None:
+            # each completion frees a slot and runs one iteration of its engine
+            # (engine.py:232-241); n_complete is the global count, equal on all ranks
+            for r in range(int(n_complete.max().item()) if n_complete.numel() else 0):
+                release = torch.where(n_complete > r, 1, -1).to(torch.int32)
+                sharded_iteration(self.gs, self.group, release)
+        self._pack()
+        relay_receive(self.packed, self.group)
+        self._unpack()
+        self.gs.run_rows(batch, n_iterations=0, keep_admitted=True, **kw)
+        self._pack()
+        relay_forward(self.packed, self.group)
+        self._unpack()
+        for _ in range(n_iterations):
+            sharded_iteration(self.gs, self.group)
 
     def run_rows(self, batch, n_iterations: int = 1, **kw) -> None:
         st = self.gs.state
         K = st.K
+        if self.global_admission:
+            if kw.get("completions") is not None:
+                raise NotImplementedError("monitor completions are single-GPU; pass n_complete")
+            self._run_global(batch, n_iterations, kw.pop("n_complete", None), kw)
+            return
         if kw.get("completions") is not None:
             # each GPU's log holds only its own dispatches while (s, c) carries
             # the global volume: recomputing from the local log would drop the

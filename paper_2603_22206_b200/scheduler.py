@@ -180,14 +180,17 @@ class GpuScheduler:
 
     # ------------------------------------------------------------------ core
     def run_rows(self, batch: RowBatch, n_iterations: int = 1, n_complete=None,
-                 with_loads: bool = True, stream=None, completions=None) -> None:
+                 with_loads: bool = True, stream=None, completions=None,
+                 keep_admitted: bool = False) -> None:
         """Enqueue one tick for `batch` on `stream` (default: current stream).
 
         completions: optional (model int32[n], key int64[n]) device tensors of
         requests that finished since the last tick (key = request_key(program,
         stage)): removed from the in-flight log (record_completion) and their
         engines' slots freed, before the batch is scheduled. n_complete: the
-        engine side only (int32[K] finished-per-engine counts)."""
+        engine side only (int32[K] finished-per-engine counts).
+        keep_admitted: append to the admission lists instead of resetting
+        them (the sharded protocol runs merged iterations before the batch)."""
         B = batch.n_rows
         if B > self.buf.max_rows:
             raise ValueError(f"batch of {B} rows exceeds max_rows={self.buf.max_rows}")
@@ -198,8 +201,9 @@ class GpuScheduler:
         dec_c = buf.decisions_struct(with_loads)
         with torch.cuda.stream(s):
             buf.error.copy_(buf.error_init)
-            st.q_n_admitted.zero_()
-            st.q_n_promoted.zero_()
+            if not keep_admitted:
+                st.q_n_admitted.zero_()
+                st.q_n_promoted.zero_()
             if completions is not None:
                 # monitor side (record_completion) -> per-engine counts -> engines
                 if n_complete is not None:
@@ -246,6 +250,43 @@ class GpuScheduler:
             self.state.pool_c, self.state.monitor_c, _p(m), _p(k), _p(e), int(m.numel()),
             _p(self.buf.error), s.cuda_stream), "chm_monitor_note_progress")
         self._keep = (m, k, e)  # alive until the stream has consumed them
+
+    # -- sharded engine queues: cross-GPU admission --------
+    def candidate_width(self) -> int:
+        """F of chm_queue_candidates: the largest max_batch_size in the pool."""
+        return max(self.pool[mid].max_batch_size for mid in self.ids)
+
+    def queue_candidates(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """This rank's STJF head of every engine sub-queue, as chm_queue_key
+        records in an int64 tensor [K, F, 5] (level, priority bits, arrival
+        bits, seq, handle; level INT64_MAX = no candidate)."""
+        F = self.candidate_width()
+        if out is None:
+            out = torch.empty((self.K, F, 5), dtype=torch.int64, device=self.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = self.state
+        _lib.check(self.lib.chm_queue_candidates(st.pool_c, st.monitor_c, st.queue_c, F,
+                                                 _p(out), s.cuda_stream),
+                   "chm_queue_candidates")
+        return out
+
+    def queue_admit_merged(self, gathered: torch.Tensor, rank: int, release=None,
+                           stream=None) -> None:
+        """One scheduling iteration of every engine against the gathered
+        candidates of all G ranks ([G, K, F, 5], rank-major): admit this
+        rank's share of the global top, count the global admissions as
+        running, age the rest. release: optional int32[K] device tensor
+        (1 = a running request finished first, -1 = engine idle this call)."""
+        G, K, F = int(gathered.shape[0]), int(gathered.shape[1]), int(gathered.shape[2])
+        if K != self.K or F != self.candidate_width() or gathered.dtype != torch.int64:
+            raise ValueError("gathered candidates do not match this pool")
+        gathered = gathered.contiguous()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = self.state
+        _lib.check(self.lib.chm_queue_admit_merged(st.pool_c, self.aging_c, st.monitor_c,
+                                                   st.queue_c, _p(gathered), G, F, int(rank),
+                                                   _p(release), _p(self.buf.error),
+                                                   s.cuda_stream), "chm_queue_admit_merged")
 
     def check_errors(self, context: str = "") -> None:
         _lib.raise_device_error(self.buf.error.cpu().tolist(), context)

@@ -139,3 +139,166 @@ def test_shard_of_is_stable_and_balanced():
     assert ranks == [shard_of(f"p{i:06d}", 8) for i in range(8000)]
     counts = np.bincount(ranks, minlength=8)
     assert counts.min() > 850 and counts.max() < 1150
+
+
+# ---------------------------------------------------------------------------
+# Sharded engine queues with global admission (dist.sharded_iteration and the
+# counter relay of ShardedScheduler(global_admission=True)) over gloo. The
+# per-rank device kernels are replaced by a CPU sub-queue with the same
+# contract (chm_queue_candidates / chm_queue_admit_merged, include/
+# chimera_b200.h); the golden EngineSim scripts fix the expected result.
+
+class _SubQueueShard:
+    """CPU stand-in for one rank's GpuScheduler queue side (K = 1)."""
+
+    def __init__(self, b, S):
+        import types
+        self.b, self.S = b, S
+        self.entries = []  # dicts: level, prio, arr, seq, handle, count
+        z = lambda dt: torch.zeros(1, dtype=dt)  # noqa: E731
+        self.state = types.SimpleNamespace(
+            K=1, device=torch.device("cpu"), inflight_sum=z(torch.float64),
+            inflight_comp=z(torch.float64), engine_running=z(torch.int32),
+            engine_seq=z(torch.int64), engine_clock=z(torch.float64),
+            engine_iterations=z(torch.int64), q_n_admitted=z(torch.int32),
+            q_n_promoted=z(torch.int32))
+        self.admitted = []
+
+    def _key(self, e):
+        return (e["level"], e["prio"], e["arr"], e["seq"])
+
+    def _age(self):
+        for e in self.entries:
+            e["count"] += 1
+            if e["count"] >= self.S:
+                e["level"] -= 1
+                e["count"] = 0
+
+    def run_rows(self, rows, n_iterations=0, keep_admitted=False):
+        st = self.state
+        for handle, prio, arr in rows:
+            seq = int(st.engine_seq[0])
+            st.engine_seq[0] += 1
+            self.entries.append(dict(level=0, prio=prio, arr=arr, seq=seq, handle=handle, count=0))
+            if int(st.engine_running[0]) < self.b:  # EngineSim.enqueue -> _iterate
+                st.engine_iterations[0] += 1
+                self.entries.sort(key=self._key)
+                self.admitted.append(self.entries.pop(0)["handle"])
+                st.engine_running[0] += 1
+                self._age()
+
+    def queue_candidates(self):
+        head = sorted(self.entries, key=self._key)[:self.b]
+        out = torch.full((1, self.b, 5), 0, dtype=torch.int64)
+        out[0, :, 0] = torch.iinfo(torch.int64).max
+        for j, e in enumerate(head):
+            out[0, j, 0] = e["level"]
+            out[0, j, 1] = int(np.array([e["prio"]]).view(np.int64)[0])
+            out[0, j, 2] = int(np.array([e["arr"]]).view(np.int64)[0])
+            out[0, j, 3] = e["seq"]
+            out[0, j, 4] = e["handle"]
+        return out
+
+    def queue_admit_merged(self, gathered, rank, release=None):
+        st = self.state
+        rel = 0 if release is None else int(release[0])
+        if rel < 0:
+            return
+        run = max(int(st.engine_running[0]) - rel, 0)
+        cands = []
+        for g in range(gathered.shape[0]):
+            for c in gathered[g, 0].tolist():
+                if c[0] == torch.iinfo(torch.int64).max:
+                    continue
+                pr = float(np.array([c[1]], dtype=np.int64).view(np.float64)[0])
+                ar = float(np.array([c[2]], dtype=np.int64).view(np.float64)[0])
+                cands.append(((c[0], pr, ar, c[3]), g, c[4]))
+        cands.sort()
+        take = cands[:max(0, min(self.b - run, len(cands)))]
+        mine = {h for _, g, h in take if g == rank}
+        self.entries.sort(key=self._key)
+        for e in list(self.entries):
+            if e["handle"] in mine:
+                self.entries.remove(e)
+        self.admitted.append([h for _, _, h in take])
+        st.engine_running[0] = run + len(take)
+        st.engine_iterations[0] += 1
+        self._age()
+
+
+def _queue_worker(rank, world, port, name, q):
+    import math
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_22206_b200 import dist as D
+    qd = H.load_queue(name)
+    shard = _SubQueueShard(qd["b"], qd["S"] if qd["S"] else math.inf)
+    ss = D.ShardedScheduler.__new__(D.ShardedScheduler)
+    ss.gs, ss.mode, ss.group, ss.global_admission = shard, "B", None, True
+    ss.packed = torch.empty((2 + len(D._RELAYED)) * 1, dtype=torch.float64)
+    enq, pos = qd["enq"], 0
+    log = []  # per step: handles admitted on enqueue (this rank) / per iteration (global)
+
+    def enqueue(n):
+        nonlocal pos
+        o = enq[pos:pos + n]
+        pos += n
+        bounds = np.linspace(0, n, world + 1).astype(int)
+        part = [(int(h), float(p), float(t)) for h, p, t in o[bounds[rank]:bounds[rank + 1]]]
+        shard.admitted = []
+        ss._pack()
+        D.relay_receive(ss.packed)
+        ss._unpack()
+        shard.run_rows(part)
+        ss._pack()
+        D.relay_forward(ss.packed)
+        ss._unpack()
+        got = [None] * world
+        dist.all_gather_object(got, shard.admitted)
+        log.extend(sum(got, []))
+
+    def iteration(release=None):
+        shard.admitted = []
+        D.sharded_iteration(shard, None, None if release is None else torch.tensor([release]))
+        log.extend(shard.admitted[0])
+
+    enqueue(qd["n_pre"])
+    for op, n in qd["script"]:
+        if op == "enq":
+            enqueue(n)
+        else:
+            for _ in range(n):
+                iteration(None if op == "iter" else 1)
+    rows = [(shard._key(e), e["handle"], e["count"]) for e in shard.entries]
+    got = [None] * world
+    dist.all_gather_object(got, rows)
+    if rank == 0:
+        allrows = sorted(sum(got, []))
+        q.put(dict(admitted=log, order=[r[1] for r in allrows], level=[r[0][0] for r in allrows],
+                   count=[r[2] for r in allrows], running=int(shard.state.engine_running[0]),
+                   iterations=int(shard.state.engine_iterations[0])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["q_basic", "q_promote", "q_complete"])
+def test_sharded_queue_protocol_equals_single_queue(name):
+    """Global admission over world_size 2 (gloo): relayed engine counters +
+    all-gathered STJF candidates reproduce the golden single EngineSim."""
+    qd = H.load_queue(name)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_queue_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_array_equal(res["admitted"], qd["admitted"])
+    np.testing.assert_array_equal(res["order"], qd["order"])
+    np.testing.assert_array_equal(res["level"], qd["level"])
+    np.testing.assert_array_equal(res["count"], qd["count"])
+    assert res["running"] == qd["running"]
+    assert res["iterations"] == qd["iterations"]
