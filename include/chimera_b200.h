@@ -124,6 +124,8 @@ typedef struct chm_rows {
   const double* arrival;     /* [B] Request.arrival_time (ms)                  */
   const int32_t* out_tokens; /* [B*K] rec.out_tokens(stage, m) per model       */
   const int64_t* handle;     /* [B] opaque request handle stored in the queue  */
+  const int32_t* input_tokens; /* [B] Request.input_tokens (prefill time; only
+                                  read by the engine clock, may be NULL)       */
 } chm_rows;
 
 /* Scratch produced by chm_prepare_rows and consumed by chm_schedule_rows. */
@@ -168,7 +170,34 @@ typedef struct chm_queue_state {
   void* scratch;             /* K * chm_queue_scratch_bytes(cap) bytes; required
                                 when capacity > 10240 (sort keys then live in
                                 L2/HBM instead of shared memory)               */
+  const struct chm_engine_run* run; /* engine execution clock (NULL = off)    */
 } chm_queue_state;
+
+/* Engine execution clock (EngineSim running set,
+ * engine.py:165-241): every admission (at enqueue, in an iteration, or after a
+ * stint ends) starts a stint of out_tokens decode steps after a prefill of
+ * prefill_ms_per_token * input_tokens; chm_engine_advance finishes stints in
+ * (stint_end, seq) order up to a target time, running a scheduling iteration
+ * at each end. Requires capacity <= 2^18 (not the grid-wide path); with it,
+ * chm_queue_complete (external completions) and the merged admission are
+ * CHM_ERR_UNSUPPORTED. */
+typedef struct chm_engine_run {
+  int32_t capacity;                      /* running entries per engine (>= b) */
+  int32_t done_capacity;                 /* completion records per engine     */
+  double prefill_ms_per_token[CHM_MAX_MODELS];
+  int32_t* queue_input_tokens;           /* [K*queue cap] parallel to the queue */
+  int64_t* handle;                       /* [K*cap] running set (unordered)   */
+  int64_t* seq;                          /* [K*cap] QueueEntry.seq            */
+  double* stint_end;                     /* [K*cap]                           */
+  double* decode_start;                  /* [K*cap]                           */
+  int32_t* stint_tokens;                 /* [K*cap]                           */
+  int32_t* n;                            /* [K] live entries                  */
+  int64_t* tokens_emitted;               /* [K] tokens_emitted_total          */
+  int64_t* served;                       /* [K] requests_served               */
+  int64_t* done_handle;                  /* [K*done cap] completions, in order */
+  double* done_time;                     /* [K*done cap] Completion.time       */
+  int32_t* n_done;                       /* [K] appended since the host zeroed */
+} chm_engine_run;
 
 /* One STJF candidate of an engine sub-queue, for the cross-GPU admission
  * merge: the reference sort key (QueueEntry.sort_key, engine.py:55-69) plus
@@ -358,6 +387,17 @@ chm_status chm_queue_admit_merged(const chm_pool* pool, const chm_aging_cfg* agi
                                   const chm_queue_key* gathered, int32_t G, int32_t F,
                                   int32_t rank, const int32_t* release, int32_t* error,
                                   void* stream);
+
+/* EngineSim.advance_to(target[m]) for every engine (engine.py:174-183): finish
+ * the running stints ending at or before the target in (stint_end, seq)
+ * order; each frees its slot, is appended to the completion list and runs one
+ * scheduling iteration at its end time (admissions start new stints, which
+ * may end before the target too). The clock then moves to the target
+ * (CHM_ERR_TIME_BACKWARDS if that is more than 1e-9 ms in the past). Needs
+ * q->run. */
+chm_status chm_engine_advance(const chm_pool* pool, const chm_aging_cfg* aging,
+                              const chm_monitor_state* mon, const chm_queue_state* q,
+                              const double* target, int32_t* error, void* stream);
 
 /* ActivityMonitor.note_progress (monitor.py:108-111) for n (model index,
  * request key, emitted tokens) updates, in call order (a later update of the

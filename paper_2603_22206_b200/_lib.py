@@ -88,6 +88,7 @@ class Rows(ctypes.Structure):
         ("arrival", c_void_p),
         ("out_tokens", c_void_p),
         ("handle", c_void_p),
+        ("input_tokens", c_void_p),
     ]
 
 
@@ -132,6 +133,27 @@ class QueueState(ctypes.Structure):
         ("n_promoted", c_void_p),
         ("arrival_unsorted", c_void_p),
         ("scratch", c_void_p),
+        ("run", c_void_p),
+    ]
+
+
+class EngineRun(ctypes.Structure):
+    _fields_ = [
+        ("capacity", c_int32),
+        ("done_capacity", c_int32),
+        ("prefill_ms_per_token", c_double * MAX_MODELS),
+        ("queue_input_tokens", c_void_p),
+        ("handle", c_void_p),
+        ("seq", c_void_p),
+        ("stint_end", c_void_p),
+        ("decode_start", c_void_p),
+        ("stint_tokens", c_void_p),
+        ("n", c_void_p),
+        ("tokens_emitted", c_void_p),
+        ("served", c_void_p),
+        ("done_handle", c_void_p),
+        ("done_time", c_void_p),
+        ("n_done", c_void_p),
     ]
 
 
@@ -234,6 +256,9 @@ _SIGNATURES = [
     ("chm_queue_admit_merged", c_int32,
      [POINTER(Pool), POINTER(AgingCfg), POINTER(MonitorState), POINTER(QueueState), c_void_p,
       c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    ("chm_engine_advance", c_int32,
+     [POINTER(Pool), POINTER(AgingCfg), POINTER(MonitorState), POINTER(QueueState), c_void_p,
+      c_void_p, c_void_p]),
     ("chm_encoder_forward", c_int32,
      [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p,
       c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),

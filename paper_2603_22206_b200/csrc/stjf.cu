@@ -185,7 +185,25 @@ struct MergeArgs {
   const chm_queue_key* gathered;  // [G][K][F]
   int G, F, rank;
   const int32_t* release;         // [K] slots freed before the iteration (nullable)
+  const double* target;           // [K] mode 3: advance_to target per engine
 };
+
+// Engine clock: start a stint for an admitted entry at `now`
+// (_BatchEngine._admit, engine.py:202-227). Plain (unfused) double rounding,
+// as Python evaluates now + prefill and decode_start + tokens * d.
+__device__ __forceinline__ bool run_admit(const chm_engine_run& er, int m, int n_run,
+                                          int64_t handle, int64_t seq, int32_t tokens,
+                                          int32_t input, double now, double d) {
+  if (n_run >= er.capacity) return false;
+  const size_t b = (size_t)m * er.capacity + n_run;
+  const double ds = __dadd_rn(now, __dmul_rn(er.prefill_ms_per_token[m], (double)input));
+  er.handle[b] = handle;
+  er.seq[b] = seq;
+  er.decode_start[b] = ds;
+  er.stint_end[b] = __dadd_rn(ds, __dmul_rn((double)tokens, d));
+  er.stint_tokens[b] = tokens;
+  return true;
+}
 
 __device__ __forceinline__ bool cand_less(const chm_queue_key& a, const chm_queue_key& b) {
   if (a.level != b.level) return a.level < b.level;
@@ -257,7 +275,7 @@ template <typename Idx, bool kBig>
 __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
     QueueParams prm, chm_monitor_state mon, chm_queue_state q, chm_rows rows,
     chm_decisions dec, const int32_t* __restrict__ n_complete, int n_iterations, int mode,
-    int32_t* err, MergeArgs ma) {
+    int32_t* err, MergeArgs ma, chm_engine_run er) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QueueCtl& s = *reinterpret_cast<QueueCtl*>(smem_raw);
   const int m = blockIdx.x;
@@ -294,6 +312,16 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   int n = mon.engine_queued[m];
   int run = mon.engine_running[m];
   const int bmax = prm.b[m];
+  // engine clock (running set) tracking
+  const bool track = er.handle != nullptr;
+  int n_run = track ? er.n[m] : 0;
+  double clock = mon.engine_clock[m];
+  int32_t* qin_g = track ? er.queue_input_tokens + seg : nullptr;
+  const double tgt = mode == 3 ? ma.target[m] : 0.0;
+  if (mode == 3 && tgt < clock - 1e-9) {  // EngineSim._advance_clock (engine.py:140-143)
+    if (tid == 0) report_error(err, CHM_ERR_TIME_BACKWARDS, 0, m, 0);
+    return;
+  }
 
   // ---- mode 1: append rows queued on this engine by chm_schedule_rows ----
   if (mode == 1) {
@@ -305,7 +333,40 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
                                  0, m, n);
       return;
     }
-    append_queued_rows(m, prm.K, rows, dec, seg, q, n_old, s.scan, s.misc);
+    append_queued_rows(m, prm.K, rows, dec, seg, q, n_old, s.scan, s.misc,
+                       track ? er.queue_input_tokens : nullptr);
+    if (track) {
+      // rows admitted at enqueue (EngineSim.enqueue -> _iterate, engine.py:145-158)
+      // start their stints at their arrival, in row (= seq) order
+      const int n_rows = *dec.n_committed;
+      for (int blk = 0; blk < n_rows; blk += blockDim.x) {
+        const int i = blk + tid;
+        const bool take = i < n_rows && dec.model[i] == m && (dec.flags[i] & 2u);
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) s.scan[warp] = __popc(bal);
+        __syncthreads();
+        if (warp == 0) {
+          int v = lane < kQWarps ? s.scan[lane] : 0, incl = v;
+          for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          if (lane < kQWarps) s.scan[lane] = incl - v;
+          if (lane == 31) s.misc[1] = incl;
+        }
+        __syncthreads();
+        if (take) {
+          const int pos = n_run + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
+          if (!run_admit(er, m, pos, rows.handle ? rows.handle[i] : (int64_t)i, dec.seq[i],
+                         rows.out_tokens ? rows.out_tokens[(size_t)i * prm.K + m] : 0,
+                         rows.input_tokens ? rows.input_tokens[i] : 1, rows.arrival[i],
+                         prm.d[m]))
+            report_error(err, CHM_ERR_CAPACITY, i, m, pos);
+        }
+        n_run += s.misc[1];
+        __syncthreads();
+      }
+    }
     __threadfence_block();
   } else {
     if (n > cap) {
@@ -326,7 +387,9 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   unsorted = __syncthreads_or(unsorted);
   const bool use_arr = unsorted != 0;
 
-  const int R = (mode == 0) ? n_complete[m] : (mode == 2 ? 1 : n_iterations);
+  const int R = (mode == 0) ? n_complete[m]
+                : (mode == 2 ? 1 : (mode == 3 ? 0x7fffffff : n_iterations));
+  int iters = 0;  // scheduling iterations run by this call
   // mode 2: this rank's and the global admission counts from the gathered keys
   // release[m] < 0: engine m runs no iteration this call
   const int rel = (mode == 2 && ma.release) ? ma.release[m] : 0;
@@ -392,7 +455,56 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
     // ---- R scheduling iterations (warp 0) ----
     if (warp == 0) {
       int remaining = n;
+      const size_t rb = (size_t)m * (track ? er.capacity : 0);
       for (int r = 0; r < R; ++r) {
+        double t_iter = clock;
+        if (mode == 3) {
+          // next stint end: min (stint_end, seq) of the running set (engine.py:178-183)
+          double bt = 0;
+          long long bs = LLONG_MAX;
+          int bj = -1;
+          for (int j = lane; j < n_run; j += 32) {
+            const double te = er.stint_end[rb + j];
+            const long long sq = er.seq[rb + j];
+            if (bj < 0 || te < bt || (te == bt && sq < bs)) { bt = te; bs = sq; bj = j; }
+          }
+          for (int off = 16; off; off >>= 1) {
+            const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+            const long long os = __shfl_xor_sync(0xffffffffu, bs, off);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+            if (oj >= 0 && (bj < 0 || ot < bt || (ot == bt && os < bs))) { bt = ot; bs = os; bj = oj; }
+          }
+          if (bj < 0 || !(bt <= tgt)) break;
+          if (bt < clock - 1e-9) {  // _finish_stint -> _advance_clock (engine.py:140-143, 233)
+            if (lane == 0) report_error(err, CHM_ERR_TIME_BACKWARDS, 0, m, 1);
+            break;
+          }
+          if (lane == 0) {
+            // _finish_stint (engine.py:229-239) + EngineSim._on_stint_end
+            const int nd = er.n_done[m];
+            if (nd < er.done_capacity) {
+              er.done_handle[(size_t)m * er.done_capacity + nd] = er.handle[rb + bj];
+              er.done_time[(size_t)m * er.done_capacity + nd] = bt;
+              er.n_done[m] = nd + 1;
+            } else {
+              report_error(err, CHM_ERR_CAPACITY, 0, m, nd);
+            }
+            er.tokens_emitted[m] += er.stint_tokens[rb + bj];
+            er.served[m] += 1;
+            const size_t last = rb + n_run - 1, at = rb + bj;
+            er.handle[at] = er.handle[last];
+            er.seq[at] = er.seq[last];
+            er.stint_end[at] = er.stint_end[last];
+            er.decode_start[at] = er.decode_start[last];
+            er.stint_tokens[at] = er.stint_tokens[last];
+          }
+          __syncwarp();
+          --n_run;
+          run = max(run - 1, 0);
+          clock = bt;
+          t_iter = bt;
+        }
+        ++iters;
         if (mode == 0) run = max(run - 1, 0);
         if (mode == 2) run = max(run - rel, 0);
         const int a = mode == 2 ? min(a_local, remaining) : max(0, min(bmax - run, remaining));
@@ -425,7 +537,11 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
           if (lane == 0) {
             q.admitted[seg + n_adm0 + n_adm] = handle_g[best.e];
             s.g_cur[best.g] += 1;
+            if (track && !run_admit(er, m, n_run, handle_g[best.e], seq_g[best.e],
+                                    out_g[best.e], qin_g[best.e], t_iter, prm.d[m]))
+              report_error(err, CHM_ERR_CAPACITY, 0, m, n_run);
           }
+          if (track) ++n_run;
           __syncwarp();
           ++n_adm;
           --remaining;
@@ -447,12 +563,19 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
         }
       }
       for (int off = 16; off; off >>= 1) n_prom += __shfl_xor_sync(0xffffffffu, n_prom, off);
-      if (lane == 0) { s.misc[3] = n_adm; s.misc[4] = n_prom; s.misc[5] = run; }
+      if (lane == 0) {
+        s.misc[3] = n_adm; s.misc[4] = n_prom; s.misc[5] = run;
+        s.misc[0] = iters; s.misc[7] = n_run;
+        reinterpret_cast<double*>(s.red_or)[0] = clock;
+      }
     }
     __syncthreads();
     n_adm = s.misc[3];
     n_prom = s.misc[4];
     run = s.misc[5];
+    iters = s.misc[0];
+    n_run = s.misc[7];
+    clock = reinterpret_cast<double*>(s.red_or)[0];
     // ---- per-entry outcome: spare[e] = group or kAdmitted ----
     for (int p = tid; p < n; p += blockDim.x) {
       int lo = 0, hi = G - 1;
@@ -473,10 +596,11 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
       const bool keep = valid && g != (Idx)kAdmitted;
       double pr = 0, ar = 0;
       int64_t sq = 0, hd = 0;
-      int ot = 0, lv = 0, ct = 0, qn = 0;
+      int ot = 0, lv = 0, ct = 0, qn = 0, in = 0;
       unsigned long long pk = 0;
       if (keep) {
         pr = prio_g[i]; ar = arr_g[i]; sq = seq_g[i]; hd = handle_g[i]; ot = out_g[i];
+        if (track) in = qin_g[i];
         lv = (int)k.lvl[i] - 32768 + s.g_lvloff[g];
         ct = prm.aging_enabled ? s.g_count[g] : cnt_g[i];
         qn = (s.g_lvloff[g] != 0) ? 0 : qnt_g[i];
@@ -499,6 +623,7 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
         const int pos = out_base + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
         prio_g[pos] = pr; arr_g[pos] = ar; seq_g[pos] = sq; handle_g[pos] = hd;
         out_g[pos] = ot; lvl_g[pos] = lv; cnt_g[pos] = ct; qnt_g[pos] = qn;
+        if (track) qin_g[pos] = in;
         k.prio[pos] = pk;
         k.lvl[pos] = (uint16_t)(lv + 32768);
         k.cnt[pos] = (uint16_t)ct;
@@ -526,7 +651,9 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
     q.n_promoted[m] += n_prom;
     mon.engine_queued[m] = n;
     mon.engine_running[m] = run;
-    mon.engine_iterations[m] += R;
+    mon.engine_iterations[m] += iters;
+    if (track) er.n[m] = n_run;
+    if (mode == 3) mon.engine_clock[m] = fmax(clock, tgt);
   }
 }
 
@@ -546,8 +673,24 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   const bool huge = q->capacity > kQHuge;
   QueueParams prm{};
   prm.K = K;
-  for (int m = 0; m < K; ++m) prm.b[m] = pool->max_batch_size[m];
+  for (int m = 0; m < K; ++m) {
+    prm.b[m] = pool->max_batch_size[m];
+    prm.d[m] = pool->decode_ms_per_token[m];
+  }
   prm.aging_enabled = aging->enabled;
+  chm_engine_run er{};
+  if (q->run) {
+    er = *q->run;
+    if (mode == 0 || mode == 2 || huge) return CHM_ERR_UNSUPPORTED;
+    if (!er.handle || !er.seq || !er.stint_end || !er.decode_start || !er.stint_tokens ||
+        !er.n || !er.tokens_emitted || !er.served || !er.done_handle || !er.done_time ||
+        !er.n_done || !er.queue_input_tokens || er.capacity < 1 || er.done_capacity < 0)
+      return CHM_ERR_INVALID_ARG;
+    for (int m = 0; m < K; ++m)
+      if (er.capacity < pool->max_batch_size[m]) return CHM_ERR_INVALID_ARG;
+  } else if (mode == 3) {
+    return CHM_ERR_INVALID_ARG;
+  }
   prm.S = aging->starvation_threshold;
   prm.cap_limit = big ? 0x7fffffff : kQMax;
   chm_rows r{};
@@ -570,13 +713,13 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
     cudaFuncSetAttribute(queue_kernel<uint32_t, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     queue_kernel<uint32_t, true><<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete,
-                                                             n_iterations, mode, err, ma);
+                                                             n_iterations, mode, err, ma, er);
   } else {
     const size_t smem = sizeof(QueueCtl) + sizeof(SmallKeysSmem);
     cudaFuncSetAttribute(queue_kernel<uint16_t, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     queue_kernel<uint16_t, false><<<K, kQThreads, smem, s>>>(prm, *mon, *q, r, d, n_complete,
-                                                              n_iterations, mode, err, ma);
+                                                              n_iterations, mode, err, ma, er);
   }
   prof::end(prof::K_QUEUE, s, 0.0);
   CHM_LAUNCH_CHECK();
@@ -635,5 +778,16 @@ extern "C" chm_status chm_queue_admit_merged(const chm_pool* pool, const chm_agi
   if (!gathered || G < 1 || F < 1 || rank < 0 || rank >= G) return CHM_ERR_INVALID_ARG;
   chm::MergeArgs ma{gathered, G, F, rank, release};
   return chm::launch_queue(pool, aging, mon, q, nullptr, nullptr, nullptr, 1, 2, error,
+                           (cudaStream_t)stream, ma);
+}
+
+extern "C" chm_status chm_engine_advance(const chm_pool* pool, const chm_aging_cfg* aging,
+                                         const chm_monitor_state* mon,
+                                         const chm_queue_state* q, const double* target,
+                                         int32_t* error, void* stream) {
+  if (!target || !q || !q->run) return CHM_ERR_INVALID_ARG;
+  chm::MergeArgs ma{};
+  ma.target = target;
+  return chm::launch_queue(pool, aging, mon, q, nullptr, nullptr, nullptr, 0, 3, error,
                            (cudaStream_t)stream, ma);
 }

@@ -11,6 +11,7 @@ constexpr uint32_t kAdmitted = 0xffffffffu;
 struct QueueParams {
   int K;
   int b[CHM_MAX_MODELS];
+  double d[CHM_MAX_MODELS];  // decode_ms_per_token (engine clock)
   int aging_enabled;
   int S;
   int cap_limit;  // largest segment this kernel variant can hold
@@ -45,7 +46,8 @@ __device__ __forceinline__ bool key_less(const HeadKey& x, const HeadKey& y) {
 __device__ __forceinline__ int append_queued_rows(int m, int K, const chm_rows& rows,
                                                   const chm_decisions& dec, size_t seg,
                                                   const chm_queue_state& q, int n_old,
-                                                  int* scan, int* misc) {
+                                                  int* scan, int* misc,
+                                                  int32_t* q_input = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n_warps = blockDim.x >> 5;
   const int n_rows = *dec.n_committed;
@@ -76,6 +78,7 @@ __device__ __forceinline__ int append_queued_rows(int m, int K, const chm_rows& 
       q.level[pos] = 0;
       q.count[pos] = 0;
       q.quantum[pos] = 0;
+      if (q_input) q_input[pos] = rows.input_tokens ? rows.input_tokens[i] : 1;
     }
     pos_base += misc[1];
     __syncthreads();

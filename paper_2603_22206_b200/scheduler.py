@@ -58,7 +58,7 @@ class RowBatch:
 
     def rows_struct(self) -> _lib.Rows:
         return _lib.Rows(self.n_rows, _p(self.program), _p(self.stage), _p(self.arrival),
-                         _p(self.out_tokens), _p(self.handle))
+                         _p(self.out_tokens), _p(self.handle), _p(self.input_tokens))
 
     @staticmethod
     def from_numpy(device, **cols) -> "RowBatch":
@@ -159,7 +159,8 @@ class GpuScheduler:
                  aging: AgingConfig = AgingConfig(), *, router=None, predictor=None,
                  n_programs: int = 1 << 20, max_rows: int = 16384,
                  queue_capacity: int = 10240, device="cuda", inflight_capacity=None,
-                 decay_in_flight: bool = False):
+                 decay_in_flight: bool = False, engine_clock: bool = False,
+                 completion_capacity: int | None = None):
         self.lib = _lib.load()
         self.pool = pool
         self.ids = pool.model_ids
@@ -172,6 +173,11 @@ class GpuScheduler:
         self.state = DeviceState(pool, n_programs, queue_capacity, self.device,
                                  inflight_capacity=inflight_capacity,
                                  decay_in_flight=decay_in_flight)
+        if engine_clock:
+            # running sets + stint clock on the device
+            self.state.enable_engine_run(
+                completion_capacity if completion_capacity is not None
+                else queue_capacity + max(p.max_batch_size for p in pool.profiles))
         self.buf = BatchBuffers(self.K, max_rows, self.device)
         self.bal_c = balancer_struct(balancer)
         self.aging_c = aging_struct(aging)
@@ -250,6 +256,30 @@ class GpuScheduler:
             self.state.pool_c, self.state.monitor_c, _p(m), _p(k), _p(e), int(m.numel()),
             _p(self.buf.error), s.cuda_stream), "chm_monitor_note_progress")
         self._keep = (m, k, e)  # alive until the stream has consumed them
+
+    # -- engine execution clock ----------------------------
+    def advance_to(self, target, stream=None, keep_completions: bool = False):
+        """EngineSim.advance_to(target) on every engine (engine.py:174-183):
+        finish the stints ending by `target` (float, or float64[K] per engine),
+        each running one scheduling iteration at its end. Returns nothing; the
+        completions are in `state.completions(m)` (appended to the previous
+        call's when keep_completions)."""
+        st = self.state
+        if st.run_c is None:
+            raise RuntimeError("GpuScheduler(engine_clock=True) is required")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not torch.is_tensor(target):
+            target = torch.full((self.K,), float(target), dtype=torch.float64,
+                                device=self.device)
+        with torch.cuda.stream(s):
+            if not keep_completions:
+                st.run_n_done.zero_()
+            st.q_n_admitted.zero_()
+            st.q_n_promoted.zero_()
+            self.buf.error.copy_(self.buf.error_init)
+            _lib.check(self.lib.chm_engine_advance(st.pool_c, self.aging_c, st.monitor_c,
+                                                   st.queue_c, _p(target), _p(self.buf.error),
+                                                   s.cuda_stream), "chm_engine_advance")
 
     # -- sharded engine queues: cross-GPU admission (SURVEY §8f row 1) --------
     def candidate_width(self) -> int:

@@ -20,6 +20,8 @@ assignment + 4 of stage bits + 8 of stamp per program, 10^8 programs take
 
 from __future__ import annotations
 
+import ctypes
+
 import math
 
 import numpy as np
@@ -124,6 +126,61 @@ class DeviceState:
             _ptr(self.q_count), _ptr(self.q_quantum), _ptr(self.q_order),
             _ptr(self.q_admitted), _ptr(self.q_n_admitted), _ptr(self.q_n_promoted),
             _ptr(self.q_arrival_unsorted), _ptr(self.q_scratch))
+
+    # -- engine execution clock ----------------------------
+    run_c = None
+
+    def enable_engine_run(self, done_capacity: int) -> None:
+        """Allocate the per-engine running sets (EngineSim.running) and the
+        completion lists, and attach them to the queue state: from now on
+        every admission starts a stint and chm_engine_advance finishes them."""
+        d, K = self.device, self.K
+        cap = max(self.pool[mid].max_batch_size for mid in self.ids)
+        f64, i64, i32 = torch.float64, torch.int64, torch.int32
+        self.q_input_tokens = torch.ones(K * self.capacity, dtype=i32, device=d)
+        self.run_handle = torch.zeros(K * cap, dtype=i64, device=d)
+        self.run_seq = torch.zeros(K * cap, dtype=i64, device=d)
+        self.run_stint_end = torch.zeros(K * cap, dtype=f64, device=d)
+        self.run_decode_start = torch.zeros(K * cap, dtype=f64, device=d)
+        self.run_stint_tokens = torch.zeros(K * cap, dtype=i32, device=d)
+        self.run_n = torch.zeros(K, dtype=i32, device=d)
+        self.tokens_emitted = torch.zeros(K, dtype=i64, device=d)
+        self.served = torch.zeros(K, dtype=i64, device=d)
+        self.done_capacity = int(done_capacity)
+        self.done_handle = torch.zeros(K * self.done_capacity, dtype=i64, device=d)
+        self.done_time = torch.zeros(K * self.done_capacity, dtype=f64, device=d)
+        self.run_n_done = torch.zeros(K, dtype=i32, device=d)
+        self.run_capacity = cap
+        er = _lib.EngineRun()
+        er.capacity = cap
+        er.done_capacity = self.done_capacity
+        for i, mid in enumerate(self.ids):
+            er.prefill_ms_per_token[i] = self.pool[mid].prefill_ms_per_token
+        for name, t in (("queue_input_tokens", self.q_input_tokens),
+                        ("handle", self.run_handle), ("seq", self.run_seq),
+                        ("stint_end", self.run_stint_end),
+                        ("decode_start", self.run_decode_start),
+                        ("stint_tokens", self.run_stint_tokens), ("n", self.run_n),
+                        ("tokens_emitted", self.tokens_emitted), ("served", self.served),
+                        ("done_handle", self.done_handle), ("done_time", self.done_time),
+                        ("n_done", self.run_n_done)):
+            setattr(er, name, _ptr(t))
+        self.run_c = er
+        self.queue_c.run = ctypes.addressof(er)
+
+    def completions(self, model: int) -> tuple[np.ndarray, np.ndarray]:
+        """(handles, finish times) of engine `model`'s completions, in order."""
+        n = int(self.run_n_done[model])
+        b = model * self.done_capacity
+        return (self.done_handle[b:b + n].cpu().numpy(), self.done_time[b:b + n].cpu().numpy())
+
+    def running_set(self, model: int) -> list[tuple[int, int, float]]:
+        """(seq, handle, stint_end) of engine `model`'s running requests by seq."""
+        n = int(self.run_n[model])
+        b = model * self.run_capacity
+        rows = zip(self.run_seq[b:b + n].tolist(), self.run_handle[b:b + n].tolist(),
+                   self.run_stint_end[b:b + n].tolist())
+        return sorted(rows)
 
     # -- host-side setup (not on the tick path) ------------------------------
     def seed_inflight(self, per_model_values: dict[str, list[float]]) -> None:

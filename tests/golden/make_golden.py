@@ -20,6 +20,11 @@ Fixtures
   queue_*.npz         EngineSim STJF + aging: enqueue / iterate / complete
                       scripts and the resulting admission and queue orders
                       (engine.py:265-394)
+  e_*.npz             the engine execution clock: enqueue (with input / output
+                      tokens) / iterate / advance_to scripts on one EngineSim
+                      with prefill and decode times; completions with their
+                      finish times, admissions, the running set's stint ends,
+                      final queue, counters (engine.py:165-241)
   quantile.npz        EmpiricalQuantilePredictor on synthesize_trace(2000, 1)
                       (predictor.py:65-108) over a (wf, stage, model) grid
   synth.json          fingerprints of synthesize_trace outputs (workload.py:334-416)
@@ -773,7 +778,93 @@ def make_completions(only=None):
     return out
 
 
+# ------------------------------------------------------------- engine clock
+def run_engine_script(seed, b, S, d, p, n_pre, script):
+    """One EngineSim with decode d / prefill p ms per token. Steps: ("enq", n, dt)
+    enqueue n requests at t += dt; ("iter", n) n scheduling iterations at the
+    current clock; ("adv", dt) advance_to(t += dt)."""
+    rng = np.random.default_rng(seed)
+    prof = profiles.ModelProfile("m0", d, b, prefill_ms_per_token=p)
+    aging = engine.AgingConfig(starvation_threshold=S if S else math.inf)
+    eng = engine.EngineSim(prof, aging=aging)
+    t = 0.0
+    ordinal = 0
+    enq_log, admitted, done = [], [], []
+    orig_admit = eng._admit
+
+    def spy(entry, now):
+        admitted.append(int(entry.request.program_id[1:]))
+        return orig_admit(entry, now)
+    eng._admit = spy
+
+    def enqueue(n):
+        nonlocal ordinal
+        for _ in range(n):
+            prio = float(rng.integers(1, 400))
+            if seed % 2:
+                prio /= 3.0
+            inp = int(rng.integers(1, 3000))
+            out = int(rng.integers(1, 400))
+            rq = workload.Request(f"e{ordinal}", 1, inp, t, "wf", "x")
+            eng.enqueue(rq, priority=prio, out_tokens=out, now=t)
+            enq_log.append((ordinal, prio, t, inp, out))
+            ordinal += 1
+
+    enqueue(n_pre)
+    for step in script:
+        if step[0] == "enq":
+            t += step[2]
+            enqueue(step[1])
+        elif step[0] == "iter":
+            for _ in range(step[1]):
+                eng.scheduling_iteration(eng.now)
+        else:
+            t += step[1]
+            for c in eng.advance_to(t):
+                done.append((int(c.request.program_id[1:]), c.time))
+    order = [int(e.request.program_id[1:]) for e in sorted(eng._queued.values(),
+                                                             key=lambda e: e.sort_key())]
+    lv = {int(e.request.program_id[1:]): (e.starvation_level, e.starvation_count)
+          for e in eng._queued.values()}
+    running = [(s, int(rr.entry.request.program_id[1:]), rr.stint_end)
+               for s, rr in sorted(eng.running.items())]
+    return dict(enq=np.array(enq_log, dtype=np.float64), admitted=np.array(admitted),
+                done=np.array(done, dtype=np.float64).reshape(-1, 2),
+                order=np.array(order), level=np.array([lv[o][0] for o in order]),
+                count=np.array([lv[o][1] for o in order]),
+                running=np.array(running, dtype=np.float64).reshape(-1, 3),
+                now=eng.now, tokens=eng.tokens_emitted_total, served=eng.requests_served,
+                iterations=eng.iterations)
+
+
+def make_engines():
+    scripts = {
+        "e_basic": (11, 4, 8, 0.75, 0.02, 20,
+                    [("adv", 50.0), ("iter", 2), ("enq", 10, 1.0), ("adv", 200.0),
+                     ("adv", 150.0)]),
+        "e_nondyadic": (12, 3, 3, 1.0 / 3.0, 0.013, 40,
+                        [("adv", 30.0), ("enq", 7, 0.5), ("adv", 95.25), ("iter", 3),
+                         ("adv", 400.0), ("enq", 12, 0.0), ("adv", 2500.0)]),
+        "e_noaging": (13, 2, 0, 1.5, 0.0, 15,
+                      [("adv", 100.0), ("enq", 5, 2.0), ("adv", 700.0), ("adv", 5000.0)]),
+        "e_big": (15, 32, 8, 0.05, 0.001, 600,
+                  [("adv", 5.0), ("adv", 20.0), ("enq", 200, 0.0), ("iter", 4), ("adv", 60.0),
+                   ("adv", 150.0), ("enq", 50, 0.0), ("adv", 40.0)]),
+        "e_S1": (17, 2, 1, 2.0, 0.5, 25, [("adv", 800.0), ("iter", 3), ("adv", 3000.0)]),
+    }
+    out = {}
+    for name, (seed, b, S, d, p, n_pre, script) in scripts.items():
+        res = run_engine_script(seed, b, S, d, p, n_pre, script)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), seed=seed, b=b, S=S, d=d, p=p,
+                            n_pre=n_pre, script=json.dumps(script), **res)
+        out[name] = (len(res["done"]), len(res["order"]), len(res["running"]))
+    return out
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["engines"]:
+        print("engines:", make_engines())
+        sys.exit(0)
     if sys.argv[1:] == ["completions"]:
         print("completions:", make_completions())
         sys.exit(0)
@@ -782,6 +873,7 @@ if __name__ == "__main__":
     print("schedule:", make_schedules())
     print("errors:", make_errors())
     make_queues()
+    print("engines:", make_engines())
     make_quantile()
     make_synth()
     print("trace programs:", make_trace())

@@ -250,3 +250,19 @@ def run_port_queue(qd):
                 level=np.array([e.level for e in eng.queue_order()]),
                 count=np.array([e.count for e in eng.queue_order()]),
                 running=eng.running_count, iterations=eng.iterations)
+
+
+# ------------------------------------------------------------ engine clock
+def engine_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "e_*.npz")))
+
+
+def load_engine(name):
+    z = np.load(os.path.join(GOLDEN, f"{name}.npz"), allow_pickle=False)
+    d = {k: z[k] for k in z.files}
+    d["script"] = json.loads(str(d["script"]))
+    for k in ("seed", "b", "S", "n_pre", "tokens", "served", "iterations"):
+        d[k] = int(d[k])
+    for k in ("d", "p", "now"):
+        d[k] = float(d[k])
+    return d
