@@ -257,6 +257,23 @@ class GpuScheduler:
             _p(self.buf.error), s.cuda_stream), "chm_monitor_note_progress")
         self._keep = (m, k, e)  # alive until the stream has consumed them
 
+    def scheduling_iteration(self, n_iterations: int = 1, stream=None) -> None:
+        """EngineSim.scheduling_iteration on every engine, n times, with no new
+        arrivals (engine.py:160-163): chm_queue_tick on an empty batch, at
+        each engine's current clock. Admissions go to `state.admitted(m)`."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st, buf = self.state, self.buf
+        rows_c = _lib.Rows(0, None, None, None, None, None, None)
+        with torch.cuda.stream(s):
+            buf.error.copy_(buf.error_init)
+            buf.n_committed.zero_()
+            st.q_n_admitted.zero_()
+            st.q_n_promoted.zero_()
+            _lib.check(self.lib.chm_queue_tick(st.pool_c, self.aging_c, st.monitor_c,
+                                               st.queue_c, rows_c,
+                                               buf.decisions_struct(False), int(n_iterations),
+                                               _p(buf.error), s.cuda_stream), "chm_queue_tick")
+
     # -- engine execution clock (SURVEY §8f row 3) ----------------------------
     def advance_to(self, target, stream=None, keep_completions: bool = False):
         """EngineSim.advance_to(target) on every engine (engine.py:174-183):
