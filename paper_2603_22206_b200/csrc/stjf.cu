@@ -268,6 +268,54 @@ __global__ void candidates_kernel(QueueParams prm, chm_monitor_state mon, chm_qu
   }
 }
 
+// Engine clock, one warp: the running request with the smallest
+// (stint_end, seq) ends if stint_end <= target (advance_to, engine.py:174-183):
+// lane 0 records the completion (_finish_stint + _on_stint_end, 229-239,
+// 396-407) and moves the last entry into its slot. Returns 1 when a stint
+// ended (bt = its end), 0 when none is due, 2 on a clock violation.
+__device__ int finish_next_stint(const chm_engine_run& er, int m, size_t rb, int n_run, int lane,
+                                 double tgt, double clock, int32_t* err, double& bt_out) {
+  double bt = 0;
+  long long bs = LLONG_MAX;
+  int bj = -1;
+  for (int j = lane; j < n_run; j += 32) {
+    const double te = er.stint_end[rb + j];
+    const long long sq = er.seq[rb + j];
+    if (bj < 0 || te < bt || (te == bt && sq < bs)) { bt = te; bs = sq; bj = j; }
+  }
+  for (int off = 16; off; off >>= 1) {
+    const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
+    const long long os = __shfl_xor_sync(0xffffffffu, bs, off);
+    const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+    if (oj >= 0 && (bj < 0 || ot < bt || (ot == bt && os < bs))) { bt = ot; bs = os; bj = oj; }
+  }
+  bt_out = bt;
+  if (bj < 0 || !(bt <= tgt)) return 0;
+  if (bt < clock - 1e-9) {  // _finish_stint -> _advance_clock (engine.py:140-143, 233)
+    if (lane == 0) report_error(err, CHM_ERR_TIME_BACKWARDS, 0, m, 1);
+    return 2;
+  }
+  if (lane == 0) {
+    const int nd = er.n_done[m];
+    if (nd < er.done_capacity) {
+      er.done_handle[(size_t)m * er.done_capacity + nd] = er.handle[rb + bj];
+      er.done_time[(size_t)m * er.done_capacity + nd] = bt;
+      er.n_done[m] = nd + 1;
+    } else {
+      report_error(err, CHM_ERR_CAPACITY, 0, m, nd);
+    }
+    er.tokens_emitted[m] += er.stint_tokens[rb + bj];
+    er.served[m] += 1;
+    const size_t last = rb + n_run - 1, at = rb + bj;
+    er.handle[at] = er.handle[last];
+    er.seq[at] = er.seq[last];
+    er.stint_end[at] = er.stint_end[last];
+    er.decode_start[at] = er.decode_start[last];
+    er.stint_tokens[at] = er.stint_tokens[last];
+  }
+  return 1;
+}
+
 // mode 0: completions (R = n_complete[m], each frees one running slot first)
 // mode 1: tick (append queued rows, then R = n_iterations explicit iterations)
 // mode 2: one iteration with a cross-GPU admission merge (MergeArgs)
@@ -409,7 +457,164 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
   const int n_adm0 = q.n_admitted[m];
   int n_adm = 0, n_prom = 0;
 
-  if (R > 0) {
+  if (R > 0 && prm.demote) {
+    // ---- generic iterations (demote_while_queued, engine.py:340-374): a
+    // promoted entry's quantum runs per entry, so equal-count entries no
+    // longer age in lock step. Per admission a block-wide argmin of the live
+    // entries' keys; aging per entry, in place. ----
+    Idx* flag = k.b;  // 1 = admitted this call
+    for (int i = tid; i < n; i += blockDim.x) flag[i] = 0;
+    __shared__ int gen_e[kQWarps];
+    __shared__ int gen_l[kQWarps];
+    __shared__ unsigned long long gen_p[kQWarps], gen_a[kQWarps];
+    __shared__ double gen_t;
+    __shared__ int gen_prom;
+    if (tid == 0) gen_prom = 0;
+    __syncthreads();
+    int remaining = n;
+    const size_t rb = (size_t)m * (track ? er.capacity : 0);
+    auto less = [](int l1, unsigned long long p1, unsigned long long a1, int e1, int l2,
+                   unsigned long long p2, unsigned long long a2, int e2) {
+      if (e2 < 0) return e1 >= 0;
+      if (e1 < 0) return false;
+      if (l1 != l2) return l1 < l2;
+      if (p1 != p2) return p1 < p2;
+      if (a1 != a2) return a1 < a2;
+      return e1 < e2;
+    };
+    for (int r = 0; r < R; ++r) {
+      double t_iter = clock;
+      if (mode == 3) {
+        if (warp == 0) {
+          double bt;
+          const int st3 = finish_next_stint(er, m, rb, n_run, lane, tgt, clock, err, bt);
+          if (lane == 0) { s.misc[6] = st3; gen_t = bt; }
+        }
+        __syncthreads();
+        const int st3 = s.misc[6];
+        const double bt = gen_t;
+        __syncthreads();
+        if (st3 != 1) break;
+        --n_run;
+        run = max(run - 1, 0);
+        clock = bt;
+        t_iter = bt;
+      }
+      ++iters;
+      if (mode == 0) run = max(run - 1, 0);
+      if (mode == 2) run = max(run - rel, 0);
+      const int a = mode == 2 ? min(a_local, remaining) : max(0, min(bmax - run, remaining));
+      for (int t = 0; t < a; ++t) {
+        int bl = 0, be = -1;
+        unsigned long long bp = 0, ba = 0;
+        for (int i = tid; i < n; i += blockDim.x) {
+          if (flag[i]) continue;
+          const int l = lvl_g[i];
+          const unsigned long long pk = k.prio[i];
+          const unsigned long long av = use_arr ? f64_key(arr_g[i]) : 0ull;
+          if (less(l, pk, av, i, bl, bp, ba, be)) { bl = l; bp = pk; ba = av; be = i; }
+        }
+        for (int off = 16; off; off >>= 1) {
+          const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+          const unsigned long long op = __shfl_xor_sync(0xffffffffu, bp, off);
+          const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ba, off);
+          const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+          if (less(ol, op, oa, oe, bl, bp, ba, be)) { bl = ol; bp = op; ba = oa; be = oe; }
+        }
+        if (lane == 0) { gen_l[warp] = bl; gen_p[warp] = bp; gen_a[warp] = ba; gen_e[warp] = be; }
+        __syncthreads();
+        if (warp == 0) {
+          bl = gen_l[lane]; bp = gen_p[lane]; ba = gen_a[lane]; be = gen_e[lane];
+          for (int off = 16; off; off >>= 1) {
+            const int ol = __shfl_xor_sync(0xffffffffu, bl, off);
+            const unsigned long long op = __shfl_xor_sync(0xffffffffu, bp, off);
+            const unsigned long long oa = __shfl_xor_sync(0xffffffffu, ba, off);
+            const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+            if (less(ol, op, oa, oe, bl, bp, ba, be)) { bl = ol; bp = op; ba = oa; be = oe; }
+          }
+          if (lane == 0) {
+            flag[be] = 1;
+            q.admitted[seg + n_adm0 + n_adm + t] = handle_g[be];
+            if (track && !run_admit(er, m, n_run + t, handle_g[be], seq_g[be], out_g[be],
+                                    qin_g[be], t_iter, prm.d[m]))
+              report_error(err, CHM_ERR_CAPACITY, 0, m, n_run + t);
+          }
+        }
+        __syncthreads();
+      }
+      n_adm += a;
+      remaining -= a;
+      run += mode == 2 ? a_global : a;
+      if (track) n_run += a;
+      if (prm.aging_enabled && remaining > 0) {
+        int np = 0;
+        for (int i = tid; i < n; i += blockDim.x) {
+          if (flag[i]) continue;
+          const int c2 = cnt_g[i] + 1;
+          if (c2 >= prm.S) {  // promote
+            cnt_g[i] = 0;
+            lvl_g[i] -= 1;
+            qnt_g[i] = 0;
+            ++np;
+          } else {
+            cnt_g[i] = c2;
+            if (lvl_g[i] < 0) {  // demote_while_queued
+              const int q2 = qnt_g[i] + 1;
+              if (q2 >= prm.Q) {
+                qnt_g[i] = 0;
+                lvl_g[i] += 1;
+              } else {
+                qnt_g[i] = q2;
+              }
+            }
+          }
+        }
+        for (int off = 16; off; off >>= 1) np += __shfl_xor_sync(0xffffffffu, np, off);
+        if (lane == 0 && np) atomicAdd(&gen_prom, np);
+      }
+      __syncthreads();
+    }
+    n_prom = gen_prom;
+    // ---- compact survivors in seq (storage) order ----
+    int out_base = 0;
+    for (int blk = 0; blk < n; blk += blockDim.x) {
+      const int i = blk + tid;
+      const bool keep = i < n && !flag[i];
+      double pr = 0, ar = 0;
+      int64_t sq = 0, hd = 0;
+      int ot = 0, lv = 0, ct = 0, qn = 0, in = 0;
+      if (keep) {
+        pr = prio_g[i]; ar = arr_g[i]; sq = seq_g[i]; hd = handle_g[i]; ot = out_g[i];
+        lv = lvl_g[i]; ct = cnt_g[i]; qn = qnt_g[i];
+        if (track) in = qin_g[i];
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) s.scan[warp] = __popc(bal);
+      __syncthreads();
+      if (warp == 0) {
+        int v = s.scan[lane], incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        s.scan[lane] = incl - v;
+        if (lane == 31) s.misc[6] = incl;
+      }
+      __syncthreads();
+      if (keep) {
+        const int pos = out_base + s.scan[warp] + __popc(bal & ((1u << lane) - 1u));
+        prio_g[pos] = pr; arr_g[pos] = ar; seq_g[pos] = sq; handle_g[pos] = hd;
+        out_g[pos] = ot; lvl_g[pos] = lv; cnt_g[pos] = ct; qnt_g[pos] = qn;
+        if (track) qin_g[pos] = in;
+        k.prio[pos] = f64_key(pr);
+        k.lvl[pos] = (uint16_t)(lv + 32768);
+        k.cnt[pos] = (uint16_t)min(max(ct, 0), 65535);
+      }
+      out_base += s.misc[6];
+      __syncthreads();
+    }
+    n = out_base;
+  } else if (R > 0) {
     // ---- sort by (count, level, priority[, arrival]) and form count groups ----
     const int srcs[4] = {0, 1, 2, 3};
     Idx *sorted, *spare;
@@ -460,44 +665,9 @@ __global__ void __launch_bounds__(kQThreads, 1) queue_kernel(
         double t_iter = clock;
         if (mode == 3) {
           // next stint end: min (stint_end, seq) of the running set (engine.py:178-183)
-          double bt = 0;
-          long long bs = LLONG_MAX;
-          int bj = -1;
-          for (int j = lane; j < n_run; j += 32) {
-            const double te = er.stint_end[rb + j];
-            const long long sq = er.seq[rb + j];
-            if (bj < 0 || te < bt || (te == bt && sq < bs)) { bt = te; bs = sq; bj = j; }
-          }
-          for (int off = 16; off; off >>= 1) {
-            const double ot = __shfl_xor_sync(0xffffffffu, bt, off);
-            const long long os = __shfl_xor_sync(0xffffffffu, bs, off);
-            const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
-            if (oj >= 0 && (bj < 0 || ot < bt || (ot == bt && os < bs))) { bt = ot; bs = os; bj = oj; }
-          }
-          if (bj < 0 || !(bt <= tgt)) break;
-          if (bt < clock - 1e-9) {  // _finish_stint -> _advance_clock (engine.py:140-143, 233)
-            if (lane == 0) report_error(err, CHM_ERR_TIME_BACKWARDS, 0, m, 1);
-            break;
-          }
-          if (lane == 0) {
-            // _finish_stint (engine.py:229-239) + EngineSim._on_stint_end
-            const int nd = er.n_done[m];
-            if (nd < er.done_capacity) {
-              er.done_handle[(size_t)m * er.done_capacity + nd] = er.handle[rb + bj];
-              er.done_time[(size_t)m * er.done_capacity + nd] = bt;
-              er.n_done[m] = nd + 1;
-            } else {
-              report_error(err, CHM_ERR_CAPACITY, 0, m, nd);
-            }
-            er.tokens_emitted[m] += er.stint_tokens[rb + bj];
-            er.served[m] += 1;
-            const size_t last = rb + n_run - 1, at = rb + bj;
-            er.handle[at] = er.handle[last];
-            er.seq[at] = er.seq[last];
-            er.stint_end[at] = er.stint_end[last];
-            er.decode_start[at] = er.decode_start[last];
-            er.stint_tokens[at] = er.stint_tokens[last];
-          }
+          double bt;
+          const int st3 = finish_next_stint(er, m, rb, n_run, lane, tgt, clock, err, bt);
+          if (st3 != 1) break;
           __syncwarp();
           --n_run;
           run = max(run - 1, 0);
@@ -667,7 +837,11 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
   if (K < 1 || K > CHM_MAX_MODELS || q->capacity < 1) return CHM_ERR_INVALID_ARG;
   if (aging->enabled && (aging->starvation_threshold < 1 || aging->starvation_threshold > 65535))
     return CHM_ERR_UNSUPPORTED;
-  if (aging->enabled && aging->demote_while_queued) return CHM_ERR_UNSUPPORTED;
+  // demote_while_queued: the generic per-entry path (not on the grid-wide one)
+  if (aging->enabled && aging->demote_while_queued && q->capacity > kQHuge)
+    return CHM_ERR_UNSUPPORTED;
+  if (aging->enabled && aging->demote_while_queued && aging->running_quantum < 1)
+    return CHM_ERR_INVALID_ARG;
   const bool big = q->capacity > kQMax;
   if (big && !q->scratch) return CHM_ERR_INVALID_ARG;
   const bool huge = q->capacity > kQHuge;
@@ -692,6 +866,8 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
     return CHM_ERR_INVALID_ARG;
   }
   prm.S = aging->starvation_threshold;
+  prm.Q = aging->running_quantum;
+  prm.demote = aging->enabled && aging->demote_while_queued;
   prm.cap_limit = big ? 0x7fffffff : kQMax;
   chm_rows r{};
   chm_decisions d{};

@@ -14,6 +14,8 @@ struct QueueParams {
   double d[CHM_MAX_MODELS];  // decode_ms_per_token (engine clock)
   int aging_enabled;
   int S;
+  int Q;       // running_quantum
+  int demote;  // AgingConfig.demote_while_queued
   int cap_limit;  // largest segment this kernel variant can hold
 };
 

@@ -344,13 +344,14 @@ def make_errors():
 
 
 # ------------------------------------------------------------------ queues
-def run_queue_script(seed, b, S, n_pre, script):
+def run_queue_script(seed, b, S, n_pre, script, Q=4, demote=False):
     """Drive one EngineSim. `script` is a list of ("enq", n) / ("iter", n) /
     ("complete", n) steps. Returns admission order and final queue order as
     lists of request ordinals, plus the queued entries' (level, count)."""
     rng = np.random.default_rng(seed)
     prof = profiles.ModelProfile("m0", 1.0, b)
-    aging = engine.AgingConfig(starvation_threshold=S if S else math.inf)
+    aging = engine.AgingConfig(starvation_threshold=S if S else math.inf, running_quantum=Q,
+                               demote_while_queued=demote)
     eng = engine.EngineSim(prof, aging=aging)
     t = 0.0
     ordinal = 0
@@ -406,7 +407,7 @@ def run_queue_script(seed, b, S, n_pre, script):
                 iterations=eng.iterations)
 
 
-def make_queues():
+def make_queues(only=None):
     scripts = {
         "q_basic": (1, 4, 8, 20, [("iter", 3), ("enq", 10), ("iter", 2)]),
         "q_promote": (2, 2, 3, 12, [("iter", 4), ("enq", 5), ("iter", 5)]),
@@ -418,9 +419,24 @@ def make_queues():
         "q_S1": (6, 2, 1, 30, [("iter", 3), ("complete", 2), ("iter", 2)]),
     }
     for name, (seed, b, S, n_pre, script) in scripts.items():
+        if only is not None and name not in only:
+            continue
         res = run_queue_script(seed, b, S, n_pre, script)
         np.savez_compressed(os.path.join(OUT, f"{name}.npz"), seed=seed, b=b, S=S, n_pre=n_pre,
                             script=json.dumps(script), **res)
+    # AgingConfig.demote_while_queued (engine.py:360-374): promoted entries that
+    # stay queued lose a level every Q further iterations
+    demote = {
+        "q_demote": (7, 3, 2, 2, 30, [("iter", 6), ("complete", 2), ("enq", 6), ("iter", 5)]),
+        "q_demote_big": (8, 16, 3, 3, 1500, [("iter", 9), ("complete", 16), ("enq", 100),
+                                              ("iter", 7), ("complete", 5), ("iter", 4)]),
+    }
+    for name, (seed, b, S, Q, n_pre, script) in demote.items():
+        if only is not None and name not in only:
+            continue
+        res = run_queue_script(seed, b, S, n_pre, script, Q=Q, demote=True)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), seed=seed, b=b, S=S, n_pre=n_pre,
+                            Q=Q, demote=1, script=json.dumps(script), **res)
 
 
 # ---------------------------------------------------------------- quantile
@@ -862,6 +878,9 @@ def make_engines():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["queues"]:
+        make_queues(sys.argv[2:] or None)
+        sys.exit(0)
     if sys.argv[1:] == ["engines"]:
         print("engines:", make_engines())
         sys.exit(0)

@@ -215,6 +215,8 @@ def load_queue(name):
     d["script"] = json.loads(str(d["script"]))
     for k in ("seed", "b", "S", "n_pre", "running", "iterations"):
         d[k] = int(d[k])
+    d["Q"] = int(d["Q"]) if "Q" in d else 4
+    d["demote"] = bool(int(d["demote"])) if "demote" in d else False
     return d
 
 
@@ -222,7 +224,8 @@ def run_port_queue(qd):
     """Replay a golden queue script on the oracle port engine."""
     import math
     S = qd["S"] if qd["S"] else math.inf
-    eng = hp.PortEngine(qd["b"], starvation_threshold=S)
+    eng = hp.PortEngine(qd["b"], starvation_threshold=S, running_quantum=qd["Q"],
+                        demote_while_queued=qd["demote"])
     enq = qd["enq"]
     pos = 0
     t = 0.0

@@ -22,7 +22,9 @@ def replay_on_gpu(qd, capacity=10240):
     pool = Pool((ModelProfile("m0", 1.0, qd["b"]),))
     rt, pr = ScoreTableRouter(), PrecomputedPredictor()
     enq = qd["enq"]
-    gs = GpuScheduler(pool, BalancerConfig(), AgingConfig(starvation_threshold=S), router=rt,
+    aging = AgingConfig(starvation_threshold=S, running_quantum=qd["Q"],
+                        demote_while_queued=qd["demote"])
+    gs = GpuScheduler(pool, BalancerConfig(), aging, router=rt,
                       predictor=pr, n_programs=len(enq) + 1, max_rows=max(len(enq), 1),
                       queue_capacity=capacity)
     dev = gs.device
@@ -71,6 +73,8 @@ def replay_on_gpu(qd, capacity=10240):
 @pytest.mark.parametrize("name", H.queue_names())
 def test_queue_matches_reference(name, capacity):
     qd = H.load_queue(name)
+    if qd["demote"] and capacity > (1 << 18):
+        pytest.skip("demote_while_queued runs on the per-engine paths only")
     res = replay_on_gpu(qd, capacity)
     np.testing.assert_array_equal(res["admitted"], qd["admitted"])
     np.testing.assert_array_equal(res["order"], qd["order"])

@@ -41,7 +41,9 @@ def replay_sharded(qd, G, capacity=10240):
     shards = []
     for _ in range(G):
         rt, pr = ScoreTableRouter(), PrecomputedPredictor()
-        gs = GpuScheduler(pool, BalancerConfig(), AgingConfig(starvation_threshold=S), router=rt,
+        aging = AgingConfig(starvation_threshold=S, running_quantum=qd["Q"],
+                            demote_while_queued=qd["demote"])
+        gs = GpuScheduler(pool, BalancerConfig(), aging, router=rt,
                           predictor=pr, n_programs=len(enq) + 1, max_rows=max(len(enq), 1),
                           queue_capacity=capacity)
         shards.append((gs, rt, pr))
