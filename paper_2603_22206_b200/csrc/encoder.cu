@@ -147,8 +147,7 @@ __global__ void __launch_bounds__(160, 4)
     attention_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
                      __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ uint8_t smem_raw[];
-  AttnSmem& s = *reinterpret_cast<AttnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  AttnSmem& s = sm100::align_smem_1024<AttnSmem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int item = blockIdx.x;
   const int seq = item / n_heads, h = item - seq * n_heads;
@@ -294,8 +293,7 @@ __global__ void __launch_bounds__(160, 1)
     attention_long_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
                           int S, __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ uint8_t smem_raw[];
-  AttnLongSmem& s = *reinterpret_cast<AttnLongSmem*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  AttnLongSmem& s = sm100::align_smem_1024<AttnLongSmem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int n_qb = S / kAttnS, n_kb = S / kAttnS;
   const int item = blockIdx.x;
@@ -494,8 +492,7 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
                            int S, int n_items, __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ uint8_t smem_raw[];
-  FlashSmem& s = *reinterpret_cast<FlashSmem*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  FlashSmem& s = sm100::align_smem_1024<FlashSmem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int n_kb = S / kAttnS;
   const int n_qp = S / (2 * kAttnS);

@@ -178,8 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Smem = SmemT<kStages, kBoxes, kLN>;
   const int ln_groups = kLN ? N / BN : 1;
   extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                     ~uintptr_t(1023));
+  Smem& s = sm100::align_smem_1024<Smem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
   const uint32_t px = rank & 1;          // position in the pair (M half)

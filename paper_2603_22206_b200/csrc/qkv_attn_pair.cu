@@ -102,8 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               int n_seq, int n_heads, int hidden,
                               __nv_bfloat16* __restrict__ ctx, int lag, int dbg) {
   extern __shared__ uint8_t smem_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                     ~uintptr_t(1023));
+  Smem& s = sm100::align_smem_1024<Smem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int k_blocks = hidden / 64;
   const uint32_t px = sm100::cluster_ctarank() & 1;

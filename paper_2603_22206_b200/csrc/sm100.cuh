@@ -97,6 +97,16 @@ __device__ __forceinline__ int warp_id() {
   return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
 }
 
+// 1024-byte aligned view of the dynamic shared memory. The offset is added to
+// the shared pointer itself (not through uintptr_t), so the compiler keeps the
+// shared address space: STS / LDS instead of generic ST.E / LD.E, which pay
+// the generic-to-shared resolution on every access.
+template <typename T>
+__device__ __forceinline__ T& align_smem_1024(uint8_t* raw) {
+  const uint32_t pad = (1024u - (smem_u32(raw) & 1023u)) & 1023u;
+  return *reinterpret_cast<T*>(raw + pad);
+}
+
 // A value every lane holds (e.g. the TMEM base read back from shared memory),
 // made provably warp-uniform so tcgen05 operands derived from it live in
 // uniform registers.
