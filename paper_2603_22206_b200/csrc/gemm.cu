@@ -326,6 +326,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::tma_load_2d(s.stage_out[ew][c], &tmap_r, &s.res_bar[ew][c], n_tile0 + c * 64,
                                mrow0);
           }
+          // the next tile's residual rows into L2 now, so its loads do not wait
+          // on HBM when the epilogue is the critical path (out-proj: tensor
+          // pipe 48 -> 52 % per cycle, tools/experiments/res_prefetch_l2.sh)
+          const int tn = t + n_cl;
+          if (tn < n_tiles) {
+            const int mrow_n = (tn / n_tiles_n) * BM + (int)px * CM + quarter * 32;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) sm100::tma_prefetch_2d(&tmap_r, n_tile0 + c * 64, mrow_n);
+          }
         }
         __syncwarp();
         sm100::mbar_wait(&s.tmem_full[acc], acc_phase);
@@ -459,6 +468,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sm100::tma_load_2d(s.stage_out[ew][c], &tmap_r, &s.res_bar[ew][c],
                                    n_tile0 + c * 64, mrow0);
               }
+            }
+            // the next tile's residual boxes into L2 (see the LN epilogue)
+            const int tn = t + n_cl;
+            if (tn < n_tiles) {
+              const int mrow_n = (tn / n_tiles_n) * BM + (int)px * CM + quarter * 32;
+              const int ncol_n = (tn % n_tiles_n) * BN + half * 128;
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                if (ncol_n + c * 64 < N) sm100::tma_prefetch_2d(&tmap_r, ncol_n + c * 64, mrow_n);
             }
           }
           __syncwarp();
