@@ -182,11 +182,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           if (sm100::elect_one()) {
-          sm100::mbar_arrive_expect_tx(&s.full[stage], kStageBytes);
+          // (dbg 14 / 15: full kernel, but only x / only W is loaded -- an
+          // operand-traffic probe; results are garbage)
+          sm100::mbar_arrive_expect_tx(&s.full[stage], dbg == 14   ? kATile
+                                                       : dbg == 15 ? kStageBytes - kATile
+                                                                   : kStageBytes);
           uint8_t* st = s.stages[stage];
-          sm100::tma_load_2d_mc(st + cj * kARows * 128, &tm_x, &s.full[stage], kb * 64, a_row,
-                                row_mask);
-          if constexpr (TS || CS != 2) {
+          if (dbg != 15)
+            sm100::tma_load_2d_mc(st + cj * kARows * 128, &tm_x, &s.full[stage], kb * 64, a_row,
+                                  row_mask);
+          if (dbg == 14) {
+          } else if constexpr (TS || CS != 2) {
 #pragma unroll
             for (int bb = 0; bb < kBoxes; ++bb) {
               const int b = ci * kBoxes + bb;  // box of the head's 6: part b/2, half b%2
