@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(160, 4)
         __align__(16) __nv_bfloat162 o[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
-          const float p1 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
+          const float p0 = sm100::ex2_approx(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
+          const float p1 = sm100::ex2_approx(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
           o[e] = __floats2bfloat162_rn(p0, p1);
           // accumulate the bf16-rounded values so the normaliser matches P
           const float2 back = __bfloat1622float2(o[e]);
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(160, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(raw[j]));
       }
-      const float alpha = exp2f((m_run - mx) * kLog2e);  // 0 on the first block
+      const float alpha = sm100::ex2_approx((m_run - mx) * kLog2e);  // 0 on the first block
       const float mxl = mx * kLog2e;
       float sum = 0.f;
       // P of the previous block may still be read by its P.V MMA
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(160, 1)
           __align__(16) __nv_bfloat162 pv[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float p0 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
-            const float p1 = exp2f(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
+            const float p0 = sm100::ex2_approx(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -mxl));
+            const float p1 = sm100::ex2_approx(fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -mxl));
             pv[e] = __floats2bfloat162_rn(p0, p1);
             const float2 back = __bfloat1622float2(pv[e]);
             sum += back.x + back.y;

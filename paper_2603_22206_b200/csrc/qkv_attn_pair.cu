@@ -351,9 +351,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float p0 =
-              exp2f(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e]), kLog2e, -mxl));
+              sm100::ex2_approx(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e]), kLog2e, -mxl));
           const float p1 =
-              exp2f(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e + 1]), kLog2e, -mxl));
+              sm100::ex2_approx(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e + 1]), kLog2e, -mxl));
           pv[e] = __floats2bfloat162_rn(p0, p1);
           const float2 back = __bfloat1622float2(pv[e]);
           sum += back.x + back.y;
