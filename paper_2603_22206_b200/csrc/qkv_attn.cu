@@ -60,13 +60,18 @@ constexpr uint32_t kWBox = 32;                 // W rows per TMA box (6 per head
 constexpr uint32_t kHeadTile = kS * 64 * 2;    // Q/K/V [128][64] bf16, 16 KB
 constexpr uint32_t kAccCols = 192;
 constexpr uint32_t kSCol = 384;
+constexpr int kPairStages = 5;  // PAIR ring depth (28 KB stages)
 
 struct __align__(1024) Smem {
+  // the operand ring: 4 x 40 KB (cta_group::1) or kPairStages x 28 KB (PAIR)
   uint8_t stages[kStages][kStageBytes];
-  uint8_t qkv[3][kHeadTile];  // Q, K, V; P key halves [0,64) / [64,128) overwrite Q / K
+  uint8_t stages_pair_extra[kPairStages * (kATile + kBTile / 2) > kStages * kStageBytes
+                                ? kPairStages * (kATile + kBTile / 2) - kStages * kStageBytes
+                                : 1];
+  alignas(1024) uint8_t qkv[3][kHeadTile];  // Q, K, V; P key halves [0,64) / [64,128) overwrite Q / K
   float red_max[2][kS];
   float red_sum[2][kS];
-  uint64_t full[kStages], empty[kStages], kdone[kStages];
+  uint64_t full[8], empty[8], kdone[8];
   uint64_t acc_full[2], acc_empty[2];
   uint64_t qkv_ready, s_full, p_ready, o_full;
   uint32_t tmem_base;
@@ -99,7 +104,12 @@ __device__ __forceinline__ void epi_sync() {
 // S = Q K^T and O = P V MMAs read their A operand from TMEM (tcgen05.mma
 // [d], [a_tmem], b_desc), saving the Q and P shared-memory round trips
 // (96 KB per item) of a kernel bound by shared-memory traffic.
-template <int CS, int CH, bool FOLD, bool TS>
+// PAIR (CS = 2, CH = 1): the projection is one cta_group::2 pair MMA per
+// k-block (M = 256 = the two sequences, N = 192 split 96 / 96: each CTA stages
+// its own x tile and half of the head's W rows, 28 KB instead of 40 KB, in
+// kPairStages stages), issued by the leader into both CTAs' TMEM; each CTA runs its own
+// sequence's S and O as cta_group::1 MMAs (tools/cta_group_mix_probe.cu).
+template <int CS, int CH, bool FOLD, bool TS, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     qkv_attention_kernel(const __grid_constant__ CUtensorMap tm_x,
                          const __grid_constant__ CUtensorMap tm_w,
@@ -112,6 +122,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int k_blocks = hidden / 64;
   const uint32_t rank = sm100::cluster_ctarank();
+  static_assert(!PAIR || (CS == 2 && CH == 1 && !TS), "pair projection: 2 sequences, one head");
+  constexpr int NST = PAIR ? kPairStages : kStages;                // ring stages
+  constexpr uint32_t SB = PAIR ? kATile + kBTile / 2 : kStageBytes;  // bytes per stage (per CTA)
+  const bool leader = !PAIR || rank == 0;
+  auto stage_ptr = [&](int i) { return &s.stages[0][0] + (size_t)i * SB; };
   const int ci = (int)rank / CH, cj = (int)rank % CH;
   const uint16_t row_mask = (uint16_t)(((1u << CH) - 1) << (ci * CH));  // same sequence
   uint16_t col_mask = 0;                                                 // same head
@@ -139,14 +154,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tm_x);
     sm100::tma_prefetch(&tm_w);
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < NST; ++i) {
       sm100::mbar_init(&s.full[i], 1);
-      sm100::mbar_init(&s.empty[i], CS + CH - 1);  // consumers of this CTA's slices
+      sm100::mbar_init(&s.empty[i], PAIR ? 1 : CS + CH - 1);  // consumers of this CTA's slices
       sm100::mbar_init(&s.kdone[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&s.acc_full[i], 1);
-      sm100::mbar_init(&s.acc_empty[i], 256);
+      sm100::mbar_init(&s.acc_empty[i], PAIR ? 2 * 8 : 256);  // PAIR: epilogue warps of both CTAs
     }
     sm100::mbar_init(&s.qkv_ready, 256);
     sm100::mbar_init(&s.s_full, 1);
@@ -154,7 +169,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&s.o_full, 1);
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      sm100::tmem_alloc_cg2<512>(&s.tmem_base);
+    else
+      sm100::tmem_alloc<512>(&s.tmem_base);
+  }
   sm100::tc_fence_before();
   sm100::cluster_sync();
   sm100::tc_fence_after();
@@ -175,6 +195,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < k_blocks; ++kb) {
           // every sharer of this stage has consumed its previous contents
           sm100::mbar_wait(&s.empty[stage], phase ^ 1);
+          if constexpr (PAIR) {
+            // own x tile + own half of the head's W rows (Q|K|V rows
+            // [32 ci, +32) of each part), both signalling the leader's barrier
+            if (sm100::elect_one()) {
+              if (leader) sm100::mbar_arrive_expect_tx(&s.full[stage], 2 * SB);
+              const uint32_t full_leader = sm100::mapa(sm100::smem_u32(&s.full[stage]), 0);
+              uint8_t* st = stage_ptr(stage);
+              sm100::tma_load_2d_cg2(st, &tm_x, full_leader, kb * 64, a_row);
+              sm100::tma_load_3d_cg2(st + kATile, &tm_w, full_leader, kb * 64, h * 64 + ci * 32, 0);
+            }
+            __syncwarp();
+            if (lane == 0 && (kb == 0 || kb == k_blocks - 1)) stamp(dbg, ctx, it, kb == 0 ? 11 : 12);
+            if (++stage == NST) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (dbg >= 4 && dbg <= 10) {  // measurement: no operand loads (MMAs on stale smem)
             if (lane == 0) sm100::mbar_arrive(&s.full[stage]);
             __syncwarp();
@@ -233,6 +268,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int g = 0;  // projection k-blocks issued so far
       auto gemm_kb = [&](int it, int kb) {
+        if constexpr (PAIR) {
+          // leader: one pair MMA group into both CTAs' accumulators
+          sm100::mbar_wait(&s.full[stage], phase);
+          sm100::tc_fence_after();
+          const uint32_t a = sm100::smem_u32(stage_ptr(stage));
+          const uint32_t b = a + kATile;
+          const uint32_t d = tmem + (uint32_t)(it & 1) * kAccCols;
+          constexpr uint32_t idesc_p = sm100::umma_idesc_bf16(256, 192);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            sm100::mma_bf16_cg2_w(d, sm100::umma_desc_sw128(a + k * 32),
+                                  sm100::umma_desc_sw128(b + k * 32), idesc_p, (kb | k) != 0);
+          sm100::mma_commit_cg2_mc_w(&s.empty[stage], 0x3);
+          if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc_w(&s.acc_full[it & 1], 0x3);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+          return;
+        }
         if (lag > 0 && g >= lag) {
           const int d = g - lag;
           sm100::mbar_wait(&s.kdone[d % kStages], (d / kStages) & 1);
@@ -319,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             try_event();
         sm100::tc_fence_after();
       };
-      for (int it = 0; it < n_my; ++it) {
+      for (int it = 0; it < (leader ? n_my : 0); ++it) {  // PAIR: the leader projects for both
         acc_wait(it);
         if (lane == 0) stamp(dbg, ctx, it, 8);
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -357,9 +409,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tc_fence_after();
       const bool tl = warp == 2 && lane == 0;
       if (tl) stamp(dbg, ctx, it, 0);
-      if (dbg == 1 || (dbg >= 3 && dbg <= 10) || dbg == 12) {
+      // accumulator a drained: PAIR -> one arrive per warp on the leader's barrier
+      auto release_acc = [&]() {
         sm100::tc_fence_before();
-        sm100::mbar_arrive(&s.acc_empty[a]);
+        if constexpr (PAIR) {
+          __syncwarp();
+          if (lane == 0)
+            sm100::mbar_arrive_remote(sm100::mapa(sm100::smem_u32(&s.acc_empty[a]), 0));
+        } else {
+          sm100::mbar_arrive(&s.acc_empty[a]);
+        }
+      };
+      if (dbg == 1 || (dbg >= 3 && dbg <= 10) || dbg == 12) {
+        release_acc();
         continue;
       }
       uint32_t qp[32];  // TS: this row's Q in bf16 pairs (hf == 0 threads)
@@ -418,8 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm100::tmem_st_32x32b_x32(lane_base + (uint32_t)a * kAccCols, qp);
         sm100::tmem_st_wait();
       }
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(&s.acc_empty[a]);
+      release_acc();
       sm100::fence_proxy_async_smem();
       sm100::mbar_arrive(&s.qkv_ready);
       if (tl) stamp(dbg, ctx, it, 1);
@@ -501,7 +562,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::cluster_sync();
   if (warp == 1) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc<512>(tmem);
+    if constexpr (PAIR)
+      sm100::tmem_dealloc_cg2<512>(tmem);
+    else
+      sm100::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -524,7 +588,7 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-template <int CS, int CH, bool FOLD, bool TS = false>
+template <int CS, int CH, bool FOLD, bool TS = false, bool PAIR = false>
 static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
                          void* ctx, int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
@@ -545,7 +609,7 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   } else if (!gemm::make_tmap_qkv3(&tm_w, w_qkv, (uint64_t)hidden, 64 / CS)) {
     return CHM_ERR_CUDA;
   }
-  auto kern = qa::qkv_attention_kernel<CS, CH, FOLD, TS>;
+  auto kern = qa::qkv_attention_kernel<CS, CH, FOLD, TS, PAIR>;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(qa::kThreads, 1, 1);
   cfg.dynamicSmemBytes = qa::kSmemBytes;
@@ -593,7 +657,16 @@ chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
                          void* ctx, int n_seq, int hidden, cudaStream_t st) {
   if (stats_in && (!c_qkv || n_part < 1 || n_part > kLnMaxParts)) return CHM_ERR_INVALID_ARG;
   // CHM_QA_PAIR=1: the cta_group::2 kernel (qkv_attn_pair.cu)
-  static const int pair = env_int("CHM_QA_PAIR", 0);
+  // default: the pair-projection kernel (fused 1.69 vs 1.76 ms for the
+  // cta_group::1 one, tools/experiments/qa_pair2.sh); CHM_QA_PAIR=0 selects
+  // the cta_group::1 kernel, 1 the all-cta_group::2 experiment
+  static const int pair = env_int("CHM_QA_PAIR", 2);
+  if (pair == 2)  // pair-projection variant of the fused kernel (cta_group::2 + ::1)
+    return stats_in ? launch<2, 1, true, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part,
+                                                      eps, ctx, n_seq, hidden, 0, 0, st)
+                    : launch<2, 1, false, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part,
+                                                       eps, ctx, n_seq, hidden, 0,
+                                                       env_int("CHM_QA_DEBUG", 0), st);
   if (pair)
     return qkv_attention_pair(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden,
                               st);
