@@ -6,6 +6,11 @@
 // the head's 64 Q + 64 K + 64 V output features of W_qkv), and its attention
 // consumes the result straight from tensor memory.
 //
+// Default build path (PAIR, see the kernel template): two sequences of one
+// head per CTA pair, the projection as a cta_group::2 pair MMA (28 KB of
+// operands per SM per k-block), attention per CTA with cta_group::1 MMAs.
+// The cta_group::1 description below is the CHM_QA_PAIR=0 path.
+//
 // Operand traffic: a lone CTA would stream 40 KB (x 16 KB + W 24 KB) from L2
 // per 384 tensor cycles, ~2x what L2 can deliver to every SM at once. CTAs
 // are therefore grouped in clusters of CS sequences x CH heads: the CH CTAs
