@@ -58,9 +58,9 @@ def parse_args():
     p.add_argument("--layernorm", default="cluster", choices=["deferred", "cluster"],
                    help="post-LN sublayers: normalised in a cluster-row GEMM epilogue "
                         "(default) or deferred and folded into the next GEMM (A/B)")
-    p.add_argument("--graph", action="store_true",
-                   help="replay the tick as a CUDA graph (1 GPU; per-kernel timing from an "
-                        "eager profiled pass)")
+    p.add_argument("--eager", action="store_true",
+                   help="time the eager launch sequence instead of the CUDA graph replay "
+                        "(the default on 1 GPU)")
     return p.parse_args()
 
 
@@ -189,7 +189,7 @@ def cpu_reference_tick(wl, cols, q_rows, hp):
 
 
 def prepare_cpu_inputs(wl, cols, q, hp):
-    from paper_2603_22206_b200.workload import first_stage_request
+    from workloads.tracegen import first_stage_request
     ids = wl.pool.model_ids
     reqs = [first_stage_request(rec, float(cols["arrival"][i]))
             for i, rec in enumerate(cols["records"])]
@@ -225,33 +225,69 @@ def cpu_router_sample(wl, n_sample: int, seed: int = 77):
     return (time.perf_counter() - t0) / n_sample
 
 
-def cpu_baseline(wl, q_tick0, n_ticks=3, n_router=16):
+def cpu_baseline(wl, q_tick, batch, model_gpu, gs, n_ticks=3, n_router=16):
     """Bounded-sample CPU baseline: (i) oracle port of the reference selection
     path on 1 thread over `n_ticks` full ticks, (ii) fp32 encoder restatement
-    on all host threads over `n_router` sequences, extrapolated per request."""
+    on all host threads over `n_router` sequences, extrapolated per request.
+    Also the tie-band replay (checker only, outside every timed region): the
+    fp32 restatement's scores for the whole last batch (torch on the GPU),
+    the selection replayed on the port with them, and the decisions that
+    differ from the device's (north star: ties inside the tolerance band are
+    reported)."""
+    import numpy as np
     import torch
 
     from oracle import hetsched_port as hp
+    from oracle.replay import port_state, replay_batch, router_fp32
     B = wl.batch_size
     sel = []
     for t in range(n_ticks):
-        cols = prepare_cpu_inputs(wl, wl.host_columns(t), q_tick0, hp)
-        sel.append(cpu_reference_tick(wl, cols, q_tick0, hp))
+        cols = prepare_cpu_inputs(wl, wl.host_columns(t), q_tick, hp)
+        sel.append(cpu_reference_tick(wl, cols, q_tick, hp))
     t_sel = statistics.median(sel)
     threads = torch.get_num_threads()
     t_req = cpu_router_sample(wl, n_router)
     tick = t_sel + B * t_req
-    return {
+    out = {
         "value": B / tick, "unit": UNIT, "cores": threads, "kind": "port",
         "sample": (f"selection+STJF: {n_ticks} full ticks of {B} rows through the oracle port "
                    f"(1 thread, p50 {t_sel * 1e3:.1f} ms/tick); router: {n_router} of {B} "
                    f"sequences through the fp32 encoder restatement on {threads} threads "
                    f"({t_req * 1e3:.1f} ms/request), extrapolated to {B}"),
+        "modelled": True, "router_extrapolation_factor": B / n_router,
         "selection_decisions_per_s": B / t_sel,
         "router_ms_per_request": t_req * 1e3,
         "cpu_model": _cpu_model(),
         "affinity_cores": len(os.sched_getaffinity(0)),
     }
+    q_ref = router_fp32(wl, batch.token_ids, B, chunk=512 if wl.spec.encoder.seq_len <= 128
+                        else 64)
+    mon, eng = port_state(wl)
+    m_ref, _, _ = replay_batch(wl, batch, q_ref, mon, eng)
+    diff = np.nonzero(m_ref != model_gpu)[0]
+    fl = gs.buf.dflags[:B].cpu().numpy()
+    loads = gs.buf.loads[:B * len(wl.pool)].view(B, -1).cpu().numpy()
+    ids = wl.pool.model_ids
+    local = local_in = 0
+    for i in np.nonzero((fl & 1) == 0)[0]:
+        m = hp.port_select_model({m: float(q_ref[i, k]) for k, m in enumerate(ids)},
+                                 {m: float(loads[i, k]) for k, m in enumerate(ids)},
+                                 wl.balancer.latency_slack, wl.balancer.confidence_margin)
+        if ids.index(m) != model_gpu[i]:
+            local += 1
+            local_in += bool(fl[i] & 24)
+    out["tie_band_replay"] = {
+        "router_max_abs_dq": float(np.abs(q_tick - q_ref).max()),
+        "decisions_flipped_with_fp32_scores": int(len(diff)),
+        "first_flip_row": int(diff[0]) if len(diff) else None,
+        "first_flip_in_tie_band": bool(fl[diff[0]] & 24) if len(diff) else None,
+        "local_flips": local, "local_flips_in_tie_band": local_in,
+        "how": ("fp32 encoder restatement on the last timed batch, selection replayed on the "
+                "oracle port from the same tick-start state (flips cascade through the "
+                "in-flight loads after the first); local flips re-decide each row with the "
+                "fp32 scores and the loads the device saw"),
+    }
+    return out
 
 
 def _cpu_model():
@@ -267,6 +303,7 @@ def _cpu_model():
 # --------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     import numpy as np
@@ -276,35 +313,45 @@ def run_reference(args):
     torch.set_num_threads(max(1, len(os.sched_getaffinity(0))))
 
     from oracle import hetsched_port as hp
-    from paper_2603_22206_b200 import synth
+    from workloads import synth
     wl = synth.make_workload(args.config, device="cpu", with_router=False)
     B = wl.batch_size
     K = len(wl.pool)
     rng = np.random.default_rng(0)
-    q = rng.random((B, K)).astype(np.float32)
+    q = rng.random((B, K))
     n_router = 8 if wl.spec.encoder.hidden >= 768 else 64
-    times = []
+    times, walls = [], []
     for step in range(args.warmup + args.steps):
+        w0 = time.perf_counter()
         cols = prepare_cpu_inputs(wl, wl.host_columns(step), q, hp)
         t_sel = cpu_reference_tick(wl, cols, q, hp)
         t_req = cpu_router_sample(wl, n_router, seed=1000 + step)
         if step >= args.warmup:
             times.append(t_sel + B * t_req)
+            walls.append(time.perf_counter() - w0)
     tick = statistics.median(times)
     value = B / tick
+    threads = torch.get_num_threads()
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tick * 1e3,
         "p50_tick_ms": tick * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32+fp64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {wl.spec.description}", "batch": B,
-                   "models": K, "router": _router_desc(wl)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": torch.get_num_threads(),
-                         "kind": "port",
+        "config": bench_config(args, wl, world),
+        "modelled": True,
+        "measured_wall_ms_per_step": statistics.median(walls) * 1e3,
+        "router_extrapolation_factor": B / n_router,
+        "model": (f"ms_per_step = measured selection+STJF tick ({B} rows, oracle port, 1 "
+                  f"thread) + {B} x the measured per-sequence time of the fp32 encoder "
+                  f"restatement on a {n_router}-sequence sample ({threads} threads): a full "
+                  f"step would take ~{tick:.0f} s, so {n_router} of {B} sequences are timed "
+                  f"per step to fit the driver's run"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "modelled": True, "router_extrapolation_factor": B / n_router,
                          "sample": (f"per step: one full tick of {B} rows through the oracle "
                                     f"port of the reference selection+STJF path (1 thread) + "
                                     f"{n_router} sequences of the fp32 encoder restatement "
-                                    f"({torch.get_num_threads()} threads), extrapolated to {B}")},
+                                    f"({threads} threads), extrapolated to {B}")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -317,12 +364,30 @@ def _router_desc(wl):
 
 
 # --------------------------------------------------------------------------- our arm
+def bench_config(args, wl, world):
+    """The `config` both arms print (identical keys and values, so the driver
+    can pair the lines); implementation details go to `impl_config`."""
+    B = wl.batch_size
+    return {"workload": f"{args.config}: {wl.spec.description}", "batch_per_gpu": B,
+            "global_batch": B * world, "models": len(wl.pool), "router": _router_desc(wl),
+            "parallelism": (f"request-sharded x{world}, mode {args.mode}" if world > 1
+                            else "single GPU"),
+            "l2": "inputs larger than L2 (router activations >1 GB per layer)",
+            "state": "fresh monitor/queues per tick (restored every tick)"}
+
+
+def _pct(xs, p):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, max(0, int(math.ceil(p * len(xs))) - 1))]
+
+
 def run_ours(args):
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2603_22206_b200 import _lib, synth
+    from paper_2603_22206_b200 import _lib
+    from workloads import synth
     from paper_2603_22206_b200.dist import ShardedScheduler
     from paper_2603_22206_b200.scheduler import GpuScheduler, HostStaging
     from paper_2603_22206_b200.tick import TickGraph
@@ -373,15 +438,16 @@ def run_ours(args):
     # N > 1: request-sharded ticks; Mode A all-reduces the per-engine in-flight
     # vector over NCCL after each GPU's chain, Mode B relays it (serial-exact).
     sched = ShardedScheduler(gs, args.mode) if world > 1 else gs
+    # the headline tick is a CUDA graph replay on one GPU (no host launches,
+    # no per-kernel timing hooks); --eager times the eager launch sequence
     graph = None
-    if args.graph and world == 1:
-        gbatch = wl.batch(0)
-        graph = TickGraph(gs, gbatch, n_iterations=1, restore_snapshot=snap,
+    if world == 1 and not args.eager:
+        graph = TickGraph(gs, wl.batch(0), n_iterations=1, restore_snapshot=snap,
                           n_complete=n_complete, completions=completions)
 
-    def tick(i, batch=None):
+    def tick(i, batch=None, eager=False):
         src = batch if batch is not None else batches[i % n_distinct]
-        if graph is not None:
+        if graph is not None and not eager:
             for name in ("program", "stage", "arrival", "out_tokens", "handle", "workflow",
                          "input_tokens", "token_ids"):
                 getattr(graph.batch, name).copy_(getattr(src, name), non_blocking=True)
@@ -392,20 +458,17 @@ def run_ours(args):
         sched.run_rows(src, n_iterations=1, n_complete=n_complete, stream=stream, **kw)
 
     clocks = ClockSampler(local, not args.no_clocks)
+    _lib.profile_enable(False)
     for i in range(args.warmup):
         tick(i)
     torch.cuda.synchronize()
     gs.check_errors("warmup")
-    q_tick0 = gs.buf.scores[:B * K].view(B, K).cpu().numpy().copy()
 
-    # ---------------- timed region (device) ----------------
+    # ---------------- timed region (device, uninstrumented) ----------------
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark_start()
-    _lib.profile_read()  # reset timings
-    _lib.profile_enable(graph is None)
-    launches0 = _lib.profile_read()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     for i in range(args.steps):
@@ -417,21 +480,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark_end(args.steps)
-    prof = _lib.profile_read()
-    _lib.profile_enable(False)
     clk = clocks.stop()
-    if graph is not None:
-        # graph replays bypass the host-side launch hooks: time the same
-        # ticks eagerly once more for the per-kernel breakdown / roofline
-        launches0 = _lib.profile_read()
-        _lib.profile_enable(True)
-        for i in range(args.steps):
-            gs.state.restore(snap)
-            gs.run_rows(batches[i % n_distinct], n_iterations=1, n_complete=n_complete,
-                        stream=stream, completions=completions)
-        torch.cuda.synchronize()
-        prof = _lib.profile_read()
-        _lib.profile_enable(False)
     gs.check_errors("timed")
     tick_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
@@ -440,7 +489,28 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     value = args.steps * B * world / (total_ms / 1e3)
-    n_launch = sum(prof[k]["launches"] - launches0[k]["launches"] for k in prof)
+    tie = gs.tie_band()  # the last timed tick's batch
+    q_last = gs.buf.scores[:B * K].view(B, K).cpu().numpy().copy()
+    model_last = gs.buf.model[:B].cpu().numpy().copy()
+    last_batch = (args.steps - 1) % n_distinct
+
+    # ------- instrumented eager pass: per-stage times, launches, rooflines -------
+    _lib.profile_read()
+    _lib.profile_enable(True)
+    iev = []
+    for i in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tick(i, eager=True)
+        b.record(stream)
+        iev.append((a, b))
+    torch.cuda.synchronize()
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    inst_ms = statistics.mean(a.elapsed_time(b) for a, b in iev)
+    n_launch = sum(v["launches"] for v in prof.values()) / args.steps
+    queued_end = int(gs.state.engine_queued.sum().item())
+    n_queued_rows = int(((gs.buf.dflags[:B] & 4) != 0).sum().item())
 
     # ---------------- end-to-end through the public API ----------------
     e2e = None
@@ -468,13 +538,16 @@ def run_ours(args):
         e2e = {"value": args.steps * B * world / float(tw.item()), "unit": UNIT,
                "h2d_bytes_per_step": stages[0].h2d_bytes,
                "d2h_bytes_per_step": stages[0].d2h_bytes,
-               "p50_step_ms": statistics.median(wall) * 1e3}
+               "p50_step_ms": statistics.median(wall) * 1e3,
+               "path": ("pinned host columns -> HostStaging.upload -> GpuScheduler tick "
+                        "(graph replay) -> decision read-back")}
 
-    # ---------------- roofline of the dominant kernel ----------------
+    # ---------------- rooflines (from the instrumented pass) ----------------
     peaks, peak_src = load_peaks()
+    peak_t = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    peak_bw = float(peaks.get("hbm_gbs", 6553.6))
     g = prof["gemm"]
     gemm_tflops = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
-    peak_t = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tpath):
@@ -486,51 +559,82 @@ def run_ours(args):
                 "frac": gemm_tflops / peak_t if peak_t else None, "traffic": traffic,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (GEMMs run inside a long step)",
                 "launches_timed": g["timed"],
-                "share_of_step": (g["ms"] / args.steps) / statistics.mean(tick_ms)}
+                "share_of_step": (g["ms"] / args.steps) / inst_ms,
+                "timing": "CUDA events around every launch in a separate instrumented eager pass"}
+    sec = []
     fq = prof["qkv_attention"]
     if fq["timed"] and fq["ms"] > 0:
         fq_t = fq["work"] / (fq["ms"] / 1e3) / 1e12
-        roofline["secondary"] = {
-            "kernel": "chm::qa::qkv_attention_kernel (fused QKV projection + attention)",
-            "achieved": fq_t, "frac": fq_t / peak_t if peak_t else None,
-            "share_of_step": (fq["ms"] / args.steps) / statistics.mean(tick_ms)}
+        sec.append({"kernel": "chm::qa::qkv_attention_kernel (fused QKV projection + attention)",
+                    "bound": "tensor", "achieved": fq_t, "unit": "TFLOP/s", "peak": peak_t,
+                    "frac": fq_t / peak_t, "ms_per_tick": fq["ms"] / args.steps,
+                    "share_of_step": (fq["ms"] / args.steps) / inst_ms})
+    at = prof["attention"]
+    if at["timed"] and at["ms"] > 0 and at["work"] > 0:
+        at_t = at["work"] / (at["ms"] / 1e3) / 1e12
+        sec.append({"kernel": "chm::attention (flash / CLS-row attention)", "bound": "tensor",
+                    "achieved": at_t, "unit": "TFLOP/s", "peak": peak_t, "frac": at_t / peak_t,
+                    "ms_per_tick": at["ms"] / args.steps})
+    for kind, kname, per in (("predict", "K5 predict_quantile_kernel", "8 + 8K B per row"),
+                             ("prepare", "prepare_rows_kernel", "26 B per row"),
+                             ("select", "K6 schedule_rows_kernel (serial-exact chain)",
+                              "24K + 53 B per row")):
+        v = prof[kind]
+        if not v["timed"] or v["ms"] <= 0:
+            continue
+        gbs = v["work"] / (v["ms"] / 1e3) / 1e9
+        ent = {"kernel": kname, "bound": "hbm", "achieved": gbs, "unit": "GB/s",
+               "peak": peak_bw, "frac": gbs / peak_bw, "ms_per_tick": v["ms"] / args.steps,
+               "algorithmic_bytes": per}
+        if kind == "select":
+            ent["ns_per_decision"] = v["ms"] / args.steps * 1e6 / B
+            ent["note"] = ("the serial decision recurrence is latency-bound: ns/decision is "
+                           "its figure of merit, GB/s is reported for completeness")
+        sec.append(ent)
+    qv = prof["queue"]
+    if qv["timed"] and qv["ms"] > 0:
+        # K7: read + write each queued entry record (40 B) + the appended rows
+        qbytes = 80.0 * queued_end + 40.0 * n_queued_rows
+        gbs = qbytes / (qv["ms"] / args.steps / 1e3) / 1e9
+        sec.append({"kernel": "K7 queue_kernel (STJF+aging radix sort, one CTA per engine)",
+                    "bound": "hbm", "achieved": gbs, "unit": "GB/s", "peak": peak_bw,
+                    "frac": gbs / peak_bw, "ms_per_tick": qv["ms"] / args.steps,
+                    "algorithmic_bytes": f"80 B per queued entry ({queued_end}) + 40 B per "
+                                         f"appended row ({n_queued_rows})"})
+    roofline["secondary"] = sec
     stage_ms = {k: v["ms"] / args.steps for k, v in prof.items() if v["timed"]}
     # executed (trimmed) FLOPs: the last layer is computed for the CLS row only
     router_flops = B * wl.spec.encoder.flops_executed_per_request(K)
+    router_ms = (prof["gemm"]["ms"] + prof["attention"]["ms"] + prof["rowwise"]["ms"] +
+                 prof["qkv_attention"]["ms"])
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "p50_tick_ms": statistics.median(tick_ms),
-        "p99_tick_ms": sorted(tick_ms)[min(len(tick_ms) - 1, int(math.ceil(0.99 * len(tick_ms))) - 1)],
+        "p50_tick_ms": statistics.median(tick_ms), "p99_tick_ms": _pct(tick_ms, 0.99),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": ("synthetic: first-stage requests from synthesize_trace(B, seed=100+tick), "
                  "[CLS]+U[1000,30522) token ids, BERT-init router weights (seed 0), "
                  "quantile predictor trained on synthesize_trace(2000, seed=1)"),
-        "config": {"workload": f"{args.config}: {wl.spec.description}", "batch_per_gpu": B,
-                   "global_batch": B * world, "models": K, "router": _router_desc(wl),
-                   "parallelism": (f"request-sharded x{world}, mode {args.mode} "
-                                   f"({'NCCL all-reduce' if args.mode == 'A' else 'NCCL relay'}"
-                                   f" of the in-flight vector)") if world > 1 else "single GPU",
-                   "cuda_graph": graph is not None,
-                   "layernorm": args.layernorm,
-                   "attention": (args.attention if wl.spec.encoder.seq_len == 128
-                                 else "flash (S>128)"),
-                   "l2": "inputs larger than L2 (router activations >1 GB per layer)",
-                   "state": "fresh monitor/queues per tick (device-side restore, timed)"},
+        "config": bench_config(args, wl, world),
+        "impl_config": {"cuda_graph": graph is not None, "layernorm": args.layernorm,
+                        "attention": (args.attention if wl.spec.encoder.seq_len == 128
+                                      else "flash (S>128)"),
+                        "timing": ("value: CUDA events around each uninstrumented tick"
+                                   + (" (graph replay)" if graph is not None else "")
+                                   + "; stages/roofline: a separate instrumented eager pass "
+                                   f"({inst_ms:.2f} ms/tick)")},
         "roofline": roofline,
         "gpu_launches": n_launch,
         "stages_ms_per_tick": stage_ms,
-        "router_tflops_achieved": router_flops * args.steps /
-                                  ((prof["gemm"]["ms"] + prof["attention"]["ms"] +
-                                    prof["rowwise"]["ms"] + prof["qkv_attention"]["ms"])
-                                   / 1e3) / 1e12,
+        "router_tflops_achieved": router_flops * args.steps / (router_ms / 1e3) / 1e12,
+        "tie_band": tie,
         "clocks": clk,
     }
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(wl, q_tick0)
+        line["cpu_baseline"] = cpu_baseline(wl, q_last, batches[last_batch], model_last, gs)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -70,10 +70,15 @@ typedef struct chm_pool {
   double decode_ms_per_token[CHM_MAX_MODELS];
 } chm_pool;
 
-/* BalancerConfig (balancer.py:26-37). */
+/* BalancerConfig (balancer.py:26-37) + the tie band reported per decision:
+ * a routed decision is flagged when its confidence gate or its descending-q
+ * choice compares two scores within tie_tolerance (chm_decisions.flags bits
+ * 3/4). With the north star's router tolerance eps = 1e-2 on each score, a
+ * band of 2*eps holds every decision a router error could flip. */
 typedef struct chm_balancer_cfg {
   double latency_slack;
   double confidence_margin;
+  double tie_tolerance;
 } chm_balancer_cfg;
 
 /* AgingConfig (engine.py:36-52). enabled=0 <=> starvation_threshold = inf. */
@@ -134,9 +139,12 @@ typedef struct chm_row_scratch {
   int8_t* pre_model;         /* [B] assignment before the batch (-1 none)      */
   int32_t* route_rows;       /* [B] compacted rows that need the router        */
   int32_t* n_route;          /* [1]                                            */
-  uint64_t* qual;            /* [B] per-row qualify masks (K*K bits)           */
+  uint64_t* qual;            /* [B] per-row gate sets, byte f = models clearing
+                                q_f + margin, as descending-q rank bits        */
   uint32_t* rank;            /* [B] per-row packed descending-q rank (4b/model)*/
   uint32_t* flags;           /* [B] per-row precomputed flags                  */
+  double* lnew;              /* [B] load of the chosen engine after the row's
+                                dispatch (estimated_loads are rebuilt from it) */
 } chm_row_scratch;
 
 typedef struct chm_decisions {
@@ -148,6 +156,8 @@ typedef struct chm_decisions {
   double* loads;             /* [B*K] Decision.estimated_loads (NULL = skip)   */
   int32_t* n_committed;      /* [1] rows fully applied                         */
   int32_t* error;            /* [4] {code,row,model,aux}                       */
+  int32_t* tie_counts;       /* [3] out (may be NULL): routed rows of this batch
+                                with bit3, with bit4, with either              */
 } chm_decisions;
 
 /* ---- STJF + aging engine queues (device state, SoA, seq order) ----------- */
@@ -327,10 +337,12 @@ chm_status chm_predict_input_length(const int32_t* input_tokens, int32_t n_model
 
 /* K6: serial-exact fused monitor + load estimate + selection + dispatch for a
  * batch (B calls of schedule_request in row order). `scores` [B*K] must hold
- * router output for every routed row; `yhat` [B*K] the predictor output. */
+ * router output for every routed row, in fp64 like the reference's
+ * ConfidenceVector (router.py:21-31: Python floats); `yhat` [B*K] the
+ * predictor output. */
 chm_status chm_schedule_rows(const chm_pool* pool, const chm_balancer_cfg* cfg,
                              const chm_monitor_state* mon, const chm_rows* rows,
-                             const chm_row_scratch* scratch, const float* scores,
+                             const chm_row_scratch* scratch, const double* scores,
                              const double* yhat, const chm_decisions* out,
                              void* stream);
 
@@ -490,11 +502,12 @@ chm_status chm_encoder_fold_weights(const chm_encoder_cfg* cfg, const chm_encode
 
 /* Router encoder forward over `n_seq` sequences of `seq_len` token ids, only
  * for the rows listed in `rows` (NULL = all, n_seq rows). Writes
- * q[rows[i]*K + m] = sigmoid(head(h_CLS)). `scratch_q` may be NULL. */
+ * q[rows[i]*K + m] = sigmoid(head(h_CLS)) as fp64 (the scheduler's score
+ * buffer is fp64). */
 chm_status chm_encoder_forward(const chm_encoder_cfg* cfg, const chm_encoder_weights* w,
                                const chm_encoder_workspace* ws, const int32_t* token_ids,
                                const int32_t* rows, const int32_t* n_rows_dev,
-                               int32_t n_seq, int32_t seq_len, float* q_out,
+                               int32_t n_seq, int32_t seq_len, double* q_out,
                                void* stream);
 
 /* Standalone tcgen05 GEMM: C[M,N] = A[M,K] . B[N,K]^T (+bias[N]) (+GELU)

@@ -119,6 +119,27 @@ def port_select_model(scores: dict, loads: dict, latency_slack: float,
     return fastest
 
 
+def port_tie_band(scores: dict, loads: dict, chosen: str, latency_slack: float,
+                  confidence_margin: float, tol: float = 2e-2) -> tuple[bool, bool]:
+    """Tie band of one routed decision (north star: "ties inside the tolerance
+    band are reported"; the reference has no such report, this is the
+    definition the device flags are checked against). Inside the latency
+    slack of m_fast (balancer.py:71-72):
+      gate  some model m != m_fast has |q_m - (q_fast + margin)| <= tol, so a
+            router error of tol could flip its confidence gate (balancer.py:75)
+      rank  the chosen candidate and another candidate have q within tol, so
+            the descending-q order (balancer.py:73) could flip between them
+    Returns (rank, gate)."""
+    fastest = min(loads, key=lambda mid: (loads[mid], mid))
+    ceiling = (1.0 + latency_slack) * loads[fastest]
+    need = scores[fastest] + confidence_margin
+    ok = [m for m in loads if loads[m] <= ceiling]
+    gate = any(m != fastest and abs(scores[m] - need) <= tol for m in ok)
+    cand = [m for m in ok if scores[m] >= need]
+    rank = bool(cand) and any(m != chosen and scores[chosen] - scores[m] <= tol for m in cand)
+    return rank, gate
+
+
 @dataclass
 class PortDecision:
     model: str

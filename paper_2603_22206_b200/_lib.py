@@ -47,7 +47,8 @@ class Pool(ctypes.Structure):
 
 
 class BalancerCfg(ctypes.Structure):
-    _fields_ = [("latency_slack", c_double), ("confidence_margin", c_double)]
+    _fields_ = [("latency_slack", c_double), ("confidence_margin", c_double),
+                ("tie_tolerance", c_double)]
 
 
 class AgingCfg(ctypes.Structure):
@@ -101,6 +102,7 @@ class RowScratch(ctypes.Structure):
         ("qual", c_void_p),
         ("rank", c_void_p),
         ("flags", c_void_p),
+        ("lnew", c_void_p),
     ]
 
 
@@ -113,6 +115,7 @@ class Decisions(ctypes.Structure):
         ("loads", c_void_p),
         ("n_committed", c_void_p),
         ("error", c_void_p),
+        ("tie_counts", c_void_p),
     ]
 
 

@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restri
                                                    const int32_t* __restrict__ n_rows_dev,
                                                    const float* __restrict__ w,
                                                    const float* __restrict__ bias, int K,
-                                                   float* __restrict__ q) {
+                                                   double* __restrict__ q) {
   constexpr int H = 32 * 8 * VEC;
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -812,7 +812,10 @@ __global__ void __launch_bounds__(256) head_kernel(const __nv_bfloat16* __restri
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) q[(size_t)row * K + m] = 1.0f / (1.0f + __expf(-(acc + bias[m])));
+    // q = sigmoid(logit), evaluated in fp64 on the fp32 logit:
+    // the selection compares fp64 scores (balancer.py:73-75), so the score
+    // buffer is fp64 end to end and table/constant routers keep full precision
+    if (lane == 0) q[(size_t)row * K + m] = 1.0 / (1.0 + exp(-(double)(acc + bias[m])));
   }
 }
 
@@ -962,7 +965,7 @@ template <int VEC>
 static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weights& w,
                               const chm_encoder_workspace& ws, const int32_t* ids,
                               const int32_t* rows, const int32_t* n_rows_dev, int n_seq, int S,
-                              float* q_out, cudaStream_t st) {
+                              double* q_out, cudaStream_t st) {
   const int H = cfg.hidden, F = cfg.ffn, L = cfg.n_layers;
   const long long T = (long long)n_seq * S;
   auto* x = reinterpret_cast<__nv_bfloat16*>(ws.x);
@@ -1196,7 +1199,7 @@ extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
                                           const chm_encoder_workspace* ws,
                                           const int32_t* token_ids, const int32_t* rows,
                                           const int32_t* n_rows_dev, int32_t n_seq,
-                                          int32_t seq_len, float* q_out, void* stream) {
+                                          int32_t seq_len, double* q_out, void* stream) {
   if (!cfg || !w || !ws || !token_ids || !q_out) return CHM_ERR_INVALID_ARG;
   if (n_seq < 0) return CHM_ERR_INVALID_ARG;
   if (n_seq == 0) return CHM_OK;

@@ -40,6 +40,25 @@ __global__ void __launch_bounds__(256) predict_quantile_kernel_dyn(
   }
 }
 
+// Same gather straight from global memory, for tables larger than the
+// shared-memory budget (the reference has no size limit): the table stays
+// L2-resident (126 MB) across the grid.
+__global__ void __launch_bounds__(256) predict_quantile_kernel_l2(
+    const double* __restrict__ table, int n_wf, int s_cap, int K,
+    const int32_t* __restrict__ workflow, const int32_t* __restrict__ stage, int n_rows,
+    double* __restrict__ yhat) {
+  const long long total = (long long)n_rows * K;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int row = (int)(e / K), m = (int)(e - (long long)row * K);
+    int wf = __ldg(workflow + row);
+    int st = __ldg(stage + row);
+    wf = (wf < 0 || wf >= n_wf) ? n_wf : wf;
+    st = (st < 1 || st > s_cap) ? 0 : st;
+    yhat[e] = __ldg(table + ((size_t)wf * (s_cap + 1) + st) * K + m);
+  }
+}
+
 // OraclePredictor.predict = rec.remaining_tokens(stage, model)
 // (predictor.py:30-36, workload.py:160-165): integer suffix sum, exact.
 __global__ void __launch_bounds__(256) predict_oracle_kernel(
@@ -96,8 +115,16 @@ extern "C" chm_status chm_predict_quantile(const double* table, int32_t n_wf, in
   if (n_rows == 0) return CHM_OK;
   if (!table || !workflow || !stage || !yhat) return CHM_ERR_INVALID_ARG;
   size_t smem = (size_t)(n_wf + 1) * (s_cap + 1) * n_models * sizeof(double);
-  if (smem > 160 * 1024) return CHM_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
+  if (smem > 160 * 1024) {
+    chm::prof::begin(chm::prof::K_PREDICT, s);
+    chm::predict_quantile_kernel_l2<<<chm::grid_for((long long)n_rows * n_models, 256), 256, 0,
+                                      s>>>(table, n_wf, s_cap, n_models, workflow, stage,
+                                           n_rows, yhat);
+    chm::prof::end(chm::prof::K_PREDICT, s, (double)n_rows * (8.0 + 8.0 * n_models));
+    CHM_LAUNCH_CHECK();
+    return CHM_OK;
+  }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(chm::predict_quantile_kernel_dyn,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -122,6 +122,7 @@ struct SelectParams {
   uint32_t b_pow2_mask;
   double one_plus_slack;          // (1.0 + cfg.latency_slack), balancer.py:72
   double margin;                  // cfg.confidence_margin
+  double tie_tol;                 // tie band of the router tolerance (north star)
 };
 
 constexpr int kChunk = 256;
@@ -145,11 +146,11 @@ __device__ __forceinline__ void log_append(const chm_monitor_state& mon, int m, 
 
 template <int K>
 struct ChunkBuf {
-  uint64_t qual[kChunk];
+  uint64_t qual[kChunk];   // byte f: models clearing the gate of m_fast = f, rank space
+  uint64_t rbits[kChunk];  // byte k: rank-space bit of model k
   double yhat[kChunk * K];
   double arrival[kChunk];
-  uint32_t rank[kChunk];
-  uint32_t perm[kChunk];
+  uint32_t perm[kChunk];   // nibble (7 - r): the model of rank r
   uint32_t flags[kChunk];
   int32_t out_tokens[kChunk * K];
   int32_t first_row[kChunk];
@@ -180,9 +181,9 @@ __device__ __forceinline__ void neumaier_add(double& s, double& c, double x) {
 
 // v[m] for a run-time m in [0, K) as a log-depth select tree over registers
 // (dynamic indexing would spill the array to local memory).
-template <int K>
-__device__ __forceinline__ double tree_select(const double (&v)[K], int m) {
-  double a[K];
+template <int K, typename T>
+__device__ __forceinline__ T tree_select(const T (&v)[K], int m) {
+  T a[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) a[k] = v[k];
 #pragma unroll
@@ -192,25 +193,121 @@ __device__ __forceinline__ double tree_select(const double (&v)[K], int m) {
   return a[0];
 }
 
+// select_model (balancer.py:63-77) on load bit patterns (non-negative doubles
+// order like their IEEE bits): m_fast = argmin (L, index) as a log-depth
+// tournament whose left operand always carries the lower indices (strict <
+// keeps the lowest index on ties); limit = (1 + tau) * L_fast; the candidates
+// {m : L_m <= limit and q_m >= q_fast + margin}; the first one in
+// descending-q order. Rank space: rank r is bit (7 - r), so the first
+// candidate is the highest set bit (one FLO) and `perm` nibble (7 - r) holds
+// the model of rank r. `qual` byte f holds the gate set of m_fast = f in rank
+// space, `rbits` byte k the rank bit of model k (both precomputed per row).
 template <int K>
+__device__ __forceinline__ int select_bits(const unsigned long long (&Lb)[K], double one_plus_slack,
+                                           uint64_t qual, uint64_t rbits, uint32_t perm) {
+  // (1 + tau) * L_k for every k and the gate set of every candidate ride
+  // along the tournament: no multiply or shift after the argmin
+  unsigned long long tv[K], tl[K];
+  uint32_t tq[K];
+  int ti[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    tv[k] = Lb[k];
+    tl[k] = (unsigned long long)__double_as_longlong(
+        __dmul_rn(one_plus_slack, __longlong_as_double((long long)Lb[k])));
+    tq[k] = (uint32_t)(qual >> (8 * k)) & 0xffu;
+    ti[k] = k;
+  }
+#pragma unroll
+  for (int step = 1; step < K; step *= 2)
+#pragma unroll
+    for (int k = 0; k + step < K; k += 2 * step) {
+      const bool lt = tv[k + step] < tv[k];
+      tv[k] = lt ? tv[k + step] : tv[k];
+      tl[k] = lt ? tl[k + step] : tl[k];
+      tq[k] = lt ? tq[k + step] : tq[k];
+      ti[k] = lt ? ti[k + step] : ti[k];
+    }
+  const unsigned long long limb = tl[0];
+  uint32_t okr = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    okr |= (Lb[k] <= limb) ? ((uint32_t)(rbits >> (8 * k)) & 0xffu) : 0u;
+  const uint32_t crk = tq[0] & okr;
+  const int pos = (31 - __clz(crk)) & 7;
+  const int mc = (int)((perm >> (4 * pos)) & 15u);
+  return crk ? mc : ti[0];
+}
+
+// Tie band (north star: "ties inside the tolerance band are reported"): for a
+// routed row with scores q and the loads L it saw, TIE_QUAL = some model
+// inside the latency slack other than m_fast has |q_m - (q_fast + margin)| <=
+// tol (the confidence gate could flip under a router error of tol);
+// TIE_RANK = the chosen candidate and another candidate differ by <= tol in q
+// (their descending-q order could flip). Same fp64 operations as the decision.
+enum : uint8_t { DF_TIE_RANK = 8u, DF_TIE_QUAL = 16u };
+
+template <int K>
+__device__ __forceinline__ uint8_t tie_bits(const double (&q)[K], const double (&L)[K],
+                                            const SelectParams& prm, int m) {
+  int mf = 0;
+  double lmin = L[0];
+#pragma unroll
+  for (int k = 1; k < K; ++k) {
+    const bool lt = L[k] < lmin;
+    mf = lt ? k : mf;
+    lmin = lt ? L[k] : lmin;
+  }
+  const double limit = __dmul_rn(prm.one_plus_slack, lmin);
+  double qf = q[0];
+#pragma unroll
+  for (int k = 1; k < K; ++k) qf = (k == mf) ? q[k] : qf;
+  const double thr = __dadd_rn(qf, prm.margin);
+  double qm = q[0];
+#pragma unroll
+  for (int k = 1; k < K; ++k) qm = (k == m) ? q[k] : qm;
+  bool any_cand = false, tq = false, tr = false;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool ok = L[k] <= limit;
+    if (ok && k != mf && fabs(__dsub_rn(q[k], thr)) <= prm.tie_tol) tq = true;
+    const bool cand = ok && q[k] >= thr;
+    any_cand |= cand;
+    if (cand && k != m && __dsub_rn(qm, q[k]) <= prm.tie_tol) tr = true;
+  }
+  return (uint8_t)((tq ? DF_TIE_QUAL : 0) | ((any_cand && tr) ? DF_TIE_RANK : 0));
+}
+
+template <int K, bool SPEC>
 __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     SelectParams prm, chm_monitor_state mon, chm_rows rows, chm_row_scratch sc,
-    const float* __restrict__ scores, const double* __restrict__ yhat, chm_decisions out) {
+    const double* __restrict__ scores, const double* __restrict__ yhat, chm_decisions out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ChunkBuf<K>* bufs = reinterpret_cast<ChunkBuf<K>*>(smem_raw);
   __shared__ int s_committed;
   const int B = rows.n_rows;
   const int tid = threadIdx.x;
+  // A predictor / trace-gather error already recorded for row r stops the
+  // batch there: rows < r are scheduled, row r gets the effects the reference
+  // applied before predictor.predict raised (monitor.assign for a routed
+  // row, balancer.py:113-115), later rows nothing.
+  const int pred_stop = (out.error && out.error[0] != 0) ? min(out.error[1], B) : B;
 
   // ---- phase P: per-row precompute (independent of the in-flight state) ----
-  // It also decides the chain mode: the fast chain defers the engine
-  // bookkeeping (seq, admission, clock) to a parallel post-pass, which is
-  // exact unless a row could raise inside EngineSim.enqueue (clock going
-  // backwards, negative out_tokens) or needs the in-batch duplicate scan.
+  // It also decides the chain mode: the fast chain has no error exits and
+  // defers the engine bookkeeping (seq, admission, clock) to a parallel
+  // post-pass, which is exact unless a row could raise (bad score, negative /
+  // NaN prediction, clock going backwards, negative out_tokens, predictor
+  // error) or needs the in-batch duplicate scan.
   double max_clk0 = 0.0;
 #pragma unroll
   for (int m = 0; m < K; ++m) max_clk0 = fmax(max_clk0, mon.engine_clock[m]);
-  int slow = 0;
+  int slow = pred_stop < B;
+  // Dyadic mode: every prediction a multiple of 2^-8 below 2^29 (and the
+  // tick-start sums likewise, compensation 0). Every partial sum is then a
+  // multiple of 2^-8 below 2^44, exact in fp64, so Neumaier's compensation
+  // stays exactly 0 and the running sum is a plain add (bit-identical).
+  int dyadic_rows = 1;
   for (int i = tid; i < B; i += blockDim.x) {
     const int p = rows.program[i];
     const int st = rows.stage[i];
@@ -218,9 +315,13 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       const double a = rows.arrival[i];
       const double prev = i ? rows.arrival[i - 1] : max_clk0;
       if (i ? (a < prev) : (a < __dsub_rn(prev, 1e-9))) slow = 1;
-      if (rows.out_tokens) {
 #pragma unroll
-        for (int m = 0; m < K; ++m) slow |= rows.out_tokens[(size_t)i * K + m] < 0;
+      for (int m = 0; m < K; ++m) {
+        if (rows.out_tokens) slow |= rows.out_tokens[(size_t)i * K + m] < 0;
+        const double y = yhat[(size_t)i * K + m];
+        slow |= !(y >= 0.0);
+        const double y8 = y * 256.0;
+        dyadic_rows &= (y < 536870912.0 && y8 == trunc(y8)) ? 1 : 0;
       }
     }
     uint32_t fl = 0;
@@ -245,13 +346,14 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       bool bad = false;
 #pragma unroll
       for (int m = 0; m < K; ++m) {
-        float qf = scores[(size_t)i * K + m];
+        const double qm = scores[(size_t)i * K + m];
         // ConfidenceVector.__post_init__: `not 0.0 <= q <= 1.0` (NaN fails too).
-        if (!(qf >= 0.0f && qf <= 1.0f)) bad = true;
-        q[m] = (double)qf;
+        if (!(qm >= 0.0 && qm <= 1.0)) bad = true;
+        q[m] = qm;
       }
       if (bad) fl |= RF_BAD_SCORE;
       // rank[m] = position of m in sorted(models, key=(-q[m], m)).
+      uint32_t rbit[K];
 #pragma unroll
       for (int m = 0; m < K; ++m) {
         uint32_t r = 0;
@@ -259,15 +361,17 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
         for (int o = 0; o < K; ++o)
           r += (q[o] > q[m] || (q[o] == q[m] && o < m)) ? 1u : 0u;
         rank |= r << (4 * m);
+        rbit[m] = 0x80u >> r;
       }
-      // qual[mf] = { m : q[m] >= q[mf] + margin } (balancer.py:73-75).
+      // qual byte mf = { m : q[m] >= q[mf] + margin } (balancer.py:73-75),
+      // as rank-space bits
 #pragma unroll
       for (int mf = 0; mf < K; ++mf) {
         const double thr = __dadd_rn(q[mf], prm.margin);
         uint64_t bits = 0;
 #pragma unroll
-        for (int m = 0; m < K; ++m) bits |= (q[m] >= thr ? 1ull : 0ull) << m;
-        qual |= bits << (K * mf);
+        for (int m = 0; m < K; ++m) bits |= q[m] >= thr ? rbit[m] : 0u;
+        qual |= bits << (8 * mf);
       }
     }
     if (fl & ~(RF_ROUTE | RF_CACHED_PRE)) slow = 1;
@@ -276,6 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     sc.rank[i] = rank;
   }
   const bool exact = __syncthreads_or(slow) != 0;
+  bool dyadic = __syncthreads_and(dyadic_rows) != 0;
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    const double f = mon.inflight_sum[m];
+    dyadic = dyadic && mon.inflight_comp[m] == 0.0 && f >= 0.0 &&
+             f * 256.0 == trunc(f * 256.0) && f + (double)B * 536870912.0 < 17592186044416.0;
+  }
 
   auto load_chunk = [&](int chunk, ChunkBuf<K>* buf, int t0, int nt) {
     const int r0 = chunk * kChunk;
@@ -284,11 +395,16 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     for (int j = t0; j < n; j += nt) {
       buf->qual[j] = __ldcg(sc.qual + r0 + j);
       const uint32_t rk = __ldcg(sc.rank + r0 + j);
-      buf->rank[j] = rk;
-      uint32_t pm = 0;  // perm: rank r -> model (inverse of rank)
+      uint32_t pm = 0;  // perm: rank r -> model, at nibble 7 - r
+      uint64_t rb = 0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) pm |= (uint32_t)k << (4 * ((rk >> (4 * k)) & 15u));
+      for (int k = 0; k < K; ++k) {
+        const uint32_t r = (rk >> (4 * k)) & 15u;
+        pm |= (uint32_t)k << (4 * (7 - r));
+        rb |= (uint64_t)(0x80u >> r) << (8 * k);
+      }
       buf->perm[j] = pm;
+      buf->rbits[j] = rb;
       buf->flags[j] = __ldcg(sc.flags + r0 + j);
       buf->arrival[j] = rows.arrival[r0 + j];
       buf->first_row[j] = sc.first_row[r0 + j];
@@ -305,12 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   if (tid == 0) s_committed = B;
   __syncthreads();
 
-  // Chain state (lane 0 of warp 0 only). The loads L[K] feed the next row's
-  // argmin, so they live in registers; everything else is indexed by the
-  // chosen model directly in shared memory (one LDS/STS each, no K-way
-  // predicated updates on the critical path).
+  // Chain state (thread 0 only). Per-engine counters that do not feed back
+  // into the selection live in shared memory.
   double L[K];
-  __shared__ double s_f[K], s_c[K], s_clk[K], s_d[K], s_b[K], s_invb[K];
+  __shared__ double s_f[K], s_c[K], s_clk[K], s_d[K], s_b[K], s_invb[K], s_L0[K];
   __shared__ long long s_seq[K], s_cnt[K], s_it[K];
   __shared__ int s_run[K], s_que[K], s_bmax[K], s_pow2[K];
   bool stop = false;
@@ -320,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       const double f = mon.inflight_sum[m], c = mon.inflight_comp[m];
       const bool pw = (prm.b_pow2_mask >> m) & 1u;
       L[m] = load_of(neumaier_value(f, c), prm.d[m], prm.b[m], prm.inv_b[m], pw);
+      s_L0[m] = L[m];
       s_f[m] = f;
       s_c[m] = c;
       s_d[m] = prm.d[m];
@@ -345,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   // Loads are compared as IEEE bit patterns (all non-negative), which orders
   // them exactly like the fp64 values, with integer compares.
   unsigned long long Lb[K];
-  double fr[K], cv[K], dd[K], bdiv[K];
+  double fr[K], cv[K], dd[K], bdiv[K], dq[K];
 #pragma unroll
   for (int m = 0; m < K; ++m) {
     Lb[m] = (unsigned long long)__double_as_longlong(L[m]);
@@ -353,94 +468,121 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     cv[m] = s_c[m];
     dd[m] = prm.d[m];
     bdiv[m] = ((prm.b_pow2_mask >> m) & 1u) ? prm.inv_b[m] : prm.b[m];
+    dq[m] = __dmul_rn(prm.d[m], prm.inv_b[m]);  // d / b, exact for b = 2^k
   }
   const uint32_t pow2_mask = prm.b_pow2_mask;
+  const double one_plus_slack = prm.one_plus_slack;
 
   for (int ch = 0; ch < n_chunks; ++ch) {
     ChunkBuf<K>* cur = &bufs[ch & 1];
     if (tid >= 32) {
       if (ch + 1 < n_chunks) load_chunk(ch + 1, &bufs[(ch + 1) & 1], tid - 32, blockDim.x - 32);
     } else if (tid == 0 && !stop && !exact) {
-      // ---------------- fast chain ----------------
+      // ---------------- fast chain (no error exits) ----------------
+      // Per row: decision from the loads (the only loop-carried input), then
+      // the chosen model's in-flight update and new load. With SPEC (every b
+      // a power of two) the K candidate updates are computed while the
+      // decision resolves and the chosen one is selected afterwards, so the
+      // loop-carried path is the decision alone. In dyadic mode every
+      // partial sum is exact, the Neumaier compensation stays 0 and an
+      // update is one add and one multiply (L = s * (d / b), exact scaling).
       const int r0 = ch * kChunk;
       const int n = min(kChunk, B - r0);
-      for (int j = 0; j < n; ++j) {
-        const int i = r0 + j;
-        const uint32_t fl = cur->flags[j];
-        double yr[K];
+      if (SPEC && dyadic) {
+        // software-pipelined: row j + 1's inputs are read from shared memory
+        // while row j resolves
+        uint32_t nfl = cur->flags[0];
+        uint64_t nqual = cur->qual[0], nrb = cur->rbits[0];
+        uint32_t npm = cur->perm[0];
+        int npre = cur->pre_model[0];
+        double ny[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) yr[k] = cur->yhat[j * K + k];
-        int m;
-        bool cached;
-        if (fl & RF_CACHED_PRE) {
-          m = cur->pre_model[j];
-          cached = true;
-        } else {
-          if (fl & RF_BAD_SCORE) {
-            report_error(out.error, CHM_ERR_VALIDATION, i, -1, 1);
-            s_committed = i;
-            stop = true;
-            break;
-          }
-          cached = false;
-          unsigned long long tv[K];
-          int ti[K];
+        for (int k = 0; k < K; ++k) ny[k] = cur->yhat[k];
+        for (int j = 0; j < n; ++j) {
+          const int i = r0 + j;
+          const uint32_t fl = nfl;
+          const uint64_t qual = nqual, rb = nrb;
+          const uint32_t pm = npm;
+          const int pre = npre;
+          double ls_d[K];
+          unsigned long long ls[K];
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            tv[k] = Lb[k];
-            ti[k] = k;
+            ls_d[k] = __dadd_rn(fr[k], ny[k]);
+            ls[k] = (unsigned long long)__double_as_longlong(__dmul_rn(ls_d[k], dq[k]));
           }
+          const int jn = j + 1 < n ? j + 1 : j;
+          nfl = cur->flags[jn];
+          nqual = cur->qual[jn];
+          nrb = cur->rbits[jn];
+          npm = cur->perm[jn];
+          npre = cur->pre_model[jn];
 #pragma unroll
-          for (int step = 1; step < K; step *= 2)
+          for (int k = 0; k < K; ++k) ny[k] = cur->yhat[jn * K + k];
+          int m = select_bits<K>(Lb, one_plus_slack, qual, rb, pm);
+          m = (fl & RF_CACHED_PRE) ? pre : m;
 #pragma unroll
-            for (int k = 0; k + step < K; k += 2 * step)
-              if (tv[k + step] < tv[k]) {
-                tv[k] = tv[k + step];
-                ti[k] = ti[k + step];
-              }
-          const int mf = ti[0];
-          const unsigned long long limb = (unsigned long long)__double_as_longlong(
-              __dmul_rn(prm.one_plus_slack, __longlong_as_double((long long)tv[0])));
-          uint32_t ok = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) ok |= (Lb[k] <= limb ? 1u : 0u) << k;
-          const uint32_t cand = (uint32_t)(cur->qual[j] >> (K * mf)) & ok;
-          const uint32_t rk = cur->rank[j];
-          uint32_t crk = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) crk |= ((cand >> k) & 1u) << ((rk >> (4 * k)) & 15u);
-          m = crk ? (int)((cur->perm[j] >> (4 * (__ffs(crk) - 1))) & 15u) : mf;
-          if (out.loads) {
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-              out.loads[(size_t)i * K + k] = __longlong_as_double((long long)Lb[k]);
+          for (int k = 0; k < K; ++k) {
+            const bool hit = k == m;
+            fr[k] = hit ? ls_d[k] : fr[k];
+            Lb[k] = hit ? ls[k] : Lb[k];
           }
+          out.model[i] = m;
+          sc.lnew[i] = __longlong_as_double((long long)tree_select<K>(ls, m));
         }
-        const double y = tree_select<K>(yr, m);
-        if (!(y >= 0.0)) {  // NaN or negative prediction (monitor.py:89-90)
-          report_error(out.error, y < 0.0 ? CHM_ERR_NEGATIVE_PREDICTION : CHM_ERR_NAN_PREDICTION,
-                       i, m, 0);
-          if (!cached) mon.assignment[rows.program[i]] = (int8_t)m;
-          s_committed = i;
-          stop = true;
-          break;
-        }
-        double fm = tree_select<K>(fr, m), cm = tree_select<K>(cv, m);
-        neumaier_add(fm, cm, y);
-        const double num = __dmul_rn(neumaier_value(fm, cm), tree_select<K>(dd, m));
-        const double bdm = tree_select<K>(bdiv, m);
-        const double lm = ((pow2_mask >> m) & 1u) ? __dmul_rn(num, bdm) : __ddiv_rn(num, bdm);
-        const unsigned long long lmb = (unsigned long long)__double_as_longlong(lm);
+      } else {
+#pragma unroll 2
+        for (int j = 0; j < n; ++j) {
+          const int i = r0 + j;
+          const uint32_t fl = cur->flags[j];
+          const uint64_t qual = cur->qual[j], rb = cur->rbits[j];
+          const uint32_t pm = cur->perm[j];
+          const int pre = cur->pre_model[j];
+          double yr[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const bool hit = k == m;
-          fr[k] = hit ? fm : fr[k];
-          cv[k] = hit ? cm : cv[k];
-          Lb[k] = hit ? lmb : Lb[k];
+          for (int k = 0; k < K; ++k) yr[k] = cur->yhat[j * K + k];
+          int m = select_bits<K>(Lb, one_plus_slack, qual, rb, pm);
+          m = (fl & RF_CACHED_PRE) ? pre : m;
+          unsigned long long lmb;
+          if constexpr (SPEC) {
+            double fs[K], cs[K];
+            unsigned long long ls[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              fs[k] = fr[k];
+              cs[k] = cv[k];
+              neumaier_add(fs[k], cs[k], yr[k]);
+              ls[k] = (unsigned long long)__double_as_longlong(
+                  __dmul_rn(__dmul_rn(neumaier_value(fs[k], cs[k]), dd[k]), bdiv[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const bool hit = k == m;
+              fr[k] = hit ? fs[k] : fr[k];
+              cv[k] = hit ? cs[k] : cv[k];
+              Lb[k] = hit ? ls[k] : Lb[k];
+            }
+            lmb = tree_select<K>(ls, m);
+          } else {
+            const double y = tree_select<K>(yr, m);
+            double fm = tree_select<K>(fr, m), cm = tree_select<K>(cv, m);
+            neumaier_add(fm, cm, y);
+            const double num = __dmul_rn(neumaier_value(fm, cm), tree_select<K>(dd, m));
+            const double bdm = tree_select<K>(bdiv, m);
+            const double lm =
+                ((pow2_mask >> m) & 1u) ? __dmul_rn(num, bdm) : __ddiv_rn(num, bdm);
+            lmb = (unsigned long long)__double_as_longlong(lm);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const bool hit = k == m;
+              fr[k] = hit ? fm : fr[k];
+              cv[k] = hit ? cm : cv[k];
+              Lb[k] = hit ? lmb : Lb[k];
+            }
+          }
+          out.model[i] = m;
+          sc.lnew[i] = __longlong_as_double((long long)lmb);
         }
-        out.model[i] = m;
-        out.priority[i] = y;
-        out.flags[i] = cached ? DF_CACHED : 0;  // admission bits: post-pass
       }
     } else if (tid == 0 && !stop && exact) {
       const int r0 = ch * kChunk;
@@ -474,43 +616,18 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
             break;
           }
           cached = false;
-          // min over (L, id) as a log-depth tournament; the left operand always
-          // carries the lower indices, so strict < keeps the lowest index on
-          // ties (balancer.py:71).
-          double tv[K];
-          int ti[K];
+          unsigned long long lb[K];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            tv[k] = L[k];
-            ti[k] = k;
-          }
-#pragma unroll
-          for (int step = 1; step < K; step *= 2)
-#pragma unroll
-            for (int k = 0; k + step < K; k += 2 * step)
-              if (tv[k + step] < tv[k]) {
-                tv[k] = tv[k + step];
-                ti[k] = ti[k + step];
-              }
-          const int mf = ti[0];
-          const double limit = __dmul_rn(prm.one_plus_slack, tv[0]);
-          uint32_t ok = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) ok |= (L[k] <= limit ? 1u : 0u) << k;
-          const uint32_t cand = (uint32_t)(cur->qual[j] >> (K * mf)) & ok;
-          // the first qualifying model in descending-q order = the candidate
-          // with the smallest rank: move the candidate bits to rank space and
-          // take the lowest set bit
-          const uint32_t rk = cur->rank[j];
-          uint32_t cr = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) cr |= ((cand >> k) & 1u) << ((rk >> (4 * k)) & 15u);
-          m = cr ? (int)((cur->perm[j] >> (4 * (__ffs(cr) - 1))) & 15u) : mf;
-          if (out.loads) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) out.loads[(size_t)i * K + k] = L[k];
-          }
+          for (int k = 0; k < K; ++k) lb[k] = (unsigned long long)__double_as_longlong(L[k]);
+          m = select_bits<K>(lb, prm.one_plus_slack, cur->qual[j], cur->rbits[j], cur->perm[j]);
           partial = 1;  // monitor.assign (balancer.py:113)
+        }
+        if (i == pred_stop) {
+          // predictor.predict raised for this row (error already recorded)
+          if (partial >= 1) mon.assignment[rows.program[i]] = (int8_t)m;
+          s_committed = i;
+          stop = true;
+          break;
         }
         // predictor.predict + record_dispatch (balancer.py:115-116, monitor.py:86-96)
         const double y = cur->yhat[j * K + m];
@@ -536,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
                                     s_pow2[m] != 0);
 #pragma unroll
           for (int k = 0; k < K; ++k) L[k] = (k == m) ? lm : L[k];
+          sc.lnew[i] = lm;
           log_append(mon, m, s_cnt[m], rows.program[i], rows.stage[i], y, out.error, i);
           s_cnt[m] += 1;
           // EngineSim.enqueue: _advance_clock (engine.py:140-143), then
@@ -585,70 +703,85 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     __syncthreads();
   }
 
+  // Per-thread contiguous row ranges for the parallel post-passes.
+  __shared__ int s_cntm[K][kThreads];
+  __shared__ int s_lastm[K][kThreads];
+  __shared__ int s_tot[K], s_last[K];
+  const int n_ok = s_committed;
+  const int per = (n_ok + kThreads - 1) / kThreads;
+  const int lo = min(tid * per, n_ok), hi = min(lo + per, n_ok);
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0 && !exact) {
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      s_f[m] = fr[m];
+      s_c[m] = cv[m];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    s_cntm[m][tid] = 0;
+    s_lastm[m][tid] = -1;
+  }
+  for (int i = lo; i < hi; ++i) {
+    const int m = out.model[i];
+    s_cntm[m][tid] += 1;
+    s_lastm[m][tid] = i;
+  }
+  __syncthreads();
+  // per model (warp m): exclusive prefix sums of the counts and exclusive
+  // running max of the last row index over the thread ranges
+  if (warp < K) {
+    int v[kThreads / 32], lv[kThreads / 32], sum = 0, last = -1;
+#pragma unroll
+    for (int e = 0; e < kThreads / 32; ++e) {
+      v[e] = s_cntm[warp][lane * (kThreads / 32) + e];
+      lv[e] = s_lastm[warp][lane * (kThreads / 32) + e];
+      sum += v[e];
+      last = max(last, lv[e]);
+    }
+    int incl = sum, linc = last;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      const int tl = __shfl_up_sync(0xffffffffu, linc, o);
+      if (lane >= o) {
+        incl += t;
+        linc = max(linc, tl);
+      }
+    }
+    int run = incl - sum;
+    int lrun = __shfl_up_sync(0xffffffffu, linc, 1);
+    if (lane == 0) lrun = -1;
+#pragma unroll
+    for (int e = 0; e < kThreads / 32; ++e) {
+      s_cntm[warp][lane * (kThreads / 32) + e] = run;
+      s_lastm[warp][lane * (kThreads / 32) + e] = lrun;
+      run += v[e];
+      lrun = max(lrun, lv[e]);
+    }
+    if (lane == 31) {
+      s_tot[warp] = incl;
+      s_last[warp] = linc;
+    }
+  }
+  __syncthreads();
+
   if (!exact) {
     // ---- fast-chain bookkeeping, in parallel (EngineSim.enqueue effects) ----
     // Rows choosing engine m take consecutive seq numbers; the first
     // max(0, b - running) of them are admitted by the enqueue-triggered
     // iteration, the rest queue; the engine clock ends at the arrival of the
     // last row it received (arrivals are non-decreasing in fast mode).
-    __shared__ int s_cntm[K][kThreads];
-    __shared__ int s_lastm[K][kThreads];
-    __shared__ int s_tot[K], s_last[K];
-    if (tid == 0) {
-#pragma unroll
-      for (int m = 0; m < K; ++m) {
-        s_f[m] = fr[m];
-        s_c[m] = cv[m];
-      }
-    }
-    const int n_ok = s_committed;
-    const int per = (n_ok + kThreads - 1) / kThreads;
-    const int lo = min(tid * per, n_ok), hi = min(lo + per, n_ok);
-#pragma unroll
-    for (int m = 0; m < K; ++m) {
-      s_cntm[m][tid] = 0;
-      s_lastm[m][tid] = -1;
-    }
-    for (int i = lo; i < hi; ++i) {
-      const int m = out.model[i];
-      s_cntm[m][tid] += 1;
-      s_lastm[m][tid] = i;
-    }
-    __syncthreads();
-    const int warp = tid >> 5, lane = tid & 31;
-    if (warp < K) {
-      int v[kThreads / 32], sum = 0, last = -1;
-#pragma unroll
-      for (int e = 0; e < kThreads / 32; ++e) {
-        v[e] = s_cntm[warp][lane * (kThreads / 32) + e];
-        sum += v[e];
-        last = max(last, s_lastm[warp][lane * (kThreads / 32) + e]);
-      }
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-      int run = incl - sum;
-#pragma unroll
-      for (int e = 0; e < kThreads / 32; ++e) {
-        s_cntm[warp][lane * (kThreads / 32) + e] = run;
-        run += v[e];
-      }
-      if (lane == 31) s_tot[warp] = incl;
-      if (lane == 0) s_last[warp] = last;
-    }
-    __syncthreads();
     for (int i = lo; i < hi; ++i) {
       const int m = out.model[i];
       const int r = s_cntm[m][tid]++;
-      log_append(mon, m, s_cnt[m] + r, rows.program[i], rows.stage[i], yhat[(size_t)i * K + m],
-                 out.error, i);
+      const double y = yhat[(size_t)i * K + m];
+      log_append(mon, m, s_cnt[m] + r, rows.program[i], rows.stage[i], y, out.error, i);
+      out.priority[i] = y;
       out.seq[i] = s_seq[m] + r;
-      out.flags[i] |= (s_run[m] + r < s_bmax[m]) ? DF_ADMITTED : DF_QUEUED;
+      out.flags[i] = ((sc.flags[i] & RF_CACHED_PRE) ? DF_CACHED : 0) |
+                     ((s_run[m] + r < s_bmax[m]) ? DF_ADMITTED : DF_QUEUED);
     }
     __syncthreads();
     if (tid < K) {
@@ -661,7 +794,50 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       s_cnt[m] += tot;
       if (tot) s_clk[m] = fmax(s_clk[m], rows.arrival[s_last[m]]);
     }
+  }
+  // ---- Decision.estimated_loads + tie band, in parallel ----
+  // The loads row i saw: L0, then for each model the new load recorded by the
+  // last earlier row that dispatched to it (lnew).
+  {
+    double Lc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = s_lastm[k][tid];
+      Lc[k] = c >= 0 ? sc.lnew[c] : s_L0[k];
+    }
+    int n_rank = 0, n_qual = 0, n_any = 0;
+    for (int i = lo; i < hi; ++i) {
+      const int m = out.model[i];
+      if (sc.flags[i] & RF_ROUTE) {
+        double q[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = scores[(size_t)i * K + k];
+        if (out.loads) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) out.loads[(size_t)i * K + k] = Lc[k];
+        }
+        const uint8_t tb = tie_bits<K>(q, Lc, prm, m);
+        if (tb) {
+          out.flags[i] |= tb;  // this thread wrote the row's other flag bits
+          n_rank += (tb & DF_TIE_RANK) ? 1 : 0;
+          n_qual += (tb & DF_TIE_QUAL) ? 1 : 0;
+          n_any += 1;
+        }
+      }
+      const double ln = sc.lnew[i];
+#pragma unroll
+      for (int k = 0; k < K; ++k) Lc[k] = (k == m) ? ln : Lc[k];
+    }
+    __shared__ int s_ties[3];
+    if (tid < 3) s_ties[tid] = 0;
     __syncthreads();
+    if (n_any) {
+      atomicAdd(&s_ties[0], n_rank);
+      atomicAdd(&s_ties[1], n_qual);
+      atomicAdd(&s_ties[2], n_any);
+    }
+    __syncthreads();
+    if (tid < 3 && out.tie_counts) out.tie_counts[tid] = s_ties[tid];
   }
 
   if (tid == 0) {
@@ -678,9 +854,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     }
     *out.n_committed = s_committed;
   }
-  __syncthreads();
   // ---- post-pass: commit assignments and in-flight stage bits ----
-  const int n_ok = s_committed;
   for (int i = tid; i < n_ok; i += blockDim.x) {
     const int p = rows.program[i];
     if (sc.flags[i] & RF_ROUTE) mon.assignment[p] = (int8_t)out.model[i];
@@ -691,13 +865,14 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
 template <int K>
 static chm_status launch_schedule(const SelectParams& prm, const chm_monitor_state& mon,
                                   const chm_rows& rows, const chm_row_scratch& sc,
-                                  const float* scores, const double* yhat,
+                                  const double* scores, const double* yhat,
                                   const chm_decisions& out, cudaStream_t s) {
   const size_t smem = 2 * sizeof(ChunkBuf<K>);
-  cudaFuncSetAttribute(schedule_rows_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  const bool spec = prm.b_pow2_mask == (1u << K) - 1u;
+  auto kern = spec ? schedule_rows_kernel<K, true> : schedule_rows_kernel<K, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   prof::begin(prof::K_SELECT, s);
-  schedule_rows_kernel<K><<<1, kThreads, smem, s>>>(prm, mon, rows, sc, scores, yhat, out);
+  kern<<<1, kThreads, smem, s>>>(prm, mon, rows, sc, scores, yhat, out);
   // bytes per row: q 4K + yhat 8K + out_tokens 4K + program/stage/arrival 16 +
   // scratch 16 + outputs 21 (+ loads 8K)
   prof::end(prof::K_SELECT, s, (double)rows.n_rows * (24.0 * K + 53.0));
@@ -722,7 +897,7 @@ extern "C" chm_status chm_prepare_rows(const chm_monitor_state* mon, const chm_r
 
 extern "C" chm_status chm_schedule_rows(const chm_pool* pool, const chm_balancer_cfg* cfg,
                                         const chm_monitor_state* mon, const chm_rows* rows,
-                                        const chm_row_scratch* scratch, const float* scores,
+                                        const chm_row_scratch* scratch, const double* scores,
                                         const double* yhat, const chm_decisions* out,
                                         void* stream) {
   if (!pool || !cfg || !mon || !rows || !scratch || !out || !yhat || !scores)
@@ -746,6 +921,8 @@ extern "C" chm_status chm_schedule_rows(const chm_pool* pool, const chm_balancer
   }
   prm.one_plus_slack = 1.0 + cfg->latency_slack;
   prm.margin = cfg->confidence_margin;
+  prm.tie_tol = cfg->tie_tolerance;
+  if (!scratch->lnew) return CHM_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   switch (K) {
     case 1: return chm::launch_schedule<1>(prm, *mon, *rows, *scratch, scores, yhat, *out, s);

@@ -111,16 +111,40 @@ class _PtrArray:
         return ctypes.cast(self.arr, ctypes.c_void_p).value
 
 
+PAD_ID = 0  # BERT [PAD]
+
+
+def pack_tokens(seqs, seq_len: int, pad_id: int = PAD_ID) -> np.ndarray:
+    """Token id sequences -> int32 [B, seq_len]: truncated to seq_len, shorter
+    ones padded with `pad_id`. The encoder has no attention mask, so pad
+    positions are attended like any token -- in the fp32 restatement too."""
+    out = np.full((len(seqs), seq_len), pad_id, np.int32)
+    for i, s in enumerate(seqs):
+        a = np.asarray(s, dtype=np.int64)[:seq_len]
+        out[i, :len(a)] = a
+    return out
+
+
 class GpuEncoderRouter:
-    """Router backed by the sm_100a encoder (`score_rows` is the hot path)."""
+    """Router backed by the sm_100a encoder (`score_rows` is the hot path).
+
+    Drop-in for hetsched's `Router` (router.py:34-45): `score(req, rec, pool)`
+    returns a ConfidenceVector over `pool.model_ids`, and `columns_for(reqs,
+    recs)` supplies the token-id column `GpuScheduler.schedule_batch` batches.
+    The token ids come from `tokens(req, rec) -> sequence of int` (the caller's
+    tokenizer or token store; e.g. a dict lookup by request or program id),
+    packed to `cfg.seq_len` by `pack_tokens`. Head row m scores the m-th
+    model of `pool.model_ids` (sorted ids, the device's model order)."""
 
     name = "encoder"
 
     def __init__(self, cfg: EncoderConfig, n_models: int, weights: dict | None = None,
-                 max_rows: int = 4096, seed: int = 0, head_std: float = 0.02, device="cuda"):
+                 max_rows: int = 4096, seed: int = 0, head_std: float = 0.02, device="cuda",
+                 tokens=None):
         self.lib = _lib.load()
         self.cfg = cfg
         self.K = n_models
+        self.tokens = tokens
         self.device = torch.device(device)
         self.weights = weights if weights is not None else init_weights(
             cfg, n_models, seed, head_std, self.device)
@@ -171,6 +195,8 @@ class GpuEncoderRouter:
                 n_seq: int | None = None, stream=None) -> None:
         """q_out[row*K + m] for the listed rows (all rows when `rows` is None)."""
         n_seq = token_ids.shape[0] if n_seq is None else n_seq
+        if q_out.dtype != torch.float64:
+            raise TypeError("q_out must be float64 (the scheduler's score buffer is fp64)")
         if n_seq > self.max_rows:
             raise ValueError(f"{n_seq} sequences exceed max_rows={self.max_rows}")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -187,9 +213,23 @@ class GpuEncoderRouter:
         self.forward(batch.token_ids, scores, rows=route_rows, n_rows=n_route,
                      n_seq=batch.n_rows, stream=stream)
 
-    def score(self, req, rec, pool, token_ids: np.ndarray) -> dict:
-        """Single-request compatibility path (router.py:39-42)."""
-        ids = torch.as_tensor(token_ids.reshape(1, -1).astype(np.int32), device=self.device)
-        q = torch.empty(self.K, dtype=torch.float32, device=self.device)
+    def _token_ids(self, reqs, recs) -> np.ndarray:
+        if self.tokens is None:
+            raise ValueError("GpuEncoderRouter needs a token source: GpuEncoderRouter(..., "
+                             "tokens=lambda req, rec: ids)")
+        return pack_tokens([self.tokens(r, rc) for r, rc in zip(reqs, recs)], self.cfg.seq_len)
+
+    def columns_for(self, reqs, recs) -> dict:
+        """The router's batch column (GpuScheduler.rows_from_requests)."""
+        return {"token_ids": self._token_ids(reqs, recs)}
+
+    def score(self, req, rec, pool) -> "ConfidenceVector":
+        """Router.score (router.py:39-42) for one request: one sequence through
+        the same device encoder, fp64 scores keyed by pool.model_ids."""
+        from .router import ConfidenceVector
+        if len(pool.model_ids) != self.K:
+            raise ValueError(f"router has {self.K} heads, pool has {len(pool.model_ids)} models")
+        ids = torch.as_tensor(self._token_ids([req], [rec]), device=self.device)
+        q = torch.empty(self.K, dtype=torch.float64, device=self.device)
         self.forward(ids, q)
-        return dict(zip(pool.model_ids, q.cpu().tolist()))
+        return ConfidenceVector(dict(zip(pool.model_ids, q.cpu().tolist())))

@@ -131,7 +131,7 @@ class BatchBuffers:
         self.qual = torch.empty(B, dtype=torch.int64, device=d)
         self.rank = torch.empty(B, dtype=torch.int32, device=d)
         self.flags = torch.empty(B, dtype=torch.int32, device=d)
-        self.scores = torch.zeros(B * K, dtype=torch.float32, device=d)
+        self.scores = torch.zeros(B * K, dtype=torch.float64, device=d)  # fp64 like ConfidenceVector
         self.yhat = torch.zeros(B * K, dtype=torch.float64, device=d)
         self.model = torch.full((B,), -1, dtype=torch.int32, device=d)
         self.priority = torch.zeros(B, dtype=torch.float64, device=d)
@@ -140,16 +140,22 @@ class BatchBuffers:
         self.loads = torch.zeros(B * K, dtype=torch.float64, device=d)
         self.n_committed = torch.zeros(1, dtype=torch.int32, device=d)
         self.n_complete = torch.zeros(K, dtype=torch.int32, device=d)
+        self.lnew = torch.zeros(B, dtype=torch.float64, device=d)
+        self.tie_counts = torch.zeros(3, dtype=torch.int32, device=d)
+        # error words: the batch's (predictor / K6 / K7, lowest row wins) and
+        # the completions' (record_completion runs before the batch)
         self.error = torch.zeros(4, dtype=torch.int32, device=d)
+        self.error_complete = torch.zeros(4, dtype=torch.int32, device=d)
         self.error_init = torch.tensor([0, INT32_MAX, -1, 0], dtype=torch.int32, device=d)
+        self.error_complete.copy_(self.error_init)
         self.scratch_c = _lib.RowScratch(
             _p(self.first_row), _p(self.pre_model), _p(self.route_rows), _p(self.n_route),
-            _p(self.qual), _p(self.rank), _p(self.flags))
+            _p(self.qual), _p(self.rank), _p(self.flags), _p(self.lnew))
 
     def decisions_struct(self, with_loads: bool = True) -> _lib.Decisions:
         return _lib.Decisions(_p(self.model), _p(self.priority), _p(self.dflags), _p(self.seq),
                               _p(self.loads) if with_loads else None, _p(self.n_committed),
-                              _p(self.error))
+                              _p(self.error), _p(self.tie_counts))
 
 
 class GpuScheduler:
@@ -160,7 +166,7 @@ class GpuScheduler:
                  n_programs: int = 1 << 20, max_rows: int = 16384,
                  queue_capacity: int = 10240, device="cuda", inflight_capacity=None,
                  decay_in_flight: bool = False, engine_clock: bool = False,
-                 completion_capacity: int | None = None):
+                 completion_capacity: int | None = None, tie_tolerance: float = 2e-2):
         self.lib = _lib.load()
         self.pool = pool
         self.ids = pool.model_ids
@@ -179,7 +185,8 @@ class GpuScheduler:
                 completion_capacity if completion_capacity is not None
                 else queue_capacity + max(p.max_batch_size for p in pool.profiles))
         self.buf = BatchBuffers(self.K, max_rows, self.device)
-        self.bal_c = balancer_struct(balancer)
+        self.tie_tolerance = float(tie_tolerance)
+        self.bal_c = balancer_struct(balancer, self.tie_tolerance)
         self.aging_c = aging_struct(aging)
         self._program_index: dict[str, int] = {}
         self._handles: list = []
@@ -207,6 +214,7 @@ class GpuScheduler:
         dec_c = buf.decisions_struct(with_loads)
         with torch.cuda.stream(s):
             buf.error.copy_(buf.error_init)
+            buf.error_complete.copy_(buf.error_init)
             if not keep_admitted:
                 st.q_n_admitted.zero_()
                 st.q_n_promoted.zero_()
@@ -217,13 +225,15 @@ class GpuScheduler:
                 c_model, c_key = completions
                 _lib.check(lib.chm_monitor_complete(st.pool_c, st.monitor_c, _p(c_model),
                                                     _p(c_key), int(c_model.numel()),
-                                                    _p(buf.n_complete), _p(buf.error), sh),
+                                                    _p(buf.n_complete), _p(buf.error_complete),
+                                                    sh),
                            "chm_monitor_complete")
                 n_complete = buf.n_complete
             if n_complete is not None:
                 _lib.check(lib.chm_queue_complete(st.pool_c, self.aging_c, st.monitor_c,
-                                                  st.queue_c, _p(n_complete), _p(buf.error),
-                                                  sh), "chm_queue_complete")
+                                                  st.queue_c, _p(n_complete),
+                                                  _p(buf.error_complete), sh),
+                           "chm_queue_complete")
             _lib.check(lib.chm_prepare_rows(st.monitor_c, rows_c, buf.scratch_c,
                                             _p(st.epoch), sh), "chm_prepare_rows")
             if self.router is None:
@@ -336,7 +346,25 @@ class GpuScheduler:
                                                    s.cuda_stream), "chm_queue_admit_merged")
 
     def check_errors(self, context: str = "") -> None:
+        """Raise the reference exception for the last tick, if any: a
+        completion error first (record_completion ran before the batch),
+        then the batch's lowest-row error."""
+        _lib.raise_device_error(self.buf.error_complete.cpu().tolist(),
+                                (context + " completions").strip())
         _lib.raise_device_error(self.buf.error.cpu().tolist(), context)
+
+    def tie_band(self) -> dict:
+        """Tie-band report of the last batch (north star: "ties inside the
+        tolerance band are reported"): routed decisions whose descending-q
+        choice (`rank`) or confidence gate q_m >= q_fast + margin (`gate`)
+        compares two router outputs that are within `tie_tolerance`, and
+        either (`any`). The default 2e-2 is twice the router's 1e-2 tolerance
+        (both sides of each comparison carry router error), so every decision
+        a router error <= 1e-2 could flip is counted. Per-row bits: Decision
+        flags 8 / 16 (`buf.dflags`)."""
+        r, g, a = (int(x) for x in self.buf.tie_counts.cpu().tolist())
+        return {"tolerance": self.tie_tolerance, "rank": r, "gate": g, "any": a,
+                "routed": int(self.buf.n_route.item())}
 
     # ------------------------------------------------------ reference-style API
     def program_index(self, program_id: str) -> int:
@@ -387,6 +415,10 @@ class GpuScheduler:
         buf, K = self.buf, self.K
         B = batch.n_rows
         n_ok = int(buf.n_committed.item())
+        err_code, err_row = (int(x) for x in buf.error[:2].cpu().tolist())
+        if err_code:
+            # the reference raised at err_row: no decisions for it or later rows
+            n_ok = min(n_ok, err_row)
         model = buf.model[:n_ok].cpu().numpy()
         prio = buf.priority[:n_ok].cpu().numpy()
         fl = buf.dflags[:n_ok].cpu().numpy()

@@ -281,8 +281,9 @@ def request_key(program: int, stage: int) -> int:
     return int(program) * 32 + (int(stage) - 1)
 
 
-def balancer_struct(cfg: BalancerConfig) -> _lib.BalancerCfg:
-    return _lib.BalancerCfg(float(cfg.latency_slack), float(cfg.confidence_margin))
+def balancer_struct(cfg: BalancerConfig, tie_tolerance: float = 2e-2) -> _lib.BalancerCfg:
+    return _lib.BalancerCfg(float(cfg.latency_slack), float(cfg.confidence_margin),
+                            float(tie_tolerance))
 
 
 def aging_struct(aging: AgingConfig) -> _lib.AgingCfg:

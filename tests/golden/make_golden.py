@@ -80,6 +80,20 @@ def make_select_kat():
         tau = float(rng.choice([0.0, 0.25, 0.5, 1.0, 3.0, 1e6]))
         dm = float(rng.choice([0.0, 0.05, 0.1, 0.3, 1.0]))
         cases.append((list(q), list(loads), tau, dm))
+    # decimal table scores (TableRouter-style 0.1 steps, not fp32-representable):
+    # with margin 0.1, (0.9 vs 0.8) and (0.4 vs 0.3) clear the margin in fp64
+    # but (0.3 vs 0.2) does not -- fp32-rounded scores get each of them wrong
+    cases.append(([0.8, 0.9], [100.0, 120.0], 0.5, 0.1))
+    cases.append(([0.3, 0.4], [100.0, 120.0], 0.5, 0.1))
+    cases.append(([0.2, 0.3], [100.0, 120.0], 0.5, 0.1))
+    rng2 = np.random.default_rng(8)
+    for _ in range(1000):
+        k = int(rng2.integers(2, 9))
+        q = rng2.integers(0, 11, size=k) / 10.0
+        loads = rng2.integers(0, 6, size=k).astype(np.float64) * 100.0
+        tau = float(rng2.choice([0.0, 0.5, 1.0, 1e6]))
+        dm = float(rng2.choice([0.1, 0.2, 0.3]))
+        cases.append((list(q), list(loads), tau, dm))
     K = 8
     Q = np.full((len(cases), K), np.nan)
     L = np.full((len(cases), K), np.nan)
@@ -125,7 +139,7 @@ class ShimPredictor(predictor.Predictor):
 
 def build_scenario(seed, k, n_rows, *, dyadic=True, p0_entries=0, pre_assigned=0.0,
                    repeats=0.0, batch=None, decode=None, pre_running=None, tau=0.5,
-                   margin=0.1, spread=1.0, tied_q=False):
+                   margin=0.1, spread=1.0, tied_q=False, table_q=False):
     rng = np.random.default_rng(seed)
     ids = model_ids(k)
     decode = decode or [5.0 * (i + 1) for i in range(k)]
@@ -153,6 +167,8 @@ def build_scenario(seed, k, n_rows, *, dyadic=True, p0_entries=0, pre_assigned=0
     if tied_q:
         q = np.round(q * 4) / 4
     q = np.clip(q, 0, 1).astype(np.float32)
+    if table_q:  # TableRouter-style decimal scores, exact fp64 (router.py:71-88)
+        q = rng.integers(0, 11, size=(n_rows, k)) / 10.0
     if dyadic:
         yhat = rng.integers(0, 4000, size=(n_rows, k)).astype(np.float64) / 2.0
     else:
@@ -283,6 +299,9 @@ def make_schedules():
         "k5_slack_big": dict(seed=7, k=5, n_rows=1000, tau=1e6, margin=0.0),
         "k2_spread": dict(seed=8, k=2, n_rows=800, spread=0.2, pre_running=[31, 0]),
         "k1_single": dict(seed=9, k=1, n_rows=300),
+        "k3_table": dict(seed=11, k=3, n_rows=700, table_q=True, margin=0.1, tau=1.0),
+        "k5_table": dict(seed=12, k=5, n_rows=900, table_q=True, margin=0.2, tau=0.5,
+                         dyadic=False, p0_entries=40),
         "k6_running": dict(seed=10, k=6, n_rows=1000, pre_running=[5, 16, 8, 0, 2, 1],
                            repeats=0.1, pre_assigned=0.1),
     }
@@ -883,6 +902,10 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["engines"]:
         print("engines:", make_engines())
+        sys.exit(0)
+    if sys.argv[1:] == ["select"]:
+        print("select cases:", make_select_kat())
+        print("schedule:", make_schedules())
         sys.exit(0)
     if sys.argv[1:] == ["completions"]:
         print("completions:", make_completions())

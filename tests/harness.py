@@ -10,7 +10,7 @@ import numpy as np
 
 from oracle import hetsched_port as hp
 from paper_2603_22206_b200.config import ModelProfile, Pool
-from paper_2603_22206_b200.workload import ModelStageOutput, Request, StageTrace, TraceRecord
+from workloads.tracegen import ModelStageOutput, Request, StageTrace, TraceRecord
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 

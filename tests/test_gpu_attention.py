@@ -100,10 +100,10 @@ def test_encoder_fused_equals_unfused():
     K, B = 5, 48
     r = GpuEncoderRouter(SMALL, K, max_rows=B, seed=11, head_std=2 / math.sqrt(256))
     ids = torch.as_tensor(synthetic_token_ids(B, 128, seed=3), device="cuda")
-    q_f = torch.zeros(B * K, device="cuda")
+    q_f = torch.zeros(B * K, dtype=torch.float64, device="cuda")
     r.forward(ids, q_f)
     r.cfg_c.flags = _lib.ENC_UNFUSED_ATTENTION
-    q_u = torch.zeros(B * K, device="cuda")
+    q_u = torch.zeros(B * K, dtype=torch.float64, device="cuda")
     r.forward(ids, q_u)
     r.cfg_c.flags = 0
     torch.cuda.synchronize()

@@ -59,7 +59,7 @@ def test_evaluate_predictor_on_trace(gold):
     from paper_2603_22206_b200.predictor import (GpuInputLengthPredictor, GpuOraclePredictor,
                                                  GpuQuantilePredictor)
     from paper_2603_22206_b200.trace import TraceStore, columns_from_records, load_ndjson
-    from paper_2603_22206_b200.workload import ModelStageOutput, StageTrace, TraceRecord
+    from workloads.tracegen import ModelStageOutput, StageTrace, TraceRecord
 
     cols = load_ndjson(os.path.join(GOLD, "trace_small.ndjson"))
     ids = cols.model_ids
@@ -92,7 +92,7 @@ def test_quantile_training_on_device(q):
     the reference's EmpiricalQuantilePredictor (tests/golden/quantile.npz grid)."""
     from paper_2603_22206_b200.predictor import GpuQuantilePredictor
     from paper_2603_22206_b200.trace import TraceStore
-    from paper_2603_22206_b200.workload import MATH_WORKFLOWS, LengthStats, synthesize_trace
+    from workloads.tracegen import MATH_WORKFLOWS, LengthStats, synthesize_trace
     from tests.test_oracle import MATH_STATS, MATH_SUCCESS  # the golden generator's inputs
 
     stats = {m: LengthStats(*v) for m, v in MATH_STATS.items()}

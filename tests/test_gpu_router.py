@@ -92,7 +92,7 @@ def test_encoder_matches_fp32(cfg, head_std):
     K, B = 5, 24
     r = GpuEncoderRouter(cfg, K, max_rows=B, seed=3, head_std=head_std)
     ids = torch.as_tensor(synthetic_token_ids(B, cfg.seq_len, seed=11), device="cuda")
-    q = torch.zeros(B * K, dtype=torch.float32, device="cuda")
+    q = torch.zeros(B * K, dtype=torch.float64, device="cuda")
     r.forward(ids, q)
     torch.cuda.synchronize()
     got = q.view(B, K).cpu().numpy()
@@ -110,7 +110,7 @@ def test_encoder_long_prompts(S):
     K, B = 5, 6
     r = GpuEncoderRouter(cfg, K, max_rows=B, seed=8, head_std=2 / math.sqrt(256))
     ids = torch.as_tensor(synthetic_token_ids(B, S, seed=21), device="cuda")
-    q = torch.zeros(B * K, dtype=torch.float32, device="cuda")
+    q = torch.zeros(B * K, dtype=torch.float64, device="cuda")
     r.forward(ids, q)
     torch.cuda.synchronize()
     err = np.abs(q.view(B, K).cpu().numpy() - _ref_q(r, ids)).max()
@@ -125,7 +125,7 @@ def test_encoder_routed_rows_only():
     rows = torch.tensor([3, 7, 8, 15, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0], dtype=torch.int32,
                         device="cuda")
     n = torch.tensor([4], dtype=torch.int32, device="cuda")
-    q = torch.full((B * K,), -1.0, device="cuda")
+    q = torch.full((B * K,), -1.0, dtype=torch.float64, device="cuda")
     r.forward(ids, q, rows=rows, n_rows=n, n_seq=B)
     torch.cuda.synchronize()
     got = q.view(B, K).cpu().numpy()
@@ -232,7 +232,7 @@ def test_encoder_random_layernorm_params(cfg, S, flags):
                 t.copy_(0.2 * torch.randn(t.shape, device="cuda", generator=gen))
     r.refold()
     ids = torch.as_tensor(synthetic_token_ids(B, S, seed=31), device="cuda")
-    q = torch.zeros(B * K, dtype=torch.float32, device="cuda")
+    q = torch.zeros(B * K, dtype=torch.float64, device="cuda")
     r.forward(ids, q)
     torch.cuda.synchronize()
     err = np.abs(q.view(B, K).cpu().numpy() - _ref_q(r, ids)).max()

@@ -12,6 +12,7 @@ from paper_2603_22206_b200.config import AgingConfig, BalancerConfig
 from paper_2603_22206_b200.predictor import PrecomputedPredictor
 from paper_2603_22206_b200.router import ScoreTableRouter
 from paper_2603_22206_b200.scheduler import GpuScheduler, RowBatch
+from oracle import hetsched_port as hp
 from tests import harness as H
 
 pytestmark = pytest.mark.gpu
@@ -90,6 +91,21 @@ def test_schedule_matches_reference(name):
         assert res["error"][1] == sc["err_row"]
     else:
         assert res["error"][0] == 0
+    # tie band (flag bits 3 / 4) against the oracle's definition on the same keys
+    ids = sc["ids"]
+    want_rank = np.zeros(n, np.uint8)
+    want_gate = np.zeros(n, np.uint8)
+    for i in np.nonzero(routed)[0]:
+        q = {m: float(sc["q"][i, k]) for k, m in enumerate(ids)}
+        loads = {m: float(sc["out_loads"][i, k]) for k, m in enumerate(ids)}
+        rk, gt = hp.port_tie_band(q, loads, ids[sc["out_model"][i]], sc["tau"], sc["margin"],
+                                  gs.tie_tolerance)
+        want_rank[i], want_gate[i] = rk, gt
+    np.testing.assert_array_equal((res["flags"][:n] >> 3) & 1, want_rank)
+    np.testing.assert_array_equal((res["flags"][:n] >> 4) & 1, want_gate)
+    tb = gs.tie_band()
+    assert (tb["rank"], tb["gate"], tb["any"]) == (
+        int(want_rank.sum()), int(want_gate.sum()), int((want_rank | want_gate).sum()))
 
 
 def test_schedule_batch_object_api():
@@ -110,8 +126,7 @@ def test_schedule_batch_object_api():
         assert d.used_cached_assignment == bool(port["cached"][i])
         if not d.used_cached_assignment:
             assert [d.estimated_loads[m] for m in sc["ids"]] == port["loads"][i].tolist()
-            assert d.scores == {m: float(np.float32(sc["q"][i, k]))
-                                for k, m in enumerate(sc["ids"])}
+            assert d.scores == {m: float(sc["q"][i, k]) for k, m in enumerate(sc["ids"])}
 
 
 def test_nan_prediction_rejected():
@@ -142,3 +157,46 @@ def test_two_batches_continue_state():
         outs.append(gs.buf.model[:hi - lo].cpu().numpy().copy())
     np.testing.assert_array_equal(np.concatenate(outs), sc["out_model"])
     assert np.array(gs.state.in_flight_sums()).tobytes() == sc["out_final_p"].tobytes()
+
+
+@pytest.mark.parametrize("exact_chain", [False, True])
+def test_select_kat_through_k6(exact_chain):
+    """Every select_model case of tests/golden/select_kat.npz (5,006: SPEC
+    examples, AC2 random instances with ties, tau in {0, 1e6}, margin in
+    {0, 1}, decimal table scores) as a one-row batch through K6: loads are
+    installed as in-flight sums with d = b = 1 (L = P exactly). exact_chain
+    adds a repeat row so the batch takes K6's exact (erroring) chain instead
+    of the fast one. balancer.py:63-77."""
+    import os
+    z = np.load(os.path.join(H.GOLDEN, "select_kat.npz"))
+    from paper_2603_22206_b200.config import ModelProfile, Pool
+    n_cases = len(z["k"])
+    by_k = {}
+    for k in range(1, 9):
+        pool = Pool(tuple(ModelProfile(f"m{i}", 1.0, 1) for i in range(k)))
+        rt, pr = ScoreTableRouter(), PrecomputedPredictor()
+        gs = GpuScheduler(pool, BalancerConfig(0.5, 0.1), AgingConfig(), router=rt, predictor=pr,
+                          n_programs=2 * n_cases + 2, max_rows=2, queue_capacity=16)
+        by_k[k] = (gs, rt, pr)
+    dev = torch.device("cuda")
+    got = np.full(n_cases, -1, np.int32)
+    for i in range(n_cases):
+        k = int(z["k"][i])
+        gs, rt, pr = by_k[k]
+        st = gs.state
+        tau, dm = (float(x) for x in z["cfg"][i])
+        gs.bal_c.latency_slack, gs.bal_c.confidence_margin = tau, dm
+        st.inflight_sum.copy_(torch.as_tensor(z["loads"][i, :k]))
+        st.inflight_comp.zero_()
+        st.engine_running.zero_()
+        st.engine_queued.zero_()
+        rows = 2 if exact_chain else 1
+        rt.set(torch.as_tensor(np.repeat(z["q"][i:i + 1, :k], rows, 0), device=dev))
+        pr.set(torch.zeros((rows, k), dtype=torch.float64, device=dev))
+        batch = RowBatch.from_numpy(dev, program=[2 * i] * rows, stage=list(range(1, rows + 1)),
+                                    arrival=[0.0] * rows, out_tokens=np.zeros((rows, k)),
+                                    handle=np.arange(rows))
+        gs.run_rows(batch, n_iterations=0)
+        got[i] = int(gs.buf.model[0].item())
+        assert int(gs.buf.n_committed.item()) == rows
+    np.testing.assert_array_equal(got, z["chosen"])

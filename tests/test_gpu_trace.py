@@ -196,7 +196,7 @@ def test_two_tick_stage_chaining_vs_oracle_port(store):
 
     def run(program, stage, arrival):
         n = len(program)
-        q = rng.random((n, K)).astype(np.float32).astype(np.float64)  # router scores are fp32
+        q = rng.random((n, K))  # fp64 scores (ConfidenceVector holds Python floats)
         rt.set(torch.as_tensor(q, device=d))
         P = torch.as_tensor(np.asarray(program, np.int32), device=d)
         batch = store.make_batch(P, torch.as_tensor(np.asarray(stage, np.int32), device=d),
@@ -225,3 +225,85 @@ def test_two_tick_stage_chaining_vs_oracle_port(store):
     assert n2 == int(np.sum(cols.n_stages > 1))
     p2 = nxt["program"][:n2].cpu().tolist()
     run(p2, nxt["stage"][:n2].cpu().tolist(), nxt["arrival"][:n2].cpu().tolist())
+
+
+@pytest.mark.parametrize("source", ["store", "columns"])
+def test_predictor_error_stops_the_batch(store, source):
+    """An UnknownStage raised by OraclePredictor.predict at row r (stage past
+    the program's last) stops the batch there, as the reference's serial loop
+    does: rows < r are scheduled, row r keeps only monitor.assign
+    (balancer.py:113-115), later rows are untouched."""
+    from oracle import hetsched_port as hp
+    from paper_2603_22206_b200.config import BalancerConfig, ModelProfile, Pool
+    from paper_2603_22206_b200.predictor import GpuOraclePredictor
+    from paper_2603_22206_b200.router import ScoreTableRouter
+    from paper_2603_22206_b200.scheduler import GpuScheduler, RowBatch
+
+    cols, ids, K, d = store.cols, store.model_ids, store.K, "cuda"
+    NP = store.n_programs
+    n = min(NP, 40)
+    r = 17
+    pool = Pool(tuple(ModelProfile(m, 5.0 * (k + 1), max(1, 8 >> k)) for k, m in enumerate(ids)))
+    rt = ScoreTableRouter()
+    S = int(cols.n_stages.max())
+    pred = GpuOraclePredictor(max_stages=S, trace=store if source == "store" else None)
+    gs = GpuScheduler(pool, BalancerConfig(0.5, 0.1), router=rt, predictor=pred,
+                      n_programs=NP, max_rows=n)
+    prog = np.arange(n, dtype=np.int32)
+    stage = np.ones(n, np.int32)
+    stage[r] = int(cols.n_stages[r]) + 1  # UnknownStage at row r
+    q = np.random.default_rng(5).random((n, K))
+    rt.set(torch.as_tensor(q, device=d))
+    extra = {}
+    if source == "columns":
+        extra = dict(n_stages=cols.n_stages[:n], stage_out=cols.out_tokens[:n, :S])
+    batch = RowBatch.from_numpy(d, program=prog, stage=stage, arrival=np.zeros(n),
+                                out_tokens=cols.out_tokens[prog, 0], handle=np.arange(n),
+                                **extra)
+    gs.run_rows(batch, n_iterations=0)
+    torch.cuda.synchronize()
+    with pytest.raises(errors.UnknownStage):
+        gs.check_errors("predictor error")
+    assert int(gs.buf.n_committed.item()) == r
+
+    class _Rec:
+        def __init__(self, p):
+            self.p = p
+
+        def remaining_tokens(self, s, m):
+            if not 1 <= s <= cols.n_stages[self.p]:
+                raise hp.PortError("UnknownStage", f"stage {s}")
+            k = ids.index(m)
+            return int(cols.out_tokens[self.p, s - 1:cols.n_stages[self.p], k].astype(np.int64).sum())
+
+        def out_tokens(self, s, m):
+            return int(cols.out_tokens[self.p, s - 1, ids.index(m)])
+
+    class _Req:
+        def __init__(self, p, s):
+            self.program_id, self.stage_index, self.arrival_time = f"t{p}", s, 0.0
+            self.request_id = f"t{p}:{s}"
+
+    mon = hp.PortMonitor(ids)
+    engines = {m: hp.PortEngine(pool[m].max_batch_size) for m in ids}
+    got_m = gs.buf.model[:r].cpu().numpy()
+    for i in range(n):
+        try:
+            dec = hp.port_schedule_request(
+                _Req(prog[i], stage[i]), _Rec(prog[i]), pool, mon, engines,
+                lambda rq, rc, i=i: {m: float(q[i, k]) for k, m in enumerate(ids)},
+                hp.port_oracle_predict, 0.5, 0.1)
+        except hp.PortError as exc:
+            assert exc.kind == "UnknownStage" and i == r
+            break
+        assert ids[got_m[i]] == dec.model
+    want_p = np.array([mon.in_flight_sum(m) for m in ids])
+    assert np.array(gs.state.in_flight_sums()).tobytes() == want_p.tobytes()
+    assign = gs.state.assignment[:n].cpu().numpy()
+    for p in range(n):
+        a = mon.assignment(f"t{p}")
+        assert assign[p] == (-1 if a is None else ids.index(a)), p
+    # decisions for the rows before the error ride on the exception
+    with pytest.raises(errors.UnknownStage) as ei:
+        gs.collect(batch)
+    assert len(ei.value.decisions) == r

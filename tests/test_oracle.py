@@ -34,6 +34,29 @@ def test_spec_examples():
     assert 1000.0 * 20.0 / 8 == 2500.0
 
 
+def test_tie_band_definition():
+    """port_tie_band (the definition the device tie flags are checked against):
+    a decision is flagged when a router error of tol could flip it."""
+    # gate: B at 0.9 vs A's 0.4 + 0.1 = 0.5 -> clear by 0.4; no tie
+    assert hp.port_tie_band({"A": 0.4, "B": 0.9}, {"A": 100.0, "B": 140.0}, "B", 0.5, 0.1) == \
+        (False, False)
+    # gate: B at 0.505 sits within 1e-2 of 0.5
+    assert hp.port_tie_band({"A": 0.4, "B": 0.505}, {"A": 100.0, "B": 140.0}, "B", 0.5, 0.1) == \
+        (False, True)
+    # B outside the slack: its gate comparison cannot matter
+    assert hp.port_tie_band({"A": 0.4, "B": 0.505}, {"A": 100.0, "B": 300.0}, "A", 0.5, 0.1) == \
+        (False, False)
+    # rank: B and C both qualify and differ by 0.005
+    assert hp.port_tie_band({"A": 0.3, "B": 0.7, "C": 0.695}, {"A": 10.0, "B": 10.0, "C": 10.0},
+                            "B", 0.5, 0.0) == (True, False)
+    # exact q tie between candidates (broken by id) is a rank tie
+    assert hp.port_tie_band({"A": 0.3, "B": 0.7, "C": 0.7}, {"A": 10.0, "B": 10.0, "C": 10.0},
+                            "B", 0.5, 0.0)[0]
+    # no candidate: m_fast chosen, no rank tie
+    assert hp.port_tie_band({"A": 0.5, "B": 0.55}, {"A": 1.0, "B": 1.0}, "A", 0.0, 0.2) == \
+        (False, False)
+
+
 @pytest.mark.parametrize("name", H.schedule_names())
 def test_schedule_port_matches_reference(name):
     sc = H.load_schedule(name)
@@ -84,7 +107,7 @@ MATH_SUCCESS = {"m0": {"easy": 0.55, "hard": 0.12}, "m1": {"easy": 0.72, "hard":
 
 
 def _math_trace():
-    from paper_2603_22206_b200 import workload as W
+    from workloads import tracegen as W
     stats = {m: W.LengthStats(*v) for m, v in MATH_STATS.items()}
     return W.synthesize_trace(W.MATH_WORKFLOWS, stats, MATH_SUCCESS, 2000, 1)
 
@@ -109,7 +132,7 @@ def _digest(tr):
 
 
 def test_synthesize_trace_matches_reference():
-    from paper_2603_22206_b200 import workload as W
+    from workloads import tracegen as W
     gold = json.load(open(os.path.join(H.GOLDEN, "synth.json")))
     assert _digest(_math_trace()) == gold["math_2000_1"]
     cs = {"fast": W.LengthStats(447, 1276), "strong": W.LengthStats(649, 534)}

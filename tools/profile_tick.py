@@ -20,7 +20,7 @@ def main():
     a = p.parse_args()
     import torch
 
-    from paper_2603_22206_b200 import synth
+    from workloads import synth
     from paper_2603_22206_b200.scheduler import GpuScheduler
 
     wl = synth.make_workload(a.config)

@@ -19,11 +19,12 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .config import AgingConfig, BalancerConfig, ModelProfile, Pool
-from .encoder import BERT_BASE, SMALL, EncoderConfig, GpuEncoderRouter, synthetic_token_ids
-from .predictor import GpuQuantilePredictor
-from .scheduler import RowBatch
-from . import workload as W
+from paper_2603_22206_b200.config import AgingConfig, BalancerConfig, ModelProfile, Pool
+from paper_2603_22206_b200.encoder import (BERT_BASE, SMALL, EncoderConfig, GpuEncoderRouter,
+                                           synthetic_token_ids)
+from paper_2603_22206_b200.predictor import GpuQuantilePredictor
+from paper_2603_22206_b200.scheduler import RowBatch
+from . import tracegen as W
 
 APPS = ((447.0, 1276.0), (649.0, 534.0))
 MATH = ((606.0, 2587.0), (709.0, 715.0))
@@ -195,12 +196,6 @@ class Workload:
         return (torch.tensor(models, dtype=torch.int32, device=self.device),
                 torch.tensor(keys, dtype=torch.int64, device=self.device))
 
-    def router_reference(self, batch: RowBatch) -> np.ndarray:
-        from oracle.encoder_ref import encoder_forward_fp32  # test infrastructure
-        r = self.router
-        return encoder_forward_fp32(r.weights, batch.token_ids, r.cfg.n_layers, r.cfg.n_heads,
-                                    r.cfg.ln_eps).cpu().numpy()
-
 
 def make_workload(name: str, device="cuda", with_router: bool = True) -> Workload:
     sp = SPECS[name]
@@ -217,44 +212,3 @@ def make_workload(name: str, device="cuda", with_router: bool = True) -> Workloa
                                   device=dev)
     return Workload(sp, pool, BalancerConfig(0.5, 0.1), AgingConfig(8, 4), router, pred,
                     training, dev, n_programs=4 * sp.batch)
-
-
-def oracle_tick(wl: Workload, batch: RowBatch, q: np.ndarray, hp, n_iterations: int = 1):
-    """Replay the batch through the CPU oracle (hp = oracle.hetsched_port) with
-    the GPU's router output as the scores. Returns models / priorities."""
-    ids = wl.pool.model_ids
-    mon = hp.PortMonitor(ids)
-    engines = {m: hp.PortEngine(wl.pool[m].max_batch_size) for m in ids}
-    port_pred = hp.PortQuantilePredictor(wl.training, 0.5)
-    prog = batch.program.cpu().numpy()
-    arr = batch.arrival.cpu().numpy()
-    wf_idx = batch.workflow.cpu().numpy()
-    inv_wf = {v: k for k, v in wl.predictor.workflow_index.items()}
-    out_tok = batch.out_tokens.cpu().numpy()
-
-    class _Req:
-        __slots__ = ("program_id", "stage_index", "arrival_time", "workflow_id", "request_id")
-
-    class _Rec:
-        def __init__(self, row):
-            self.row = row
-
-        def out_tokens(self, stage, m):
-            return int(out_tok[self.row, ids.index(m)])
-
-    models = np.empty(len(prog), np.int32)
-    prios = np.empty(len(prog))
-    for i in range(len(prog)):
-        r = _Req()
-        r.program_id = f"p{int(prog[i])}"
-        r.stage_index = 1
-        r.arrival_time = float(arr[i])
-        r.workflow_id = inv_wf.get(int(wf_idx[i]), "?")
-        r.request_id = f"{r.program_id}:1"
-        d = hp.port_schedule_request(
-            r, _Rec(i), wl.pool, mon, engines,
-            lambda rq, rc, i=i: {m: float(q[i, k]) for k, m in enumerate(ids)},
-            port_pred, wl.balancer.latency_slack, wl.balancer.confidence_margin)
-        models[i] = ids.index(d.model)
-        prios[i] = d.priority
-    return {"model": models, "priority": prios, "engines": engines, "monitor": mon}

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import InvalidStats, UnknownStage, ValidationError
+from paper_2603_22206_b200.errors import InvalidStats, UnknownStage, ValidationError
 
 
 @dataclass(frozen=True)
