@@ -512,6 +512,23 @@ def run_ours(args):
     queued_end = int(gs.state.engine_queued.sum().item())
     n_queued_rows = int(((gs.buf.dflags[:B] & 4) != 0).sum().item())
 
+    # ---------- N > 1: decisions Mode A changes against Mode B ----------
+    divergence = None
+    if world > 1:
+        from paper_2603_22206_b200.dist import divergence as _div
+        got = {}
+        for mode in ("A", "B"):
+            sched.mode = mode
+            gs.state.restore(snap)
+            kw = {"completions": completions} if completions is not None else {}
+            sched.run_rows(batches[0], n_iterations=1, n_complete=n_complete, stream=stream,
+                           **kw)
+            torch.cuda.synchronize()
+            got[mode] = gs.buf.model[:B].to(torch.int64).clone()
+        sched.mode = args.mode
+        divergence = {"decisions_differing_a_vs_b": _div(got["A"], got["B"], sched.comm, stream),
+                      "of": B * world}
+
     # ---------------- end-to-end through the public API ----------------
     e2e = None
     if not args.no_e2e:
@@ -631,6 +648,8 @@ def run_ours(args):
         "tie_band": tie,
         "clocks": clk,
     }
+    if divergence is not None:
+        line["mode_divergence"] = divergence
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

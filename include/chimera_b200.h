@@ -57,7 +57,8 @@ typedef enum chm_status {
   CHM_ERR_UNSUPPORTED = 9,          /* option not implemented on device */
   CHM_ERR_CUDA = 10,                /* CUDA launch / runtime failure */
   CHM_ERR_UNKNOWN_REQUEST = 11,     /* errors.UnknownRequest (monitor.py:104-105) */
-  CHM_ERR_UNKNOWN_STAGE = 12        /* errors.UnknownStage (workload.py:143-147) */
+  CHM_ERR_UNKNOWN_STAGE = 12,       /* errors.UnknownStage (workload.py:143-147) */
+  CHM_ERR_NCCL = 13                 /* NCCL missing (libnccl.so.2) or a NCCL call failed */
 } chm_status;
 
 /* ---- static configuration ------------------------------------------------ */
@@ -560,6 +561,71 @@ chm_status chm_qkv_attention_bf16(const void* x, const void* w_qkv, const float*
  * work -- FLOPs or bytes --, cumulative launch counts) and clears the timings. */
 chm_status chm_profile_enable(int32_t enable);
 chm_status chm_profile_read(int32_t* timed, double* total_ms, double* work, int64_t* launches);
+
+/* ---- multi-GPU: request shards exchange the in-flight vector --
+ *
+ * One process per GPU. Requests shard by program, so router, predictor,
+ * assignment map, in-flight logs and engine sub-queues are rank-local; the
+ * only cross-GPU state is the per-engine Neumaier pair (s, c) of P_m
+ * (ActivityMonitor.in_flight_sum, monitor.py:122-129). NCCL is resolved at
+ * run time (dlopen libnccl.so.2; CHM_NCCL_LIB overrides the path). The
+ * canonical tick-end state of both modes is P_prev folded with rank 0's
+ * dispatches in row order, then rank 1's, ... = the monitor of one serial
+ * schedule_request loop (balancer.py:116) over the concatenated batch. */
+#define CHM_COMM_ID_BYTES 128
+typedef struct chm_comm chm_comm;
+
+/* CHM_OK when libnccl could be loaded. */
+chm_status chm_comm_available(void);
+/* ncclGetUniqueId on one rank; the caller distributes the bytes. */
+chm_status chm_comm_unique_id(uint8_t* id_out /* CHM_COMM_ID_BYTES */);
+/* ncclCommInitRank on `device` (cudaSetDevice first; -1 = current). */
+chm_status chm_comm_init(const uint8_t* id, int32_t rank, int32_t world, int32_t device,
+                         chm_comm** out);
+chm_status chm_comm_destroy(chm_comm* comm);
+/* Plain collectives on the caller's stream (candidate gather of the merged
+ * admission; the sharded-completion sums). */
+chm_status chm_comm_allgather(chm_comm* comm, const void* send, void* recv, uint64_t bytes,
+                              void* stream);
+chm_status chm_comm_allreduce_i64(chm_comm* comm, int64_t* buf, int32_t n, void* stream);
+
+/* Mode A tick end: every rank's chain started from the tick-start (s0, c0);
+ * pack this rank's committed (model, yhat) rows, all-gather the records and
+ * fold them in rank order into mon->inflight_sum / inflight_comp (an int64
+ * sum when every value is a multiple of 2^-8 -- exact in any order -- else
+ * the Neumaier recurrence on the device). workspace: (world + 1) *
+ * chm_inflight_record_bytes(K, max_rows) bytes. The pack / fold halves are
+ * exported for transports other than NCCL (the gloo tests). */
+uint64_t chm_inflight_record_bytes(int32_t n_models, int32_t max_rows);
+chm_status chm_inflight_pack(const chm_pool* pool, const chm_decisions* dec, int32_t max_rows,
+                             void* record, void* stream);
+chm_status chm_inflight_fold(const chm_pool* pool, const chm_monitor_state* mon,
+                             const double* s0, const double* c0, const void* gathered,
+                             int32_t world, int32_t max_rows, int32_t* error, void* stream);
+chm_status chm_allreduce_inflight(chm_comm* comm, const chm_pool* pool,
+                                  const chm_monitor_state* mon, const double* s0,
+                                  const double* c0, const chm_decisions* dec, int32_t max_rows,
+                                  void* workspace, int32_t* error, void* stream);
+
+/* Mode B relay around the selection kernel only: rank g > 0 receives the
+ * packed state (n doubles: (s, c) [+ relayed engine counters]) from g - 1
+ * before chm_schedule_rows; after it, sends to g + 1 and the last rank
+ * broadcasts the tick-end state. Routers / predictors are enqueued before
+ * the receive, so they overlap the predecessors' chains. */
+chm_status chm_inflight_relay_recv(chm_comm* comm, double* state, int32_t n, void* stream);
+chm_status chm_inflight_relay_send(chm_comm* comm, double* state, int32_t n, void* stream);
+
+/* Sharded completions (record_completion, monitor.py:98-106, on a log that
+ * holds only this rank's dispatches): out[0..K) = exact sum of this rank's
+ * live terms per engine in units of 2^-8, out[K] = number of non-dyadic
+ * terms; all-reduce the K + 1 words (chm_comm_allreduce_i64), then
+ * chm_inflight_set_sum installs (sum, 0) -- builtin sum() of the survivors
+ * in any order -- or reports UNSUPPORTED (non-dyadic survivors have no
+ * order-free exact sum). */
+chm_status chm_inflight_local_sum(const chm_pool* pool, const chm_monitor_state* mon,
+                                  int64_t* out, void* stream);
+chm_status chm_inflight_set_sum(const chm_pool* pool, const chm_monitor_state* mon,
+                                const int64_t* summed, int32_t* error, void* stream);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,8 @@ CHM_ERR_UNSUPPORTED = 9
 CHM_ERR_CUDA = 10
 CHM_ERR_UNKNOWN_REQUEST = 11
 CHM_ERR_UNKNOWN_STAGE = 12
+CHM_ERR_NCCL = 13
+COMM_ID_BYTES = 128
 
 
 class Pool(ctypes.Structure):
@@ -308,6 +310,27 @@ _SIGNATURES = [
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p]),
     ("chm_qkv_attention_bf16", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
+    ("chm_comm_available", c_int32, []),
+    ("chm_comm_unique_id", c_int32, [c_void_p]),
+    ("chm_comm_init", c_int32, [c_void_p, c_int32, c_int32, c_int32, c_void_p]),
+    ("chm_comm_destroy", c_int32, [c_void_p]),
+    ("chm_comm_allgather", c_int32, [c_void_p, c_void_p, c_void_p, ctypes.c_uint64, c_void_p]),
+    ("chm_comm_allreduce_i64", c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("chm_inflight_record_bytes", ctypes.c_uint64, [c_int32, c_int32]),
+    ("chm_inflight_pack", c_int32,
+     [POINTER(Pool), POINTER(Decisions), c_int32, c_void_p, c_void_p]),
+    ("chm_inflight_fold", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+      c_void_p, c_void_p]),
+    ("chm_allreduce_inflight", c_int32,
+     [c_void_p, POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, POINTER(Decisions),
+      c_int32, c_void_p, c_void_p, c_void_p]),
+    ("chm_inflight_relay_recv", c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("chm_inflight_relay_send", c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("chm_inflight_local_sum", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p]),
+    ("chm_inflight_set_sum", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_void_p]),
     ("chm_profile_enable", c_int32, [c_int32]),
     ("chm_profile_read", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]
@@ -372,6 +395,8 @@ def check(status: int, what: str) -> None:
         raise RuntimeError(f"{what}: CUDA launch failed ({msg})")
     if status == CHM_ERR_UNSUPPORTED:
         raise NotImplementedError(f"{what}: {msg}")
+    if status == CHM_ERR_NCCL:
+        raise RuntimeError(f"{what}: {msg}")
     raise errors.ValidationError(f"{what}: {msg} (status {status})")
 
 

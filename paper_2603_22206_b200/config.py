@@ -94,10 +94,13 @@ class AgingConfig:
 AGING_DISABLED = AgingConfig(starvation_threshold=math.inf)
 
 
-@dataclass(frozen=True)
-class Decision:
-    model: str
-    priority: float
-    estimated_loads: dict[str, float]
-    used_cached_assignment: bool
-    scores: dict[str, float] | None = None
+try:  # the reference's own record when hetsched is importable (balancer.py:40-46)
+    from hetsched.balancer import Decision  # pragma: no cover
+except ImportError:
+    @dataclass(frozen=True)
+    class Decision:
+        model: str
+        priority: float
+        estimated_loads: dict[str, float]
+        used_cached_assignment: bool
+        scores: dict[str, float] | None = None

@@ -18,6 +18,7 @@ extern "C" const char* chm_status_string(int32_t status) {
     case CHM_ERR_CUDA: return "CUDA error";
     case CHM_ERR_UNKNOWN_REQUEST: return "unknown request";
     case CHM_ERR_UNKNOWN_STAGE: return "unknown stage";
+    case CHM_ERR_NCCL: return "NCCL unavailable or failed";
     default: return "unknown status";
   }
 }

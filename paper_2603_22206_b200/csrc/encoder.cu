@@ -715,7 +715,8 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
 constexpr int kClsWarps = 8;
 template <int S>
 __global__ void __launch_bounds__(kClsWarps * 32)
-    attention_cls_kernel(const __nv_bfloat16* __restrict__ qk, int n_items, int n_heads,
+    attention_cls_kernel(const __nv_bfloat16* __restrict__ qc,
+                         const __nv_bfloat16* __restrict__ kv, int n_items, int n_heads,
                          int hidden, __nv_bfloat16* __restrict__ ctx_c) {
   constexpr int KPL = S / 32;  // keys per lane
   __shared__ float s_q[kClsWarps][64];
@@ -724,18 +725,21 @@ __global__ void __launch_bounds__(kClsWarps * 32)
   const int item = blockIdx.x * kClsWarps + w;
   if (item >= n_items) return;
   const int seq = item / n_heads, h = item - seq * n_heads;
-  const size_t ld = 3 * (size_t)hidden;
+  // q: the CLS rows' bf16 projections [n_seq, H] (unscaled; x 1/8 here is
+  // exact, the same value the QKV epilogue's scaled rounding gives);
+  // kv: K | V of every token [T, 2H]
+  const size_t ld = 2 * (size_t)hidden;
   const __nv_bfloat162 q2 = *reinterpret_cast<const __nv_bfloat162*>(
-      qk + (size_t)seq * S * ld + h * 64 + 2 * lane);
+      qc + (size_t)seq * hidden + h * 64 + 2 * lane);
   const float2 qf = __bfloat1622float2(q2);
-  s_q[w][2 * lane] = qf.x;
-  s_q[w][2 * lane + 1] = qf.y;
+  s_q[w][2 * lane] = qf.x * 0.125f;
+  s_q[w][2 * lane + 1] = qf.y * 0.125f;
   __syncwarp();
   float sc[KPL];
 #pragma unroll
   for (int t = 0; t < KPL; ++t) {
     const uint4* kp = reinterpret_cast<const uint4*>(
-        qk + ((size_t)seq * S + lane + 32 * t) * ld + hidden + h * 64);
+        kv + ((size_t)seq * S + lane + 32 * t) * ld + h * 64);
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -768,7 +772,7 @@ __global__ void __launch_bounds__(kClsWarps * 32)
   const float inv = 1.0f / sum;
   // o[d] = sum_j p_j V[j][d]: lane owns d = 2*lane, 2*lane+1; each key row is
   // one coalesced 128-byte warp load
-  const __nv_bfloat16* vbase = qk + (size_t)seq * S * ld + 2 * hidden + h * 64 + 2 * lane;
+  const __nv_bfloat16* vbase = kv + (size_t)seq * S * ld + hidden + h * 64 + 2 * lane;
   float a0 = 0.f, a1 = 0.f;
 #pragma unroll 8
   for (int j = 0; j < S; ++j) {
@@ -1013,46 +1017,48 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
     const float2* st_in = (l == 0 || cluster_ln) ? nullptr : st_u;
     const float* g_prev = l == 0 ? nullptr : w.ln2_g[l - 1];
     const float* b_prev = l == 0 ? nullptr : w.ln2_b[l - 1];
-    if (fused && l < L - 1) {
-      // QKV projection + attention in one kernel (qkv_attn.cu)
-      rc = qkv_attention(x, wq, bq, cq, st_in, P, eps, ctx, n_seq, H, st);
-      if (rc != CHM_OK) return rc;
-    } else {
-      GemmArgs g;
-      g.epilogue = 4;
-      g.bias = bq;
-      g.hidden = H;
-      g.stats_in = st_in;
-      g.n_part = P;
-      g.colsum = cq;
-      g.eps = eps;
-      rc = gemm_run(x, wq, qk, (int)T, 3 * H, H, g, st);
-      if (rc != CHM_OK) return rc;
-    }
     if (l == L - 1) {
-      // Last layer: only h_[CLS] reaches the router head, so attention runs
-      // for the CLS query of every (sequence, head) and the rest of the layer
-      // for n_seq rows. ctx_c = ctx[:n_seq], xc = tmp[:n_seq], hc = the
-      // normalised layer input of the CLS rows (in the qkv buffer, free once
-      // the CLS attention has read it).
+      // Last layer: only h_[CLS] reaches the router head. K and V are
+      // projected for every token ([T, 2H] into the ffn buffer), Q only for
+      // the CLS rows (normalised into hc, then hc . Wq^T + b_q); attention
+      // runs for the CLS query of every (sequence, head) and the rest of the
+      // layer for n_seq rows. ctx_c = ctx[:n_seq], xc = tmp[:n_seq], hc / qc
+      // = the qkv buffer's first 2 n_seq rows of H.
       auto* ctx_c = ctx;
       auto* xc = tmp;
       auto* hc = qk;
-      const int items = n_seq * NH;
-      const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
-      prof::begin(prof::K_ATTENTION, st);
-      switch (S) {
-        case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
-        case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
-        case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
-        default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qk, items, NH, H, ctx_c); break;
-      }
-      prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
-      CHM_LAUNCH_CHECK();
+      auto* qc = qk + (size_t)n_seq * H;
+      auto* kvb = ffn;
+      GemmArgs gkv;
+      gkv.epilogue = 1;  // bias
+      gkv.bias = bq + H;
+      gkv.stats_in = st_in;
+      gkv.n_part = P;
+      gkv.colsum = cq + H;
+      gkv.eps = eps;
+      rc = gemm_run(x, reinterpret_cast<const __nv_bfloat16*>(wq) + (size_t)H * H, kvb, (int)T,
+                    2 * H, H, gkv, st);
+      if (rc != CHM_OK) return rc;
       prof::begin(prof::K_ROWWISE, st);
       ln_rows_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(x, S, n_seq, st_in, P,
                                                                        g_prev, b_prev, eps, hc);
       prof::end(prof::K_ROWWISE, st, (double)n_seq * (4.0 * H + 8.0 * P));
+      CHM_LAUNCH_CHECK();
+      GemmArgs gq;
+      gq.epilogue = 1;
+      gq.bias = w.b_qkv[l];
+      rc = gemm_run(hc, w.w_qkv[l], qc, n_seq, H, H, gq, st);
+      if (rc != CHM_OK) return rc;
+      const int items = n_seq * NH;
+      const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
+      prof::begin(prof::K_ATTENTION, st);
+      switch (S) {
+        case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
+        case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
+        case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
+        default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
+      }
+      prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
       CHM_LAUNCH_CHECK();
       GemmArgs go;
       go.epilogue = 5;
@@ -1079,7 +1085,21 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       if (rc != CHM_OK) return rc;
       break;
     }
-    if (!fused) {
+    if (fused) {
+      // QKV projection + attention in one kernel (qkv_attn.cu)
+      rc = qkv_attention(x, wq, bq, cq, st_in, P, eps, ctx, n_seq, H, st);
+      if (rc != CHM_OK) return rc;
+    } else {
+      GemmArgs g;
+      g.epilogue = 4;
+      g.bias = bq;
+      g.hidden = H;
+      g.stats_in = st_in;
+      g.n_part = P;
+      g.colsum = cq;
+      g.eps = eps;
+      rc = gemm_run(x, wq, qk, (int)T, 3 * H, H, g, st);
+      if (rc != CHM_OK) return rc;
       rc = run_attention(qk, ctx, n_seq, S, H, st);
       if (rc != CHM_OK) return rc;
     }
@@ -1208,6 +1228,8 @@ extern "C" chm_status chm_encoder_forward(const chm_encoder_cfg* cfg,
   if (cfg->n_heads * 64 != cfg->hidden || cfg->n_models < 1 ||
       cfg->n_models > CHM_MAX_MODELS || cfg->ffn % 64 != 0)
     return CHM_ERR_INVALID_ARG;
+  // the last layer's K|V projection ([T, 2H]) lives in the FFN buffer
+  if (cfg->ffn < 2 * cfg->hidden) return CHM_ERR_UNSUPPORTED;
   if ((long long)n_seq * seq_len > ws->max_tokens) return CHM_ERR_INVALID_ARG;
   if (!ws->stats || !ws->folded) return CHM_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;

@@ -239,6 +239,33 @@ __device__ __forceinline__ int select_bits(const unsigned long long (&Lb)[K], do
   return crk ? mc : ti[0];
 }
 
+// argmin (L, index) over load bit patterns with the winner's limit carried
+// along (the tournament of select_bits on its own).
+template <int K>
+__device__ __forceinline__ void argmin_limit(const unsigned long long (&L)[K],
+                                             const unsigned long long (&Lim)[K], int& mf,
+                                             unsigned long long& lim) {
+  unsigned long long tv[K], tl[K];
+  int ti[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    tv[k] = L[k];
+    tl[k] = Lim[k];
+    ti[k] = k;
+  }
+#pragma unroll
+  for (int step = 1; step < K; step *= 2)
+#pragma unroll
+    for (int k = 0; k + step < K; k += 2 * step) {
+      const bool lt = tv[k + step] < tv[k];
+      tv[k] = lt ? tv[k + step] : tv[k];
+      tl[k] = lt ? tl[k + step] : tl[k];
+      ti[k] = lt ? ti[k + step] : ti[k];
+    }
+  mf = ti[0];
+  lim = tl[0];
+}
+
 // Tie band (north star: "ties inside the tolerance band are reported"): for a
 // routed row with scores q and the loads L it saw, TIE_QUAL = some model
 // inside the latency slack other than m_fast has |q_m - (q_fast + margin)| <=
@@ -472,6 +499,15 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   }
   const uint32_t pow2_mask = prm.b_pow2_mask;
   const double one_plus_slack = prm.one_plus_slack;
+  // dyadic chain: the current m_fast and its limit, every engine's limit
+  unsigned long long Lim[K];
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+    Lim[m] = (unsigned long long)__double_as_longlong(
+        __dmul_rn(one_plus_slack, __longlong_as_double((long long)Lb[m])));
+  int cmf;
+  unsigned long long climb;
+  argmin_limit<K>(Lb, Lim, cmf, climb);
 
   for (int ch = 0; ch < n_chunks; ++ch) {
     ChunkBuf<K>* cur = &bufs[ch & 1];
@@ -489,8 +525,12 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       const int r0 = ch * kChunk;
       const int n = min(kChunk, B - r0);
       if (SPEC && dyadic) {
-        // software-pipelined: row j + 1's inputs are read from shared memory
-        // while row j resolves
+        // Loads only grow and only the dispatched engine's changes, so
+        // m_fast moves only when the row dispatches to m_fast itself. The
+        // argmin for that case is computed speculatively while the row's
+        // decision resolves; the loop-carried path is then: slack mask ->
+        // first candidate in rank order -> m -> state select. Row j + 1's
+        // inputs are read from shared memory while row j resolves.
         uint32_t nfl = cur->flags[0];
         uint64_t nqual = cur->qual[0], nrb = cur->rbits[0];
         uint32_t npm = cur->perm[0];
@@ -504,13 +544,21 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
           const uint64_t qual = nqual, rb = nrb;
           const uint32_t pm = npm;
           const int pre = npre;
+          // speculative: every engine's sum, load and limit after this row
           double ls_d[K];
-          unsigned long long ls[K];
+          unsigned long long ls[K], lsl[K], lt[K], ltl[K];
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             ls_d[k] = __dadd_rn(fr[k], ny[k]);
-            ls[k] = (unsigned long long)__double_as_longlong(__dmul_rn(ls_d[k], dq[k]));
+            const double lv = __dmul_rn(ls_d[k], dq[k]);
+            ls[k] = (unsigned long long)__double_as_longlong(lv);
+            lsl[k] = (unsigned long long)__double_as_longlong(__dmul_rn(one_plus_slack, lv));
+            lt[k] = k == cmf ? ls[k] : Lb[k];
+            ltl[k] = k == cmf ? lsl[k] : Lim[k];
           }
+          int mf2;
+          unsigned long long lim2;
+          argmin_limit<K>(lt, ltl, mf2, lim2);  // m_fast if this row dispatches to m_fast
           const int jn = j + 1 < n ? j + 1 : j;
           nfl = cur->flags[jn];
           nqual = cur->qual[jn];
@@ -519,14 +567,26 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
           npre = cur->pre_model[jn];
 #pragma unroll
           for (int k = 0; k < K; ++k) ny[k] = cur->yhat[jn * K + k];
-          int m = select_bits<K>(Lb, one_plus_slack, qual, rb, pm);
+          // the decision (select_model with m_fast and its limit known)
+          const uint32_t tq = (uint32_t)(qual >> (8 * cmf)) & 0xffu;
+          uint32_t okr = 0;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            okr |= (Lb[k] <= climb) ? ((uint32_t)(rb >> (8 * k)) & 0xffu) : 0u;
+          const uint32_t crk = tq & okr;
+          const int pos = (31 - __clz(crk)) & 7;
+          int m = crk ? (int)((pm >> (4 * pos)) & 15u) : cmf;
           m = (fl & RF_CACHED_PRE) ? pre : m;
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             const bool hit = k == m;
             fr[k] = hit ? ls_d[k] : fr[k];
             Lb[k] = hit ? ls[k] : Lb[k];
+            Lim[k] = hit ? lsl[k] : Lim[k];
           }
+          const bool moved = m == cmf;
+          cmf = moved ? mf2 : cmf;
+          climb = moved ? lim2 : climb;
           out.model[i] = m;
           sc.lnew[i] = __longlong_as_double((long long)tree_select<K>(ls, m));
         }

@@ -1,34 +1,53 @@
 """Request-sharded multi-GPU scheduling: one process per GPU.
 
 Requests shard by program (`shard_of`), so every stage of a program lands on
-the same GPU and the assignment map stays local. Router, predictor and the
-per-row precompute are shard-local; the only cross-GPU state is the
-per-engine in-flight predicted-token vector P (K doubles, Neumaier (s, c)).
+the same GPU and the assignment map stays local. Router, predictor, the
+per-row precompute, the in-flight logs and the engine sub-queues are
+shard-local; the only cross-GPU state is the per-engine in-flight
+predicted-token vector P (K doubles, the Neumaier (s, c) of
+ActivityMonitor.in_flight_sum, monitor.py:122-129).
 
-Two decision semantics (the caller picks one):
+Every tick runs the P-independent half (prepare, router, predictor:
+`GpuScheduler.route_predict`) on all GPUs at once; only the serial selection
+chain (`select_enqueue`, record_dispatch inside every schedule_request,
+balancer.py:116) depends on P. Two decision semantics:
 
-  Mode A (north-star literal): every GPU runs its shard's serial chain from
-      the tick-start global P; afterwards the per-engine deltas are summed
-      with one all-reduce (NCCL over NVLink, 64 B for K = 8). Decisions equal
-      G independent serial replays that all start from P0.
-  Mode B (serial-exact relay): the chains run in rank order; rank g receives
-      (s, c) from rank g-1 before its selection kernel, sends its final
-      (s, c) to rank g+1, and the last rank broadcasts the tick-end state.
-      Decisions equal ONE serial replay of the concatenated batch (rank 0's
-      rows, then rank 1's, ...) -- bit for bit, because (s, c) is exactly
-      the reference's Neumaier state. Routers and predictors still run in
-      parallel; only the short serial chains are ordered.
+  Mode A (north-star literal): every GPU runs its chain from the tick-start
+      global P; afterwards the ranks' committed (model, yhat) rows are
+      all-gathered and folded on the device in rank order
+      (chm_allreduce_inflight). Decisions equal G independent serial replays
+      that all start from P_prev; the tick-end P is exactly the state of one
+      serial replay of the concatenated batch (rank 0's rows, then rank 1's..).
+  Mode B (serial-exact relay): rank g receives (s, c) from rank g-1 right
+      before its selection kernel and forwards it after; the last rank
+      broadcasts the tick-end state (chm_inflight_relay_recv / _send). The
+      routers and predictors are already enqueued, so they overlap the
+      predecessors' chains. Decisions equal ONE serial replay of the
+      concatenated batch, bit for bit.
 
-The functions below operate on torch tensors on any device, so the same
-protocol code runs over NCCL on GPUs and over gloo on CPUs (tests).
+Both modes end every tick in the same state, so they can be mixed tick by
+tick and `divergence` counts how many decisions Mode A changes.
+
+Completions are sharded too: each rank removes its own finished requests from
+its own log, reduces the survivors exactly (int64 units of 2^-8) and the K
+sums are all-reduced (chm_inflight_local_sum / chm_comm_allreduce_i64 /
+chm_inflight_set_sum).
+
+Transport: `NcclComm` drives the C-ABI's NCCL entry points (the product path,
+NCCL over NVLink); `TorchComm` runs the same packing / folding kernels over a
+torch.distributed group (gloo in the tests: two ranks can share one GPU, NCCL
+refuses that).
 """
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 
 import torch
 import torch.distributed as dist
+
+from . import _lib
 
 
 def shard_of(program_id: str, world: int) -> int:
@@ -37,71 +56,118 @@ def shard_of(program_id: str, world: int) -> int:
     return int.from_bytes(h, "big") % world
 
 
-def neumaier_value_t(s: torch.Tensor, c: torch.Tensor) -> torch.Tensor:
-    """Elementwise CPython-sum value of (s, c): s + c when c is finite and != 0."""
-    use = torch.isfinite(c) & (c != 0)
-    return torch.where(use, s + c, s)
-
-
-def mode_a_allreduce(s: torch.Tensor, c: torch.Tensor, s0: torch.Tensor,
-                     c0: torch.Tensor, group=None) -> None:
-    """Mode A tick end: P = P0 + sum_g (P_g - P0); (s, c) <- (P, 0) in place."""
-    p0 = neumaier_value_t(s0, c0)
-    delta = neumaier_value_t(s, c) - p0
-    dist.all_reduce(delta, group=group)
-    s.copy_(p0 + delta)
-    c.zero_()
-
-
-def _p2p_buffer(state: torch.Tensor, group) -> torch.Tensor:
-    # gloo point-to-point needs host tensors (NCCL takes the device tensor)
-    if state.is_cuda and dist.get_backend(group) == "gloo":
-        return state.cpu()
-    return state
-
-
-def relay_receive(state: torch.Tensor, group=None) -> None:
-    """Mode B: before the selection chain, rank g > 0 receives the packed
-    monitor state [2K] = (s, c) from rank g-1 (in place)."""
-    rank = dist.get_rank(group)
-    if rank > 0:
-        buf = _p2p_buffer(state, group)
-        dist.recv(buf, src=_global(rank - 1, group), group=group)
-        if buf is not state:
-            state.copy_(buf)
-
-
-def relay_forward(state: torch.Tensor, group=None) -> None:
-    """Mode B: after the chain, pass (s, c) on; the last rank broadcasts the
-    tick-end state so every rank starts the next tick from it."""
-    rank = dist.get_rank(group)
-    world = dist.get_world_size(group)
-    buf = _p2p_buffer(state, group)
-    if rank + 1 < world:
-        dist.send(buf, dst=_global(rank + 1, group), group=group)
-    dist.broadcast(buf, src=_global(world - 1, group), group=group)
-    if buf is not state:
-        state.copy_(buf)
-
-
-def sharded_iteration(gs, group=None, release=None) -> None:
-    """One scheduling iteration of every engine over the G sub-queues
-    (SURVEY §8f row 1, global admission): each rank's STJF head candidates
-    are all-gathered (NCCL; gloo over host copies), then every rank admits its
-    share of the global top and ages its sub-queue (chm_queue_admit_merged).
-    Equal to one EngineSim._iterate on the union queue (engine.py:328-338)."""
-    cand = gs.queue_candidates()
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    send = _p2p_buffer(cand, group)
-    parts = [torch.empty_like(send) for _ in range(world)]
-    dist.all_gather(parts, send, group=group)
-    gathered = torch.stack(parts).to(cand.device)
-    gs.queue_admit_merged(gathered, rank, release)
+def _p(t):
+    return None if t is None else t.data_ptr()
 
 
 def _global(rank: int, group) -> int:
     return rank if group is None else dist.get_global_rank(group, rank)
+
+
+class TorchComm:
+    """Exchange over a torch.distributed group (gloo: host staging copies)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.host = dist.get_backend(group) == "gloo"
+
+    def _buf(self, t):
+        return t.cpu() if (t.is_cuda and self.host) else t
+
+    def allgather(self, send: torch.Tensor, recv: torch.Tensor, stream) -> None:
+        """recv [world, *send.shape] <- every rank's send."""
+        b = self._buf(send)
+        parts = [torch.empty_like(b) for _ in range(self.world)]
+        dist.all_gather(parts, b, group=self.group)
+        recv.copy_(torch.stack(parts).view_as(recv))
+
+    def allreduce_i64(self, buf: torch.Tensor, stream) -> None:
+        b = self._buf(buf)
+        dist.all_reduce(b, group=self.group)
+        if b is not buf:
+            buf.copy_(b)
+
+    def relay_recv(self, state: torch.Tensor, stream) -> None:
+        if self.rank > 0:
+            b = self._buf(state)
+            dist.recv(b, src=_global(self.rank - 1, self.group), group=self.group)
+            if b is not state:
+                state.copy_(b)
+
+    def relay_send(self, state: torch.Tensor, stream) -> None:
+        b = self._buf(state)
+        if self.rank + 1 < self.world:
+            dist.send(b, dst=_global(self.rank + 1, self.group), group=self.group)
+        dist.broadcast(b, src=_global(self.world - 1, self.group), group=self.group)
+        if b is not state:
+            state.copy_(b)
+
+
+class NcclComm:
+    """NCCL communicator owned by libchimera_sm100a.so (chm_comm_*). The unique
+    id travels over an existing torch.distributed group once, at setup."""
+
+    def __init__(self, device, group=None):
+        self.lib = _lib.load()
+        _lib.check(self.lib.chm_comm_available(), "chm_comm_available")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = (ctypes.c_uint8 * _lib.COMM_ID_BYTES)()
+        if self.rank == 0:
+            _lib.check(self.lib.chm_comm_unique_id(ctypes.addressof(uid)), "chm_comm_unique_id")
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=_global(0, group), group=group)
+        uid = (ctypes.c_uint8 * _lib.COMM_ID_BYTES).from_buffer_copy(obj[0])
+        self.handle = ctypes.c_void_p()
+        dev = torch.device(device)
+        _lib.check(self.lib.chm_comm_init(ctypes.addressof(uid), self.rank, self.world,
+                                          dev.index if dev.index is not None else -1,
+                                          ctypes.byref(self.handle)), "chm_comm_init")
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.chm_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def allgather(self, send, recv, stream) -> None:
+        _lib.check(self.lib.chm_comm_allgather(self.handle, _p(send), _p(recv),
+                                               send.numel() * send.element_size(),
+                                               stream.cuda_stream), "chm_comm_allgather")
+
+    def allreduce_i64(self, buf, stream) -> None:
+        _lib.check(self.lib.chm_comm_allreduce_i64(self.handle, _p(buf), buf.numel(),
+                                                   stream.cuda_stream), "chm_comm_allreduce_i64")
+
+    def relay_recv(self, state, stream) -> None:
+        _lib.check(self.lib.chm_inflight_relay_recv(self.handle, _p(state), state.numel(),
+                                                    stream.cuda_stream), "chm_inflight_relay_recv")
+
+    def relay_send(self, state, stream) -> None:
+        _lib.check(self.lib.chm_inflight_relay_send(self.handle, _p(state), state.numel(),
+                                                    stream.cuda_stream), "chm_inflight_relay_send")
+
+
+def make_comm(device, group=None):
+    """NCCL (C-ABI) when the group's backend is NCCL, else the torch group."""
+    if dist.get_backend(group) == "nccl":
+        return NcclComm(device, group)
+    return TorchComm(group)
+
+
+def sharded_iteration(gs, comm, stream, release=None) -> None:
+    """One scheduling iteration of every engine over the G sub-queues
+    (SURVEY §8f row 1, global admission): each rank's STJF head candidates
+    are all-gathered, then every rank admits its share of the global top and
+    ages its sub-queue (chm_queue_admit_merged). Equal to one
+    EngineSim._iterate on the union queue (engine.py:328-338)."""
+    cand = gs.queue_candidates(stream=stream)
+    gathered = torch.empty((comm.world,) + tuple(cand.shape), dtype=cand.dtype,
+                           device=cand.device)
+    comm.allgather(cand, gathered, stream)
+    gs.queue_admit_merged(gathered, comm.rank, release, stream=stream)
 
 
 # Engine counters relayed with (s, c) under global admission: they make the
@@ -111,7 +177,7 @@ _RELAYED = ("engine_running", "engine_seq", "engine_clock", "engine_iterations")
 
 
 class ShardedScheduler:
-    """Wraps a per-rank GpuScheduler with the Mode A / Mode B exchange.
+    """A per-rank GpuScheduler with the Mode A / Mode B exchange.
 
     global_admission (Mode B only): each engine's queue is the union of the
     ranks' sub-queues, served in the reference's global STJF order. The relay
@@ -120,7 +186,8 @@ class ShardedScheduler:
     decisions, admissions and queue orders equal one serial replay of the
     concatenated batch through one EngineSim per model."""
 
-    def __init__(self, scheduler, mode: str = "B", group=None, global_admission: bool = False):
+    def __init__(self, scheduler, mode: str = "B", group=None, global_admission: bool = False,
+                 comm=None):
         if mode not in ("A", "B"):
             raise ValueError("mode must be 'A' or 'B'")
         if global_admission and mode != "B":
@@ -129,74 +196,130 @@ class ShardedScheduler:
         self.mode = mode
         self.group = group
         self.global_admission = global_admission
+        self.comm = comm if comm is not None else make_comm(scheduler.device, group)
         st = scheduler.state
-        n = (2 + len(_RELAYED)) * st.K if global_admission else 2 * st.K
-        self.packed = torch.empty(n, dtype=torch.float64, device=st.device)
+        K = st.K
+        dev = st.device
+        self.lib = _lib.load()
+        if global_admission:
+            self.packed = torch.empty((2 + len(_RELAYED)) * K, dtype=torch.float64, device=dev)
+        self.s0 = torch.empty(2 * K, dtype=torch.float64, device=dev)
+        rb = int(self.lib.chm_inflight_record_bytes(K, scheduler.buf.max_rows))
+        self.rec_bytes = rb
+        self.record = torch.empty(rb, dtype=torch.uint8, device=dev)
+        self.gathered = torch.empty((self.comm.world, rb), dtype=torch.uint8, device=dev)
+        self.sums = torch.zeros(K + 1, dtype=torch.int64, device=dev)
 
+    # -- exchange pieces ------------------------------------------------------
     def _pack(self) -> None:
         st, K = self.gs.state, self.gs.state.K
-        self.packed[:K].copy_(st.inflight_sum)
-        self.packed[K:2 * K].copy_(st.inflight_comp)
-        if self.global_admission:
-            for i, name in enumerate(_RELAYED):
-                self.packed[(2 + i) * K:(3 + i) * K].copy_(getattr(st, name))
+        self.packed[:2 * K].copy_(st.inflight_sc)
+        for i, name in enumerate(_RELAYED):
+            self.packed[(2 + i) * K:(3 + i) * K].copy_(getattr(st, name))
 
     def _unpack(self) -> None:
         st, K = self.gs.state, self.gs.state.K
-        st.inflight_sum.copy_(self.packed[:K])
-        st.inflight_comp.copy_(self.packed[K:2 * K])
-        if self.global_admission:
-            for i, name in enumerate(_RELAYED):
-                getattr(st, name).copy_(self.packed[(2 + i) * K:(3 + i) * K])
+        st.inflight_sc.copy_(self.packed[:2 * K])
+        for i, name in enumerate(_RELAYED):
+            getattr(st, name).copy_(self.packed[(2 + i) * K:(3 + i) * K])
 
-    def _run_global(self, batch, n_iterations: int, n_complete, kw) -> None:
-        st = self.gs.state
-        st.q_n_admitted.zero_()
-        st.q_n_promoted.zero_()
-        if n_complete is not None:
-            # each completion frees a slot and runs one iteration of its engine
-            # (engine.py:232-241); n_complete is the global count, equal on all ranks
-            for r in range(int(n_complete.max().item()) if n_complete.numel() else 0):
-                release = torch.where(n_complete > r, 1, -1).to(torch.int32)
-                sharded_iteration(self.gs, self.group, release)
-        self._pack()
-        relay_receive(self.packed, self.group)
-        self._unpack()
-        self.gs.run_rows(batch, n_iterations=0, keep_admitted=True, **kw)
-        self._pack()
-        relay_forward(self.packed, self.group)
-        self._unpack()
-        for _ in range(n_iterations):
-            sharded_iteration(self.gs, self.group)
+    def _relay_state(self):
+        return self.packed if self.global_admission else self.gs.state.inflight_sc
 
-    def run_rows(self, batch, n_iterations: int = 1, **kw) -> None:
-        st = self.gs.state
+    def _allreduce_inflight(self, stream) -> None:
+        """Mode A tick end: pack -> all-gather -> fold (chm_allreduce_inflight)."""
+        gs, st = self.gs, self.gs.state
         K = st.K
+        dec_c = gs.buf.decisions_struct(False)
+        if isinstance(self.comm, NcclComm):
+            ws = self._ws if hasattr(self, "_ws") else torch.empty(
+                (self.comm.world + 1) * self.rec_bytes, dtype=torch.uint8, device=st.device)
+            self._ws = ws
+            _lib.check(self.lib.chm_allreduce_inflight(
+                self.comm.handle, st.pool_c, st.monitor_c, _p(self.s0), _p(self.s0[K:]), dec_c,
+                gs.buf.max_rows, _p(ws), _p(gs.buf.error), stream.cuda_stream),
+                "chm_allreduce_inflight")
+            return
+        _lib.check(self.lib.chm_inflight_pack(st.pool_c, dec_c, gs.buf.max_rows,
+                                              _p(self.record), stream.cuda_stream),
+                   "chm_inflight_pack")
+        self.comm.allgather(self.record, self.gathered, stream)
+        _lib.check(self.lib.chm_inflight_fold(st.pool_c, st.monitor_c, _p(self.s0),
+                                              _p(self.s0[K:]), _p(self.gathered),
+                                              self.comm.world, gs.buf.max_rows,
+                                              _p(gs.buf.error), stream.cuda_stream),
+                   "chm_inflight_fold")
+
+    def _sum_completions(self, stream) -> None:
+        """Global exact in-flight sums after sharded record_completion."""
+        st = self.gs.state
+        _lib.check(self.lib.chm_inflight_local_sum(st.pool_c, st.monitor_c, _p(self.sums),
+                                                   stream.cuda_stream), "chm_inflight_local_sum")
+        self.comm.allreduce_i64(self.sums, stream)
+        _lib.check(self.lib.chm_inflight_set_sum(st.pool_c, st.monitor_c, _p(self.sums),
+                                                 _p(self.gs.buf.error_complete),
+                                                 stream.cuda_stream), "chm_inflight_set_sum")
+
+    # -- the tick ---------------------------------------------------------------
+    def run_rows(self, batch, n_iterations: int = 1, completions=None, n_complete=None,
+                 stream=None, with_loads: bool = True) -> None:
+        """One sharded tick. completions: this rank's finished requests (model,
+        key) -- the ones it dispatched; with them every rank must pass a
+        (possibly empty) tensor pair, since the sums are all-reduced.
+        n_complete: engine slots freed without monitor records (int32[K]);
+        under global admission it is the global per-engine count and
+        completions only update the monitor."""
+        gs = self.gs
+        s = stream if stream is not None else torch.cuda.current_stream(gs.device)
+        st = gs.state
         if self.global_admission:
-            if kw.get("completions") is not None:
-                raise NotImplementedError("monitor completions are single-GPU; pass n_complete")
-            self._run_global(batch, n_iterations, kw.pop("n_complete", None), kw)
+            gs.begin_tick(completions=None, keep_admitted=False, stream=s)
+            if completions is not None:
+                self._monitor_complete(completions, s)
+            if n_complete is not None:
+                # each completion frees a slot and runs one iteration of its engine
+                # (engine.py:232-241); n_complete is global, equal on all ranks
+                for r in range(int(n_complete.max().item()) if n_complete.numel() else 0):
+                    release = torch.where(n_complete > r, 1, -1).to(torch.int32)
+                    sharded_iteration(gs, self.comm, s, release)
+            gs.route_predict(batch, stream=s)
+            self._pack()
+            self.comm.relay_recv(self.packed, s)
+            self._unpack()
+            gs.select_enqueue(batch, n_iterations=0, with_loads=with_loads, stream=s)
+            self._pack()
+            self.comm.relay_send(self.packed, s)
+            self._unpack()
+            for _ in range(n_iterations):
+                sharded_iteration(gs, self.comm, s)
             return
-        if kw.get("completions") is not None:
-            # each GPU's log holds only its own dispatches while (s, c) carries
-            # the global volume: recomputing from the local log would drop the
-            # other shards' contributions
-            raise NotImplementedError("monitor completions are single-GPU; pass n_complete")
+        gs.begin_tick(completions=completions, n_complete=n_complete, stream=s)
+        if completions is not None:
+            self._sum_completions(s)
+        gs.route_predict(batch, stream=s)
         if self.mode == "A":
-            s0 = st.inflight_sum.clone()
-            c0 = st.inflight_comp.clone()
-            self.gs.run_rows(batch, n_iterations=n_iterations, **kw)
-            mode_a_allreduce(st.inflight_sum, st.inflight_comp, s0, c0, self.group)
+            self.s0.copy_(st.inflight_sc)
+            gs.select_enqueue(batch, n_iterations=n_iterations, with_loads=with_loads, stream=s)
+            self._allreduce_inflight(s)
             return
-        # Mode B: receive the predecessor's (s, c), run, forward.
-        self.packed[:K].copy_(st.inflight_sum)
-        self.packed[K:].copy_(st.inflight_comp)
-        relay_receive(self.packed, self.group)
-        st.inflight_sum.copy_(self.packed[:K])
-        st.inflight_comp.copy_(self.packed[K:])
-        self.gs.run_rows(batch, n_iterations=n_iterations, **kw)
-        self.packed[:K].copy_(st.inflight_sum)
-        self.packed[K:].copy_(st.inflight_comp)
-        relay_forward(self.packed, self.group)
-        st.inflight_sum.copy_(self.packed[:K])
-        st.inflight_comp.copy_(self.packed[K:])
+        self.comm.relay_recv(st.inflight_sc, s)
+        gs.select_enqueue(batch, n_iterations=n_iterations, with_loads=with_loads, stream=s)
+        self.comm.relay_send(st.inflight_sc, s)
+
+    def _monitor_complete(self, completions, stream) -> None:
+        gs, st = self.gs, self.gs.state
+        c_model, c_key = completions
+        _lib.check(self.lib.chm_monitor_complete(
+            st.pool_c, st.monitor_c, _p(c_model), _p(c_key), int(c_model.numel()),
+            _p(gs.buf.n_complete), _p(gs.buf.error_complete), stream.cuda_stream),
+            "chm_monitor_complete")
+        self._sum_completions(stream)
+
+
+def divergence(models_a: torch.Tensor, models_b: torch.Tensor, comm, stream) -> int:
+    """Decisions that differ between a Mode A and a Mode B run of the same
+    sharded tick, summed over the ranks."""
+    d = torch.tensor([int((models_a != models_b).sum().item())], dtype=torch.int64,
+                     device=models_a.device)
+    comm.allreduce_i64(d, stream)
+    return int(d.item())

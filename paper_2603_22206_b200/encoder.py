@@ -40,12 +40,13 @@ class EncoderConfig:
         return L * (8 * S * H * H + 4 * S * S * H + 4 * S * H * F) + 2 * H * n_models
 
     def flops_executed_per_request(self, n_models: int) -> int:
-        """FLOPs the device actually executes: the last layer runs attention
-        for the [CLS] query only and its out-projection / FFN for the CLS row
-        only (the head reads h_[CLS] alone), all S tokens still feed K and V."""
+        """FLOPs the device actually executes: the last layer projects Q and
+        runs attention for the [CLS] query only and its out-projection / FFN
+        for the CLS row only (the head reads h_[CLS] alone); all S tokens still
+        feed K and V."""
         L, S, H, F = self.n_layers, self.seq_len, self.hidden, self.ffn
         full = (L - 1) * (8 * S * H * H + 4 * S * S * H + 4 * S * H * F)
-        last = 6 * S * H * H + 4 * S * H + 2 * H * H + 4 * H * F
+        last = 4 * S * H * H + 2 * H * H + 4 * S * H + 2 * H * H + 4 * H * F
         return full + last + 2 * H * n_models
 
 

@@ -203,15 +203,27 @@ class GpuScheduler:
         engines' slots freed, before the batch is scheduled. n_complete: the
         engine side only (int32[K] finished-per-engine counts).
         keep_admitted: append to the admission lists instead of resetting
-        them (the sharded protocol runs merged iterations before the batch)."""
-        B = batch.n_rows
-        if B > self.buf.max_rows:
-            raise ValueError(f"batch of {B} rows exceeds max_rows={self.buf.max_rows}")
+        them (the sharded protocol runs merged iterations before the batch).
+
+        The tick is three phases, also callable one by one (dist.py runs the
+        P-independent ones on every GPU before the serial chain's exchange):
+        begin_tick (error words, completions), route_predict (prepare, router,
+        predictor) and select_enqueue (K6 chain + K7 queues)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.begin_tick(completions=completions, n_complete=n_complete,
+                        keep_admitted=keep_admitted, stream=s)
+        self.route_predict(batch, stream=s)
+        self.select_enqueue(batch, n_iterations=n_iterations, with_loads=with_loads, stream=s)
+
+    def begin_tick(self, completions=None, n_complete=None, keep_admitted: bool = False,
+                   stream=None) -> None:
+        """Reset the tick's error words and admission lists; apply completions
+        (record_completion -> in-flight log + sums, then the engines' freed
+        slots). On a request shard the recomputed sums cover only the local
+        log; dist.ShardedScheduler replaces them with the global exact sum."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         sh = s.cuda_stream
         st, buf, lib = self.state, self.buf, self.lib
-        rows_c = batch.rows_struct()
-        dec_c = buf.decisions_struct(with_loads)
         with torch.cuda.stream(s):
             buf.error.copy_(buf.error_init)
             buf.error_complete.copy_(buf.error_init)
@@ -234,20 +246,43 @@ class GpuScheduler:
                                                   st.queue_c, _p(n_complete),
                                                   _p(buf.error_complete), sh),
                            "chm_queue_complete")
+
+    def route_predict(self, batch: RowBatch, stream=None) -> None:
+        """The in-flight-independent half of the tick: assignment lookup and
+        router row list (chm_prepare_rows), router (K1-K4), predictor (K5)."""
+        B = batch.n_rows
+        if B > self.buf.max_rows:
+            raise ValueError(f"batch of {B} rows exceeds max_rows={self.buf.max_rows}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st, buf, lib = self.state, self.buf, self.lib
+        rows_c = batch.rows_struct()
+        with torch.cuda.stream(s):
             _lib.check(lib.chm_prepare_rows(st.monitor_c, rows_c, buf.scratch_c,
-                                            _p(st.epoch), sh), "chm_prepare_rows")
+                                            _p(st.epoch), s.cuda_stream), "chm_prepare_rows")
             if self.router is None:
                 raise RuntimeError("GpuScheduler needs a router")
             self.router.score_rows(batch, buf.route_rows, buf.n_route, buf.scores, s)
             if self.predictor is None:
                 raise RuntimeError("GpuScheduler needs a predictor")
             self.predictor.predict_rows(batch, self.K, buf.yhat, buf.error, s)
-            _lib.check(lib.chm_schedule_rows(st.pool_c, self.bal_c, st.monitor_c, rows_c,
-                                             buf.scratch_c, _p(buf.scores), _p(buf.yhat),
-                                             dec_c, sh), "chm_schedule_rows")
-            _lib.check(lib.chm_queue_tick(st.pool_c, self.aging_c, st.monitor_c, st.queue_c,
-                                          rows_c, dec_c, int(n_iterations), _p(buf.error), sh),
-                       "chm_queue_tick")
+
+    def select_enqueue(self, batch: RowBatch, n_iterations: int = 1, with_loads: bool = True,
+                       stream=None) -> None:
+        """The serial half: K6 (monitor + load + selection + dispatch, in row
+        order from the current in-flight state) and K7 (append + aging
+        iterations + STJF order)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        sh = s.cuda_stream
+        st, buf, lib = self.state, self.buf, self.lib
+        rows_c = batch.rows_struct()
+        dec_c = buf.decisions_struct(with_loads)
+        self._dec_c = dec_c  # kept alive for callers that pack the decisions
+        _lib.check(lib.chm_schedule_rows(st.pool_c, self.bal_c, st.monitor_c, rows_c,
+                                         buf.scratch_c, _p(buf.scores), _p(buf.yhat),
+                                         dec_c, sh), "chm_schedule_rows")
+        _lib.check(lib.chm_queue_tick(st.pool_c, self.aging_c, st.monitor_c, st.queue_c,
+                                      rows_c, dec_c, int(n_iterations), _p(buf.error), sh),
+                   "chm_queue_tick")
 
     def note_progress(self, models, keys, emitted, stream=None) -> None:
         """ActivityMonitor.note_progress (monitor.py:108-111) for a batch of

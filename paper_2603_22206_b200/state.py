@@ -70,8 +70,10 @@ class DeviceState:
         self.device = torch.device(device)
         d, K, NP, C = self.device, self.K, self.n_programs, self.capacity
         f64, i64, i32 = torch.float64, torch.int64, torch.int32
-        self.inflight_sum = torch.zeros(K, dtype=f64, device=d)
-        self.inflight_comp = torch.zeros(K, dtype=f64, device=d)
+        # (s, c) of every engine in one buffer: the Mode B relay moves it as is
+        self.inflight_sc = torch.zeros(2 * K, dtype=f64, device=d)
+        self.inflight_sum = self.inflight_sc[:K]
+        self.inflight_comp = self.inflight_sc[K:]
         self.inflight_count = torch.zeros(K, dtype=i64, device=d)
         self.assignment = torch.full((NP,), -1, dtype=torch.int8, device=d)
         self.stage_bits = torch.zeros(NP, dtype=i32, device=d)

@@ -1,7 +1,11 @@
 """Multi-process (gloo, world_size 2, CPU) tests of the sharded-tick protocol
-in paper_2603_22206_b200/dist.py: Mode B relay decisions equal one serial
-replay of the reference path over the concatenated batch; Mode A equals
-independent shard replays from P0 with the deltas all-reduced."""
+in paper_2603_22206_b200/dist.py over its TorchComm transport: Mode B relay
+decisions equal one serial replay of the reference path over the
+concatenated batch; Mode A equals independent shard replays from P0 with the
+tick end folded in rank order (a restatement of chm_inflight_fold); the
+global-admission queue protocol. The per-rank kernels are CPU stand-ins
+here; tests/test_gpu_dist.py runs ShardedScheduler.run_rows with the real
+kernels (two ranks sharing one GPU over gloo)."""
 
 import os
 import socket
@@ -54,10 +58,23 @@ def _p0_state(sc):
     return s, c
 
 
+def _fold(s0, c0, records):
+    """Restatement of chm_inflight_fold: the gathered (model, yhat) rows of
+    every rank folded into (s, c) in rank order (Neumaier, monitor.py:127)."""
+    s, c = list(s0), list(c0)
+    for rows in records:
+        for m, y in rows:
+            t = s[m] + y
+            c[m] += ((s[m] - t) + y) if abs(s[m]) >= abs(y) else ((y - t) + s[m])
+            s[m] = t
+    return s, c
+
+
 def _worker(rank, world, port, mode, name, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2603_22206_b200 import dist as D
+    comm = D.TorchComm()
     sc = H.load_schedule(name)
     n = len(sc["prog"])
     bounds = np.linspace(0, n, world + 1).astype(int)
@@ -65,19 +82,29 @@ def _worker(rank, world, port, mode, name, q):
     k = sc["k"]
     s0, c0 = _p0_state(sc)
     if mode == "B":
-        packed = torch.tensor(s0 + c0, dtype=torch.float64)
-        D.relay_receive(packed)
-        models, s, c = _chain(sc, rows, packed[:k].tolist(), packed[k:].tolist())
-        packed.copy_(torch.tensor(s + c, dtype=torch.float64))
-        D.relay_forward(packed)
-        final = packed.tolist()
+        state = torch.tensor(s0 + c0, dtype=torch.float64)
+        comm.relay_recv(state, None)
+        models, s, c = _chain(sc, rows, state[:k].tolist(), state[k:].tolist())
+        state.copy_(torch.tensor(s + c, dtype=torch.float64))
+        comm.relay_send(state, None)
+        final = state.tolist()
     else:
         models, s, c = _chain(sc, rows, s0, c0)
-        st = torch.tensor(s, dtype=torch.float64)
-        ct = torch.tensor(c, dtype=torch.float64)
-        D.mode_a_allreduce(st, ct, torch.tensor(s0, dtype=torch.float64),
-                           torch.tensor(c0, dtype=torch.float64))
-        final = st.tolist() + ct.tolist()
+        # pack -> all-gather -> fold (the chm_allreduce_inflight protocol)
+        rec = torch.tensor([[m, float(sc["yhat"][i, m])] for i, m in zip(rows, models)],
+                           dtype=torch.float64)
+        n_rec = torch.tensor([len(rows)], dtype=torch.int64)
+        sizes = torch.zeros(world, dtype=torch.int64)
+        comm.allgather(n_rec, sizes.view(world, 1), None)
+        cap = int(sizes.max())
+        pad = torch.zeros((cap, 2), dtype=torch.float64)
+        pad[:len(rows)] = rec
+        allrec = torch.zeros((world, cap, 2), dtype=torch.float64)
+        comm.allgather(pad, allrec, None)
+        recs = [[(int(m), float(y)) for m, y in allrec[g, :int(sizes[g])].tolist()]
+                for g in range(world)]
+        s, c = _fold(s0, c0, recs)
+        final = s + c
     gathered = [None] * world
     dist.all_gather_object(gathered, models)
     if rank == 0:
@@ -114,23 +141,30 @@ def test_mode_b_relay_equals_serial_replay(name):
     assert p.tobytes() == sc["out_final_p"].tobytes()
 
 
-def test_mode_a_equals_shard_replays_from_p0():
-    name = "k3_basic"
+@pytest.mark.parametrize("name", ["k3_basic", "k5_nondyadic_p0"])
+def test_mode_a_shard_replays_and_canonical_state(name):
+    """Mode A: each shard decides from P0; the tick end is the fold of every
+    shard's dispatches in rank order -- the Neumaier state of the reference's
+    monitor after the concatenated dispatches (same as Mode B's)."""
     sc = H.load_schedule(name)
     gathered, final = _run("A", name)
     n = len(sc["prog"])
     bounds = np.linspace(0, n, 3).astype(int)
     s0, c0 = _p0_state(sc)
-    want, deltas = [], np.zeros(sc["k"])
-    from paper_2603_22206_b200.state import neumaier_value
+    want = []
+    mon = hp.PortMonitor(sc["ids"])
+    for j, (m, v) in enumerate(sc["p0"]):
+        mon.record_dispatch(sc["ids"][int(m)], f"seed:{j}", float(v))
     for r in range(2):
-        models, s, c = _chain(sc, range(bounds[r], bounds[r + 1]), s0, c0)
+        models, _, _ = _chain(sc, range(bounds[r], bounds[r + 1]), s0, c0)
         want += models
-        deltas += np.array([neumaier_value(a, b) for a, b in zip(s, c)]) - \
-            np.array([neumaier_value(a, b) for a, b in zip(s0, c0)])
+        for i, m in zip(range(bounds[r], bounds[r + 1]), models):
+            mon.record_dispatch(sc["ids"][m], f"r{i}", float(sc["yhat"][i, m]))
     assert sum(gathered, []) == want
-    p0 = np.array([neumaier_value(a, b) for a, b in zip(s0, c0)])
-    np.testing.assert_array_equal(np.array(final[:sc["k"]]), p0 + deltas)
+    from paper_2603_22206_b200.state import neumaier_value
+    k = sc["k"]
+    p = np.array([neumaier_value(a, b) for a, b in zip(final[:k], final[k:])])
+    assert p.tobytes() == np.array([mon.in_flight_sum(m) for m in sc["ids"]]).tobytes()
 
 
 def test_shard_of_is_stable_and_balanced():
@@ -157,8 +191,8 @@ class _SubQueueShard:
         self.entries = []  # dicts: level, prio, arr, seq, handle, count
         z = lambda dt: torch.zeros(1, dtype=dt)  # noqa: E731
         self.state = types.SimpleNamespace(
-            K=1, device=torch.device("cpu"), inflight_sum=z(torch.float64),
-            inflight_comp=z(torch.float64), engine_running=z(torch.int32),
+            K=1, device=torch.device("cpu"), inflight_sc=torch.zeros(2, dtype=torch.float64),
+            engine_running=z(torch.int32),
             engine_seq=z(torch.int64), engine_clock=z(torch.float64),
             engine_iterations=z(torch.int64), q_n_admitted=z(torch.int32),
             q_n_promoted=z(torch.int32))
@@ -187,7 +221,7 @@ class _SubQueueShard:
                 st.engine_running[0] += 1
                 self._age()
 
-    def queue_candidates(self):
+    def queue_candidates(self, stream=None):
         head = sorted(self.entries, key=self._key)[:self.b]
         out = torch.full((1, self.b, 5), 0, dtype=torch.int64)
         out[0, :, 0] = torch.iinfo(torch.int64).max
@@ -199,7 +233,7 @@ class _SubQueueShard:
             out[0, j, 4] = e["handle"]
         return out
 
-    def queue_admit_merged(self, gathered, rank, release=None):
+    def queue_admit_merged(self, gathered, rank, release=None, stream=None):
         st = self.state
         rel = 0 if release is None else int(release[0])
         if rel < 0:
@@ -233,8 +267,9 @@ def _queue_worker(rank, world, port, name, q):
     from paper_2603_22206_b200 import dist as D
     qd = H.load_queue(name)
     shard = _SubQueueShard(qd["b"], qd["S"] if qd["S"] else math.inf)
+    comm = D.TorchComm()
     ss = D.ShardedScheduler.__new__(D.ShardedScheduler)
-    ss.gs, ss.mode, ss.group, ss.global_admission = shard, "B", None, True
+    ss.gs, ss.mode, ss.group, ss.global_admission, ss.comm = shard, "B", None, True, comm
     ss.packed = torch.empty((2 + len(D._RELAYED)) * 1, dtype=torch.float64)
     enq, pos = qd["enq"], 0
     log = []  # per step: handles admitted on enqueue (this rank) / per iteration (global)
@@ -247,11 +282,11 @@ def _queue_worker(rank, world, port, name, q):
         part = [(int(h), float(p), float(t)) for h, p, t in o[bounds[rank]:bounds[rank + 1]]]
         shard.admitted = []
         ss._pack()
-        D.relay_receive(ss.packed)
+        comm.relay_recv(ss.packed, None)
         ss._unpack()
         shard.run_rows(part)
         ss._pack()
-        D.relay_forward(ss.packed)
+        comm.relay_send(ss.packed, None)
         ss._unpack()
         got = [None] * world
         dist.all_gather_object(got, shard.admitted)
@@ -259,7 +294,7 @@ def _queue_worker(rank, world, port, name, q):
 
     def iteration(release=None):
         shard.admitted = []
-        D.sharded_iteration(shard, None, None if release is None else torch.tensor([release]))
+        D.sharded_iteration(shard, comm, None, None if release is None else torch.tensor([release]))
         log.extend(shard.admitted[0])
 
     enqueue(qd["n_pre"])

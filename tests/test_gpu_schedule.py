@@ -200,3 +200,63 @@ def test_select_kat_through_k6(exact_chain):
         got[i] = int(gs.buf.model[0].item())
         assert int(gs.buf.n_committed.item()) == rows
     np.testing.assert_array_equal(got, z["chosen"])
+
+
+def test_schedule_batch_with_encoder_router():
+    """The drop-in as INTEGRATION.md binds it: reference-style Request /
+    TraceRecord objects, the sm_100a encoder as the Router (token ids from a
+    caller-supplied source, ragged lengths packed to S), the Predictor
+    shim -> schedule_batch -> Decisions equal to the oracle port's serial
+    schedule_request loop fed the same router scores (balancer.py:89-129,
+    router.py:34-45). Router.score(req, rec, pool) on one request returns
+    the same ConfidenceVector as the batched forward."""
+    from oracle import hetsched_port as hp
+    from paper_2603_22206_b200.encoder import SMALL, GpuEncoderRouter
+    from paper_2603_22206_b200.router import ConfidenceVector
+
+    sc = H.load_schedule("k5_nondyadic_p0")
+    n = len(sc["prog"])
+    rng = np.random.default_rng(11)
+    toks = {}
+    for p in set(int(x) for x in sc["prog"]):
+        ln = int(rng.integers(16, 129))
+        toks[f"p{p:06d}"] = [101] + rng.integers(1000, 30522, ln - 1).tolist()
+    router = GpuEncoderRouter(SMALL, sc["k"], max_rows=n, seed=3, head_std=0.2,
+                              tokens=lambda req, rec: toks[req.program_id])
+    gs, rt, pr = make_scheduler(sc)
+    gs.router = router
+    pr.set(torch.as_tensor(sc["yhat"], device=gs.device))
+    for p in range(sc["n_prog"]):
+        gs.program_index(f"p{p:06d}")
+    reqs, recs = H.requests_of(sc)
+    decs = gs.schedule_batch(reqs, recs)
+    assert len(decs) == n
+    pool = H.pool_of(sc)
+    ids = sc["ids"]
+    q_batch = gs.buf.scores[:n * sc["k"]].view(n, sc["k"]).cpu().numpy()
+    # the port replays the serial loop with the scores the device computed
+    mon = hp.PortMonitor(ids)
+    for j, (m, v) in enumerate(sc["p0"]):
+        mon.record_dispatch(ids[int(m)], f"seed:{j}", float(v))
+    for p, m in sc["pre"]:
+        mon.assign(f"p{int(p):06d}", ids[int(m)])
+    engines = {mid: hp.PortEngine(pool[mid].max_batch_size) for mid in ids}
+    for i, (r, rec) in enumerate(zip(reqs, recs)):
+        d = hp.port_schedule_request(r, rec, pool, mon, engines,
+                                     lambda rq, rc, i=i: {m: float(q_batch[i, k])
+                                                          for k, m in enumerate(ids)},
+                                     lambda rq, rc, m, i=i: float(sc["yhat"][i, ids.index(m)]),
+                                     sc["tau"], sc["margin"])
+        assert decs[i].model == d.model, i
+        assert decs[i].priority == d.priority
+        assert decs[i].used_cached_assignment == d.used_cached_assignment
+        if not d.used_cached_assignment:
+            assert decs[i].estimated_loads == d.estimated_loads
+            assert decs[i].scores == d.scores
+    # Router.score on single requests: same encoder, same scores
+    routed = [i for i, d in enumerate(decs) if not d.used_cached_assignment][:8]
+    for i in routed:
+        cv = router.score(reqs[i], recs[i], pool)
+        assert isinstance(cv, ConfidenceVector)
+        got = np.array([cv[m] for m in ids])
+        assert np.abs(got - q_batch[i]).max() <= 1e-6, (i, got, q_batch[i])
