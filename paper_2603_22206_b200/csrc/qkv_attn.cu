@@ -274,7 +274,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int g = 0;  // projection k-blocks issued so far
       auto gemm_kb = [&](int it, int kb) {
         if constexpr (PAIR) {
-          // leader: one pair MMA group into both CTAs' accumulators
+          // leader: one pair MMA group into both CTAs' accumulators. With a
+          // lag, at most `lag` projection k-blocks are queued on the tensor
+          // pipe, so S(i) / O(i) slotted between them start soon.
+          if (lag > 0 && g >= lag) {
+            const int d = g - lag;
+            sm100::mbar_wait(&s.kdone[d % NST], (d / NST) & 1);
+          }
           sm100::mbar_wait(&s.full[stage], phase);
           sm100::tc_fence_after();
           const uint32_t a = sm100::smem_u32(stage_ptr(stage));
@@ -286,7 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm100::mma_bf16_cg2_w(d, sm100::umma_desc_sw128(a + k * 32),
                                   sm100::umma_desc_sw128(b + k * 32), idesc_p, (kb | k) != 0);
           sm100::mma_commit_cg2_mc_w(&s.empty[stage], 0x3);
+          if (lag > 0) sm100::mma_commit_cg2_mc_w(&s.kdone[stage], 0x1);
           if (kb == k_blocks - 1) sm100::mma_commit_cg2_mc_w(&s.acc_full[it & 1], 0x3);
+          ++g;
           if (++stage == NST) { stage = 0; phase ^= 1; }
           return;
         }
@@ -666,11 +674,15 @@ chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
   // cta_group::1 one, tools/experiments/qa_pair2.sh); CHM_QA_PAIR=0 selects
   // the cta_group::1 kernel, 1 the all-cta_group::2 experiment
   static const int pair = env_int("CHM_QA_PAIR", 2);
+  // CHM_QA_PAIR_LAG: projection k-blocks the pair kernel keeps queued ahead of
+  // S / O (0 = the operand ring's depth)
+  static const int pair_lag = env_int("CHM_QA_PAIR_LAG", 0) < qa::kPairStages
+                                  ? env_int("CHM_QA_PAIR_LAG", 0) : qa::kPairStages - 1;
   if (pair == 2)  // pair-projection variant of the fused kernel (cta_group::2 + ::1)
     return stats_in ? launch<2, 1, true, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part,
-                                                      eps, ctx, n_seq, hidden, 0, 0, st)
+                                                      eps, ctx, n_seq, hidden, pair_lag, 0, st)
                     : launch<2, 1, false, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part,
-                                                       eps, ctx, n_seq, hidden, 0,
+                                                       eps, ctx, n_seq, hidden, pair_lag,
                                                        env_int("CHM_QA_DEBUG", 0), st);
   if (pair)
     return qkv_attention_pair(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden,

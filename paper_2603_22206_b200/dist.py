@@ -204,6 +204,13 @@ class ShardedScheduler:
         if global_admission:
             self.packed = torch.empty((2 + len(_RELAYED)) * K, dtype=torch.float64, device=dev)
         self.s0 = torch.empty(2 * K, dtype=torch.float64, device=dev)
+        # the Mode A records are all-gathered: every rank needs the same size
+        mr = torch.tensor([scheduler.buf.max_rows], dtype=torch.int64, device=dev)
+        all_mr = torch.empty((self.comm.world, 1), dtype=torch.int64, device=dev)
+        self.comm.allgather(mr, all_mr, torch.cuda.current_stream(dev))
+        if int(all_mr.min()) != int(all_mr.max()):
+            raise ValueError(f"ranks use different max_rows {all_mr.view(-1).tolist()}: the "
+                             "sharded exchange needs one batch capacity on every rank")
         rb = int(self.lib.chm_inflight_record_bytes(K, scheduler.buf.max_rows))
         self.rec_bytes = rb
         self.record = torch.empty(rb, dtype=torch.uint8, device=dev)

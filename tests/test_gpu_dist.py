@@ -139,7 +139,7 @@ def _run_rank(rank, name):
         rt, pr = ScoreTableRouter(), PrecomputedPredictor()
         gs = GpuScheduler(pool, BalancerConfig(sc["tau"], sc["margin"]), AgingConfig(),
                           router=rt, predictor=pr, n_programs=sc["n_prog"],
-                          max_rows=max(len(mine), 1), queue_capacity=10240)
+                          max_rows=n, queue_capacity=10240)  # same on every rank
         per_model = {m: [] for m in ids}
         for m, v in sc["p0"]:
             per_model[ids[int(m)]].append(float(v))
