@@ -20,7 +20,8 @@ namespace chm {
 
 chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
-                         void* ctx, int n_seq, int hidden, cudaStream_t st);
+                         void* ctx, int n_seq, int hidden, cudaStream_t st,
+                         const int32_t* n_live = nullptr);
 namespace gemm {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                     uint32_t box_rows, uint32_t box_cols, uint64_t ld);
@@ -103,8 +104,9 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(
   if (t >= (long long)n_seq * S) return;
   const int seq = (int)(t / S), pos = (int)(t - (long long)seq * S);
   const int n_live = n_rows_dev ? *n_rows_dev : n_seq;
+  if (seq >= n_live) return;  // rows on the reuse branch are never encoded
   int row = seq;
-  if (rows) row = rows[seq < n_live ? seq : 0];
+  if (rows) row = rows[seq];
   int id = ids[(size_t)row * S + pos];
   id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
   float v[VEC * 8], w[VEC * 8];
@@ -145,12 +147,13 @@ constexpr size_t kAttnSmemBytes = sizeof(AttnSmem) + 1024;
 
 __global__ void __launch_bounds__(160, 4)
     attention_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
-                     __nv_bfloat16* __restrict__ ctx) {
+                     __nv_bfloat16* __restrict__ ctx, const int32_t* __restrict__ n_live) {
   extern __shared__ uint8_t smem_raw[];
   AttnSmem& s = sm100::align_smem_1024<AttnSmem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
   const int item = blockIdx.x;
   const int seq = item / n_heads, h = item - seq * n_heads;
+  if (n_live && seq >= *n_live) return;  // whole block: before any barrier / TMEM
   if (warp == 4 && lane == 0) {
     sm100::mbar_init(&s.bar_load, 1);
     sm100::mbar_init(&s.bar_s, 1);
@@ -291,7 +294,8 @@ constexpr size_t kAttnLongSmemBytes = sizeof(AttnLongSmem) + 1024;
 
 __global__ void __launch_bounds__(160, 1)
     attention_long_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
-                          int S, __nv_bfloat16* __restrict__ ctx) {
+                          int S, __nv_bfloat16* __restrict__ ctx,
+                          const int32_t* __restrict__ n_live) {
   extern __shared__ uint8_t smem_raw[];
   AttnLongSmem& s = sm100::align_smem_1024<AttnLongSmem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(160, 1)
   const int sh = item / n_qb;
   const int seq = sh / n_heads, h = sh - seq * n_heads;
   const int row0 = seq * S;
+  if (n_live && seq >= *n_live) return;  // whole block: before any barrier / TMEM
   if (warp == 4 && lane == 0) {
     sm100::mbar_init(&s.bar_q, 1);
     sm100::mbar_init(&s.bar_kv[0], 1);
@@ -490,7 +495,8 @@ constexpr size_t kFlashSmemBytes = sizeof(FlashSmem) + 1024;
 
 __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
-                           int S, int n_items, __nv_bfloat16* __restrict__ ctx) {
+                           int S, int n_items, __nv_bfloat16* __restrict__ ctx,
+                           const int32_t* __restrict__ n_live) {
   extern __shared__ uint8_t smem_raw[];
   FlashSmem& s = sm100::align_smem_1024<FlashSmem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
@@ -515,6 +521,8 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = sm100::uniform(s.tmem_base);
+  // items are sequence-major: only the routed (live) sequences' items run
+  if (n_live) n_items = min(n_items, *n_live * n_heads * n_qp);
   const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (warp == 0) {
@@ -717,13 +725,14 @@ template <int S>
 __global__ void __launch_bounds__(kClsWarps * 32)
     attention_cls_kernel(const __nv_bfloat16* __restrict__ qc,
                          const __nv_bfloat16* __restrict__ kv, int n_items, int n_heads,
-                         int hidden, __nv_bfloat16* __restrict__ ctx_c) {
+                         int hidden, __nv_bfloat16* __restrict__ ctx_c,
+                         const int32_t* __restrict__ n_live) {
   constexpr int KPL = S / 32;  // keys per lane
   __shared__ float s_q[kClsWarps][64];
   __shared__ float s_p[kClsWarps][S];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kClsWarps + w;
-  if (item >= n_items) return;
+  if (item >= n_items || (n_live && item >= *n_live * n_heads)) return;
   const int seq = item / n_heads, h = item - seq * n_heads;
   // q: the CLS rows' bf16 projections [n_seq, H] (unscaled; x 1/8 here is
   // exact, the same value the QKV epilogue's scaled rounding gives);
@@ -875,11 +884,12 @@ __global__ void __launch_bounds__(256) ln_rows_kernel(const __nv_bfloat16* __res
                                                       int n_seq, const float2* __restrict__ stats,
                                                       int P, const float* __restrict__ g,
                                                       const float* __restrict__ be, float eps,
-                                                      __nv_bfloat16* __restrict__ out) {
+                                                      __nv_bfloat16* __restrict__ out,
+                                                      const int32_t* __restrict__ n_live) {
   constexpr int H = 32 * 8 * VEC;
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (i >= n_seq) return;
+  if (i >= n_seq || (n_live && i >= *n_live)) return;
   float v[VEC * 8];
   load_row<VEC>(x + (size_t)i * S * H, lane, v);
   float a = 1.f, b = 0.f;
@@ -932,7 +942,7 @@ static int n_sms() {
 
 // ctx = attention(qkv) for n_seq sequences of S tokens (S % 128 == 0, <= 512).
 chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq, int S, int H,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int32_t* n_live = nullptr) {
   const long long T = (long long)n_seq * S;
   CUtensorMap tm_qkv;
   if (!gemm::make_tmap_bf16(&tm_qkv, qk, (uint64_t)T, (uint64_t)3 * H, 128, 64, 0))
@@ -950,15 +960,16 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
   const int NH = H / 64;
   prof::begin(prof::K_ATTENTION, st);
   if (S == kAttnS) {
-    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx);
+    attention_kernel<<<(unsigned)(n_seq * NH), 160, kAttnSmemBytes, st>>>(tm_qkv, NH, H, ctx,
+                                                                          n_live);
   } else if (S % (2 * kAttnS) == 0) {
     const int items = n_seq * NH * (S / (2 * kAttnS));
     const unsigned grid = (unsigned)(items < n_sms() ? items : n_sms());
     attention_flash_kernel<<<grid, kFlashThreads, kFlashSmemBytes, st>>>(tm_qkv, NH, H, S,
-                                                                         items, ctx);
+                                                                         items, ctx, n_live);
   } else {
     attention_long_kernel<<<(unsigned)(n_seq * NH * (S / kAttnS)), 160, kAttnLongSmemBytes,
-                            st>>>(tm_qkv, NH, H, S, ctx);
+                            st>>>(tm_qkv, NH, H, S, ctx, n_live);
   }
   prof::end(prof::K_ATTENTION, st, 4.0 * S * S * 64.0 * n_seq * NH);
   CHM_LAUNCH_CHECK();
@@ -1030,6 +1041,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       auto* qc = qk + (size_t)n_seq * H;
       auto* kvb = ffn;
       GemmArgs gkv;
+      gkv.live_rows = n_rows_dev;
+      gkv.live_mult = S;
       gkv.epilogue = 1;  // bias
       gkv.bias = bq + H;
       gkv.stats_in = st_in;
@@ -1041,10 +1054,13 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       if (rc != CHM_OK) return rc;
       prof::begin(prof::K_ROWWISE, st);
       ln_rows_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(x, S, n_seq, st_in, P,
-                                                                       g_prev, b_prev, eps, hc);
+                                                                       g_prev, b_prev, eps, hc,
+                                                                       n_rows_dev);
       prof::end(prof::K_ROWWISE, st, (double)n_seq * (4.0 * H + 8.0 * P));
       CHM_LAUNCH_CHECK();
       GemmArgs gq;
+      gq.live_rows = n_rows_dev;
+      gq.live_mult = 1;
       gq.epilogue = 1;
       gq.bias = w.b_qkv[l];
       rc = gemm_run(hc, w.w_qkv[l], qc, n_seq, H, H, gq, st);
@@ -1053,14 +1069,16 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
       prof::begin(prof::K_ATTENTION, st);
       switch (S) {
-        case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
-        case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
-        case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
-        default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c); break;
+        case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+        case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+        case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+        default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
       }
       prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
       CHM_LAUNCH_CHECK();
       GemmArgs go;
+      go.live_rows = n_rows_dev;
+      go.live_mult = 1;
       go.epilogue = 5;
       go.bias = w.b_o[l];
       go.residual = hc;
@@ -1070,11 +1088,15 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       rc = gemm_run(ctx_c, w.w_o[l], xc, n_seq, H, H, go, st);
       if (rc != CHM_OK) return rc;
       GemmArgs g1;
+      g1.live_rows = n_rows_dev;
+      g1.live_mult = 1;
       g1.epilogue = 2;
       g1.bias = w.b_1[l];
       rc = gemm_run(xc, w.w_1[l], ffn, n_seq, F, H, g1, st);
       if (rc != CHM_OK) return rc;
       GemmArgs g2;
+      g2.live_rows = n_rows_dev;
+      g2.live_mult = 1;
       g2.epilogue = 5;
       g2.bias = w.b_2[l];
       g2.residual = xc;
@@ -1087,10 +1109,12 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
     }
     if (fused) {
       // QKV projection + attention in one kernel (qkv_attn.cu)
-      rc = qkv_attention(x, wq, bq, cq, st_in, P, eps, ctx, n_seq, H, st);
+      rc = qkv_attention(x, wq, bq, cq, st_in, P, eps, ctx, n_seq, H, st, n_rows_dev);
       if (rc != CHM_OK) return rc;
     } else {
       GemmArgs g;
+      g.live_rows = n_rows_dev;
+      g.live_mult = S;
       g.epilogue = 4;
       g.bias = bq;
       g.hidden = H;
@@ -1100,11 +1124,13 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       g.eps = eps;
       rc = gemm_run(x, wq, qk, (int)T, 3 * H, H, g, st);
       if (rc != CHM_OK) return rc;
-      rc = run_attention(qk, ctx, n_seq, S, H, st);
+      rc = run_attention(qk, ctx, n_seq, S, H, st, n_rows_dev);
       if (rc != CHM_OK) return rc;
     }
     if (cluster_ln) {
       GemmArgs go;
+      go.live_rows = n_rows_dev;
+      go.live_mult = S;
       go.epilogue = 5;
       go.bias = w.b_o[l];
       go.residual = x;
@@ -1114,11 +1140,15 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       rc = gemm_run(ctx, w.w_o[l], x, (int)T, H, H, go, st);
       if (rc != CHM_OK) return rc;
       GemmArgs g1;
+      g1.live_rows = n_rows_dev;
+      g1.live_mult = S;
       g1.epilogue = 2;
       g1.bias = w.b_1[l];
       rc = gemm_run(x, w.w_1[l], ffn, (int)T, F, H, g1, st);
       if (rc != CHM_OK) return rc;
       GemmArgs g2;
+      g2.live_rows = n_rows_dev;
+      g2.live_mult = S;
       g2.epilogue = 5;
       g2.bias = w.b_2[l];
       g2.residual = x;
@@ -1131,6 +1161,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
     }
     // out-projection: v = ctx.Wo^T + b_o + LN2_{l-1}(u_l) -> tmp, statistics -> st_v
     GemmArgs go;
+    go.live_rows = n_rows_dev;
+    go.live_mult = S;
     go.epilogue = 6;
     go.bias = w.b_o[l];
     go.residual = x;
@@ -1144,6 +1176,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
     if (rc != CHM_OK) return rc;
     // FFN1 on LN1(v), folded: W1' = W1 diag(ln1_g), b1' = b1 + W1 ln1_b
     GemmArgs g1;
+    g1.live_rows = n_rows_dev;
+    g1.live_mult = S;
     g1.epilogue = 2;
     g1.bias = reinterpret_cast<const float*>(fb + FL.b1);
     g1.colsum = reinterpret_cast<const float*>(fb + FL.c1);
@@ -1154,6 +1188,8 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
     if (rc != CHM_OK) return rc;
     // FFN2: u_{l+1} = f.W2^T + b_2 + LN1(v) -> x, statistics -> st_u
     GemmArgs g2;
+    g2.live_rows = n_rows_dev;
+    g2.live_mult = S;
     g2.epilogue = 6;
     g2.bias = w.b_2[l];
     g2.residual = tmp;

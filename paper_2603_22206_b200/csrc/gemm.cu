@@ -83,6 +83,8 @@ struct EpiParams {
   int n_part;              //   [M][n_part] partial (mean, M2) over 128 columns each
   const float* colsum;     // fold: c_n = sum_k B'[n][k]
   float2* stats_out;       // EPI 6: [M][N/128]
+  const int32_t* live_rows;  // rows computed: min(M, *live_rows * live_mult) (nullptr: M)
+  int live_mult;
   int dbg;             // measurement only: 1 = epilogue drains TMEM without math/stores,
                        // 2 = also no operand loads (MMAs on stale shared memory)
 };
@@ -191,6 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // LN: a cluster tile is one 256-row block (all three N tiles); otherwise a
   // pair tile (256 x 256), row-block major.
   const int n_tiles_n = kLN ? 1 : (N + BN - 1) / BN;
+  // only the live rows' tiles run (the routed sequences of the tick)
+  if (ep.live_rows) M = min(M, __ldg(ep.live_rows) * ep.live_mult);
   const int n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
   const int k_blocks = K / BK;
 
@@ -750,6 +754,8 @@ chm_status gemm_run(const void* A, const void* B, void* C, int M, int N, int K,
   ep.n_part = g.n_part;
   ep.colsum = g.colsum;
   ep.stats_out = g.stats_out;
+  ep.live_rows = g.live_rows;
+  ep.live_mult = g.live_mult;
   const float* bias = g.bias;
   const void* residual = g.residual;
   // measurement overrides: CHM_GEMM_STAGES (4 or 6 operand stages for the

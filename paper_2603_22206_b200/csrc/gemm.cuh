@@ -21,6 +21,10 @@ struct GemmArgs {
   int n_part = 0;
   const float* colsum = nullptr;     // fold: per output column sum of the folded weights
   float2* stats_out = nullptr;       // 6: [M][N/128]
+  // rows actually computed: min(M, *live_rows * live_mult) read on the device
+  // (the routed sequences of a tick; nullptr = all M rows)
+  const int32_t* live_rows = nullptr;
+  int live_mult = 1;
 };
 
 chm_status gemm_run(const void* A, const void* B, void* C, int M, int N, int K,

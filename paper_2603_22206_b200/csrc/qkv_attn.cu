@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const float* __restrict__ b_qkv, const float* __restrict__ c_qkv,
                          const float2* __restrict__ stats_in, int n_part, float eps, int n_seq,
                          int n_heads, int hidden, __nv_bfloat16* __restrict__ ctx, int lag,
-                         int dbg, int contiguous) {
+                         int dbg, int contiguous, const int32_t* __restrict__ n_live) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = sm100::align_smem_1024<Smem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
   for (int i = 0; i < CS; ++i) col_mask |= (uint16_t)(1u << (i * CH + cj));
   const int head_groups = n_heads / CH;
+  // only the routed (live) sequences are encoded (balancer.py:104-114)
+  if (n_live) n_seq = min(n_seq, __ldg(n_live));
   const int n_citems = ((n_seq + CS - 1) / CS) * head_groups;
   const int cl = (int)sm100::cluster_id_x(), n_cl = (int)sm100::n_clusters_x();
   // Item order: interleaved (cluster cl takes items cl, cl + n_cl, ...: the
@@ -604,7 +606,8 @@ static int env_int(const char* name, int dflt) {
 template <int CS, int CH, bool FOLD, bool TS = false, bool PAIR = false>
 static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
-                         void* ctx, int n_seq, int hidden, int lag, int dbg, cudaStream_t st) {
+                         void* ctx, int n_seq, int hidden, int lag, int dbg, cudaStream_t st,
+                         const int32_t* n_live = nullptr) {
   // CHM_QA_ORDER: 0 interleaved, 1 contiguous (measurement override)
   static const int order_env = env_int("CHM_QA_ORDER", -1);
   const int order = order_env >= 0 ? order_env : 0;
@@ -649,7 +652,8 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   prof::begin(prof::K_QKV_ATTENTION, st);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, c_qkv, stats_in, n_part, eps,
                                      n_seq, n_heads, hidden,
-                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg, order);
+                                     reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg, order,
+                                     n_live);
   // tensor work: the projection (2 T 3H H) + S and O (4 S^2 64 per item)
   prof::end(prof::K_QKV_ATTENTION, st,
             2.0 * T * 3.0 * hidden * hidden + 4.0 * qa::kS * qa::kS * 64.0 * n_seq * n_heads);
@@ -667,7 +671,8 @@ chm_status qkv_attention_pair(const void* x, const void* w_qkv, const float* b_q
 
 chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
-                         void* ctx, int n_seq, int hidden, cudaStream_t st) {
+                         void* ctx, int n_seq, int hidden, cudaStream_t st,
+                         const int32_t* n_live = nullptr) {
   if (stats_in && (!c_qkv || n_part < 1 || n_part > kLnMaxParts)) return CHM_ERR_INVALID_ARG;
   // CHM_QA_PAIR=1: the cta_group::2 kernel (qkv_attn_pair.cu)
   // default: the pair-projection kernel (fused 1.69 vs 1.76 ms for the
@@ -680,10 +685,11 @@ chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
                                   ? env_int("CHM_QA_PAIR_LAG", 0) : qa::kPairStages - 1;
   if (pair == 2)  // pair-projection variant of the fused kernel (cta_group::2 + ::1)
     return stats_in ? launch<2, 1, true, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part,
-                                                      eps, ctx, n_seq, hidden, pair_lag, 0, st)
+                                                      eps, ctx, n_seq, hidden, pair_lag, 0, st,
+                                                      n_live)
                     : launch<2, 1, false, false, true>(x, w_qkv, b_qkv, c_qkv, stats_in, n_part,
                                                        eps, ctx, n_seq, hidden, pair_lag,
-                                                       env_int("CHM_QA_DEBUG", 0), st);
+                                                       env_int("CHM_QA_DEBUG", 0), st, n_live);
   if (pair)
     return qkv_attention_pair(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden,
                               st);
