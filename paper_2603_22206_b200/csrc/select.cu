@@ -126,6 +126,7 @@ struct SelectParams {
 };
 
 constexpr int kChunk = 256;
+constexpr bool warp_chain_smem = true;  // the warp chain's prefix-sum rebuild of the loads
 constexpr int kThreads = 256;
 
 // record_dispatch's insertion into _in_flight[model] (monitor.py:95): the
@@ -147,7 +148,9 @@ __device__ __forceinline__ void log_append(const chm_monitor_state& mon, int m, 
 template <int K>
 struct ChunkBuf {
   uint64_t qual[kChunk];   // byte f: models clearing the gate of m_fast = f, rank space
+  uint64_t qualm[kChunk];  // byte f: the same set in model space (bit k = model k)
   uint64_t rbits[kChunk];  // byte k: rank-space bit of model k
+  uint32_t rank[kChunk];   // nibble k: descending-q rank of model k
   double yhat[kChunk * K];
   double arrival[kChunk];
   uint32_t perm[kChunk];   // nibble (7 - r): the model of rank r
@@ -380,7 +383,6 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       }
       if (bad) fl |= RF_BAD_SCORE;
       // rank[m] = position of m in sorted(models, key=(-q[m], m)).
-      uint32_t rbit[K];
 #pragma unroll
       for (int m = 0; m < K; ++m) {
         uint32_t r = 0;
@@ -388,16 +390,15 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
         for (int o = 0; o < K; ++o)
           r += (q[o] > q[m] || (q[o] == q[m] && o < m)) ? 1u : 0u;
         rank |= r << (4 * m);
-        rbit[m] = 0x80u >> r;
       }
       // qual byte mf = { m : q[m] >= q[mf] + margin } (balancer.py:73-75),
-      // as rank-space bits
+      // model-space bits (load_chunk derives the rank-space form)
 #pragma unroll
       for (int mf = 0; mf < K; ++mf) {
         const double thr = __dadd_rn(q[mf], prm.margin);
         uint64_t bits = 0;
 #pragma unroll
-        for (int m = 0; m < K; ++m) bits |= q[m] >= thr ? rbit[m] : 0u;
+        for (int m = 0; m < K; ++m) bits |= q[m] >= thr ? (1u << m) : 0u;
         qual |= bits << (8 * mf);
       }
     }
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
     const int n = min(kChunk, B - r0);
     if (n <= 0) return;
     for (int j = t0; j < n; j += nt) {
-      buf->qual[j] = __ldcg(sc.qual + r0 + j);
+      const uint64_t qm = __ldcg(sc.qual + r0 + j);
       const uint32_t rk = __ldcg(sc.rank + r0 + j);
       uint32_t pm = 0;  // perm: rank r -> model, at nibble 7 - r
       uint64_t rb = 0;
@@ -430,6 +431,15 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
         pm |= (uint32_t)k << (4 * (7 - r));
         rb |= (uint64_t)(0x80u >> r) << (8 * k);
       }
+      uint64_t qr = 0;  // gate sets in rank space
+#pragma unroll
+      for (int f = 0; f < K; ++f)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if ((qm >> (8 * f + k)) & 1ull) qr |= ((rb >> (8 * k)) & 0xffull) << (8 * f);
+      buf->qual[j] = qr;
+      buf->qualm[j] = qm;
+      buf->rank[j] = rk;
       buf->perm[j] = pm;
       buf->rbits[j] = rb;
       buf->flags[j] = __ldcg(sc.flags + r0 + j);
@@ -451,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   // Chain state (thread 0 only). Per-engine counters that do not feed back
   // into the selection live in shared memory.
   double L[K];
-  __shared__ double s_f[K], s_c[K], s_clk[K], s_d[K], s_b[K], s_invb[K], s_L0[K];
+  __shared__ double s_f[K], s_c[K], s_clk[K], s_d[K], s_b[K], s_invb[K], s_L0[K], s_f0[K], s_dq[K];
   __shared__ long long s_seq[K], s_cnt[K], s_it[K];
   __shared__ int s_run[K], s_que[K], s_bmax[K], s_pow2[K];
   bool stop = false;
@@ -462,6 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
       const bool pw = (prm.b_pow2_mask >> m) & 1u;
       L[m] = load_of(neumaier_value(f, c), prm.d[m], prm.b[m], prm.inv_b[m], pw);
       s_L0[m] = L[m];
+      s_f0[m] = f;
+      s_dq[m] = __dmul_rn(prm.d[m], prm.inv_b[m]);
       s_f[m] = f;
       s_c[m] = c;
       s_d[m] = prm.d[m];
@@ -509,10 +521,105 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   unsigned long long climb;
   argmin_limit<K>(Lb, Lim, cmf, climb);
 
+  // ---- warp chain (dyadic, every b a power of two): lane k owns engine k ----
+  // Per row every lane tests its own engine (gate of m_fast, slack limit)
+  // and one integer min-reduction over the lanes picks the first candidate
+  // in descending-q order (key = rank * 8 + engine); m_fast for the next row
+  // is the argmin over the lanes of the loads with m_fast's speculative
+  // update in place (three min-reductions: high word, low word, lowest
+  // index), computed while the decision resolves. ~60 warp instructions per
+  // row instead of ~160 for one thread (profiles/r2_k6_chain.md).
+  const bool warp_chain = SPEC && dyadic && !exact;
+  const int lane = tid & 31;
+  double w_s = 0.0, w_L = __longlong_as_double(0x7ff0000000000000ll), w_dq = 0.0;
+  double w_Lmin = 0.0, w_lim = 0.0;
+  int w_cmf = 0;
+  bool w_stop = false;
+  if (warp_chain && tid < 32) {
+    __syncwarp();
+    w_stop = __shfl_sync(0xffffffffu, stop ? 1 : 0, 0) != 0;
+    if (lane < K) {
+      w_s = s_f[lane];  // dyadic: compensation 0
+      w_dq = __dmul_rn(prm.d[lane], prm.inv_b[lane]);
+      w_L = __dmul_rn(w_s, w_dq);
+    }
+    // argmin (L, index) over the lanes: high word, low word, index
+    const unsigned long long lb = (unsigned long long)__double_as_longlong(w_L);
+    const uint32_t hi = (uint32_t)(lb >> 32), lo = (uint32_t)lb;
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    const unsigned long long lm = ((unsigned long long)mh << 32) | ml;
+    w_cmf = (int)__reduce_min_sync(0xffffffffu, lb == lm ? (uint32_t)lane : 31u);
+    w_Lmin = __longlong_as_double((long long)lm);
+    w_lim = __dmul_rn(prm.one_plus_slack, w_Lmin);
+  }
+
   for (int ch = 0; ch < n_chunks; ++ch) {
     ChunkBuf<K>* cur = &bufs[ch & 1];
     if (tid >= 32) {
       if (ch + 1 < n_chunks) load_chunk(ch + 1, &bufs[(ch + 1) & 1], tid - 32, blockDim.x - 32);
+    } else if (warp_chain) {
+      if (!w_stop) {
+        const int r0 = ch * kChunk;
+        const int n = min(kChunk, B - r0);
+        const double ops = prm.one_plus_slack;
+        int32_t* __restrict__ model_out = out.model + r0;
+        const int rsh = 4 * lane;  // this lane's rank nibble
+        int mb = 0;  // lane l keeps the decision of row (j & ~31) + l until the group is full
+        // software pipeline: row j + 1's inputs are read while row j resolves
+        uint32_t nfl = cur->flags[0];
+        uint64_t nqm = cur->qualm[0];
+        uint32_t nrk = cur->rank[0];
+        int npre = cur->pre_model[0];
+        double ny = lane < K ? cur->yhat[lane] : 0.0;
+        for (int j = 0; j < n; ++j) {
+          const uint32_t fl = nfl;
+          const uint64_t qm = nqm;
+          const uint32_t rk = nrk;
+          const int pre = npre;
+          const double y = ny;
+          {
+            const int jn = j + 1 < n ? j + 1 : j;
+            nfl = cur->flags[jn];
+            nqm = cur->qualm[jn];
+            nrk = cur->rank[jn];
+            npre = cur->pre_model[jn];
+            ny = lane < K ? cur->yhat[jn * K + lane] : 0.0;
+          }
+          // speculative: this engine's sum and load if the row lands here
+          const double ls_d = __dadd_rn(w_s, y);
+          const double ls = lane < K ? __dmul_rn(ls_d, w_dq) : w_L;
+          // decision: candidates (gate of m_fast, within the slack) by rank
+          const bool gate = (qm >> (8 * w_cmf + lane)) & 1ull;
+          const bool cand = lane < K && gate && w_L <= w_lim;
+          const uint32_t key = cand ? (((rk >> rsh) & 15u) << 3) | (uint32_t)lane : 0xffu;
+          const uint32_t mn = __reduce_min_sync(0xffffffffu, key);
+          int m = mn == 0xffu ? w_cmf : (int)(mn & 7u);
+          m = (fl & RF_CACHED_PRE) ? pre : m;
+          // m_fast after the row if it lands on m_fast (speculative argmin)
+          const double lx = lane == w_cmf ? ls : w_L;
+          const unsigned long long lb = (unsigned long long)__double_as_longlong(lx);
+          const uint32_t hi = (uint32_t)(lb >> 32), lo = (uint32_t)lb;
+          const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+          const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+          const unsigned long long lm = ((unsigned long long)mh << 32) | ml;
+          const int mf2 = (int)__reduce_min_sync(0xffffffffu, lb == lm ? (uint32_t)lane : 31u);
+          // update
+          const bool hit = lane == m;
+          w_s = hit ? ls_d : w_s;
+          w_L = hit ? ls : w_L;
+          const bool moved = m == w_cmf;
+          const double lmd = __longlong_as_double((long long)lm);
+          w_cmf = moved ? mf2 : w_cmf;
+          w_lim = moved ? __dmul_rn(ops, lmd) : w_lim;
+          // decisions leave in coalesced groups of 32 rows; the loads each
+          // row saw are rebuilt in the post-pass from exact prefix sums
+          mb = lane == (j & 31) ? m : mb;
+          if ((j & 31) == 31 || j == n - 1) {
+            if (lane <= (j & 31)) model_out[(j & ~31) + lane] = mb;
+          }
+        }
+      }
     } else if (tid == 0 && !stop && !exact) {
       // ---------------- fast chain (no error exits) ----------------
       // Per row: decision from the loads (the only loop-carried input), then
@@ -770,8 +877,10 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   const int n_ok = s_committed;
   const int per = (n_ok + kThreads - 1) / kThreads;
   const int lo = min(tid * per, n_ok), hi = min(lo + per, n_ok);
-  const int warp = tid >> 5, lane = tid & 31;
-  if (tid == 0 && !exact) {
+  const int warp = tid >> 5;
+  if (warp_chain) {
+    if (tid < K) s_f[tid] = w_s;  // compensation stays 0 (dyadic)
+  } else if (tid == 0 && !exact) {
 #pragma unroll
     for (int m = 0; m < K; ++m) {
       s_f[m] = fr[m];
@@ -857,13 +966,56 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
   }
   // ---- Decision.estimated_loads + tie band, in parallel ----
   // The loads row i saw: L0, then for each model the new load recorded by the
-  // last earlier row that dispatched to it (lnew).
+  // last earlier row that dispatched to it (lnew). The warp chain records no
+  // loads: in dyadic mode every partial sum is exact in any order, so each
+  // thread rebuilds them as (s0 + prefix sum of the dispatched predictions) *
+  // (d / b), the chain's own arithmetic.
+  __shared__ double s_ysum[warp_chain_smem ? K : 1][warp_chain_smem ? kThreads : 1];
+  double w_run[K];
+  if (warp_chain_smem && warp_chain) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) w_run[k] = 0.0;
+    for (int i = lo; i < hi; ++i) {
+      const int m = out.model[i];
+      const double y = yhat[(size_t)i * K + m];
+#pragma unroll
+      for (int k = 0; k < K; ++k) w_run[k] = __dadd_rn(w_run[k], k == m ? y : 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) s_ysum[k][tid] = w_run[k];
+    __syncthreads();
+    if (warp < K) {  // exclusive prefix over the thread ranges (exact: dyadic)
+      double v[kThreads / 32], tot = 0.0;
+#pragma unroll
+      for (int e = 0; e < kThreads / 32; ++e) {
+        v[e] = s_ysum[warp][lane * (kThreads / 32) + e];
+        tot = __dadd_rn(tot, v[e]);
+      }
+      double incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = __dadd_rn(incl, t);
+      }
+      double run = __dsub_rn(incl, tot);
+#pragma unroll
+      for (int e = 0; e < kThreads / 32; ++e) {
+        s_ysum[warp][lane * (kThreads / 32) + e] = run;
+        run = __dadd_rn(run, v[e]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      w_run[k] = __dadd_rn(s_f0[k], s_ysum[k][tid]);
+  }
   {
     double Lc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int c = s_lastm[k][tid];
       Lc[k] = c >= 0 ? sc.lnew[c] : s_L0[k];
+      if (warp_chain_smem && warp_chain) Lc[k] = __dmul_rn(w_run[k], s_dq[k]);
     }
     int n_rank = 0, n_qual = 0, n_any = 0;
     for (int i = lo; i < hi; ++i) {
@@ -884,7 +1036,21 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
           n_any += 1;
         }
       }
-      const double ln = sc.lnew[i];
+      double ln;
+      if (warp_chain_smem && warp_chain) {
+        const double y = yhat[(size_t)i * K + m];
+#pragma unroll
+        for (int k = 0; k < K; ++k) w_run[k] = k == m ? __dadd_rn(w_run[k], y) : w_run[k];
+        double wm = w_run[0], dm = s_dq[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) {
+          wm = k == m ? w_run[k] : wm;
+          dm = k == m ? s_dq[k] : dm;
+        }
+        ln = __dmul_rn(wm, dm);
+      } else {
+        ln = sc.lnew[i];
+      }
 #pragma unroll
       for (int k = 0; k < K; ++k) Lc[k] = (k == m) ? ln : Lc[k];
     }
