@@ -487,12 +487,29 @@ struct FlashSmem {
   uint8_t q[2][2][kAttnS * 64 * 2];   // [item parity][tile] Q [128][64] SW128
   uint8_t kv[2][2][kAttnS * 64 * 2];  // [stage][K | V] [128 keys][64]
   uint8_t p[2][2][kAttnS * 64 * 2];   // [tile][key half] P [128 rows][64 keys]
+  uint8_t ones[16 * 128];             // bf16 1.0, a K-major B operand (N = 16): row sums of P
   uint64_t q_full[2], q_empty[2], kv_full[2], kv_empty[2];
   uint64_t s_full[2], p_full[2], o_full[2];
   uint32_t tmem_base;
 };
 constexpr size_t kFlashSmemBytes = sizeof(FlashSmem) + 1024;
 
+// 2^x for the polynomial share of the softmax exponentials (FlashAttention-4
+// style: part of the exps on the FMA pipe, the rest on MUFU): round-to-nearest
+// split x = i + f, f in [-0.5, 0.5], degree-3 fit of 2^f (max relative error
+// 7.5e-5, far below the bf16 rounding of P), 2^i added to the exponent bits.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: integer part in the low mantissa bits
+  const float r = t - 12582912.0f;
+  const float f = x - r;
+  float p = fmaf(0.05517153f, f, 0.24261111f);
+  p = fmaf(p, f, 0.693261f);
+  p = fmaf(p, f, 0.99992806f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+template <bool V2>
 __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
                            int S, int n_items, __nv_bfloat16* __restrict__ ctx,
@@ -517,6 +534,11 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  if (V2) {
+    for (int i = threadIdx.x; i < 16 * 128 / 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s.ones)[i] = 0x3F803F80u;  // two bf16 1.0
+    sm100::fence_proxy_async_smem();
+  }
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -586,6 +608,17 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
           sm100::mma_bf16_w(tmem + 256 + 64 * g, sm100::umma_desc_sw128(pa),
                             sm100::umma_desc_sw128(va + kk * 2048), idesc_o, kk);
         }
+        if (V2) {
+          // row sums of the bf16 P: P . ones (N = 16, every column the sum)
+          constexpr uint32_t idesc_l = sm100::umma_idesc_bf16(128, 16);
+          const uint32_t oa = sm100::smem_u32(s.ones);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t pa = sm100::smem_u32(s.p[g][kk >> 2]) + (kk & 3) * 32;
+            sm100::mma_bf16_w(tmem + 384 + 16 * g, sm100::umma_desc_sw128(pa),
+                              sm100::umma_desc_sw128(oa + (kk & 3) * 32), idesc_l, kk);
+          }
+        }
         sm100::mma_commit_w(&s.o_full[g]);
         if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
       };
@@ -611,6 +644,117 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
     const uint32_t o_tm = tmem + lane_base + 256 + 64 * g;
     constexpr float kLog2e = 1.4426950408889634f;
     int j = 0;
+    if constexpr (V2) {
+      // FlashAttention-4-style softmax: the running max moves only when a
+      // block's max exceeds it by more than 2^8 (P <= 256, exact after the
+      // final 1/l), so o / l are rarely rescaled; the row sums of P come from
+      // the P . ones MMA (no per-element unpack + add); a quarter of the
+      // exponentials run as a polynomial on the FMA pipe.
+      const uint32_t l_tm = tmem + lane_base + 384 + 16 * g;
+      for (int it = 0; it < n_my; ++it) {
+        const int item = (int)blockIdx.x + it * (int)gridDim.x;
+        const int qp = item % n_qp, sh = item / n_qp;
+        const int seq = sh / n_heads, h = sh - seq * n_heads;
+        float m_use = -INFINITY, l_run = 0.f;
+        float o[64];
+#pragma unroll
+        for (int e = 0; e < 64; ++e) o[e] = 0.f;
+        for (int kb = 0; kb < n_kb; ++kb, ++j) {
+          sm100::mbar_wait(&s.s_full[g], j & 1);
+          sm100::tc_fence_after();
+          float mx = -INFINITY;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t raw[32];
+            sm100::tmem_ld_32x32b_x32(s_tm + c * 32, raw);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(raw[e]));
+          }
+          const float mxl = mx * kLog2e;
+          float alpha = 1.f;
+          if (mxl > m_use + 8.0f) {
+            alpha = sm100::ex2_approx(m_use - mxl);  // 0 on the first block
+            m_use = mxl;
+          }
+          // P_g of the previous block is free once its P.V MMA completed;
+          // its O block and row sums (relative to the previous m_use) join
+          // o / l before the rescale
+          if (kb > 0) {
+            sm100::mbar_wait(&s.o_full[g], (j - 1) & 1);
+            sm100::tc_fence_after();
+            uint32_t ov[2][32];
+            sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+            sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+            const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              o[e] += __uint_as_float(ov[0][e]);
+              o[32 + e] += __uint_as_float(ov[1][e]);
+            }
+            l_run += __uint_as_float(lb);
+          }
+          if (alpha != 1.f) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e) o[e] *= alpha;
+            l_run *= alpha;
+          }
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t raw[32];
+            sm100::tmem_ld_32x32b_x32(s_tm + c * 32, raw);
+            sm100::tmem_ld_wait();
+            uint8_t* rowp = s.p[g][c >> 1] + r * 128;
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              __align__(16) __nv_bfloat162 pv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float x0 = fmaf(__uint_as_float(raw[q4 * 8 + 2 * e]), kLog2e, -m_use);
+                const float x1 = fmaf(__uint_as_float(raw[q4 * 8 + 2 * e + 1]), kLog2e, -m_use);
+                const float p0 = e == 3 ? exp2_poly(x0) : sm100::ex2_approx(x0);
+                const float p1 = e == 3 ? exp2_poly(x1) : sm100::ex2_approx(x1);
+                pv[e] = __floats2bfloat162_rn(p0, p1);
+              }
+              const int chunk = (c & 1) * 4 + q4;
+              *reinterpret_cast<uint4*>(rowp + ((chunk ^ (r & 7)) << 4)) =
+                  *reinterpret_cast<uint4*>(pv);
+            }
+          }
+          sm100::fence_proxy_async_smem();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&s.p_full[g]);
+        }
+        sm100::mbar_wait(&s.o_full[g], (j - 1) & 1);
+        sm100::tc_fence_after();
+        {
+          uint32_t ov[2][32];
+          sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+          sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+          const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            o[e] += __uint_as_float(ov[0][e]);
+            o[32 + e] += __uint_as_float(ov[1][e]);
+          }
+          l_run += __uint_as_float(lb);
+        }
+        sm100::tc_fence_before();
+        const float inv = 1.0f / l_run;
+        __nv_bfloat16* dst =
+            ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            pk[e] = __floats2bfloat162_rn(o[c * 8 + 2 * e] * inv, o[c * 8 + 2 * e + 1] * inv);
+          *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pk);
+        }
+      }
+    } else
     for (int it = 0; it < n_my; ++it) {
       const int item = (int)blockIdx.x + it * (int)gridDim.x;
       const int qp = item % n_qp, sh = item / n_qp;
@@ -953,8 +1097,10 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
                          (int)kAttnSmemBytes);
     cudaFuncSetAttribute(attention_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kAttnLongSmemBytes);
-    cudaFuncSetAttribute(attention_flash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kFlashSmemBytes);
+    cudaFuncSetAttribute(attention_flash_kernel<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlashSmemBytes);
+    cudaFuncSetAttribute(attention_flash_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlashSmemBytes);
     attr = true;
   }
   const int NH = H / 64;
@@ -965,8 +1111,14 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
   } else if (S % (2 * kAttnS) == 0) {
     const int items = n_seq * NH * (S / (2 * kAttnS));
     const unsigned grid = (unsigned)(items < n_sms() ? items : n_sms());
-    attention_flash_kernel<<<grid, kFlashThreads, kFlashSmemBytes, st>>>(tm_qkv, NH, H, S,
-                                                                         items, ctx, n_live);
+    // CHM_FLASH_V2=0: the round-1 softmax (A/B measurement)
+    static const int v2 = getenv("CHM_FLASH_V2") ? atoi(getenv("CHM_FLASH_V2")) : 1;
+    if (v2)
+      attention_flash_kernel<true><<<grid, kFlashThreads, kFlashSmemBytes, st>>>(
+          tm_qkv, NH, H, S, items, ctx, n_live);
+    else
+      attention_flash_kernel<false><<<grid, kFlashThreads, kFlashSmemBytes, st>>>(
+          tm_qkv, NH, H, S, items, ctx, n_live);
   } else {
     attention_long_kernel<<<(unsigned)(n_seq * NH * (S / kAttnS)), 160, kAttnLongSmemBytes,
                             st>>>(tm_qkv, NH, H, S, ctx, n_live);

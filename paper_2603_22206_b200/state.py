@@ -289,9 +289,11 @@ def balancer_struct(cfg: BalancerConfig, tie_tolerance: float = 2e-2) -> _lib.Ba
 
 
 def aging_struct(aging: AgingConfig) -> _lib.AgingCfg:
-    if aging.enabled:
-        S = aging.starvation_threshold
-        if S != int(S):
-            raise NotImplementedError("fractional starvation_threshold is not supported on device")
-        return _lib.AgingCfg(1, int(S), int(aging.running_quantum), int(aging.demote_while_queued))
-    return _lib.AgingCfg(0, 0, int(aging.running_quantum), 0)
+    """EngineSim compares integer counters with the thresholds (`count >= S`,
+    `quantum >= Q`, engine.py:346-374), so fractional thresholds act as their
+    ceilings. A NaN threshold never promotes, like S = inf."""
+    S = float(aging.starvation_threshold)
+    Q = math.ceil(float(aging.running_quantum))
+    if aging.enabled and not math.isnan(S):
+        return _lib.AgingCfg(1, int(math.ceil(S)), int(Q), int(aging.demote_while_queued))
+    return _lib.AgingCfg(0, 0, int(Q), 0)

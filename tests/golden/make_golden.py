@@ -436,6 +436,8 @@ def make_queues(only=None):
         "q_big": (5, 32, 8, 3000, [("iter", 7), ("complete", 32), ("enq", 500), ("iter", 3),
                                    ("complete", 16), ("iter", 9), ("complete", 32)]),
         "q_S1": (6, 2, 1, 30, [("iter", 3), ("complete", 2), ("iter", 2)]),
+        # a fractional threshold: count >= 2.5 with integer counts
+        "q_frac_s": (9, 3, 2.5, 25, [("iter", 4), ("enq", 6), ("complete", 2), ("iter", 3)]),
     }
     for name, (seed, b, S, n_pre, script) in scripts.items():
         if only is not None and name not in only:
@@ -449,6 +451,8 @@ def make_queues(only=None):
         "q_demote": (7, 3, 2, 2, 30, [("iter", 6), ("complete", 2), ("enq", 6), ("iter", 5)]),
         "q_demote_big": (8, 16, 3, 3, 1500, [("iter", 9), ("complete", 16), ("enq", 100),
                                               ("iter", 7), ("complete", 5), ("iter", 4)]),
+        "q_demote_frac": (10, 3, 1.5, 2.5, 30, [("iter", 6), ("complete", 2), ("enq", 6),
+                                                 ("iter", 5)]),
     }
     for name, (seed, b, S, Q, n_pre, script) in demote.items():
         if only is not None and name not in only:

@@ -213,9 +213,10 @@ def load_queue(name):
     z = np.load(os.path.join(GOLDEN, f"{name}.npz"), allow_pickle=False)
     d = {k: z[k] for k in z.files}
     d["script"] = json.loads(str(d["script"]))
-    for k in ("seed", "b", "S", "n_pre", "running", "iterations"):
+    for k in ("seed", "b", "n_pre", "running", "iterations"):
         d[k] = int(d[k])
-    d["Q"] = int(d["Q"]) if "Q" in d else 4
+    d["S"] = float(d["S"])  # fractional thresholds compare count >= S (engine.py:348)
+    d["Q"] = float(d["Q"]) if "Q" in d else 4
     d["demote"] = bool(int(d["demote"])) if "demote" in d else False
     return d
 

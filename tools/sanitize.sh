@@ -20,8 +20,8 @@ run() {  # tool, selection, log
   echo "$1 [$2] rc=$?" >> "$OUT/sanitize_summary.txt"
 }
 : > "$OUT/sanitize_summary.txt"
-run memcheck "$SEL_SMALL and not select_kat" sanitize_memcheck_small.log
+run memcheck "($SEL_SMALL) and not select_kat" sanitize_memcheck_small.log
 run memcheck "$SEL_ROUTER" sanitize_memcheck_router.log
-run racecheck "test_gpu_schedule and not select_kat or test_gpu_queue or test_gpu_complete" sanitize_racecheck.log
-run synccheck "test_gpu_schedule and not select_kat or test_gpu_queue or test_gpu_complete or test_gpu_trace" sanitize_synccheck.log
+run racecheck "(test_gpu_schedule or test_gpu_queue or test_gpu_complete) and not select_kat" sanitize_racecheck.log
+run synccheck "(test_gpu_schedule or test_gpu_queue or test_gpu_complete or test_gpu_trace) and not select_kat" sanitize_synccheck.log
 cat "$OUT/sanitize_summary.txt"
