@@ -119,6 +119,13 @@ typedef struct chm_monitor_state {
    * then the Neumaier sum of max(yhat - progress, 0) in insertion order.
    * NULL = decay off (the reference default). */
   double* inflight_progress;
+  /* Request-sharded runs (optional, NULL = off): a global insertion stamp per
+   * live entry, parallel to the log. chm_schedule_rows stamps row i with
+   * *stamp_base + i (the host sets stamp_base = tick << 40 | rank << 32 each
+   * tick), so the ranks' logs merge into the reference's one insertion order
+   * (chm_inflight_merge_sum). */
+  int64_t* inflight_stamp;
+  const int64_t* stamp_base;
 } chm_monitor_state;
 
 /* ---- one batch of requests, in arrival order ----------------------------- */
@@ -620,12 +627,24 @@ chm_status chm_inflight_relay_send(chm_comm* comm, double* state, int32_t n, voi
  * live terms per engine in units of 2^-8, out[K] = number of non-dyadic
  * terms; all-reduce the K + 1 words (chm_comm_allreduce_i64), then
  * chm_inflight_set_sum installs (sum, 0) -- builtin sum() of the survivors
- * in any order -- or reports UNSUPPORTED (non-dyadic survivors have no
- * order-free exact sum). */
+ * in any order -- or leaves the sums and reports UNSUPPORTED into `error`
+ * (if non-NULL) when a survivor is not dyadic: then the merge path below. */
 chm_status chm_inflight_local_sum(const chm_pool* pool, const chm_monitor_state* mon,
                                   int64_t* out, void* stream);
 chm_status chm_inflight_set_sum(const chm_pool* pool, const chm_monitor_state* mon,
                                 const int64_t* summed, int32_t* error, void* stream);
+/* Sharded completions with non-dyadic survivors: every rank packs its live
+ * (stamp, term) pairs per engine into [K][cap] records (16 B each; cap >=
+ * every rank's live count), the records are all-gathered ([G][K][cap]), and
+ * chm_inflight_merge_sum merges the G stamp-ordered lists per engine and
+ * replays CPython's Neumaier recurrence over them: builtin sum() of the
+ * survivors in the reference's insertion order, bit for bit. counts: the
+ * gathered live counts [G][K]. Requires inflight_stamp. */
+chm_status chm_inflight_pack_live(const chm_pool* pool, const chm_monitor_state* mon,
+                                  int32_t cap, void* records, void* stream);
+chm_status chm_inflight_merge_sum(const chm_pool* pool, const chm_monitor_state* mon,
+                                  const void* gathered, const int64_t* counts, int32_t world,
+                                  int32_t cap, void* stream);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,8 @@ class MonitorState(ctypes.Structure):
         ("inflight_key", c_void_p),
         ("inflight_yhat", c_void_p),
         ("inflight_progress", c_void_p),
+        ("inflight_stamp", c_void_p),
+        ("stamp_base", c_void_p),
     ]
 
 
@@ -331,6 +333,10 @@ _SIGNATURES = [
      [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p]),
     ("chm_inflight_set_sum", c_int32,
      [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_void_p]),
+    ("chm_inflight_pack_live", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_int32, c_void_p, c_void_p]),
+    ("chm_inflight_merge_sum", c_int32,
+     [POINTER(Pool), POINTER(MonitorState), c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
     ("chm_profile_enable", c_int32, [c_int32]),
     ("chm_profile_read", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]

@@ -26,7 +26,11 @@
 // exactly (int64 units of 2^-8, chm_inflight_local_sum), the sums are
 // all-reduced, and chm_inflight_set_sum installs the global exact sum (the
 // builtin sum() of the survivors in any order, compensation 0). Non-dyadic
-// survivors have no order-free exact sum: that case reports UNSUPPORTED.
+// survivors have no order-free exact sum: set_sum reports UNSUPPORTED and the
+// host takes the merge path -- every rank packs its survivors with their
+// global insertion stamps (chm_inflight_pack_live), the lists are
+// all-gathered, and chm_inflight_merge_sum replays the Neumaier recurrence in
+// the merged insertion order on every rank.
 #include <dlfcn.h>
 #include <nccl.h>
 #include <climits>
@@ -223,12 +227,67 @@ __global__ void __launch_bounds__(1024) local_sum_kernel(chm_monitor_state mon,
 
 __global__ void zero_flag_kernel(long long* out, int K) { out[K] = 0; }
 
+// (stamp, live term) of this rank's log, per engine, padded to cap.
+__global__ void __launch_bounds__(1024) pack_live_kernel(chm_monitor_state mon, int cap,
+                                                        long long* __restrict__ rec) {
+  const int m = blockIdx.x;
+  const int n = (int)mon.inflight_count[m];
+  const size_t base = (size_t)m * mon.inflight_capacity;
+  long long* out = rec + (size_t)m * cap * 2;
+  for (int i = threadIdx.x; i < cap; i += blockDim.x) {
+    long long st = LLONG_MAX;
+    double y = 0.0;
+    if (i < n) {
+      st = mon.inflight_stamp[base + i];
+      y = mon.inflight_yhat[base + i];
+      if (mon.inflight_progress) {  // decay_in_flight (monitor.py:122-129)
+        const double d = __dsub_rn(y, mon.inflight_progress[base + i]);
+        y = (0.0 > d) ? 0.0 : d;
+      }
+    }
+    out[2 * i] = st;
+    out[2 * i + 1] = __double_as_longlong(y);
+  }
+}
+
+// Per engine (one thread): merge the G stamp-ordered survivor lists and
+// replay builtin sum()'s Neumaier recurrence in that order.
+__global__ void merge_sum_kernel(chm_monitor_state mon, const long long* __restrict__ gathered,
+                                 const long long* __restrict__ counts, int G, int K, int cap) {
+  const int m = threadIdx.x;
+  if (m >= K) return;
+  int pos[64];
+  for (int g = 0; g < G; ++g) pos[g] = 0;
+  double s = 0.0, c = 0.0;
+  while (true) {
+    int best = -1;
+    long long bs = LLONG_MAX;
+    for (int g = 0; g < G; ++g) {
+      if (pos[g] >= (int)counts[(size_t)g * K + m]) continue;
+      const long long st = gathered[(((size_t)g * K + m) * cap + pos[g]) * 2];
+      if (st < bs) {
+        bs = st;
+        best = g;
+      }
+    }
+    if (best < 0) break;
+    const double y =
+        __longlong_as_double(gathered[(((size_t)best * K + m) * cap + pos[best]) * 2 + 1]);
+    neumaier_add(s, c, y);
+    ++pos[best];
+  }
+  mon.inflight_sum[m] = s;
+  mon.inflight_comp[m] = c;
+}
+
 __global__ void set_sum_kernel(chm_monitor_state mon, const long long* __restrict__ summed, int K,
                                int32_t* err) {
   const int m = threadIdx.x;
   if (m >= K) return;
-  if (summed[K] != 0 || summed[m] >= kMaxUnits) {
-    if (m == 0) report_error(err, CHM_ERR_UNSUPPORTED, 0, -1, 2);
+  bool exact = summed[K] == 0;
+  for (int k = 0; k < K; ++k) exact = exact && summed[k] < kMaxUnits;
+  if (!exact) {  // no order-free exact sum: the merge path (or the error) follows
+    if (m == 0 && err) report_error(err, CHM_ERR_UNSUPPORTED, 0, -1, 2);
     return;
   }
   mon.inflight_sum[m] = (double)summed[m] / kScale;
@@ -400,6 +459,32 @@ extern "C" chm_status chm_inflight_set_sum(const chm_pool* pool, const chm_monit
   if (K < 1 || K > CHM_MAX_MODELS) return CHM_ERR_INVALID_ARG;
   chm::comm::set_sum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
       *mon, reinterpret_cast<const long long*>(summed), K, error);
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_inflight_pack_live(const chm_pool* pool, const chm_monitor_state* mon,
+                                             int32_t cap, void* records, void* stream) {
+  if (!pool || !mon || !records || cap < 0 || !mon->inflight_stamp) return CHM_ERR_INVALID_ARG;
+  const int K = pool->n_models;
+  if (K < 1 || K > CHM_MAX_MODELS) return CHM_ERR_INVALID_ARG;
+  if (cap == 0) return CHM_OK;
+  chm::comm::pack_live_kernel<<<K, 1024, 0, (cudaStream_t)stream>>>(
+      *mon, cap, reinterpret_cast<long long*>(records));
+  CHM_LAUNCH_CHECK();
+  return CHM_OK;
+}
+
+extern "C" chm_status chm_inflight_merge_sum(const chm_pool* pool, const chm_monitor_state* mon,
+                                             const void* gathered, const int64_t* counts,
+                                             int32_t world, int32_t cap, void* stream) {
+  if (!pool || !mon || !gathered || !counts || world < 1 || world > 64 || cap < 0)
+    return CHM_ERR_INVALID_ARG;
+  const int K = pool->n_models;
+  if (K < 1 || K > CHM_MAX_MODELS) return CHM_ERR_INVALID_ARG;
+  chm::comm::merge_sum_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(
+      *mon, reinterpret_cast<const long long*>(gathered),
+      reinterpret_cast<const long long*>(counts), world, K, cap);
   CHM_LAUNCH_CHECK();
   return CHM_OK;
 }

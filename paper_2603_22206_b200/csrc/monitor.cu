@@ -217,13 +217,14 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
   double* prog = mon.inflight_progress;
   for (int b0 = 0; b0 < live; b0 += kThreads) {
     const int i = b0 + tid;
-    long long kk = 0;
+    long long kk = 0, sp = 0;
     double y = 0.0, pg = 0.0;
     bool keep = false;
     if (i < live) {
       kk = mon.inflight_key[base + i];
       y = mon.inflight_yhat[base + i];
       if (prog) pg = prog[base + i];
+      if (mon.inflight_stamp) sp = mon.inflight_stamp[base + i];
       int hit = find_key(s, nm, kk);
       if (hit >= 0) {
         // first occurrence among duplicates
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kThreads) complete_kernel(chm_monitor_state mo
       mon.inflight_key[pos] = kk;
       mon.inflight_yhat[pos] = y;
       if (prog) prog[pos] = pg;
+      if (mon.inflight_stamp) mon.inflight_stamp[pos] = sp;
     }
     out += s.misc[1];
     __syncthreads();

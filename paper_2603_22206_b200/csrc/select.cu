@@ -142,6 +142,7 @@ __device__ __forceinline__ void log_append(const chm_monitor_state& mon, int m, 
   const size_t at = (size_t)m * mon.inflight_capacity + pos;
   mon.inflight_key[at] = (long long)program * 32 + (stage - 1);
   mon.inflight_yhat[at] = y;
+  if (mon.inflight_stamp) mon.inflight_stamp[at] = *mon.stamp_base + row;
   if (mon.inflight_progress) mon.inflight_progress[at] = 0.0;  // nothing emitted yet
 }
 

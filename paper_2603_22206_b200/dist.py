@@ -31,7 +31,10 @@ tick and `divergence` counts how many decisions Mode A changes.
 Completions are sharded too: each rank removes its own finished requests from
 its own log, reduces the survivors exactly (int64 units of 2^-8) and the K
 sums are all-reduced (chm_inflight_local_sum / chm_comm_allreduce_i64 /
-chm_inflight_set_sum).
+chm_inflight_set_sum); when a survivor is not dyadic, the ranks' survivor
+lists (with global insertion stamps) are all-gathered and merged, and the
+Neumaier recurrence replays them in the reference's insertion order
+(chm_inflight_pack_live / chm_inflight_merge_sum).
 
 Transport: `NcclComm` drives the C-ABI's NCCL entry points (the product path,
 NCCL over NVLink); `TorchComm` runs the same packing / folding kernels over a
@@ -187,7 +190,7 @@ class ShardedScheduler:
     concatenated batch through one EngineSim per model."""
 
     def __init__(self, scheduler, mode: str = "B", group=None, global_admission: bool = False,
-                 comm=None):
+                 comm=None, completion_sums: str = "auto"):
         if mode not in ("A", "B"):
             raise ValueError("mode must be 'A' or 'B'")
         if global_admission and mode != "B":
@@ -216,6 +219,15 @@ class ShardedScheduler:
         self.record = torch.empty(rb, dtype=torch.uint8, device=dev)
         self.gathered = torch.empty((self.comm.world, rb), dtype=torch.uint8, device=dev)
         self.sums = torch.zeros(K + 1, dtype=torch.int64, device=dev)
+        # completion sums: "auto" = the exact dyadic all-reduce when every
+        # survivor is dyadic (checked on the host after it), else the
+        # stamp-ordered merge; "dyadic" = the all-reduce only (non-dyadic
+        # survivors raise); "merge" = always the merge
+        if completion_sums not in ("auto", "dyadic", "merge"):
+            raise ValueError("completion_sums must be auto, dyadic or merge")
+        self.completion_sums = completion_sums
+        st.enable_stamps()
+        self.tick = 0
 
     # -- exchange pieces ------------------------------------------------------
     def _pack(self) -> None:
@@ -258,14 +270,39 @@ class ShardedScheduler:
                    "chm_inflight_fold")
 
     def _sum_completions(self, stream) -> None:
-        """Global exact in-flight sums after sharded record_completion."""
+        """Global exact in-flight sums after sharded record_completion
+        (monitor.py:98-129): the dyadic all-reduce, or the merge of every
+        rank's survivors in the global insertion order."""
         st = self.gs.state
-        _lib.check(self.lib.chm_inflight_local_sum(st.pool_c, st.monitor_c, _p(self.sums),
-                                                   stream.cuda_stream), "chm_inflight_local_sum")
-        self.comm.allreduce_i64(self.sums, stream)
-        _lib.check(self.lib.chm_inflight_set_sum(st.pool_c, st.monitor_c, _p(self.sums),
-                                                 _p(self.gs.buf.error_complete),
-                                                 stream.cuda_stream), "chm_inflight_set_sum")
+        K = st.K
+        if self.completion_sums != "merge":
+            _lib.check(self.lib.chm_inflight_local_sum(st.pool_c, st.monitor_c, _p(self.sums),
+                                                       stream.cuda_stream),
+                       "chm_inflight_local_sum")
+            self.comm.allreduce_i64(self.sums, stream)
+            err = _p(self.gs.buf.error_complete) if self.completion_sums == "dyadic" else None
+            _lib.check(self.lib.chm_inflight_set_sum(st.pool_c, st.monitor_c, _p(self.sums),
+                                                     err, stream.cuda_stream),
+                       "chm_inflight_set_sum")
+            if self.completion_sums == "dyadic":
+                return
+            s = self.sums.cpu()  # host check (syncs the stream)
+            if int(s[K]) == 0 and int(s[:K].max()) < (1 << 53):
+                return
+        # merge path: every rank's (stamp, term) lists, all-gathered
+        counts = torch.empty((self.comm.world, K), dtype=torch.int64, device=st.device)
+        self.comm.allgather(st.inflight_count.contiguous(), counts, stream)
+        cap = int(counts.max().item())
+        rec = torch.empty(K * max(cap, 1) * 2, dtype=torch.int64, device=st.device)
+        _lib.check(self.lib.chm_inflight_pack_live(st.pool_c, st.monitor_c, cap, _p(rec),
+                                                   stream.cuda_stream), "chm_inflight_pack_live")
+        gathered = torch.empty((self.comm.world, rec.numel()), dtype=torch.int64,
+                               device=st.device)
+        self.comm.allgather(rec, gathered, stream)
+        _lib.check(self.lib.chm_inflight_merge_sum(st.pool_c, st.monitor_c, _p(gathered),
+                                                   _p(counts), self.comm.world, cap,
+                                                   stream.cuda_stream), "chm_inflight_merge_sum")
+        self._keep = (counts, rec, gathered)
 
     # -- the tick ---------------------------------------------------------------
     def run_rows(self, batch, n_iterations: int = 1, completions=None, n_complete=None,
@@ -279,6 +316,9 @@ class ShardedScheduler:
         gs = self.gs
         s = stream if stream is not None else torch.cuda.current_stream(gs.device)
         st = gs.state
+        # global insertion stamps of this tick's dispatches: (tick, rank, row)
+        st.stamp_base.fill_((self.tick << 40) | (self.comm.rank << 32))
+        self.tick += 1
         if self.global_admission:
             gs.begin_tick(completions=None, keep_admitted=False, stream=s)
             if completions is not None:

@@ -93,6 +93,10 @@ class DeviceState:
         self.decay_in_flight = bool(decay_in_flight)
         self.inflight_progress = (torch.zeros(K * self.inflight_capacity, dtype=f64, device=d)
                                   if self.decay_in_flight else None)
+        # request-sharded runs: global insertion stamps of the live log
+        # (enable_stamps(); dist.ShardedScheduler sets stamp_base every tick)
+        self.inflight_stamp = None
+        self.stamp_base = torch.zeros(1, dtype=i64, device=d)
         n = K * C
         self.q_priority = torch.zeros(n, dtype=f64, device=d)
         self.q_arrival = torch.zeros(n, dtype=f64, device=d)
@@ -121,13 +125,29 @@ class DeviceState:
             _ptr(self.assignment), _ptr(self.stage_bits), _ptr(self.batch_stamp),
             _ptr(self.engine_clock), _ptr(self.engine_seq), _ptr(self.engine_running),
             _ptr(self.engine_queued), _ptr(self.engine_iterations), self.inflight_capacity,
-            _ptr(self.inflight_key), _ptr(self.inflight_yhat), _ptr(self.inflight_progress))
+            _ptr(self.inflight_key), _ptr(self.inflight_yhat), _ptr(self.inflight_progress),
+            None, _ptr(self.stamp_base))
         self.queue_c = _lib.QueueState(
             C, _ptr(self.q_priority), _ptr(self.q_arrival), _ptr(self.q_seq),
             _ptr(self.q_handle), _ptr(self.q_out_tokens), _ptr(self.q_level),
             _ptr(self.q_count), _ptr(self.q_quantum), _ptr(self.q_order),
             _ptr(self.q_admitted), _ptr(self.q_n_admitted), _ptr(self.q_n_promoted),
             _ptr(self.q_arrival_unsorted), _ptr(self.q_scratch))
+
+    def enable_stamps(self) -> None:
+        """Keep a global insertion stamp per live entry (request-sharded
+        runs: the ranks' logs merge into one insertion order). Entries
+        already in the log (seeded) get stamps before every tick's."""
+        if self.inflight_stamp is not None:
+            return
+        K, cap = self.K, self.inflight_capacity
+        self.inflight_stamp = torch.full((K * cap,), -(1 << 62), dtype=torch.int64,
+                                         device=self.device)
+        n = self.inflight_count.cpu().tolist()
+        for k in range(K):
+            self.inflight_stamp[k * cap:k * cap + n[k]] = torch.arange(
+                n[k], dtype=torch.int64) - (1 << 62)
+        self.monitor_c.inflight_stamp = _ptr(self.inflight_stamp)
 
     # -- engine execution clock (SURVEY §8f row 3) ----------------------------
     run_c = None
@@ -208,6 +228,9 @@ class DeviceState:
                 -(n0 + 1), -(n0 + len(vals) + 1), -1, dtype=torch.int64)
             self.inflight_yhat[b:b + len(vals)] = torch.as_tensor(
                 np.asarray(vals, dtype=np.float64))
+            if self.inflight_stamp is not None:  # seeded entries precede every tick's
+                self.inflight_stamp[b:b + len(vals)] = torch.arange(
+                    n0, n0 + len(vals), dtype=torch.int64) - (1 << 62)
             s[k], c[k], n[k] = ss, cc, n0 + len(vals)
         self.inflight_sum.copy_(torch.from_numpy(s))
         self.inflight_comp.copy_(torch.from_numpy(c))
@@ -243,14 +266,15 @@ class DeviceState:
         self.engine_queued[model] = n
 
     # -- snapshot / restore (device-to-device copies, graph-capturable) ------
-    _MUTABLE = ("inflight_sum", "inflight_comp", "inflight_count", "inflight_key",
+    _MUTABLE = ("inflight_sc", "inflight_count", "inflight_key",
                 "inflight_yhat", "assignment", "stage_bits",
                 "engine_clock", "engine_seq", "engine_running", "engine_queued",
                 "engine_iterations", "q_priority", "q_arrival", "q_seq", "q_handle",
                 "q_out_tokens", "q_level", "q_count", "q_quantum")
 
     def _mutable(self):
-        return self._MUTABLE + (("inflight_progress",) if self.decay_in_flight else ())
+        return (self._MUTABLE + (("inflight_progress",) if self.decay_in_flight else ())
+                + (("inflight_stamp",) if self.inflight_stamp is not None else ()))
 
     def snapshot(self) -> dict:
         return {k: getattr(self, k).clone() for k in self._mutable()}

@@ -14,7 +14,9 @@ Checked against the oracle port:
           monitor after all dispatches in rank order (same state as Mode B);
   A vs B  the number of decisions Mode A changes (reported);
   completions  a second tick after each rank completes some of its own
-          requests: global exact sums (dyadic) and decisions vs the port.
+          requests: the global in-flight sums equal the port's bit for bit
+          (dyadic: exact int64 all-reduce; non-dyadic: the ranks' survivor
+          lists merged in insertion order).
 The expected values are computed inside the workers from the golden
 scenarios (tests/golden/schedule_*.npz)."""
 
@@ -198,20 +200,16 @@ def _run_rank(rank, name):
                                             handle=np.zeros(0)),
                         n_iterations=0, completions=(c_model, c_key), stream=stream)
             torch.cuda.synchronize()
-            if dyadic:
-                gs.check_errors("completions")
-                for g in range(WORLD):
-                    rows_g = rows_by_rank[g]
-                    for jj, i in enumerate(rows_g):
-                        if jj % 2 == 0:
-                            final.record_completion(ids[want[i][0]], _Req(sc, i).request_id)
-                want_p = np.array([final.in_flight_sum(m) for m in ids])
-                assert np.array(gs.state.in_flight_sums()).tobytes() == want_p.tobytes()
-                report["completions"] = "exact"
-            else:
-                with pytest.raises(NotImplementedError):
-                    gs.check_errors("completions")
-                report["completions"] = "non-dyadic: UNSUPPORTED reported"
+            gs.check_errors("completions")
+            for g in range(WORLD):
+                rows_g = rows_by_rank[g]
+                for jj, i in enumerate(rows_g):
+                    if jj % 2 == 0:
+                        final.record_completion(ids[want[i][0]], _Req(sc, i).request_id)
+            want_p = np.array([final.in_flight_sum(m) for m in ids])
+            assert np.array(gs.state.in_flight_sums()).tobytes() == want_p.tobytes()
+            report["completions"] = ("exact (dyadic all-reduce)" if dyadic
+                                     else "exact (stamp-ordered merge)")
     report["a_vs_b_divergence"] = D.divergence(models["A"], models["B"], comm, None)
     return report
 
