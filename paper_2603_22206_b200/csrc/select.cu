@@ -504,8 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1) schedule_rows_kernel(
 #pragma unroll
   for (int m = 0; m < K; ++m) {
     Lb[m] = (unsigned long long)__double_as_longlong(L[m]);
-    fr[m] = s_f[m];
-    cv[m] = s_c[m];
+    // only thread 0 runs these chains (and wrote s_f / s_c just above)
+    fr[m] = tid == 0 ? s_f[m] : 0.0;
+    cv[m] = tid == 0 ? s_c[m] : 0.0;
     dd[m] = prm.d[m];
     bdiv[m] = ((prm.b_pow2_mask >> m) & 1u) ? prm.inv_b[m] : prm.b[m];
     dq[m] = __dmul_rn(prm.d[m], prm.inv_b[m]);  // d / b, exact for b = 2^k
