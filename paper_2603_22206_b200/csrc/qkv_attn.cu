@@ -57,6 +57,9 @@ namespace qa {
 
 constexpr int kS = 128;                        // tokens per sequence = MMA M
 constexpr int kStages = 4;
+#ifndef CHM_QA_PAIR_STAGES
+#define CHM_QA_PAIR_STAGES 5
+#endif
 constexpr int kThreads = 320;                  // 10 warps
 constexpr uint32_t kATile = kS * 64 * 2;       // x   [128][64] bf16, 16 KB
 constexpr uint32_t kBTile = 192 * 64 * 2;      // W   [192][64] (Q | K | V rows), 24 KB
@@ -65,7 +68,7 @@ constexpr uint32_t kWBox = 32;                 // W rows per TMA box (6 per head
 constexpr uint32_t kHeadTile = kS * 64 * 2;    // Q/K/V [128][64] bf16, 16 KB
 constexpr uint32_t kAccCols = 192;
 constexpr uint32_t kSCol = 384;
-constexpr int kPairStages = 5;  // PAIR ring depth (28 KB stages)
+constexpr int kPairStages = CHM_QA_PAIR_STAGES;  // PAIR ring depth (28 KB stages)
 
 struct __align__(1024) Smem {
   // the operand ring: 4 x 40 KB (cta_group::1) or kPairStages x 28 KB (PAIR)
@@ -79,6 +82,7 @@ struct __align__(1024) Smem {
   uint64_t full[8], empty[8], kdone[8];
   uint64_t acc_full[2], acc_empty[2];
   uint64_t qkv_ready, s_full, p_ready, o_full;
+  uint64_t ev_pair;  // PAIR: both CTAs ready for the next S / O event
   uint32_t tmem_base;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
@@ -121,7 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const float* __restrict__ b_qkv, const float* __restrict__ c_qkv,
                          const float2* __restrict__ stats_in, int n_part, float eps, int n_seq,
                          int n_heads, int hidden, __nv_bfloat16* __restrict__ ctx, int lag,
-                         int dbg, int contiguous, const int32_t* __restrict__ n_live) {
+                         int dbg, int contiguous, const int32_t* __restrict__ n_live,
+                         int pair_sync) {
   extern __shared__ uint8_t smem_raw[];
   Smem& s = sm100::align_smem_1024<Smem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_init(&s.s_full, 1);
     sm100::mbar_init(&s.p_ready, 256);
     sm100::mbar_init(&s.o_full, 1);
+    sm100::mbar_init(&s.ev_pair, 2);
     sm100::fence_barrier_init();
   }
   if (warp == 1) {
@@ -363,11 +369,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       // on the accumulator (drain of item it - 2), never on attention.
       // (dbg 1-10, 12, 13: projection only)
       int ev = (dbg >= 1 && dbg <= 10) || dbg == 12 || dbg == 13 ? 2 * n_my : 0;
+      // PAIR + pair_sync: the two CTAs issue each S / O event together (each
+      // arrives on both CTAs' ev_pair once its own inputs are staged), so
+      // their cta_group::1 attention MMAs overlap instead of stalling the
+      // pair projection twice
+      bool armed = false;
       auto try_event = [&]() {
         if (ev >= 2 * n_my) return;
         const int j = ev >> 1;
         uint64_t* bar = (ev & 1) ? &s.p_ready : &s.qkv_ready;
-        if (!__shfl_sync(0xffffffffu, sm100::mbar_test(bar, j & 1), 0)) return;
+        if (PAIR && pair_sync) {
+          if (!armed) {
+            if (!__shfl_sync(0xffffffffu, sm100::mbar_test(bar, j & 1), 0)) return;
+            if (lane == 0) {
+              sm100::mbar_arrive(&s.ev_pair);
+              sm100::mbar_arrive_remote(sm100::mapa(sm100::smem_u32(&s.ev_pair), rank ^ 1u));
+            }
+            __syncwarp();
+            armed = true;
+          }
+          if (!__shfl_sync(0xffffffffu, sm100::mbar_test(&s.ev_pair, ev & 1), 0)) return;
+          armed = false;
+        } else if (!__shfl_sync(0xffffffffu, sm100::mbar_test(bar, j & 1), 0)) {
+          return;
+        }
         if (ev & 1) {
           if (lane == 0) stamp(dbg, ctx, j, 7);
           issue_o();
@@ -610,6 +635,8 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
                          const int32_t* n_live = nullptr) {
   // CHM_QA_ORDER: 0 interleaved, 1 contiguous (measurement override)
   static const int order_env = env_int("CHM_QA_ORDER", -1);
+  // CHM_QA_PAIR_SYNC: issue the two CTAs' attention MMAs together (PAIR)
+  static const int pair_sync = env_int("CHM_QA_PAIR_SYNC", 0);  // measured: no gain
   const int order = order_env >= 0 ? order_env : 0;
   const int n_heads = hidden / 64;
   if (n_heads % CH != 0) return CHM_ERR_UNSUPPORTED;
@@ -653,7 +680,7 @@ static chm_status launch(const void* x, const void* w_qkv, const float* b_qkv,
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_x, tm_w, b_qkv, c_qkv, stats_in, n_part, eps,
                                      n_seq, n_heads, hidden,
                                      reinterpret_cast<__nv_bfloat16*>(ctx), lag, dbg, order,
-                                     n_live);
+                                     n_live, pair_sync);
   // tensor work: the projection (2 T 3H H) + S and O (4 S^2 64 per item)
   prof::end(prof::K_QKV_ATTENTION, st,
             2.0 * T * 3.0 * hidden * hidden + 4.0 * qa::kS * qa::kS * 64.0 * n_seq * n_heads);
