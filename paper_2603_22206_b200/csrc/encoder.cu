@@ -859,6 +859,777 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 attention for S = 256 n, v3: 64-key blocks, double-buffered S, O in TMEM.
+// Same item as v1/v2 ((sequence, head, 256 queries) = two 128-query tiles g
+// sharing every K/V block). Per tile and key block j (64 keys):
+//   S_g(j) = Q_g K(j)^T        -> TMEM S[g][j & 1]  (2 buffers per tile, so
+//                                 S(j + 1) is computed while softmax(j) runs)
+//   P_g(j) = exp2(S log2e - m)  bf16 -> smem P[g][j & 1]
+//   O_g   += P_g(j) V(j)        TMEM-resident across the item's blocks
+//   l_g   += P_g(j) . ones      row sums by the tensor core (N = 16)
+// The running max moves only when a block's max exceeds it by more than 2^8;
+// then the softmax warp rescales O_g / l_g in TMEM (after O_g(j - 1) has
+// landed) -- the FlashAttention-4 scheme. A quarter of the exponentials run
+// as a polynomial on the FMA pipe.
+//   warp 0      TMA: Q (double-buffered across items), 4-stage K/V ring
+//   warp 1      MMA issuer: S0(0) S1(0) S0(1) S1(1) | O0(j) S0(j+2) O1(j) S1(j+2) ...
+//   warps 4-7   softmax of tile 0, warps 8-11 of tile 1 (thread = query row)
+// TMEM: S[g][b] at 128 g + 64 b, O_g at 256 + 64 g, l_g at 384 + 16 g.
+// ---------------------------------------------------------------------------
+constexpr int kF3Keys = 64;
+constexpr int kF3Stages = 4;
+struct Flash3Smem {
+  uint8_t q[2][2][kAttnS * 64 * 2];              // [item parity][tile] Q [128][64]
+  uint8_t kv[kF3Stages][2][kF3Keys * 64 * 2];    // [stage][K | V] [64 keys][64]
+  uint8_t p[2][2][kAttnS * kF3Keys * 2];         // [tile][buffer] P [128 rows][64 keys]
+  uint8_t ones[16 * 128];                        // bf16 1.0 (K-major B, N = 16)
+  uint64_t q_full[2], q_empty[2], kv_full[kF3Stages], kv_empty[kF3Stages];
+  uint64_t s_full[2][2], s_free[2][2], p_full[2][2], o_full[2][2];
+  uint32_t tmem_base;
+};
+constexpr size_t kFlash3SmemBytes = sizeof(Flash3Smem) + 1024;
+
+__global__ void __launch_bounds__(kFlashThreads, 1)
+    attention_flash3_kernel(const __grid_constant__ CUtensorMap tm_q,
+                            const __grid_constant__ CUtensorMap tm_kv, int n_heads, int hidden,
+                            int S, int n_items, __nv_bfloat16* __restrict__ ctx,
+                            const int32_t* __restrict__ n_live) {
+  extern __shared__ uint8_t smem_raw[];
+  Flash3Smem& s = sm100::align_smem_1024<Flash3Smem>(smem_raw);
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
+  const int n_kb = S / kF3Keys;
+  const int n_qp = S / (2 * kAttnS);
+  constexpr uint32_t kQTile = kAttnS * 64 * 2;
+  constexpr uint32_t kKvTile = kF3Keys * 64 * 2;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_q);
+    sm100::tma_prefetch(&tm_kv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s.q_full[i], 1);
+      sm100::mbar_init(&s.q_empty[i], 1);
+      for (int b = 0; b < 2; ++b) {
+        sm100::mbar_init(&s.s_full[i][b], 1);
+        sm100::mbar_init(&s.s_free[i][b], 128);
+        sm100::mbar_init(&s.p_full[i][b], 128);
+        sm100::mbar_init(&s.o_full[i][b], 1);
+      }
+    }
+    for (int i = 0; i < kF3Stages; ++i) {
+      sm100::mbar_init(&s.kv_full[i], 1);
+      sm100::mbar_init(&s.kv_empty[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  for (int i = threadIdx.x; i < 16 * 128 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s.ones)[i] = 0x3F803F80u;  // two bf16 1.0
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
+  // items are sequence-major: only the routed (live) sequences' items run
+  if (n_live) n_items = min(n_items, *n_live * n_heads * n_qp);
+  const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t kv_phase = 0;
+      for (int it = 0; it < n_my; ++it) {
+        const int item = (int)blockIdx.x + it * (int)gridDim.x;
+        const int qp = item % n_qp, sh = item / n_qp;
+        const int seq = sh / n_heads, h = sh - seq * n_heads;
+        const int row0 = seq * S;
+        const int qb = it & 1;
+        sm100::mbar_wait(&s.q_empty[qb], ((it >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&s.q_full[qb], 2 * kQTile);
+        sm100::tma_load_2d(s.q[qb][0], &tm_q, &s.q_full[qb], h * 64, row0 + qp * 256);
+        sm100::tma_load_2d(s.q[qb][1], &tm_q, &s.q_full[qb], h * 64, row0 + qp * 256 + 128);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          sm100::mbar_wait(&s.kv_empty[stage], kv_phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&s.kv_full[stage], 2 * kKvTile);
+          sm100::tma_load_2d(s.kv[stage][0], &tm_kv, &s.kv_full[stage], hidden + h * 64,
+                             row0 + kb * kF3Keys);
+          sm100::tma_load_2d(s.kv[stage][1], &tm_kv, &s.kv_full[stage], 2 * hidden + h * 64,
+                             row0 + kb * kF3Keys);
+          if (++stage == kF3Stages) { stage = 0; kv_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-uniform; *_w helpers elect the lane) ----------------
+    constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, kF3Keys);
+    constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
+    constexpr uint32_t idesc_l = sm100::umma_idesc_bf16(128, 16);
+    const int J = n_my * n_kb;  // flat (item, key block) index j
+    auto issue_s = [&](int g, int j) {
+      const int it = j / n_kb, kb = j - it * n_kb;
+      const int qb = it & 1, stage = j % kF3Stages, b = j & 1;
+      if (g == 0) {
+        if (kb == 0) sm100::mbar_wait(&s.q_full[qb], (it >> 1) & 1);
+        sm100::mbar_wait(&s.kv_full[stage], (j / kF3Stages) & 1);
+      }
+      // S[g][b] is free once softmax g has read S_g(j - 2) out of it
+      if (j >= 2) sm100::mbar_wait(&s.s_free[g][b], ((j - 2) >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t qa = sm100::smem_u32(s.q[qb][g]), ka = sm100::smem_u32(s.kv[stage][0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sm100::mma_bf16_w(tmem + 128 * g + 64 * b, sm100::umma_desc_sw128(qa + k * 32),
+                          sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+      sm100::mma_commit_w(&s.s_full[g][b]);
+      if (g == 1 && kb == n_kb - 1) sm100::mma_commit_w(&s.q_empty[qb]);
+    };
+    auto issue_o = [&](int g, int j) {
+      const int kb = j % n_kb, stage = j % kF3Stages, b = j & 1;
+      sm100::mbar_wait(&s.p_full[g][b], (j >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t pa = sm100::smem_u32(s.p[g][b]);
+      const uint32_t va = sm100::smem_u32(s.kv[stage][1]);
+      const uint32_t oa = sm100::smem_u32(s.ones);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        sm100::mma_bf16_w(tmem + 256 + 64 * g, sm100::umma_desc_sw128(pa + kk * 32),
+                          sm100::umma_desc_sw128(va + kk * 2048), idesc_o, (kb | kk) != 0);
+        sm100::mma_bf16_w(tmem + 384 + 16 * g, sm100::umma_desc_sw128(pa + kk * 32),
+                          sm100::umma_desc_sw128(oa + kk * 32), idesc_l, (kb | kk) != 0);
+      }
+      sm100::mma_commit_w(&s.o_full[g][b]);
+      if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
+    };
+    for (int j = 0; j < J && j < 2; ++j) {
+      issue_s(0, j);
+      issue_s(1, j);
+    }
+    for (int j = 0; j < J; ++j) {
+      issue_o(0, j);
+      if (j + 2 < J) issue_s(0, j + 2);
+      issue_o(1, j);
+      if (j + 2 < J) issue_s(1, j + 2);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------- softmax, tile g ----------------
+    const int g = (warp - 4) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t o_tm = lane_base + 256 + 64 * g;
+    const uint32_t l_tm = lane_base + 384 + 16 * g;
+    constexpr float kLog2e = 1.4426950408889634f;
+    int j = 0;
+    for (int it = 0; it < n_my; ++it) {
+      const int item = (int)blockIdx.x + it * (int)gridDim.x;
+      const int qp = item % n_qp, sh = item / n_qp;
+      const int seq = sh / n_heads, h = sh - seq * n_heads;
+      float m_use = -INFINITY;
+      for (int kb = 0; kb < n_kb; ++kb, ++j) {
+        const int b = j & 1;
+        sm100::mbar_wait(&s.s_full[g][b], (j >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t sv[2][32];
+        sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b, sv[0]);
+        sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b + 32, sv[1]);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.s_free[g][b]);  // S[g][b] may take S_g(j + 2)
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          mx = fmaxf(mx, fmaxf(__uint_as_float(sv[0][e]), __uint_as_float(sv[1][e])));
+        const float mxl = mx * kLog2e;
+        const bool grow = mxl > m_use + 8.0f;
+        if (__any_sync(0xffffffffu, grow) && kb > 0) {
+          // rescale O_g / l_g in tensor memory: O_g(j - 1) must have landed
+          sm100::mbar_wait(&s.o_full[g][b ^ 1], ((j - 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          const float alpha = grow ? sm100::ex2_approx(m_use - mxl) : 1.f;
+          uint32_t ov[32];
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, ov);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            sm100::tmem_st_32x32b_x32(o_tm + 32 * c, ov);
+          }
+          {
+            uint32_t l1 = sm100::tmem_ld_32x32b_x1(l_tm);
+            sm100::tmem_ld_wait();
+            l1 = __float_as_uint(__uint_as_float(l1) * alpha);
+            sm100::tmem_st_32x32b_x1(l_tm, l1);
+          }
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+        }
+        if (grow) m_use = mxl;
+        // P[g][b] is free once O_g(j - 2) (its last reader) completed
+        if (j >= 2) sm100::mbar_wait(&s.o_full[g][b], ((j - 2) >> 1) & 1);
+        uint8_t* rowp = s.p[g][b] + r * 128;
+#pragma unroll
+        for (int q8 = 0; q8 < 8; ++q8) {
+          __align__(16) __nv_bfloat162 pv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c0 = q8 * 8 + 2 * e;
+            const float x0 = fmaf(__uint_as_float(sv[c0 >> 5][c0 & 31]), kLog2e, -m_use);
+            const float x1 = fmaf(__uint_as_float(sv[(c0 + 1) >> 5][(c0 + 1) & 31]), kLog2e, -m_use);
+            const float p0 = e == 3 ? exp2_poly(x0) : sm100::ex2_approx(x0);
+            const float p1 = e == 3 ? exp2_poly(x1) : sm100::ex2_approx(x1);
+            pv[e] = __floats2bfloat162_rn(p0, p1);
+          }
+          *reinterpret_cast<uint4*>(rowp + ((q8 ^ (r & 7)) << 4)) = *reinterpret_cast<uint4*>(pv);
+        }
+        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.p_full[g][b]);
+      }
+      // item done: the last O_g / l_g, normalised, to ctx
+      sm100::mbar_wait(&s.o_full[g][(j - 1) & 1], ((j - 1) >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t ov[2][32];
+      sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+      sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+      const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      const float inv = 1.0f / __uint_as_float(lb);
+      __nv_bfloat16* dst =
+          ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c0 = c * 8 + 2 * e;
+          pk[e] = __floats2bfloat162_rn(__uint_as_float(ov[c0 >> 5][c0 & 31]) * inv,
+                                        __uint_as_float(ov[(c0 + 1) >> 5][(c0 + 1) & 31]) * inv);
+        }
+        *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pk);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 attention for S = 256 n, v4: P in tensor memory. Shared-memory bandwidth
+// bounds v1-v3: per 128-key block and tile, S = Q K^T reads Q + K (32 KB) and
+// O = P V reads P + V (48 KB) from shared memory for 4 MFLOP (~160 B per
+// tensor cycle, the SM moves 128). v4 keeps P in TMEM (written by the softmax
+// threads over the consumed S columns, tcgen05.st) and runs O = P V and the
+// row sums P . ones as TS MMAs (A from TMEM): ~96 B per cycle.
+//   warp 0      TMA: Q (double-buffered across items), 3-stage K/V ring
+//   warp 1      MMA issuer: S0(0) S1(0) | O0(j) O1(j) S0(j+1) S1(j+1) | ...
+//               (S_g(j+1) overwrites P_g(j): issued once O_g(j) completed)
+//   warps 4-7   softmax of tile 0, warps 8-11 of tile 1
+// TMEM: S_g / P_g at 128 g, O_g at 256 + 64 g (resident across the item's
+// blocks, rescaled in place when the running max jumps by > 2^8), l_g at
+// 384 + 16 g. When softmax_g(j) runs, O_g(j - 1) has completed (S_g(j) was
+// issued after it), so a rescale needs no extra wait.
+// ---------------------------------------------------------------------------
+constexpr int kF4Stages = 3;
+struct Flash4Smem {
+  uint8_t q[2][2][kAttnS * 64 * 2];              // [item parity][tile] Q [128][64]
+  uint8_t kv[kF4Stages][2][kAttnS * 64 * 2];     // [stage][K | V] [128 keys][64]
+  uint8_t ones[16 * 128];                        // bf16 1.0 (K-major B, N = 16)
+  uint64_t q_full[2], q_empty[2], kv_full[kF4Stages], kv_empty[kF4Stages];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kFlash4SmemBytes = sizeof(Flash4Smem) + 1024;
+
+__global__ void __launch_bounds__(kFlashThreads, 1)
+    attention_flash4_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
+                            int S, int n_items, __nv_bfloat16* __restrict__ ctx,
+                            const int32_t* __restrict__ n_live) {
+  extern __shared__ uint8_t smem_raw[];
+  Flash4Smem& s = sm100::align_smem_1024<Flash4Smem>(smem_raw);
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
+  const int n_kb = S / kAttnS;
+  const int n_qp = S / (2 * kAttnS);
+  constexpr uint32_t kTile = kAttnS * 64 * 2;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s.q_full[i], 1);
+      sm100::mbar_init(&s.q_empty[i], 1);
+      sm100::mbar_init(&s.s_full[i], 1);
+      sm100::mbar_init(&s.p_full[i], 128);
+      sm100::mbar_init(&s.o_full[i], 1);
+    }
+    for (int i = 0; i < kF4Stages; ++i) {
+      sm100::mbar_init(&s.kv_full[i], 1);
+      sm100::mbar_init(&s.kv_empty[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  for (int i = threadIdx.x; i < 16 * 128 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s.ones)[i] = 0x3F803F80u;  // two bf16 1.0
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
+  if (n_live) n_items = min(n_items, *n_live * n_heads * n_qp);
+  const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t kv_phase = 0;
+      for (int it = 0; it < n_my; ++it) {
+        const int item = (int)blockIdx.x + it * (int)gridDim.x;
+        const int qp = item % n_qp, sh = item / n_qp;
+        const int seq = sh / n_heads, h = sh - seq * n_heads;
+        const int row0 = seq * S;
+        const int qb = it & 1;
+        sm100::mbar_wait(&s.q_empty[qb], ((it >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&s.q_full[qb], 2 * kTile);
+        sm100::tma_load_2d(s.q[qb][0], &tm_qkv, &s.q_full[qb], h * 64, row0 + qp * 256);
+        sm100::tma_load_2d(s.q[qb][1], &tm_qkv, &s.q_full[qb], h * 64, row0 + qp * 256 + 128);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          sm100::mbar_wait(&s.kv_empty[stage], kv_phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&s.kv_full[stage], 2 * kTile);
+          sm100::tma_load_2d(s.kv[stage][0], &tm_qkv, &s.kv_full[stage], hidden + h * 64,
+                             row0 + kb * kAttnS);
+          sm100::tma_load_2d(s.kv[stage][1], &tm_qkv, &s.kv_full[stage], 2 * hidden + h * 64,
+                             row0 + kb * kAttnS);
+          if (++stage == kF4Stages) { stage = 0; kv_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-uniform; *_w helpers elect the lane) ----------------
+    constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 128);
+    constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
+    constexpr uint32_t idesc_l = sm100::umma_idesc_bf16(128, 16);
+    const int J = n_my * n_kb;
+    auto issue_s = [&](int g, int j) {
+      const int it = j / n_kb, kb = j - it * n_kb;
+      const int qb = it & 1, stage = j % kF4Stages;
+      if (g == 0) {
+        if (kb == 0) sm100::mbar_wait(&s.q_full[qb], (it >> 1) & 1);
+        sm100::mbar_wait(&s.kv_full[stage], (j / kF4Stages) & 1);
+      }
+      // S_g(j) overwrites P_g(j - 1): O_g(j - 1) and its row sums have read it
+      if (j > 0) sm100::mbar_wait(&s.o_full[g], (j - 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t qa = sm100::smem_u32(s.q[qb][g]), ka = sm100::smem_u32(s.kv[stage][0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sm100::mma_bf16_w(tmem + 128 * g, sm100::umma_desc_sw128(qa + k * 32),
+                          sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+      sm100::mma_commit_w(&s.s_full[g]);
+      if (g == 1 && kb == n_kb - 1) sm100::mma_commit_w(&s.q_empty[qb]);
+    };
+    auto issue_o = [&](int g, int j) {
+      const int kb = j % n_kb, stage = j % kF4Stages;
+      sm100::mbar_wait(&s.p_full[g], j & 1);
+      sm100::tc_fence_after();
+      const uint32_t va = sm100::smem_u32(s.kv[stage][1]);
+      const uint32_t oa = sm100::smem_u32(s.ones);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        sm100::mma_bf16_ts_w(tmem + 256 + 64 * g, tmem + 128 * g + kk * 8,
+                             sm100::umma_desc_sw128(va + kk * 2048), idesc_o, (kb | kk) != 0);
+        sm100::mma_bf16_ts_w(tmem + 384 + 16 * g, tmem + 128 * g + kk * 8,
+                             sm100::umma_desc_sw128(oa + (kk & 3) * 32), idesc_l, (kb | kk) != 0);
+      }
+      sm100::mma_commit_w(&s.o_full[g]);
+      if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
+    };
+    if (J > 0) {
+      issue_s(0, 0);
+      issue_s(1, 0);
+    }
+    for (int j = 0; j < J; ++j) {
+      issue_o(0, j);
+      issue_o(1, j);
+      if (j + 1 < J) {
+        issue_s(0, j + 1);
+        issue_s(1, j + 1);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------- softmax, tile g ----------------
+    const int g = (warp - 4) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t s_tm = lane_base + 128 * g;
+    const uint32_t o_tm = lane_base + 256 + 64 * g;
+    const uint32_t l_tm = lane_base + 384 + 16 * g;
+    constexpr float kLog2e = 1.4426950408889634f;
+    int j = 0;
+    for (int it = 0; it < n_my; ++it) {
+      const int item = (int)blockIdx.x + it * (int)gridDim.x;
+      const int qp = item % n_qp, sh = item / n_qp;
+      const int seq = sh / n_heads, h = sh - seq * n_heads;
+      float m_use = -INFINITY;
+      for (int kb = 0; kb < n_kb; ++kb, ++j) {
+        sm100::mbar_wait(&s.s_full[g], j & 1);
+        sm100::tc_fence_after();
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          sm100::tmem_ld_32x32b_x32(s_tm + 32 * c, raw);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(raw[e]));
+        }
+        const float mxl = mx * kLog2e;
+        const bool grow = mxl > m_use + 8.0f;
+        if (__any_sync(0xffffffffu, grow) && kb > 0) {
+          // O_g(j - 1) is complete (S_g(j) was issued after it): rescale in place
+          const float alpha = grow ? sm100::ex2_approx(m_use - mxl) : 1.f;
+          uint32_t ov[32];
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, ov);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            sm100::tmem_st_32x32b_x32(o_tm + 32 * c, ov);
+          }
+          uint32_t l1 = sm100::tmem_ld_32x32b_x1(l_tm);
+          sm100::tmem_ld_wait();
+          sm100::tmem_st_32x32b_x1(l_tm, __float_as_uint(__uint_as_float(l1) * alpha));
+        }
+        if (grow) m_use = mxl;
+        // P (bf16 pairs) over the S columns already read: chunk c of 32 keys
+        // -> columns [16 c, 16 c + 16)
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t raw[32];
+          sm100::tmem_ld_32x32b_x32(s_tm + 32 * c, raw);
+          sm100::tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float x0 = fmaf(__uint_as_float(raw[2 * e]), kLog2e, -m_use);
+            const float x1 = fmaf(__uint_as_float(raw[2 * e + 1]), kLog2e, -m_use);
+            const float p0 = (e & 3) == 3 ? exp2_poly(x0) : sm100::ex2_approx(x0);
+            const float p1 = (e & 3) == 3 ? exp2_poly(x1) : sm100::ex2_approx(x1);
+            const __nv_bfloat162 pv = __floats2bfloat162_rn(p0, p1);
+            pk[e] = *reinterpret_cast<const uint32_t*>(&pv);
+          }
+          sm100::tmem_st_32x32b_x16(s_tm + 16 * c, pk);
+        }
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.p_full[g]);
+      }
+      // item done: the last O_g / l_g, normalised, to ctx
+      sm100::mbar_wait(&s.o_full[g], (j - 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t ov[2][32];
+      sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+      sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+      const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      const float inv = 1.0f / __uint_as_float(lb);
+      __nv_bfloat16* dst =
+          ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c0 = c * 8 + 2 * e;
+          pk[e] = __floats2bfloat162_rn(__uint_as_float(ov[c0 >> 5][c0 & 31]) * inv,
+                                        __uint_as_float(ov[(c0 + 1) >> 5][(c0 + 1) & 31]) * inv);
+        }
+        *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pk);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 attention for S = 256 n, v5: 64-key blocks, double-buffered S, and every
+// A operand in tensor memory. ncu on v1-v4: the softmax warps wait for S
+// (S(j + 1) queued behind the other tile's O) and the S / O MMAs re-read Q
+// and P from shared memory. v5 issues S two blocks ahead into a second S
+// buffer per tile, copies Q into TMEM once per item and keeps P in TMEM over
+// the consumed S columns, so S = Q K^T, O += P V and l += P . ones are all
+// TS MMAs (A from TMEM) that read only K / V from shared memory (~64 B per
+// tensor cycle).
+//   warp 0      TMA: Q (double-buffered across items), 4-stage K/V ring (64 keys)
+//   warp 1      MMA issuer: S0(0) S1(0) S0(1) S1(1) | O0(j) O1(j) S0(j+2) S1(j+2) ...
+//   warps 4-7   tile 0, warps 8-11 tile 1: Q -> TMEM per item, softmax per block
+// TMEM: S[g][b] at 128 g + 64 b (P_g(j) bf16 over its first 32 columns),
+// Q_g at 256 + 32 g, O_g at 320 + 64 g (resident over the item's blocks,
+// rescaled in place when the running max jumps by > 2^8), l_g at 448 + 16 g.
+// ---------------------------------------------------------------------------
+struct Flash5Smem {
+  uint8_t q[2][2][kAttnS * 64 * 2];              // [item parity][tile] Q [128][64]
+  uint8_t kv[kF3Stages][2][kF3Keys * 64 * 2];    // [stage][K | V] [64 keys][64]
+  uint8_t ones[16 * 128];                        // bf16 1.0 (K-major B, N = 16)
+  uint64_t q_full[2], q_empty[2], kv_full[kF3Stages], kv_empty[kF3Stages];
+  uint64_t q_tmem[2], s_full[2][2], p_full[2][2], o_full[2][2];
+  uint32_t tmem_base;
+};
+constexpr size_t kFlash5SmemBytes = sizeof(Flash5Smem) + 1024;
+
+__global__ void __launch_bounds__(kFlashThreads, 1)
+    attention_flash5_kernel(const __grid_constant__ CUtensorMap tm_q,
+                            const __grid_constant__ CUtensorMap tm_kv, int n_heads, int hidden,
+                            int S, int n_items, __nv_bfloat16* __restrict__ ctx,
+                            const int32_t* __restrict__ n_live) {
+  extern __shared__ uint8_t smem_raw[];
+  Flash5Smem& s = sm100::align_smem_1024<Flash5Smem>(smem_raw);
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
+  const int n_kb = S / kF3Keys;
+  const int n_qp = S / (2 * kAttnS);
+  constexpr uint32_t kQTile = kAttnS * 64 * 2;
+  constexpr uint32_t kKvTile = kF3Keys * 64 * 2;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_q);
+    sm100::tma_prefetch(&tm_kv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s.q_full[i], 1);
+      sm100::mbar_init(&s.q_empty[i], 256);  // both tiles' softmax threads copied Q out
+      sm100::mbar_init(&s.q_tmem[i], 128);
+      for (int b = 0; b < 2; ++b) {
+        sm100::mbar_init(&s.s_full[i][b], 1);
+        sm100::mbar_init(&s.p_full[i][b], 128);
+        sm100::mbar_init(&s.o_full[i][b], 1);
+      }
+    }
+    for (int i = 0; i < kF3Stages; ++i) {
+      sm100::mbar_init(&s.kv_full[i], 1);
+      sm100::mbar_init(&s.kv_empty[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  for (int i = threadIdx.x; i < 16 * 128 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s.ones)[i] = 0x3F803F80u;  // two bf16 1.0
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
+  if (n_live) n_items = min(n_items, *n_live * n_heads * n_qp);
+  const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t kv_phase = 0;
+      for (int it = 0; it < n_my; ++it) {
+        const int item = (int)blockIdx.x + it * (int)gridDim.x;
+        const int qp = item % n_qp, sh = item / n_qp;
+        const int seq = sh / n_heads, h = sh - seq * n_heads;
+        const int row0 = seq * S;
+        const int qb = it & 1;
+        sm100::mbar_wait(&s.q_empty[qb], ((it >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&s.q_full[qb], 2 * kQTile);
+        sm100::tma_load_2d(s.q[qb][0], &tm_q, &s.q_full[qb], h * 64, row0 + qp * 256);
+        sm100::tma_load_2d(s.q[qb][1], &tm_q, &s.q_full[qb], h * 64, row0 + qp * 256 + 128);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          sm100::mbar_wait(&s.kv_empty[stage], kv_phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&s.kv_full[stage], 2 * kKvTile);
+          sm100::tma_load_2d(s.kv[stage][0], &tm_kv, &s.kv_full[stage], hidden + h * 64,
+                             row0 + kb * kF3Keys);
+          sm100::tma_load_2d(s.kv[stage][1], &tm_kv, &s.kv_full[stage], 2 * hidden + h * 64,
+                             row0 + kb * kF3Keys);
+          if (++stage == kF3Stages) { stage = 0; kv_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (warp-uniform; *_w helpers elect the lane) ----------------
+    constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, kF3Keys);
+    constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
+    constexpr uint32_t idesc_l = sm100::umma_idesc_bf16(128, 16);
+    const int J = n_my * n_kb;
+    auto issue_s = [&](int g, int j) {
+      const int it = j / n_kb, kb = j - it * n_kb;
+      const int stage = j % kF3Stages, b = j & 1;
+      if (g == 0) sm100::mbar_wait(&s.kv_full[stage], (j / kF3Stages) & 1);
+      // Q_g of this item in TMEM (its softmax warps copied it)
+      if (kb == 0) sm100::mbar_wait(&s.q_tmem[g], it & 1);
+      // S[g][b] holds P_g(j - 2) until O_g(j - 2) has read it
+      if (j >= 2) sm100::mbar_wait(&s.o_full[g][b], ((j - 2) >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t ka = sm100::smem_u32(s.kv[stage][0]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sm100::mma_bf16_ts_w(tmem + 128 * g + 64 * b, tmem + 256 + 32 * g + k * 8,
+                             sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+      sm100::mma_commit_w(&s.s_full[g][b]);
+    };
+    auto issue_o = [&](int g, int j) {
+      const int kb = j % n_kb, stage = j % kF3Stages, b = j & 1;
+      sm100::mbar_wait(&s.p_full[g][b], (j >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t va = sm100::smem_u32(s.kv[stage][1]);
+      const uint32_t oa = sm100::smem_u32(s.ones);
+      const uint32_t pa = tmem + 128 * g + 64 * b;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        sm100::mma_bf16_ts_w(tmem + 320 + 64 * g, pa + kk * 8,
+                             sm100::umma_desc_sw128(va + kk * 2048), idesc_o, (kb | kk) != 0);
+        sm100::mma_bf16_ts_w(tmem + 448 + 16 * g, pa + kk * 8,
+                             sm100::umma_desc_sw128(oa + kk * 32), idesc_l, (kb | kk) != 0);
+      }
+      sm100::mma_commit_w(&s.o_full[g][b]);
+      if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
+    };
+    for (int j = 0; j < J && j < 2; ++j) {
+      issue_s(0, j);
+      issue_s(1, j);
+    }
+    for (int j = 0; j < J; ++j) {
+      issue_o(0, j);
+      issue_o(1, j);
+      if (j + 2 < J) {
+        issue_s(0, j + 2);
+        issue_s(1, j + 2);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------- Q -> TMEM, softmax; tile g ----------------
+    const int g = (warp - 4) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t q_tm = lane_base + 256 + 32 * g;
+    const uint32_t o_tm = lane_base + 320 + 64 * g;
+    const uint32_t l_tm = lane_base + 448 + 16 * g;
+    constexpr float kLog2e = 1.4426950408889634f;
+    // Q_g (this row, SW128 in shared memory) -> TMEM as bf16 pairs. Item it + 1's
+    // copy runs right after item it's last softmax block: every S MMA reading
+    // Q_g has completed by then, and the issuer may already wait for it.
+    auto copy_q = [&](int it) {
+      const int qb = it & 1;
+      sm100::mbar_wait(&s.q_full[qb], (it >> 1) & 1);
+      const uint8_t* qrow = s.q[qb][g] + r * 128;
+      uint32_t qv[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 u = *reinterpret_cast<const uint4*>(qrow + ((c ^ (r & 7)) << 4));
+        qv[4 * c] = u.x; qv[4 * c + 1] = u.y; qv[4 * c + 2] = u.z; qv[4 * c + 3] = u.w;
+      }
+      sm100::tmem_st_32x32b_x32(q_tm, qv);
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.q_tmem[g]);
+      sm100::mbar_arrive(&s.q_empty[qb]);
+    };
+    if (n_my > 0) copy_q(0);
+    int j = 0;
+    for (int it = 0; it < n_my; ++it) {
+      const int item = (int)blockIdx.x + it * (int)gridDim.x;
+      const int qp = item % n_qp, sh = item / n_qp;
+      const int seq = sh / n_heads, h = sh - seq * n_heads;
+      float m_use = -INFINITY;
+      for (int kb = 0; kb < n_kb; ++kb, ++j) {
+        const int b = j & 1;
+        sm100::mbar_wait(&s.s_full[g][b], (j >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t sv[2][32];
+        sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b, sv[0]);
+        sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b + 32, sv[1]);
+        sm100::tmem_ld_wait();
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          mx = fmaxf(mx, fmaxf(__uint_as_float(sv[0][e]), __uint_as_float(sv[1][e])));
+        const float mxl = mx * kLog2e;
+        const bool grow = mxl > m_use + 8.0f;
+        if (__any_sync(0xffffffffu, grow) && kb > 0) {
+          // rescale O_g / l_g in tensor memory once O_g(j - 1) has landed
+          sm100::mbar_wait(&s.o_full[g][b ^ 1], ((j - 1) >> 1) & 1);
+          sm100::tc_fence_after();
+          const float alpha = grow ? sm100::ex2_approx(m_use - mxl) : 1.f;
+          uint32_t ov[32];
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, ov);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            sm100::tmem_st_32x32b_x32(o_tm + 32 * c, ov);
+          }
+          uint32_t l1 = sm100::tmem_ld_32x32b_x1(l_tm);
+          sm100::tmem_ld_wait();
+          sm100::tmem_st_32x32b_x1(l_tm, __float_as_uint(__uint_as_float(l1) * alpha));
+        }
+        if (grow) m_use = mxl;
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int c0 = 2 * e;
+          const float x0 = fmaf(__uint_as_float(sv[c0 >> 5][c0 & 31]), kLog2e, -m_use);
+          const float x1 = fmaf(__uint_as_float(sv[(c0 + 1) >> 5][(c0 + 1) & 31]), kLog2e, -m_use);
+          const float p0 = (e & 3) == 3 ? exp2_poly(x0) : sm100::ex2_approx(x0);
+          const float p1 = (e & 3) == 3 ? exp2_poly(x1) : sm100::ex2_approx(x1);
+          const __nv_bfloat162 pv = __floats2bfloat162_rn(p0, p1);
+          pk[e] = *reinterpret_cast<const uint32_t*>(&pv);
+        }
+        sm100::tmem_st_32x32b_x32(lane_base + 128 * g + 64 * b, pk);  // P over S columns 0-31
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.p_full[g][b]);
+      }
+      if (it + 1 < n_my) copy_q(it + 1);
+      // item done: the last O_g / l_g, normalised, to ctx
+      sm100::mbar_wait(&s.o_full[g][(j - 1) & 1], ((j - 1) >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t ov[2][32];
+      sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+      sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+      const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      const float inv = 1.0f / __uint_as_float(lb);
+      __nv_bfloat16* dst =
+          ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        __align__(16) __nv_bfloat162 pq[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c0 = c * 8 + 2 * e;
+          pq[e] = __floats2bfloat162_rn(__uint_as_float(ov[c0 >> 5][c0 & 31]) * inv,
+                                        __uint_as_float(ov[(c0 + 1) >> 5][(c0 + 1) & 31]) * inv);
+        }
+        *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pq);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+
 // Last layer, [CLS] query only: the router head reads h_[CLS] alone, so after
 // the last QKV projection only the CLS row of every (sequence, head) needs
 // attention (all S keys/values). One warp per (sequence, head): 128 q.k dot
@@ -1101,6 +1872,12 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlashSmemBytes);
     cudaFuncSetAttribute(attention_flash_kernel<false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlashSmemBytes);
+    cudaFuncSetAttribute(attention_flash3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kFlash3SmemBytes);
+    cudaFuncSetAttribute(attention_flash4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kFlash4SmemBytes);
+    cudaFuncSetAttribute(attention_flash5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kFlash5SmemBytes);
     attr = true;
   }
   const int NH = H / 64;
@@ -1111,14 +1888,31 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
   } else if (S % (2 * kAttnS) == 0) {
     const int items = n_seq * NH * (S / (2 * kAttnS));
     const unsigned grid = (unsigned)(items < n_sms() ? items : n_sms());
-    // CHM_FLASH_V2=0: the round-1 softmax (A/B measurement)
-    static const int v2 = getenv("CHM_FLASH_V2") ? atoi(getenv("CHM_FLASH_V2")) : 1;
-    if (v2)
+    // CHM_FLASH: 3 = 64-key blocks, double-buffered S, O in TMEM (default);
+    // 2 = 128-key blocks with the v2 softmax; 1 = the round-1 kernel
+    static const int ver = getenv("CHM_FLASH") ? atoi(getenv("CHM_FLASH")) : 5;
+    if (ver == 5) {
+      CUtensorMap tm_kv;
+      if (!gemm::make_tmap_bf16(&tm_kv, qk, (uint64_t)T, (uint64_t)3 * H, kF3Keys, 64, 0))
+        return CHM_ERR_CUDA;
+      attention_flash5_kernel<<<grid, kFlashThreads, kFlash5SmemBytes, st>>>(
+          tm_qkv, tm_kv, NH, H, S, items, ctx, n_live);
+    } else if (ver == 4) {
+      attention_flash4_kernel<<<grid, kFlashThreads, kFlash4SmemBytes, st>>>(
+          tm_qkv, NH, H, S, items, ctx, n_live);
+    } else if (ver == 3) {
+      CUtensorMap tm_kv;
+      if (!gemm::make_tmap_bf16(&tm_kv, qk, (uint64_t)T, (uint64_t)3 * H, kF3Keys, 64, 0))
+        return CHM_ERR_CUDA;
+      attention_flash3_kernel<<<grid, kFlashThreads, kFlash3SmemBytes, st>>>(
+          tm_qkv, tm_kv, NH, H, S, items, ctx, n_live);
+    } else if (ver == 2) {
       attention_flash_kernel<true><<<grid, kFlashThreads, kFlashSmemBytes, st>>>(
           tm_qkv, NH, H, S, items, ctx, n_live);
-    else
+    } else {
       attention_flash_kernel<false><<<grid, kFlashThreads, kFlashSmemBytes, st>>>(
           tm_qkv, NH, H, S, items, ctx, n_live);
+    }
   } else {
     attention_long_kernel<<<(unsigned)(n_seq * NH * (S / kAttnS)), 160, kAttnLongSmemBytes,
                             st>>>(tm_qkv, NH, H, S, ctx, n_live);
