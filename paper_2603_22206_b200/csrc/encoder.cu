@@ -509,6 +509,51 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
+// Packed fp32x2 helpers (sm_100 FFMA2 / FADD2: one issue slot for two lanes'
+// worth of fp32 math, each half rounded exactly as the scalar op).
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// exp2_poly on a pair, bit-identical to two exp2_poly calls, as bf16x2.
+__device__ __forceinline__ uint32_t exp2_poly2_bf16(uint64_t x) {
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  x = f2_pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+  const uint64_t magic = f2_pack(12582912.0f, 12582912.0f);
+  const uint64_t t = f2_add(x, magic);
+  const uint64_t f = f2_sub(x, f2_sub(t, magic));
+  uint64_t p = f2_fma(f2_pack(0.05517153f, 0.05517153f), f, f2_pack(0.24261111f, 0.24261111f));
+  p = f2_fma(p, f, f2_pack(0.693261f, 0.693261f));
+  p = f2_fma(p, f, f2_pack(0.99992806f, 0.99992806f));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  const __nv_bfloat162 v =
+      __floats2bfloat162_rn(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                            __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
 template <bool V2>
 __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
@@ -1391,6 +1436,7 @@ struct Flash5Smem {
 };
 constexpr size_t kFlash5SmemBytes = sizeof(Flash5Smem) + 1024;
 
+template <int kPoly>
 __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash5_kernel(const __grid_constant__ CUtensorMap tm_q,
                             const __grid_constant__ CUtensorMap tm_kv, int n_heads, int hidden,
@@ -1498,6 +1544,9 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       sm100::mma_commit_w(&s.o_full[g][b]);
       if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
     };
+    // (An issuer that polls both tiles and issues whichever is ready ran 45%
+    // slower: its spin loop takes issue slots from the softmax warps sharing
+    // its SM sub-partition, and the softmax is issue-bound.)
     for (int j = 0; j < J && j < 2; ++j) {
       issue_s(0, j);
       issue_s(1, j);
@@ -1540,75 +1589,13 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       sm100::mbar_arrive(&s.q_tmem[g]);
       sm100::mbar_arrive(&s.q_empty[qb]);
     };
-    if (n_my > 0) copy_q(0);
-    int j = 0;
-    for (int it = 0; it < n_my; ++it) {
+    // O_g of item it, normalised, to ctx
+    auto store_ctx = [&](int it, const uint32_t (&ov)[2][32], uint32_t lb) {
       const int item = (int)blockIdx.x + it * (int)gridDim.x;
       const int qp = item % n_qp, sh = item / n_qp;
       const int seq = sh / n_heads, h = sh - seq * n_heads;
-      float m_use = -INFINITY;
-      for (int kb = 0; kb < n_kb; ++kb, ++j) {
-        const int b = j & 1;
-        sm100::mbar_wait(&s.s_full[g][b], (j >> 1) & 1);
-        sm100::tc_fence_after();
-        uint32_t sv[2][32];
-        sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b, sv[0]);
-        sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b + 32, sv[1]);
-        sm100::tmem_ld_wait();
-        float mx = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          mx = fmaxf(mx, fmaxf(__uint_as_float(sv[0][e]), __uint_as_float(sv[1][e])));
-        const float mxl = mx * kLog2e;
-        const bool grow = mxl > m_use + 8.0f;
-        if (__any_sync(0xffffffffu, grow) && kb > 0) {
-          // rescale O_g / l_g in tensor memory once O_g(j - 1) has landed
-          sm100::mbar_wait(&s.o_full[g][b ^ 1], ((j - 1) >> 1) & 1);
-          sm100::tc_fence_after();
-          const float alpha = grow ? sm100::ex2_approx(m_use - mxl) : 1.f;
-          uint32_t ov[32];
-#pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
-            sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, ov);
-            sm100::tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            sm100::tmem_st_32x32b_x32(o_tm + 32 * c, ov);
-          }
-          uint32_t l1 = sm100::tmem_ld_32x32b_x1(l_tm);
-          sm100::tmem_ld_wait();
-          sm100::tmem_st_32x32b_x1(l_tm, __float_as_uint(__uint_as_float(l1) * alpha));
-        }
-        if (grow) m_use = mxl;
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int c0 = 2 * e;
-          const float x0 = fmaf(__uint_as_float(sv[c0 >> 5][c0 & 31]), kLog2e, -m_use);
-          const float x1 = fmaf(__uint_as_float(sv[(c0 + 1) >> 5][(c0 + 1) & 31]), kLog2e, -m_use);
-          const float p0 = (e & 3) == 3 ? exp2_poly(x0) : sm100::ex2_approx(x0);
-          const float p1 = (e & 3) == 3 ? exp2_poly(x1) : sm100::ex2_approx(x1);
-          const __nv_bfloat162 pv = __floats2bfloat162_rn(p0, p1);
-          pk[e] = *reinterpret_cast<const uint32_t*>(&pv);
-        }
-        sm100::tmem_st_32x32b_x32(lane_base + 128 * g + 64 * b, pk);  // P over S columns 0-31
-        sm100::tmem_st_wait();
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(&s.p_full[g][b]);
-      }
-      if (it + 1 < n_my) copy_q(it + 1);
-      // item done: the last O_g / l_g, normalised, to ctx
-      sm100::mbar_wait(&s.o_full[g][(j - 1) & 1], ((j - 1) >> 1) & 1);
-      sm100::tc_fence_after();
-      uint32_t ov[2][32];
-      sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
-      sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
-      const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
-      sm100::tmem_ld_wait();
-      sm100::tc_fence_before();
       const float inv = 1.0f / __uint_as_float(lb);
-      __nv_bfloat16* dst =
-          ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+      __nv_bfloat16* dst = ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         __align__(16) __nv_bfloat162 pq[4];
@@ -1620,6 +1607,90 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
         }
         *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pq);
       }
+    };
+    auto read_o = [&](int jl, uint32_t (&ov)[2][32]) -> uint32_t {
+      sm100::mbar_wait(&s.o_full[g][jl & 1], (jl >> 1) & 1);
+      sm100::tc_fence_after();
+      sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+      sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+      const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      return lb;
+    };
+    // One flat loop over the CTA's blocks; at an item's end the next item's Q
+    // goes to TMEM first (the issuer may be waiting for it), then the epilogue.
+    // (Running the epilogue inside the next item's first block, between
+    // storing P and releasing it, measured 0.7% slower.)
+    if (n_my > 0) copy_q(0);
+    const int J = n_my * n_kb;
+    float m_use = -INFINITY;
+    for (int j = 0, it = 0, kb = 0; j < J; ++j) {
+      const int b = j & 1;
+      if (kb == 0) m_use = -INFINITY;
+      sm100::mbar_wait(&s.s_full[g][b], (j >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t sv[2][32];
+      sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b, sv[0]);
+      sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b + 32, sv[1]);
+      sm100::tmem_ld_wait();
+      float mq[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) mq[t] = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        mq[e & 3] = fmaxf(mq[e & 3], fmaxf(__uint_as_float(sv[0][e]), __uint_as_float(sv[1][e])));
+      const float mxl = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * kLog2e;
+      const bool grow = mxl > m_use + 8.0f;
+      if (__any_sync(0xffffffffu, grow) && kb > 0) {
+        // rescale O_g / l_g in tensor memory once O_g(j - 1) has landed
+        sm100::mbar_wait(&s.o_full[g][b ^ 1], ((j - 1) >> 1) & 1);
+        sm100::tc_fence_after();
+        const float alpha = grow ? sm100::ex2_approx(m_use - mxl) : 1.f;
+        uint32_t ov[32];
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, ov);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          sm100::tmem_st_32x32b_x32(o_tm + 32 * c, ov);
+        }
+        uint32_t l1 = sm100::tmem_ld_32x32b_x1(l_tm);
+        sm100::tmem_ld_wait();
+        sm100::tmem_st_32x32b_x1(l_tm, __float_as_uint(__uint_as_float(l1) * alpha));
+      }
+      if (grow) m_use = mxl;
+      // x = s log2e - m in FFMA2 pairs; kPoly pairs in 8 on the FMA pipes (exp2_poly)
+      uint32_t pk[32];
+      const uint64_t l2e2 = f2_pack(kLog2e, kLog2e), negm2 = f2_pack(-m_use, -m_use);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int c0 = 2 * e;
+        const uint64_t x = f2_fma(f2_pack(__uint_as_float(sv[c0 >> 5][c0 & 31]),
+                                          __uint_as_float(sv[c0 >> 5][(c0 & 31) + 1])),
+                                  l2e2, negm2);
+        if ((e & 7) < kPoly) {
+          pk[e] = exp2_poly2_bf16(x);
+        } else {
+          float x0, x1;
+          f2_unpack(x, x0, x1);
+          const __nv_bfloat162 pv =
+              __floats2bfloat162_rn(sm100::ex2_approx(x0), sm100::ex2_approx(x1));
+          pk[e] = *reinterpret_cast<const uint32_t*>(&pv);
+        }
+      }
+      sm100::tmem_st_32x32b_x32(lane_base + 128 * g + 64 * b, pk);  // P over S columns 0-31
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.p_full[g][b]);
+      if (++kb == n_kb) {
+        kb = 0;
+        if (++it < n_my) copy_q(it);
+        uint32_t ov[2][32];
+        const uint32_t lb = read_o(j, ov);
+        store_ctx(it - 1, ov, lb);
+      }
     }
   }
   sm100::tc_fence_before();
@@ -1629,6 +1700,13 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
     sm100::tmem_dealloc<512>(tmem);
   }
 }
+
+using Flash5Fn = void (*)(const CUtensorMap, const CUtensorMap, int, int, int, int,
+                          __nv_bfloat16*, const int32_t*);
+static const Flash5Fn kFlash5Kernels[9] = {
+    attention_flash5_kernel<0>, attention_flash5_kernel<1>, attention_flash5_kernel<2>,
+    attention_flash5_kernel<3>, attention_flash5_kernel<4>, attention_flash5_kernel<5>,
+    attention_flash5_kernel<6>, attention_flash5_kernel<7>, attention_flash5_kernel<8>};
 
 // Last layer, [CLS] query only: the router head reads h_[CLS] alone, so after
 // the last QKV projection only the CLS row of every (sequence, head) needs
@@ -1876,8 +1954,8 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
                          (int)kFlash3SmemBytes);
     cudaFuncSetAttribute(attention_flash4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kFlash4SmemBytes);
-    cudaFuncSetAttribute(attention_flash5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kFlash5SmemBytes);
+    for (auto k : kFlash5Kernels)
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlash5SmemBytes);
     attr = true;
   }
   const int NH = H / 64;
@@ -1895,8 +1973,13 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
       CUtensorMap tm_kv;
       if (!gemm::make_tmap_bf16(&tm_kv, qk, (uint64_t)T, (uint64_t)3 * H, kF3Keys, 64, 0))
         return CHM_ERR_CUDA;
-      attention_flash5_kernel<<<grid, kFlashThreads, kFlash5SmemBytes, st>>>(
-          tm_qkv, tm_kv, NH, H, S, items, ctx, n_live);
+      // pairs of 8 whose exp2 runs as a polynomial on the FMA pipes; S = 512,
+      // 2048 sequences (tools/experiments/r2_flash5_ab.sh): 0 2.665 ms,
+      // 1 2.54, 2 2.51, 3 2.43, 4 2.44, 5 2.56, 6 2.71, 8 2.99
+      static const int poly = getenv("CHM_FLASH5_POLY") ? atoi(getenv("CHM_FLASH5_POLY")) : 3;
+      auto kern = kFlash5Kernels[poly < 0 ? 0 : poly > 8 ? 8 : poly];
+      kern<<<grid, kFlashThreads, kFlash5SmemBytes, st>>>(tm_qkv, tm_kv, NH, H, S, items, ctx,
+                                                          n_live);
     } else if (ver == 4) {
       attention_flash4_kernel<<<grid, kFlashThreads, kFlash4SmemBytes, st>>>(
           tm_qkv, NH, H, S, items, ctx, n_live);

@@ -5,7 +5,7 @@
 # blocks with Q, P in TMEM and S issued two blocks ahead. Kernel time at the cfg5 shape and
 # parity of the long-prompt paths.
 cd "$(dirname "$0")/../.."
-for v in 2 4 5; do
+for v in ${FLASH_VERSIONS:-2 4 5}; do
   echo "== CHM_FLASH=$v"
   CHM_FLASH=$v timeout 120 python tools/attn_micro.py --seq-len 512 --n-seq 2048 --only attention --reps 5
   CHM_FLASH=$v timeout 300 python -m pytest tests -m gpu -q -k "attention_matches or long_prompts or random_layernorm" 2>&1 | tail -1
