@@ -509,51 +509,6 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
-// Packed fp32x2 helpers (sm_100 FFMA2 / FADD2: one issue slot for two lanes'
-// worth of fp32 math, each half rounded exactly as the scalar op).
-__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(uint64_t r, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-}
-__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-// exp2_poly on a pair, bit-identical to two exp2_poly calls, as bf16x2.
-__device__ __forceinline__ uint32_t exp2_poly2_bf16(uint64_t x) {
-  float x0, x1;
-  f2_unpack(x, x0, x1);
-  x = f2_pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
-  const uint64_t magic = f2_pack(12582912.0f, 12582912.0f);
-  const uint64_t t = f2_add(x, magic);
-  const uint64_t f = f2_sub(x, f2_sub(t, magic));
-  uint64_t p = f2_fma(f2_pack(0.05517153f, 0.05517153f), f, f2_pack(0.24261111f, 0.24261111f));
-  p = f2_fma(p, f, f2_pack(0.693261f, 0.693261f));
-  p = f2_fma(p, f, f2_pack(0.99992806f, 0.99992806f));
-  float p0, p1, t0, t1;
-  f2_unpack(p, p0, p1);
-  f2_unpack(t, t0, t1);
-  const __nv_bfloat162 v =
-      __floats2bfloat162_rn(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
-                            __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
-  return *reinterpret_cast<const uint32_t*>(&v);
-}
-
 template <bool V2>
 __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
@@ -1663,18 +1618,18 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       if (grow) m_use = mxl;
       // x = s log2e - m in FFMA2 pairs; kPoly pairs in 8 on the FMA pipes (exp2_poly)
       uint32_t pk[32];
-      const uint64_t l2e2 = f2_pack(kLog2e, kLog2e), negm2 = f2_pack(-m_use, -m_use);
+      const uint64_t l2e2 = sm100::f2_pack(kLog2e, kLog2e), negm2 = sm100::f2_pack(-m_use, -m_use);
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
         const int c0 = 2 * e;
-        const uint64_t x = f2_fma(f2_pack(__uint_as_float(sv[c0 >> 5][c0 & 31]),
+        const uint64_t x = sm100::f2_fma(sm100::f2_pack(__uint_as_float(sv[c0 >> 5][c0 & 31]),
                                           __uint_as_float(sv[c0 >> 5][(c0 & 31) + 1])),
                                   l2e2, negm2);
         if ((e & 7) < kPoly) {
-          pk[e] = exp2_poly2_bf16(x);
+          pk[e] = sm100::exp2_poly2_bf16(x);
         } else {
           float x0, x1;
-          f2_unpack(x, x0, x1);
+          sm100::f2_unpack(x, x0, x1);
           const __nv_bfloat162 pv =
               __floats2bfloat162_rn(sm100::ex2_approx(x0), sm100::ex2_approx(x1));
           pk[e] = *reinterpret_cast<const uint32_t*>(&pv);

@@ -69,6 +69,10 @@ constexpr uint32_t kHeadTile = kS * 64 * 2;    // Q/K/V [128][64] bf16, 16 KB
 constexpr uint32_t kAccCols = 192;
 constexpr uint32_t kSCol = 384;
 constexpr int kPairStages = CHM_QA_PAIR_STAGES;  // PAIR ring depth (28 KB stages)
+#ifndef CHM_QA_POLY
+#define CHM_QA_POLY 0
+#endif
+constexpr int kPolyPairs = CHM_QA_POLY;  // softmax exp2 pairs (of 4) on the FMA pipes
 
 struct __align__(1024) Smem {
   // the operand ring: 4 x 40 KB (cta_group::1) or kPairStages x 28 KB (PAIR)
@@ -544,15 +548,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum = 0.f;
       uint8_t* prow = s.qkv[hf] + r * 128;  // P keys [64 hf, +64) over the Q (hf 0) / K tile
       uint32_t pp[32];  // TS: P in bf16 pairs, to TMEM over S (all S reads are done: epi_sync)
+      // x = s log2e - m as FFMA2 pairs; kPolyPairs of every 4 pairs take the
+      // FMA-pipe exp2 (sm100::exp2_poly2_bf16) instead of MUFU
+      const uint64_t l2e2 = sm100::f2_pack(kLog2e, kLog2e), negm2 = sm100::f2_pack(-mxl, -mxl);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         __align__(16) __nv_bfloat162 pv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = sm100::ex2_approx(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e]), kLog2e, -mxl));
-          const float p1 =
-              sm100::ex2_approx(fmaf(__uint_as_float(sv[q >> 2][(q & 3) * 8 + 2 * e + 1]), kLog2e, -mxl));
-          pv[e] = __floats2bfloat162_rn(p0, p1);
+          const uint32_t* src = &sv[q >> 2][(q & 3) * 8 + 2 * e];
+          const uint64_t x = sm100::f2_fma(
+              sm100::f2_pack(__uint_as_float(src[0]), __uint_as_float(src[1])), l2e2, negm2);
+          if (e < kPolyPairs) {
+            const uint32_t u = sm100::exp2_poly2_bf16(x);
+            pv[e] = *reinterpret_cast<const __nv_bfloat162*>(&u);
+          } else {
+            float x0, x1;
+            sm100::f2_unpack(x, x0, x1);
+            pv[e] = __floats2bfloat162_rn(sm100::ex2_approx(x0), sm100::ex2_approx(x1));
+          }
           const float2 back = __bfloat1622float2(pv[e]);
           sum += back.x + back.y;
         }

@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cuda_bf16.h>
 
 namespace chm {
 namespace sm100 {
@@ -480,6 +481,51 @@ __device__ __forceinline__ void mma_commit_cg2_mc_w(uint64_t* bar, uint16_t mask
       : "memory");
 }
 #undef CHM_ELECT_PREFIX
+
+// Packed fp32x2 helpers (sm_100 FFMA2 / FADD2: one issue slot for two lanes'
+// worth of fp32 math, each half rounded exactly as the scalar op).
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// exp2_poly on a pair, bit-identical to two exp2_poly calls, as bf16x2.
+__device__ __forceinline__ uint32_t exp2_poly2_bf16(uint64_t x) {
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  x = f2_pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+  const uint64_t magic = f2_pack(12582912.0f, 12582912.0f);
+  const uint64_t t = f2_add(x, magic);
+  const uint64_t f = f2_sub(x, f2_sub(t, magic));
+  uint64_t p = f2_fma(f2_pack(0.05517153f, 0.05517153f), f, f2_pack(0.24261111f, 0.24261111f));
+  p = f2_fma(p, f, f2_pack(0.693261f, 0.693261f));
+  p = f2_fma(p, f, f2_pack(0.99992806f, 0.99992806f));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  const __nv_bfloat162 v =
+      __floats2bfloat162_rn(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                            __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
 
 }  // namespace sm100
 }  // namespace chm
