@@ -232,8 +232,15 @@ typedef struct chm_queue_key {
  * 10240 entries (keys in shared memory, one CTA per engine), 20/entry up to
  * 2^18 (keys in global memory, one CTA per engine), above that the
  * grid-wide path (radix passes over 4096-entry tiles, staging copy for the
- * compaction): ~68/entry. */
+ * compaction, plus the kept STJF key order of the incremental path and its
+ * compaction halo): ~150/entry. The grid-wide path keeps state in this
+ * scratch between calls: hand every call on a queue the same scratch. */
 uint64_t chm_queue_scratch_bytes(int32_t capacity);
+
+/* Diagnostic: grid-wide queue calls (capacity > 2^18) so far that ran
+ * incrementally on the order the previous call kept (the queue unchanged
+ * since, <= 8192 appended rows, <= 512 admissions); the others re-sort. */
+uint64_t chm_queue_fast_calls(void);
 
 /* ---- columnar trace store (TraceRecord, workload.py:111-253) ------------ */
 

@@ -283,6 +283,7 @@ _SIGNATURES = [
     ("chm_encoder_fold_weights", c_int32,
      [POINTER(EncoderCfg), POINTER(EncoderWeights), POINTER(EncoderWorkspace), c_void_p]),
     ("chm_queue_scratch_bytes", ctypes.c_uint64, [c_int32]),
+    ("chm_queue_fast_calls", ctypes.c_uint64, []),
     ("chm_trace_derive", c_int32, [POINTER(Trace), c_void_p, c_void_p]),
     ("chm_kendall_tau_scratch_bytes", ctypes.c_uint64, [ctypes.c_int64]),
     ("chm_quantile_train_scratch_bytes", ctypes.c_uint64,

@@ -38,6 +38,7 @@ constexpr size_t kScratchBytesPerEntry = 8 + 2 + 2 + 4 + 4;  // prio, lvl, cnt, 
 constexpr int kQHuge = 1 << 18;    // larger segments: grid-wide passes (stjf_huge.cu)
 
 size_t queue_huge_scratch_bytes(int capacity);
+unsigned long long queue_huge_fast_calls();
 chm_status launch_queue_huge(const QueueParams& prm, const chm_monitor_state& mon,
                              const chm_queue_state& q, const chm_rows& rows,
                              const chm_decisions& dec, const int32_t* n_complete,
@@ -903,6 +904,10 @@ static chm_status launch_queue(const chm_pool* pool, const chm_aging_cfg* aging,
 }
 
 }  // namespace chm
+
+extern "C" uint64_t chm_queue_fast_calls(void) {
+  return (uint64_t)chm::queue_huge_fast_calls();
+}
 
 extern "C" uint64_t chm_queue_scratch_bytes(int32_t capacity) {
   if (capacity <= chm::kQMax) return 0;

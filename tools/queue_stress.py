@@ -4,7 +4,12 @@ levels / counts), one scheduling tick (admit into free slots + age the rest +
 final STJF order) per step, timed with CUDA events around the queue kernels
 only (the state is restored between steps, untimed).
 
-  python tools/queue_stress.py [--n 16777216] [--steps 5] [--engines 1]
+  python tools/queue_stress.py [--n 16777216] [--steps 5] [--engines 1] [--chain]
+
+--chain: consecutive ticks on the evolving queue (no restore between steps),
+the steady state in which the grid-wide path runs incrementally (a restored
+queue no longer matches the state hash the previous call kept, so the default
+mode measures the full radix path).
 
 Prints one JSON line per size: ms per tick and achieved GB/s on the
 algorithmic bytes (40 B read + 40 B written per entry + 4 B of order) against
@@ -30,7 +35,7 @@ from paper_2603_22206_b200.scheduler import GpuScheduler, RowBatch  # noqa: E402
 BYTES_PER_ENTRY = 84
 
 
-def run(n, engines, steps, iterations):
+def run(n, engines, steps, iterations, chain=False):
     rng = np.random.default_rng(1)
     pool = Pool(tuple(ModelProfile(f"m{i}", 1.0 + i, 64) for i in range(engines)))
     cap = n
@@ -60,8 +65,14 @@ def run(n, engines, steps, iterations):
     gs.check_errors()
     _lib.profile_read()
     _lib.profile_enable(True)
-    for _ in range(steps):
+    if chain:  # one untimed tick so the timed ones continue a kept order
         st.restore(snap)
+        gs.run_rows(empty, n_iterations=iterations, n_complete=n_complete)
+        torch.cuda.synchronize()
+        _lib.profile_read()
+    for _ in range(steps):
+        if not chain:
+            st.restore(snap)
         gs.run_rows(empty, n_iterations=iterations, n_complete=n_complete)
     torch.cuda.synchronize()
     prof = _lib.profile_read()
@@ -77,6 +88,7 @@ def run(n, engines, steps, iterations):
     path = ("smem keys, 1 CTA/engine" if cap <= 10240 else
             "global keys, 1 CTA/engine" if cap <= (1 << 18) else "grid-wide passes")
     return {"entries_per_engine": n, "engines": engines, "capacity": cap, "path": path,
+            "mode": "chain (incremental)" if chain else "restored (radix)",
             "iterations": iterations, "ms_per_tick": ms, "achieved_gbs": gbs,
             "peak_gbs": peak, "frac": gbs / peak,
             "bytes_per_entry": BYTES_PER_ENTRY}
@@ -88,9 +100,10 @@ def main():
     ap.add_argument("--engines", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--iterations", type=int, default=1)
+    ap.add_argument("--chain", action="store_true")
     a = ap.parse_args()
     for n in a.n:
-        print(json.dumps(run(n, a.engines, a.steps, a.iterations)), flush=True)
+        print(json.dumps(run(n, a.engines, a.steps, a.iterations, a.chain)), flush=True)
 
 
 if __name__ == "__main__":
