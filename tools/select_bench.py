@@ -31,15 +31,18 @@ def main():
     B, K = a.rows, a.k
     rng = np.random.default_rng(0)
     out = {}
-    for name, pow2, dyadic in (("dyadic_pow2", True, True), ("nondyadic_pow2", True, False),
-                               ("dyadic_nonpow2", False, True)):
+    for name, pow2, dyadic in (("dyadic_pow2", True, True), ("dyadic_pow2_clustered", True, True),
+                               ("nondyadic_pow2", True, False), ("dyadic_nonpow2", False, True)):
         pool = Pool(tuple(ModelProfile(f"m{i}", 5.0 * (i + 1),
                                        max(1, 32 >> i) if pow2 else 3 + 2 * i)
                           for i in range(K)))
         rt, pr = ScoreTableRouter(), PrecomputedPredictor()
         gs = GpuScheduler(pool, BalancerConfig(0.5, 0.1), router=rt, predictor=pr,
                           n_programs=2 * B, max_rows=B)
-        q = rng.random((B, K))
+        # clustered: router confidences near 0.5 (random-init router, cfg3): the
+        # gate rarely passes and the chain is the argmin (m_fast) regime
+        q = (np.clip(0.5 + 0.01 * rng.standard_normal((B, K)), 0, 1) if "clustered" in name
+             else rng.random((B, K)))
         y = rng.integers(0, 4000, (B, K)) / 2.0 if dyadic else rng.lognormal(6, 1, (B, K))
         rt.set(torch.as_tensor(q, device="cuda"))
         pr.set(torch.as_tensor(y, device="cuda"))
