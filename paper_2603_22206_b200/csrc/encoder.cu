@@ -1391,12 +1391,22 @@ struct Flash5Smem {
 };
 constexpr size_t kFlash5SmemBytes = sizeof(Flash5Smem) + 1024;
 
+// Measurement bits of issue_mode (CHM_FLASH5_ISSUE): 16 = CTA 0's per-block
+// timeline into ctx as int64 [64 blocks][8] = {S0 landed, P0 stored, S1
+// landed, P1 stored, O0 issued, S0(j+2) issued, O1 issued, S1(j+2) issued}
+// (clock64; ctx is not written); 32 = no softmax (the MMA pipeline alone);
+// 64 = no MMAs (the softmax alone). tools/attn_micro.py --flash-timeline.
+__device__ __forceinline__ void f5_stamp(int mode, void* ctx, int j, int k) {
+  if ((mode & 16) && blockIdx.x == 0 && j < 64)
+    reinterpret_cast<long long*>(ctx)[j * 8 + k] = clock64();
+}
+
 template <int kPoly>
 __global__ void __launch_bounds__(kFlashThreads, 1)
     attention_flash5_kernel(const __grid_constant__ CUtensorMap tm_q,
                             const __grid_constant__ CUtensorMap tm_kv, int n_heads, int hidden,
                             int S, int n_items, __nv_bfloat16* __restrict__ ctx,
-                            const int32_t* __restrict__ n_live) {
+                            const int32_t* __restrict__ n_live, int issue_mode) {
   extern __shared__ uint8_t smem_raw[];
   Flash5Smem& s = sm100::align_smem_1024<Flash5Smem>(smem_raw);
   const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
@@ -1472,15 +1482,19 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       if (g == 0) sm100::mbar_wait(&s.kv_full[stage], (j / kF3Stages) & 1);
       // Q_g of this item in TMEM (its softmax warps copied it)
       if (kb == 0) sm100::mbar_wait(&s.q_tmem[g], it & 1);
-      // S[g][b] holds P_g(j - 2) until O_g(j - 2) has read it
-      if (j >= 2) sm100::mbar_wait(&s.o_full[g][b], ((j - 2) >> 1) & 1);
+      // S[g][b] holds P_g(j - 2) until O_g(j - 2) has read it. Issue modes
+      // 1 / 2 (default): no completion wait -- tcgen05.mma ops issued by one
+      // thread execute in issue order, so S_g(j), issued after O_g(j - 2),
+      // cannot overwrite P_g(j - 2) before that MMA has read it
+      if (j >= 2 && (issue_mode & 15) == 0) sm100::mbar_wait(&s.o_full[g][b], ((j - 2) >> 1) & 1);
       sm100::tc_fence_after();
       const uint32_t ka = sm100::smem_u32(s.kv[stage][0]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < ((issue_mode & 64) ? 0 : 4); ++k)
         sm100::mma_bf16_ts_w(tmem + 128 * g + 64 * b, tmem + 256 + 32 * g + k * 8,
                              sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
       sm100::mma_commit_w(&s.s_full[g][b]);
+      if (lane == 0 && j >= 2) f5_stamp(issue_mode, ctx, j - 2, 5 + 2 * g);
     };
     auto issue_o = [&](int g, int j) {
       const int kb = j % n_kb, stage = j % kF3Stages, b = j & 1;
@@ -1490,7 +1504,7 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       const uint32_t oa = sm100::smem_u32(s.ones);
       const uint32_t pa = tmem + 128 * g + 64 * b;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < ((issue_mode & 64) ? 0 : 4); ++kk) {
         sm100::mma_bf16_ts_w(tmem + 320 + 64 * g, pa + kk * 8,
                              sm100::umma_desc_sw128(va + kk * 2048), idesc_o, (kb | kk) != 0);
         sm100::mma_bf16_ts_w(tmem + 448 + 16 * g, pa + kk * 8,
@@ -1498,6 +1512,7 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       }
       sm100::mma_commit_w(&s.o_full[g][b]);
       if (g == 1) sm100::mma_commit_w(&s.kv_empty[stage]);
+      if (lane == 0) f5_stamp(issue_mode, ctx, j, 4 + 2 * g);
     };
     // (An issuer that polls both tiles and issues whichever is ready ran 45%
     // slower: its spin loop takes issue slots from the softmax warps sharing
@@ -1507,6 +1522,13 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       issue_s(1, j);
     }
     for (int j = 0; j < J; ++j) {
+      if ((issue_mode & 15) == 1) {  // each tile's next S right behind its O
+        issue_o(0, j);
+        if (j + 2 < J) issue_s(0, j + 2);
+        issue_o(1, j);
+        if (j + 2 < J) issue_s(1, j + 2);
+        continue;
+      }
       issue_o(0, j);
       issue_o(1, j);
       if (j + 2 < J) {
@@ -1585,6 +1607,18 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       if (kb == 0) m_use = -INFINITY;
       sm100::mbar_wait(&s.s_full[g][b], (j >> 1) & 1);
       sm100::tc_fence_after();
+      if (quarter == 0 && lane == 0) f5_stamp(issue_mode, ctx, j, 2 * g);
+      if (issue_mode & 32) {  // measurement: no softmax (the MMA pipeline alone)
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&s.p_full[g][b]);
+        if (++kb == n_kb) {
+          kb = 0;
+          if (++it < n_my) copy_q(it);
+          uint32_t ov[2][32];
+          read_o(j, ov);
+        }
+        continue;
+      }
       uint32_t sv[2][32];
       sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b, sv[0]);
       sm100::tmem_ld_32x32b_x32(lane_base + 128 * g + 64 * b + 32, sv[1]);
@@ -1639,12 +1673,13 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&s.p_full[g][b]);
+      if (quarter == 0 && lane == 0) f5_stamp(issue_mode, ctx, j, 2 * g + 1);
       if (++kb == n_kb) {
         kb = 0;
         if (++it < n_my) copy_q(it);
         uint32_t ov[2][32];
         const uint32_t lb = read_o(j, ov);
-        store_ctx(it - 1, ov, lb);
+        if (!(issue_mode & 16)) store_ctx(it - 1, ov, lb);
       }
     }
   }
@@ -1657,7 +1692,7 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
 }
 
 using Flash5Fn = void (*)(const CUtensorMap, const CUtensorMap, int, int, int, int,
-                          __nv_bfloat16*, const int32_t*);
+                          __nv_bfloat16*, const int32_t*, int);
 static const Flash5Fn kFlash5Kernels[9] = {
     attention_flash5_kernel<0>, attention_flash5_kernel<1>, attention_flash5_kernel<2>,
     attention_flash5_kernel<3>, attention_flash5_kernel<4>, attention_flash5_kernel<5>,
@@ -1933,8 +1968,14 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
       // 1 2.54, 2 2.51, 3 2.43, 4 2.44, 5 2.56, 6 2.71, 8 2.99
       static const int poly = getenv("CHM_FLASH5_POLY") ? atoi(getenv("CHM_FLASH5_POLY")) : 3;
       auto kern = kFlash5Kernels[poly < 0 ? 0 : poly > 8 ? 8 : poly];
+      // CHM_FLASH5_ISSUE: 0 = S_g(j) issued after O_g(j - 2) completed; 2 = no
+      // wait (in-order tensor pipe; default, 1.1-1.3 % faster,
+      // tools/experiments/r2_flash5_issue.sh); 1 = no wait, order O0 S0 O1 S1.
+      // Bits 16 / 32 / 64: measurement modes (f5_stamp)
+      static const int issue_mode =
+          getenv("CHM_FLASH5_ISSUE") ? atoi(getenv("CHM_FLASH5_ISSUE")) : 2;
       kern<<<grid, kFlashThreads, kFlash5SmemBytes, st>>>(tm_qkv, tm_kv, NH, H, S, items, ctx,
-                                                          n_live);
+                                                          n_live, issue_mode);
     } else if (ver == 4) {
       attention_flash4_kernel<<<grid, kFlashThreads, kFlash4SmemBytes, st>>>(
           tm_qkv, NH, H, S, items, ctx, n_live);

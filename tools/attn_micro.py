@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--timeline", action="store_true",
                     help="with CHM_QA_DEBUG=11: print CTA 0's per-item stage stamps (cycles)")
+    ap.add_argument("--flash-timeline", action="store_true",
+                    help="with CHM_FLASH5_ISSUE |= 16: CTA 0's per-block flash v5 stamps (cycles)")
     a = ap.parse_args()
     lib = _lib.load()
     n, H, S = a.n_seq, a.hidden, a.seq_len
@@ -51,6 +53,21 @@ def main():
     flops_a = 4.0 * S * S * 64 * n * (H // 64)
     cases = {"fused": (fused, flops_g + flops_a), "gemm": (gemm, flops_g),
              "attention": (attn, flops_a)}
+    if a.flash_timeline:
+        attn()
+        torch.cuda.synchronize()
+        t = ctx.view(-1).view(torch.int64)[:512].cpu().view(64, 8).numpy()
+        base = int(t[8, 0])
+        names = ["S0_land", "P0_done", "S1_land", "P1_done", "O0_iss", "S0+2_iss", "O1_iss", "S1+2_iss"]
+        print("blk " + " ".join(f"{n:>9s}" for n in names) + "   (cycles from block 8 S0_land)")
+        for j in range(8, 40):
+            print(f"{j:3d} " + " ".join(f"{int(v) - base:9d}" for v in t[j]))
+        d = t[16:48]
+        per = (int(d[-1, 1]) - int(d[0, 1])) / (len(d) - 1)
+        print(f"period {per:.0f} cycles/block; softmax S->P tile0 {float((d[:,1]-d[:,0]).mean()):.0f}, "
+              f"tile1 {float((d[:,3]-d[:,2]).mean()):.0f}; P0->S0(j+1) land wait "
+              f"{float((d[1:,0]-d[:-1,1]).mean()):.0f}")
+        return
     if a.timeline:
         fused()
         torch.cuda.synchronize()

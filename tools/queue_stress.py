@@ -35,7 +35,7 @@ from paper_2603_22206_b200.scheduler import GpuScheduler, RowBatch  # noqa: E402
 BYTES_PER_ENTRY = 84
 
 
-def run(n, engines, steps, iterations, chain=False):
+def run(n, engines, steps, iterations, chain=False, graph=False):
     rng = np.random.default_rng(1)
     pool = Pool(tuple(ModelProfile(f"m{i}", 1.0 + i, 64) for i in range(engines)))
     cap = n
@@ -63,14 +63,42 @@ def run(n, engines, steps, iterations, chain=False):
         gs.run_rows(empty, n_iterations=iterations, n_complete=n_complete)
     torch.cuda.synchronize()
     gs.check_errors()
+    if graph:  # the tick as a CUDA-graph replay (how TickGraph runs it), CUDA events
+        from paper_2603_22206_b200.tick import TickGraph
+        st.restore(snap)
+        tg = TickGraph(gs, empty, n_iterations=iterations, n_complete=n_complete,
+                       restore_snapshot=None if chain else snap)
+        for _ in range(2):
+            tg.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            tg.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        gs.check_errors()
+        ms = e0.elapsed_time(e1) / steps
+        if not chain:  # the replay includes the snapshot restore: time it alone and subtract
+            e0.record()
+            for _ in range(steps):
+                st.restore(snap)
+            e1.record()
+            torch.cuda.synchronize()
+            ms -= e0.elapsed_time(e1) / steps
+        calls = 2
+    else:
+        ms, calls = None, None
     _lib.profile_read()
-    _lib.profile_enable(True)
-    if chain:  # one untimed tick so the timed ones continue a kept order
+    _lib.profile_enable(not graph)
+    if graph:
+        pass
+    elif chain:  # one untimed tick so the timed ones continue a kept order
         st.restore(snap)
         gs.run_rows(empty, n_iterations=iterations, n_complete=n_complete)
         torch.cuda.synchronize()
         _lib.profile_read()
-    for _ in range(steps):
+    for _ in range(0 if graph else steps):
         if not chain:
             st.restore(snap)
         gs.run_rows(empty, n_iterations=iterations, n_complete=n_complete)
@@ -80,15 +108,17 @@ def run(n, engines, steps, iterations, chain=False):
     gs.check_errors()
     # two queue calls per tick: completions (admit into freed slots, age) and
     # the tick itself (append, iterate, final STJF order)
-    ms = prof["queue"]["ms"] / steps
-    calls = prof["queue"]["timed"] / steps
+    if not graph:
+        ms = prof["queue"]["ms"] / steps
+        calls = prof["queue"]["timed"] / steps
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6549.1
     gbs = calls * n * engines * BYTES_PER_ENTRY / (ms / 1e3) / 1e9
     path = ("smem keys, 1 CTA/engine" if cap <= 10240 else
             "global keys, 1 CTA/engine" if cap <= (1 << 18) else "grid-wide passes")
     return {"entries_per_engine": n, "engines": engines, "capacity": cap, "path": path,
-            "mode": "chain (incremental)" if chain else "restored (radix)",
+            "mode": ("chain (incremental)" if chain else "restored (radix)")
+                    + (", graph replay" if graph else ", eager"),
             "iterations": iterations, "ms_per_tick": ms, "achieved_gbs": gbs,
             "peak_gbs": peak, "frac": gbs / peak,
             "bytes_per_entry": BYTES_PER_ENTRY}
@@ -101,9 +131,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--iterations", type=int, default=1)
     ap.add_argument("--chain", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time the tick as a CUDA-graph replay (whole tick: both queue calls)")
     a = ap.parse_args()
     for n in a.n:
-        print(json.dumps(run(n, a.engines, a.steps, a.iterations, a.chain)), flush=True)
+        print(json.dumps(run(n, a.engines, a.steps, a.iterations, a.chain, a.graph)), flush=True)
 
 
 if __name__ == "__main__":
