@@ -62,6 +62,7 @@ constexpr int kMaxPasses = kPass1 + kPass2;
 constexpr int kNewMax = 8192;    // fast path: rows appended per call
 constexpr int kAcapMax = 512;    // fast path: admissions per call (halo depth)
 constexpr int kMergeTile = 2048; // output entries per merge-path CTA
+constexpr size_t kMergeSmem = (size_t)kMergeTile * (8 + 8 + 4 + 4 + 2);
 constexpr unsigned kValidMagic = 0x5A17C0DEu;
 
 struct Ctl {
@@ -1232,11 +1233,17 @@ __device__ __forceinline__ void heads_select_tile(int tile, Args a) {
     if (need[g]) any = 1;
   }
   __syncthreads();
-  if (!any || tid >= 32) return;
+  if (!any) return;
   const KeyBuf& k1 = merged_keys(L, c);
+  // the tile's group ids staged in shared memory by the whole CTA; one warp
+  // then lists the needed members in order
+  __shared__ uint16_t s_cnt[kTile];
+  for (int r = base + tid; r < end; r += kThreads) s_cnt[r - base] = k1.cnt[r];
+  __syncthreads();
+  if (tid >= 32) return;
   for (int r0 = base; r0 < end; r0 += 32) {
     const int r = r0 + lane;
-    const int g = r < end ? (int)k1.cnt[r] : -1;
+    const int g = r < end ? (int)s_cnt[r - base] : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, g);
     if (g >= 0 && need[g]) {
       const int k = run[g] + __popc(peers & ((1u << lane) - 1u));
@@ -1253,6 +1260,11 @@ __device__ __forceinline__ void heads_select_tile(int tile, Args a) {
 __global__ void __launch_bounds__(32) fast_rounds_kernel(Args a) {
   __shared__ int g_size[kMaxGroups], g_cur[kMaxGroups], g_count[kMaxGroups],
       g_lvloff[kMaxGroups];
+  // cached head of every count group (raw level; the group's level offset
+  // is added at compare time): one admission reloads only its own group's
+  // head instead of every group's from L2
+  __shared__ int h_lvl[kMaxGroups], h_e[kMaxGroups];
+  __shared__ unsigned long long h_prio[kMaxGroups], h_arr[kMaxGroups];
   const int m = blockIdx.x, lane = threadIdx.x;
   const chm_queue_state& q = a.q;
   Layout L = layout(q.scratch, q.capacity, m);
@@ -1270,40 +1282,51 @@ __global__ void __launch_bounds__(32) fast_rounds_kernel(Args a) {
   const KeyBuf& k1 = merged_keys(L, c);
   const int bmax = a.prm.b[m];
   int run = c.run, n_adm = 0, n_prom = 0, remaining = n;
+  auto load_head = [&](int g) {
+    if (g_cur[g] < g_size[g]) {
+      const uint32_t p = L.hl[(size_t)g * kAcapMax + g_cur[g]];
+      h_e[g] = (int)k1.idx[p];
+      h_lvl[g] = k1.lvl[p];
+      h_prio[g] = k1.prio[p];
+      h_arr[g] = k1.arr[p];
+    }
+  };
+  for (int g = lane; g < kMaxGroups; g += 32) load_head(g);
+  __syncwarp();
   for (int r = 0; r < R; ++r) {
     if (a.mode == 0) run = max(run - 1, 0);
     const int adm = max(0, min(bmax - run, remaining));
     for (int t = 0; t < adm; ++t) {
-      HeadKey best;
-      best.g = -1;
-      for (int g0 = 0; g0 < kMaxGroups; g0 += 32) {
-        const int g = g0 + lane;
-        HeadKey hk;
-        hk.g = -1;
+      // this lane's best cached head, then the warp's
+      HeadKey hk;
+      hk.g = -1;
+      for (int g = lane; g < kMaxGroups; g += 32) {
         if (g_cur[g] < g_size[g]) {
-          const uint32_t p = L.hl[(size_t)g * kAcapMax + g_cur[g]];
-          hk.e = (int)k1.idx[p];
-          hk.g = g;
-          hk.lvl = k1.lvl[p] + g_lvloff[g];
-          hk.prio = k1.prio[p];
-          hk.arr = k1.arr[p];
-        }
-        for (int off = 16; off; off >>= 1) {
           HeadKey o;
-          o.lvl = __shfl_xor_sync(0xffffffffu, hk.lvl, off);
-          o.prio = __shfl_xor_sync(0xffffffffu, hk.prio, off);
-          o.arr = __shfl_xor_sync(0xffffffffu, hk.arr, off);
-          o.e = __shfl_xor_sync(0xffffffffu, hk.e, off);
-          o.g = __shfl_xor_sync(0xffffffffu, hk.g, off);
-          if (o.g >= 0 && (hk.g < 0 || key_less(o, hk))) hk = o;
+          o.g = g;
+          o.e = h_e[g];
+          o.lvl = h_lvl[g] + g_lvloff[g];
+          o.prio = h_prio[g];
+          o.arr = h_arr[g];
+          if (hk.g < 0 || key_less(o, hk)) hk = o;
         }
-        if (hk.g >= 0 && (best.g < 0 || key_less(hk, best))) best = hk;
       }
+      for (int off = 16; off; off >>= 1) {
+        HeadKey o;
+        o.lvl = __shfl_xor_sync(0xffffffffu, hk.lvl, off);
+        o.prio = __shfl_xor_sync(0xffffffffu, hk.prio, off);
+        o.arr = __shfl_xor_sync(0xffffffffu, hk.arr, off);
+        o.e = __shfl_xor_sync(0xffffffffu, hk.e, off);
+        o.g = __shfl_xor_sync(0xffffffffu, hk.g, off);
+        if (o.g >= 0 && (hk.g < 0 || key_less(o, hk))) hk = o;
+      }
+      const HeadKey best = hk;
       if (lane == 0) {
         q.admitted[seg + c.n_adm0 + n_adm] = q.handle[seg + best.e];
         L.adm_idx[n_adm] = (uint32_t)best.e;
         L.adm_pos[n_adm] = L.hl[(size_t)best.g * kAcapMax + g_cur[best.g]];
         g_cur[best.g] += 1;
+        load_head(best.g);
       }
       __syncwarp();
       ++n_adm;
@@ -1387,19 +1410,24 @@ __global__ void __launch_bounds__(kThreads) fast_prep_kernel(Args a) {
 }
 
 // Each tile's last A entries (which the next tile's shifted writes overwrite).
-__device__ __forceinline__ void halo_tile(int tile, Args a) {
-  const int m = blockIdx.y, tid = threadIdx.x;
+// Every tile's last A entries, copied before compact_fast_tile overwrites
+// them (flattened over (tile, entry): a tile holds only A <= kAcapMax of them).
+__global__ void __launch_bounds__(256) halo_kernel(Args a) {
+  const int m = blockIdx.y;
   const chm_queue_state& q = a.q;
   Layout L = layout(q.scratch, q.capacity, m);
   const Ctl& c = *L.ctl;
   if (!c.fast || c.A == 0) return;
-  const int n = c.n, base = tile * kTile;
-  if (base >= n) return;
-  const int end = min(base + kTile, n), A = c.A;
-  const int h0 = max(base, end - A);
+  const int n = c.n, A = c.A;
+  const long long T = (n + kTile - 1) / kTile;
   const size_t seg = (size_t)m * q.capacity;
-  for (int i = h0 + tid; i < end; i += kThreads) {
-    const size_t hp = (size_t)tile * kAcapMax + (i - (end - A));
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < T * A;
+       w += (long long)gridDim.x * blockDim.x) {
+    const int tile = (int)(w / A), j = (int)(w - (long long)tile * A);
+    const int base = tile * kTile, end = min(base + kTile, n);
+    const int i = end - A + j;
+    if (i < base) continue;
+    const size_t hp = (size_t)tile * kAcapMax + j;
     L.h64b(0)[hp] = (unsigned long long)__double_as_longlong(q.priority[seg + i]);
     L.h64b(1)[hp] = (unsigned long long)__double_as_longlong(q.arrival[seg + i]);
     L.h64b(2)[hp] = (unsigned long long)q.seq[seg + i];
@@ -1683,12 +1711,24 @@ __global__ void __launch_bounds__(kThreads) final2_merge_kernel(Args a) {
   const KeyBuf& out = merged_keys(L, c);
   const KeyBuf& kx = L.ksb((c.n_app > 0 ? (c.kcur ^ 1) : c.kcur) ^ 1);
   const size_t seg = (size_t)m * q.capacity;
-  __shared__ int split[2];
-  for (int o0 = blockIdx.x * kMergeTile; o0 < n; o0 += gridDim.x * kMergeTile) {
-    const int o1 = min(o0 + kMergeTile, n);
-    if (tid < 2) {
+  extern __shared__ __align__(16) unsigned char msm[];  // kMergeSmem: one staged output tile
+  unsigned long long* s_prio = reinterpret_cast<unsigned long long*>(msm);
+  unsigned long long* s_arr = s_prio + kMergeTile;
+  int32_t* s_lvl = reinterpret_cast<int32_t*>(s_arr + kMergeTile);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_lvl + kMergeTile);
+  uint16_t* s_cnt = reinterpret_cast<uint16_t*>(s_idx + kMergeTile);
+  // merge-path splits of this CTA's tiles, found in parallel (one binary
+  // search per tile boundary) for up to kSplitBatch tiles at a time: a serial
+  // search per tile costs ~2 x 11 dependent L2 round trips
+  constexpr int kSplitBatch = kThreads / 2;
+  __shared__ int split[2 * kSplitBatch];
+  const int n_tiles_all = (n + kMergeTile - 1) / kMergeTile;
+  for (int tb = blockIdx.x; tb < n_tiles_all; tb += gridDim.x * kSplitBatch) {
+  if (tid < 2 * kSplitBatch) {
+    const int tt = tb + (tid >> 1) * gridDim.x;
+    if (tt < n_tiles_all) {
       // i = #U among the first d outputs
-      const int d = tid == 0 ? o0 : o1;
+      const int d = min((tt + (tid & 1)) * kMergeTile, n);
       int lo = max(0, d - nP), hi = min(d, nU);
       while (lo < hi) {
         const int i = (lo + hi) >> 1;  // take U[i] before P[d - i - 1]?
@@ -1696,26 +1736,43 @@ __global__ void __launch_bounds__(kThreads) final2_merge_kernel(Args a) {
       }
       split[tid] = lo;
     }
-    __syncthreads();
-    const int u0 = split[0], u1 = split[1];
+  }
+  __syncthreads();
+  for (int bi = 0; bi < kSplitBatch; ++bi) {
+    const int tt = tb + bi * gridDim.x;
+    if (tt >= n_tiles_all) break;
+    const int o0 = tt * kMergeTile, o1 = min(o0 + kMergeTile, n);
+    const int u0 = split[2 * bi], u1 = split[2 * bi + 1];
     const int p0 = o0 - u0, p1 = o1 - u1;
-    // each element's output slot: own offset + #(other range < it)
-    for (int t = tid; t < (u1 - u0) + (p1 - p0); t += kThreads) {
-      const bool isU = t < u1 - u0;
-      const int src = isU ? u0 + t : nU + p0 + (t - (u1 - u0));
-      const FKey k = fk_at(kx, src);
-      int lo = isU ? p0 : u0, hi = isU ? p1 : u1;
+    const int nu = u1 - u0, tot = nu + (p1 - p0);
+    // stage the tile's U run then its P run in shared memory (coalesced)
+    for (int t = tid; t < tot; t += kThreads) {
+      const int src = t < nu ? u0 + t : nU + p0 + (t - nu);
+      s_lvl[t] = kx.lvl[src];
+      s_prio[t] = kx.prio[src];
+      s_arr[t] = kx.arr[src];
+      s_idx[t] = kx.idx[src];
+      s_cnt[t] = kx.cnt[src];
+    }
+    __syncthreads();
+    // each element's output slot: own offset + #(other run < it), by binary
+    // search over the other run in shared memory
+    for (int t = tid; t < tot; t += kThreads) {
+      const bool isU = t < nu;
+      const FKey k{s_lvl[t], s_prio[t], s_arr[t], s_idx[t]};
+      int lo = isU ? nu : 0, hi = isU ? tot : nu;
+      const int base = lo;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        const FKey o = fk_at(kx, isU ? nU + mid : mid);
+        const FKey o{s_lvl[mid], s_prio[mid], s_arr[mid], s_idx[mid]};
         if (fk_less(o, k)) lo = mid + 1; else hi = mid;
       }
-      // U[u0 + t] -> o0 + t + #(P in tile < it); P[p0 + t'] -> o0 + t' + #(U in tile < it)
-      const int d = isU ? o0 + t + (lo - p0) : o0 + (t - (u1 - u0)) + (lo - u0);
-      fk_put(out, d, k, kx.cnt[src]);
+      const int d = o0 + (isU ? t : t - nu) + (lo - base);
+      fk_put(out, d, k, s_cnt[t]);
       q.order[seg + d] = (int32_t)k.idx;
     }
     __syncthreads();
+  }
   }
 }
 
@@ -1822,6 +1879,57 @@ unsigned long long queue_huge_fast_calls() {
   return v;
 }
 
+namespace qh {
+// IF-node condition of a radix section: 1 if any engine runs it.
+__global__ void section_cond_kernel(Args a, cudaGraphConditionalHandle h, int section) {
+  if (threadIdx.x != 0) return;
+  unsigned need = 0;
+  for (int m = 0; m < a.prm.K; ++m) {
+    const Ctl& c = *layout(a.q.scratch, a.q.capacity, m).ctl;
+    need |= section == 0 ? (c.fast ? 0u : 1u) : ((!c.fast || c.need_sort2) ? 1u : 0u);
+  }
+  cudaGraphSetConditional(h, need);
+}
+
+// While `s` is being captured into a CUDA graph: a kernel sets the section's
+// condition, an IF node follows it, and `body` is captured into the node's
+// body graph on a side stream. Returns false (nothing enqueued) when `s` is
+// not capturing or the graph API refuses, so the caller launches the body.
+template <class Body>
+bool cond_section(cudaStream_t s, const Args& a, int section, Body body) {
+  cudaStreamCaptureStatus cs;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusActive)
+    return false;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(s, &cs, &id, &g, &deps, &nd) != cudaSuccess) return false;
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+    return false;
+  section_cond_kernel<<<1, 32, 0, s>>>(a, h, section);
+  if (cudaStreamGetCaptureInfo(s, &cs, &id, &g, &deps, &nd) != cudaSuccess) return false;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, deps, nd, &cp) != cudaSuccess) return false;
+  static cudaStream_t side = nullptr;
+  if (!side) cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+  if (cudaStreamBeginCaptureToGraph(side, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return false;
+  body(side);
+  cudaGraph_t done;
+  cudaStreamEndCapture(side, &done);
+  return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies) ==
+         cudaSuccess;
+}
+}  // namespace qh
+
 chm_status launch_queue_huge(const QueueParams& prm, const chm_monitor_state& mon,
                              const chm_queue_state& q, const chm_rows& rows,
                              const chm_decisions& dec, const int32_t* n_complete,
@@ -1835,6 +1943,8 @@ chm_status launch_queue_huge(const QueueParams& prm, const chm_monitor_state& mo
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(final2_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMergeSmem);
     cudaFuncSetAttribute(tiles_pass<scatter_tile, false>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(ScatterSmem));
@@ -1857,41 +1967,54 @@ chm_status launch_queue_huge(const QueueParams& prm, const chm_monitor_state& mo
   tiles<heads_select_tile, 0><<<grid, kThreads, 0, s>>>(a);
   fast_rounds_kernel<<<K, 32, 0, s>>>(a);
   fast_prep_kernel<<<K, kThreads, 0, s>>>(a);
-  tiles<halo_tile, 0><<<grid, kThreads, 0, s>>>(a);
+  halo_kernel<<<dim3(4 * sms, K), 256, 0, s>>>(a);
   tiles<compact_fast_tile, 0><<<grid, kThreads, 0, s>>>(a);
   tiles<unsorted_tile, 0><<<grid, kThreads, 0, s>>>(a);
   tiles<final1_tile, 0><<<grid, kThreads, 0, s>>>(a);
   tiles<final2_count_tile, 0><<<grid, kThreads, 0, s>>>(a);
   final2_scan_kernel<<<K, kThreads, 0, s>>>(a);
   tiles<final2_split_tile, 0><<<grid, kThreads, 0, s>>>(a);
-  final2_merge_kernel<<<dim3(2 * sms, K), kThreads, 0, s>>>(a);
+  final2_merge_kernel<<<dim3(2 * sms, K), kThreads, kMergeSmem, s>>>(a);
   tiles<keys_tile, 1><<<grid, kThreads, 0, s>>>(a);
   // ---- radix path (every kernel returns at once if ctl.fast) ----
-  tiles<stage_tile, 0><<<grid, kThreads, 0, s>>>(a);
-  auto pass = [&](int sort, int src, int byte, int p) {
+  auto pass = [&](cudaStream_t st, int sort, int src, int byte, int p) {
     PassSpec ps{sort, src, byte, p};
-    if (byte == 0) tiles_pass<gather_tile, true><<<grid, kThreads, 0, s>>>(a, ps);
-    tiles_pass<hist_tile, false><<<grid, kThreads, 0, s>>>(a, ps);
-    scan_kernel<<<dim3(256, K), kThreads, 0, s>>>(a, ps);
-    tiles_pass<scatter_tile, false><<<grid, kThreads, sizeof(ScatterSmem), s>>>(a, ps);
+    if (byte == 0) tiles_pass<gather_tile, true><<<grid, kThreads, 0, st>>>(a, ps);
+    tiles_pass<hist_tile, false><<<grid, kThreads, 0, st>>>(a, ps);
+    scan_kernel<<<dim3(256, K), kThreads, 0, st>>>(a, ps);
+    tiles_pass<scatter_tile, false><<<grid, kThreads, sizeof(ScatterSmem), st>>>(a, ps);
   };
-  int p = 0;
-  // sort 1, least significant first: arrival, priority, level, count
-  const int srcs1[4] = {0, 1, 2, 3}, bytes1[4] = {8, 8, 2, 2};
-  for (int j = 0; j < 4; ++j)
-    for (int b = 0; b < bytes1[j]; ++b) pass(0, srcs1[j], b, p++);
-  tiles<groups_tile, 0><<<grid, kThreads, 0, s>>>(a);
-  rounds_kernel<<<K, 32, 0, s>>>(a);
-  tiles<outcome_tile, 0><<<grid, kThreads, 0, s>>>(a);
-  tiles<compact_count_tile, 0><<<grid, kThreads, 0, s>>>(a);
-  compact_scan_kernel<<<K, kThreads, 0, s>>>(a);
-  tiles<compact_scatter_tile, 0><<<grid, kThreads, 0, s>>>(a);
-  // copy_back (tile 0 resets the sort-2 buffer index) runs after n_new is known
-  tiles<copy_back_tile, 1><<<grid, kThreads, 0, s>>>(a);
-  // sort 2: arrival, priority, level
-  const int srcs2[3] = {0, 1, 2}, bytes2[3] = {8, 8, 2};
-  for (int j = 0; j < 3; ++j)
-    for (int b = 0; b < bytes2[j]; ++b) pass(1, srcs2[j], b, p++);
+  // section 0: sort 1 + the rounds + compaction (radix path only)
+  auto section0 = [&](cudaStream_t st) {
+    tiles<stage_tile, 0><<<grid, kThreads, 0, st>>>(a);
+    int p = 0;
+    // sort 1, least significant first: arrival, priority, level, count
+    const int srcs1[4] = {0, 1, 2, 3}, bytes1[4] = {8, 8, 2, 2};
+    for (int j = 0; j < 4; ++j)
+      for (int b = 0; b < bytes1[j]; ++b) pass(st, 0, srcs1[j], b, p++);
+    tiles<groups_tile, 0><<<grid, kThreads, 0, st>>>(a);
+    rounds_kernel<<<K, 32, 0, st>>>(a);
+    tiles<outcome_tile, 0><<<grid, kThreads, 0, st>>>(a);
+    tiles<compact_count_tile, 0><<<grid, kThreads, 0, st>>>(a);
+    compact_scan_kernel<<<K, kThreads, 0, st>>>(a);
+    tiles<compact_scatter_tile, 0><<<grid, kThreads, 0, st>>>(a);
+    // copy_back (tile 0 resets the sort-2 buffer index) runs after n_new is known
+    tiles<copy_back_tile, 1><<<grid, kThreads, 0, st>>>(a);
+  };
+  // section 1: sort 2 (radix path, or the fast path with several promotion classes)
+  auto section1 = [&](cudaStream_t st) {
+    int p = kPass1;
+    const int srcs2[3] = {0, 1, 2}, bytes2[3] = {8, 8, 2};
+    for (int j = 0; j < 3; ++j)
+      for (int b = 0; b < bytes2[j]; ++b) pass(st, 1, srcs2[j], b, p++);
+  };
+  // Under CUDA-graph capture each section is the body of an IF node whose
+  // condition a one-thread kernel sets on the device (any engine needs it):
+  // in the incremental steady state the ~230 radix launches, which would
+  // all return at once, are skipped. Eager: launched as before.
+  static const int use_cond = getenv("CHM_QUEUE_COND") ? atoi(getenv("CHM_QUEUE_COND")) : 1;
+  if (!use_cond || !cond_section(s, a, 0, section0)) section0(s);
+  if (!use_cond || !cond_section(s, a, 1, section1)) section1(s);
   tiles<finish_tile, 1><<<grid, kThreads, 0, s>>>(a);
   tiles<ks_build_tile, 1><<<grid, kThreads, 0, s>>>(a);
   commit_kernel<<<K, 32, 0, s>>>(a);

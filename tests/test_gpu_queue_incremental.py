@@ -156,3 +156,53 @@ def test_incremental_survives_external_queue_edit():
         assert a["queued"] == b["queued"]
         for k in ("admitted", "order", "level"):
             np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_graph_replay_matches_eager(fast):
+    """The grid-wide path captured in a CUDA graph (its two radix sections as
+    IF nodes whose conditions the device sets) replays the eager ticks."""
+    from paper_2603_22206_b200.tick import TickGraph
+
+    os.environ["CHM_QUEUE_FAST"] = "1" if fast else "0"
+    try:
+        rng = np.random.default_rng(5)
+        pool = Pool((ModelProfile("m0", 1.0, B[0]), ModelProfile("m1", 2.0, B[1])))
+        gs = GpuScheduler(pool, BalancerConfig(), AgingConfig(starvation_threshold=3),
+                          router=ScoreTableRouter(), predictor=PrecomputedPredictor(),
+                          n_programs=16, max_rows=16, queue_capacity=300000)
+        st = gs.state
+        n = 180000
+        for m in range(2):
+            prio = np.round(rng.lognormal(5, 2, n))
+            prio[rng.random(n) < 0.2] = 37.0
+            st.load_queue(m, prio, np.sort(rng.random(n) * 100), np.arange(n),
+                          np.arange(n) + (m << 40), level=-rng.integers(0, 3, n),
+                          count=rng.integers(0, 3, n))
+        st.set_engine_counters(running=list(B), seq=[n, n])
+        dev = gs.device
+        gs.router.set(torch.zeros((0, 2), device=dev))
+        gs.predictor.set(torch.zeros((0, 2), dtype=torch.float64, device=dev))
+        empty = RowBatch.from_numpy(dev, program=np.zeros(0), stage=np.zeros(0),
+                                    arrival=np.zeros(0), out_tokens=np.zeros((0, 2)),
+                                    handle=np.zeros(0))
+        nc = torch.tensor([5, 3], dtype=torch.int32, device=dev)
+        snap = st.snapshot()
+        eager = []
+        for _ in range(5):
+            gs.run_rows(empty, n_iterations=2, n_complete=nc)
+            gs.check_errors()
+            eager.append(_snapshot(gs))
+        st.restore(snap)
+        tg = TickGraph(gs, empty, n_iterations=2, n_complete=nc)  # warm-up = tick 0, eager
+        torch.cuda.synchronize()
+        replay = [_snapshot(gs)]
+        for _ in range(4):
+            tg.replay()
+            torch.cuda.synchronize()
+            gs.check_errors()
+            replay.append(_snapshot(gs))
+        _same(eager, replay, "eager vs graph replay")
+        assert sum(int(s["promoted"].sum()) for s in eager) > 0
+    finally:
+        os.environ.pop("CHM_QUEUE_FAST", None)
