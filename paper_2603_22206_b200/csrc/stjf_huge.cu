@@ -1282,8 +1282,10 @@ __global__ void __launch_bounds__(32) fast_rounds_kernel(Args a) {
   const KeyBuf& k1 = merged_keys(L, c);
   const int bmax = a.prm.b[m];
   int run = c.run, n_adm = 0, n_prom = 0, remaining = n;
+  // (a call admits at most A_cap entries, so no group needs a head past its
+  // first A_cap members -- the only ones heads_select_tile lists in hl)
   auto load_head = [&](int g) {
-    if (g_cur[g] < g_size[g]) {
+    if (g_cur[g] < g_size[g] && g_cur[g] < c.A_cap) {
       const uint32_t p = L.hl[(size_t)g * kAcapMax + g_cur[g]];
       h_e[g] = (int)k1.idx[p];
       h_lvl[g] = k1.lvl[p];
