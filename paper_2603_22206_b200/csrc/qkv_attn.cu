@@ -710,11 +710,22 @@ chm_status qkv_attention_pair(const void* x, const void* w_qkv, const float* b_q
                               const float* c_qkv, const float2* stats_in, int n_part, float eps,
                               void* ctx, int n_seq, int hidden, cudaStream_t st);
 
+chm_status qkv_attention_duo(const void* x, const void* w_qkv, const float* b_qkv,
+                             const float* c_qkv, const float2* stats_in, int n_part, float eps,
+                             void* ctx, int n_seq, int hidden, cudaStream_t st,
+                             const int32_t* n_live);
+
 chm_status qkv_attention(const void* x, const void* w_qkv, const float* b_qkv,
                          const float* c_qkv, const float2* stats_in, int n_part, float eps,
                          void* ctx, int n_seq, int hidden, cudaStream_t st,
                          const int32_t* n_live = nullptr) {
   if (stats_in && (!c_qkv || n_part < 1 || n_part > kLnMaxParts)) return CHM_ERR_INVALID_ARG;
+  // CHM_QA_DUO (default 1): the two-epilogue-group kernel (qkv_attn_duo.cu);
+  // 0 selects the kernels below (measurement / A-B)
+  static const int duo = env_int("CHM_QA_DUO", 1);
+  if (duo && !env_int("CHM_QA_DEBUG", 0))
+    return qkv_attention_duo(x, w_qkv, b_qkv, c_qkv, stats_in, n_part, eps, ctx, n_seq, hidden,
+                             st, n_live);
   // CHM_QA_PAIR=1: the cta_group::2 kernel (qkv_attn_pair.cu)
   // default: the pair-projection kernel (fused 1.69 vs 1.76 ms for the
   // cta_group::1 one, tools/experiments/qa_pair2.sh); CHM_QA_PAIR=0 selects

@@ -53,6 +53,17 @@ def main():
     flops_a = 4.0 * S * S * 64 * n * (H // 64)
     cases = {"fused": (fused, flops_g + flops_a), "gemm": (gemm, flops_g),
              "attention": (attn, flops_a)}
+    if os.environ.get("CHM_QA_DUO_TL"):
+        fused()
+        torch.cuda.synchronize()
+        t = ctx.view(-1).view(torch.int64)[:32 * 12].cpu().view(32, 12).numpy()
+        base = int(t[8, 0])
+        names = ["acc_full", "staged", "s_full", "p_ready", "o_full", "out", "S_iss", "O_iss",
+                 "buf_free", "kb0", "kbN"]
+        print("item " + " ".join(f"{n:>8s}" for n in names) + "   (cycles from item 8 acc_full)")
+        for i in range(8, 20):
+            print(f"{i:4d} " + " ".join(f"{int(v) - base:8d}" for v in t[i][:11]))
+        return
     if a.flash_timeline:
         attn()
         torch.cuda.synchronize()

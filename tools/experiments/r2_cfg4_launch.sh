@@ -1,0 +1,6 @@
+#!/usr/bin/env bash
+cd "$(dirname "$0")/../.."
+mkdir -p gpurun_out/c4
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c4/launches_cfg4.csv python tools/profile_tick.py --config cfg4 --ticks 2 > gpurun_out/c4/l.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c4/launches_cfg1.csv python tools/profile_tick.py --config cfg1 --ticks 2 > gpurun_out/c4/l1.log 2>&1
+tail -1 gpurun_out/c4/l.log
