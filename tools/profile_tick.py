@@ -28,9 +28,11 @@ def main():
                       n_programs=wl.n_programs, max_rows=wl.batch_size)
     snap = gs.state.snapshot()
     batches = [wl.batch(t) for t in range(2)]
+    completions = wl.completions()  # cfg4: every engine's running batch turns over (as bench.py)
+    kw = {"completions": completions} if completions is not None else {}
     for t in range(a.ticks):
         gs.state.restore(snap)
-        gs.run_rows(batches[t % 2], n_iterations=1)
+        gs.run_rows(batches[t % 2], n_iterations=1, **kw)
     torch.cuda.synchronize()
     gs.check_errors()
     print("ticks done")
