@@ -426,7 +426,6 @@ def run_ours(args):
     if completions is not None and world > 1:
         n_complete = torch.bincount(completions[0].long(), minlength=K).to(torch.int32)
         completions = None
-    snap = gs.state.snapshot()
     n_distinct = 4
     host_cols = []
     batches = []
@@ -438,6 +437,8 @@ def run_ours(args):
     # N > 1: request-sharded ticks; Mode A all-reduces the per-engine in-flight
     # vector over NCCL after each GPU's chain, Mode B relays it (serial-exact).
     sched = ShardedScheduler(gs, args.mode) if world > 1 else gs
+    # (after the sharded scheduler: it adds the in-flight insertion stamps to the state)
+    snap = gs.state.snapshot()
     # the headline tick is a CUDA graph replay on one GPU (no host launches,
     # no per-kernel timing hooks); --eager times the eager launch sequence
     graph = None

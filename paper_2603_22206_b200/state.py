@@ -280,6 +280,10 @@ class DeviceState:
         return {k: getattr(self, k).clone() for k in self._mutable()}
 
     def restore(self, snap: dict) -> None:
+        missing = [k for k in self._mutable() if k not in snap]
+        if missing:
+            raise KeyError(f"snapshot taken before {missing} existed (e.g. before "
+                           "ShardedScheduler enabled the in-flight stamps); take it again")
         for k in self._mutable():
             getattr(self, k).copy_(snap[k], non_blocking=True)
 
