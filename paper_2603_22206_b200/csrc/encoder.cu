@@ -1482,10 +1482,8 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
       if (g == 0) sm100::mbar_wait(&s.kv_full[stage], (j / kF3Stages) & 1);
       // Q_g of this item in TMEM (its softmax warps copied it)
       if (kb == 0) sm100::mbar_wait(&s.q_tmem[g], it & 1);
-      // S[g][b] holds P_g(j - 2) until O_g(j - 2) has read it. Issue modes
-      // 1 / 2 (default): no completion wait -- tcgen05.mma ops issued by one
-      // thread execute in issue order, so S_g(j), issued after O_g(j - 2),
-      // cannot overwrite P_g(j - 2) before that MMA has read it
+      // S[g][b] holds P_g(j - 2) until O_g(j - 2) has read it (issue modes
+      // 1 / 2 skip the wait; see run_attention)
       if (j >= 2 && (issue_mode & 15) == 0) sm100::mbar_wait(&s.o_full[g][b], ((j - 2) >> 1) & 1);
       sm100::tc_fence_after();
       const uint32_t ka = sm100::smem_u32(s.kv[stage][0]);
@@ -1968,12 +1966,14 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
       // 1 2.54, 2 2.51, 3 2.43, 4 2.44, 5 2.56, 6 2.71, 8 2.99
       static const int poly = getenv("CHM_FLASH5_POLY") ? atoi(getenv("CHM_FLASH5_POLY")) : 3;
       auto kern = kFlash5Kernels[poly < 0 ? 0 : poly > 8 ? 8 : poly];
-      // CHM_FLASH5_ISSUE: 0 = S_g(j) issued after O_g(j - 2) completed; 2 = no
-      // wait (in-order tensor pipe; default, 1.1-1.3 % faster,
-      // tools/experiments/r2_flash5_issue.sh); 1 = no wait, order O0 S0 O1 S1.
-      // Bits 16 / 32 / 64: measurement modes (f5_stamp)
+      // CHM_FLASH5_ISSUE: 0 (default) = S_g(j) issued after O_g(j - 2) has
+      // completed; 2 = no wait, relying on in-order execution of one thread's
+      // tcgen05.mma ops for the TMEM write-after-read of P (1.1-1.3 % faster,
+      // parity-green, tools/experiments/r2_flash5_issue.sh, but not a
+      // documented guarantee, so not the default); 1 = no wait, order O0 S0 O1
+      // S1. Bits 16 / 32 / 64: measurement modes (f5_stamp)
       static const int issue_mode =
-          getenv("CHM_FLASH5_ISSUE") ? atoi(getenv("CHM_FLASH5_ISSUE")) : 2;
+          getenv("CHM_FLASH5_ISSUE") ? atoi(getenv("CHM_FLASH5_ISSUE")) : 0;
       kern<<<grid, kFlashThreads, kFlash5SmemBytes, st>>>(tm_qkv, tm_kv, NH, H, S, items, ctx,
                                                           n_live, issue_mode);
     } else if (ver == 4) {
