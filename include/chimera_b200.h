@@ -567,6 +567,15 @@ chm_status chm_attention_bf16(const void* qkv, void* ctx, int32_t n_seq, int32_t
 chm_status chm_qkv_attention_bf16(const void* x, const void* w_qkv, const float* b_qkv,
                                   void* ctx, int32_t n_seq, int32_t hidden, void* stream);
 
+/* Fused feed-forward sublayer for hidden = 256 (the small router):
+ *   x <- LayerNorm(x + GELU(x . w1^T + b1) . w2^T + b2) * gamma + beta
+ * in place, the [M, F] intermediate kept on chip. w1 = [F, 256], w2 = [256, F]
+ * bf16, F % 128 == 0, 128 <= F <= 4096; replaces chm_gemm_bf16 (epilogue 2)
+ * + chm_gemm_bf16_ln for the encoder's FFN (router.py:34-45's paper encoder). */
+chm_status chm_ffn_fused_bf16(void* x, const void* w1, const float* b1, const void* w2,
+                              const float* b2, const float* gamma, const float* beta, float eps,
+                              int32_t M, int32_t hidden, int32_t ffn, void* stream);
+
 /* Profiling: launch counters per kernel class (always on) and opt-in CUDA
  * event timing around every launch on its own stream. Classes: 0 GEMM,
  * 1 attention, 2 row-wise (embedding+LN, LayerNorm, head), 3 predictor,

@@ -313,6 +313,9 @@ _SIGNATURES = [
      [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p]),
     ("chm_qkv_attention_bf16", c_int32,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
+    ("chm_ffn_fused_bf16", c_int32,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_float,
+      c_int32, c_int32, c_int32, c_void_p]),
     ("chm_comm_available", c_int32, []),
     ("chm_comm_unique_id", c_int32, [c_void_p]),
     ("chm_comm_init", c_int32, [c_void_p, c_int32, c_int32, c_int32, c_void_p]),

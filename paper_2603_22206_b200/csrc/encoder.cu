@@ -2001,6 +2001,17 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
   return CHM_OK;
 }
 
+}  // namespace enc
+chm_status ffn_fused(const void* x, const void* w1, const float* b1, const void* w2,
+                     const float* b2, const float* gamma, const float* beta, float eps, int M,
+                     int H, int F, const int32_t* live_rows, int live_mult, cudaStream_t st);
+namespace enc {
+// CHM_FFN_FUSED (default 1): the fused FFN sublayer for H = 256 routers
+static bool ffn_fused_on(int H, int F) {
+  static const int on = getenv("CHM_FFN_FUSED") ? atoi(getenv("CHM_FFN_FUSED")) : 1;
+  return on && H == 256 && F % 128 == 0 && F >= 128 && F <= 4096;
+}
+
 template <int VEC>
 static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weights& w,
                               const chm_encoder_workspace& ws, const int32_t* ids,
@@ -2164,6 +2175,14 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       go.eps = eps;
       rc = gemm_run(ctx, w.w_o[l], x, (int)T, H, H, go, st);
       if (rc != CHM_OK) return rc;
+      if (ffn_fused_on(H, F)) {
+        // H = 256: FFN1 + GELU + FFN2 + residual + LayerNorm in one kernel,
+        // the [T, F] intermediate never reaching HBM (ffn_fused.cu)
+        rc = ffn_fused(x, w.w_1[l], w.b_1[l], w.w_2[l], w.b_2[l], w.ln2_g[l], w.ln2_b[l], eps,
+                       (int)T, H, F, n_rows_dev, S, st);
+        if (rc != CHM_OK) return rc;
+        continue;
+      }
       GemmArgs g1;
       g1.live_rows = n_rows_dev;
       g1.live_mult = S;

@@ -237,3 +237,45 @@ def test_encoder_random_layernorm_params(cfg, S, flags):
     torch.cuda.synchronize()
     err = np.abs(q.view(B, K).cpu().numpy() - _ref_q(r, ids)).max()
     assert err <= Q_TOL, err
+
+
+@pytest.mark.parametrize("M,Fd", [(256, 1024), (1000, 1024), (131072, 1024), (777, 512),
+                                  (300, 128), (5000, 2048)])
+def test_ffn_fused_matches_two_gemms(M, Fd):
+    """Fused H = 256 FFN sublayer (ffn_fused.cu) vs fp32 and vs the unfused
+    FFN1 (bias + GELU) + FFN2 (bias + residual + LayerNorm) GEMMs on the same
+    bf16 operands."""
+    H = 256
+    g = torch.Generator(device="cuda").manual_seed(M + Fd)
+    x = (torch.randn(M, H, device="cuda", generator=g) + 0.3).to(torch.bfloat16)
+    w1 = (torch.randn(Fd, H, device="cuda", generator=g) / math.sqrt(H)).to(torch.bfloat16)
+    w2 = (torch.randn(H, Fd, device="cuda", generator=g) / math.sqrt(Fd)).to(torch.bfloat16)
+    b1 = 0.1 * torch.randn(Fd, device="cuda", generator=g)
+    b2 = 0.1 * torch.randn(H, device="cuda", generator=g)
+    gamma = 1 + 0.1 * torch.randn(H, device="cuda", generator=g)
+    beta = 0.1 * torch.randn(H, device="cuda", generator=g)
+    st = torch.cuda.current_stream().cuda_stream
+    h = F.gelu(x.float() @ w1.float().T + b1, approximate="tanh").to(torch.bfloat16)
+    ref = F.layer_norm(h.float() @ w2.float().T + b2 + x.float(), (H,), gamma, beta, 1e-12)
+    # unfused path
+    hu = gemm(x, w1, b1, None, 2)
+    yu = torch.empty_like(x)
+    _lib.check(_lib.load().chm_gemm_bf16_ln(
+        hu.data_ptr(), w2.data_ptr(), yu.data_ptr(), b2.data_ptr(), x.data_ptr(),
+        gamma.data_ptr(), beta.data_ptr(), 1e-12, M, H, Fd, st), "gemm_ln")
+    # fused, in place
+    y = x.clone()
+    _lib.check(_lib.load().chm_ffn_fused_bf16(
+        y.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+        gamma.data_ptr(), beta.data_ptr(), 1e-12, M, H, Fd, st), "ffn_fused")
+    torch.cuda.synchronize()
+    torch.testing.assert_close(y.float(), ref, rtol=GEMM_RTOL, atol=GEMM_ATOL)
+    assert (y.float() - yu.float()).abs().max().item() <= 2e-2
+
+
+def test_ffn_fused_rejects_shapes():
+    lib = _lib.load()
+    assert lib.chm_ffn_fused_bf16(1, 1, 1, 1, 1, 1, 1, 1e-12, 10, 768, 1024, None) == \
+        _lib.CHM_ERR_UNSUPPORTED
+    assert lib.chm_ffn_fused_bf16(1, 1, 1, 1, 1, 1, 1, 1e-12, 10, 256, 1000, None) == \
+        _lib.CHM_ERR_UNSUPPORTED

@@ -14,7 +14,7 @@ __global__ void probe(long long* cyc, uint32_t* sink, float seed) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const float f = -0.001f * (threadIdx.x + i) + seed;
-    if (KIND == 0) v[i] = __float_as_uint(f);
+    if (KIND == 0 || KIND == 3) v[i] = __float_as_uint(f);
     else if (KIND == 1) { __half2 h = __floats2half2_rn(f, f * 0.5f); v[i] = *reinterpret_cast<uint32_t*>(&h); }
     else { v[i] = (__float_as_uint(f) >> 16) | (__float_as_uint(f * 0.5f) & 0xffff0000u); }
   }
@@ -25,7 +25,8 @@ __global__ void probe(long long* cyc, uint32_t* sink, float seed) {
     for (int i = 0; i < 8; ++i) {
       if (KIND == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+r"(v[i]));
       else if (KIND == 1) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v[i]));
-      else asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(v[i]));
+      else if (KIND == 2) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(v[i]));
+      else asm volatile("tanh.approx.f32 %0, %0;" : "+r"(v[i]));
     }
   }
   const long long t1 = clock64();
@@ -42,18 +43,20 @@ int main() {
   uint32_t* sink;
   cudaMalloc(&cyc, 8);
   cudaMalloc(&sink, 4096);
-  const char* names[3] = {"ex2.approx.ftz.f32", "ex2.approx.f16x2", "ex2.approx.ftz.bf16x2"};
-  for (int k = 0; k < 3; ++k) {
+  const char* names[4] = {"ex2.approx.ftz.f32", "ex2.approx.f16x2", "ex2.approx.ftz.bf16x2",
+                          "tanh.approx.f32"};
+  for (int k = 0; k < 4; ++k) {
     for (int threads : {128, 512}) {
       if (k == 0) probe<0><<<1, threads>>>(cyc, sink, 0.3f);
       if (k == 1) probe<1><<<1, threads>>>(cyc, sink, 0.3f);
       if (k == 2) probe<2><<<1, threads>>>(cyc, sink, 0.3f);
+      if (k == 3) probe<3><<<1, threads>>>(cyc, sink, 0.3f);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
       long long c;
       cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       const double instrs = (double)threads * N * 8;  // thread-level MUFU ops
-      const double results = instrs * (k == 0 ? 1 : 2);
+      const double results = instrs * (k == 0 || k == 3 ? 1 : 2);
       printf("%-22s threads %3d: %.2f thread-ops/cycle/SM, %.2f exp2 results/cycle/SM\n", names[k],
              threads, instrs / c, results / c);
     }
