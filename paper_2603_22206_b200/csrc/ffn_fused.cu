@@ -232,9 +232,7 @@ __global__ void __maxnreg__(96)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           sm100::mma_bf16_cg2_w(tmem + b * kChunk, sm100::umma_desc_sw128(a + k * 32),
-                                sm100::umma_desc_sw128(w + k * 32),
-                                (dbg & 2) ? sm100::umma_idesc_bf16(256, 256) : idesc1,
-                                (kb | k) != 0);
+                                sm100::umma_desc_sw128(w + k * 32), idesc1, (kb | k) != 0);
         sm100::mma_commit_cg2_mc_w(&s.empty1[slot1], 0x3);
         if (++slot1 == kSlots1) { slot1 = 0; ph1 ^= 1; }
       }
