@@ -91,7 +91,10 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ src, 
 
 // K1: x[t] = LN(word_emb[id] + pos_emb[pos] + type_emb), t = seq*S + pos.
 // Sequence i reads token ids of batch row rows[i] (rows == nullptr: row i).
-template <int VEC>
+// A warp handles R consecutive tokens with all their gathers in flight at
+// once (one dependent id -> embedding-row chain per token is otherwise the
+// whole cost: the kernel is latency-bound, ~0.55 of HBM bandwidth with R = 1).
+template <int VEC, int R>
 __global__ void __launch_bounds__(256) embed_ln_kernel(
     const int32_t* __restrict__ ids, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ n_rows_dev, int n_seq, int S, int vocab,
@@ -100,24 +103,38 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(
     const float* __restrict__ b, float eps, __nv_bfloat16* __restrict__ x) {
   constexpr int H = 32 * 8 * VEC;
   const int lane = threadIdx.x & 31;
-  const long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= (long long)n_seq * S) return;
-  const int seq = (int)(t / S), pos = (int)(t - (long long)seq * S);
+  const long long t0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  const long long T = (long long)n_seq * S;
+  if (t0 >= T) return;
   const int n_live = n_rows_dev ? *n_rows_dev : n_seq;
-  if (seq >= n_live) return;  // rows on the reuse branch are never encoded
-  int row = seq;
-  if (rows) row = rows[seq];
-  int id = ids[(size_t)row * S + pos];
-  id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
-  float v[VEC * 8], w[VEC * 8];
-  load_row<VEC>(wemb + (size_t)id * H, lane, v);
-  load_row<VEC>(pemb + (size_t)pos * H, lane, w);
+  int id[R], pos[R];
+  bool ok[R];
 #pragma unroll
-  for (int j = 0; j < VEC * 8; ++j) v[j] += w[j];
+  for (int r = 0; r < R; ++r) {
+    const long long t = t0 + r;
+    const int seq = (int)(t / S);
+    pos[r] = (int)(t - (long long)seq * S);
+    ok[r] = t < T && seq < n_live;  // rows on the reuse branch are never encoded
+    int row = seq;
+    if (ok[r] && rows) row = rows[seq];
+    int i = ok[r] ? ids[(size_t)row * S + pos[r]] : 0;
+    id[r] = i < 0 ? 0 : (i >= vocab ? vocab - 1 : i);
+  }
+  float w[VEC * 8];
   load_row<VEC>(temb, lane, w);
+  float v[R][VEC * 8];
 #pragma unroll
-  for (int j = 0; j < VEC * 8; ++j) v[j] += w[j];
-  ln_row_store<VEC>(v, g, b, eps, lane, x + (size_t)t * H);
+  for (int r = 0; r < R; ++r) load_row<VEC>(wemb + (size_t)id[r] * H, lane, v[r]);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float p[VEC * 8];
+    load_row<VEC>(pemb + (size_t)pos[r] * H, lane, p);
+#pragma unroll
+    for (int j = 0; j < VEC * 8; ++j) v[r][j] += p[j] + w[j];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (ok[r]) ln_row_store<VEC>(v[r], g, b, eps, lane, x + (size_t)(t0 + r) * H);
 }
 
 // ---------------------------------------------------------------------------
@@ -2024,10 +2041,17 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
   auto* ctx = reinterpret_cast<__nv_bfloat16*>(ws.ctx);
   auto* tmp = reinterpret_cast<__nv_bfloat16*>(ws.tmp);
   auto* ffn = reinterpret_cast<__nv_bfloat16*>(ws.ffn);
-  const int rows_per_cta = 256 / 32;
+  // tokens per warp in the embedding kernel (CHM_EMBED_ROWS: 1 / 2 / 4;
+  // tools/experiments/r2_embed_rows.sh: H 256 -> 4 (148 -> 137 us at cfg4),
+  // H 768 -> 2 (376 -> 372 us at cfg3; 4 spills occupancy: 606 us))
+  static const int er_env = getenv("CHM_EMBED_ROWS") ? atoi(getenv("CHM_EMBED_ROWS")) : 0;
+  const int er = er_env ? er_env : (VEC == 1 ? 4 : 2);
+  const int rows_per_cta = (256 / 32) * er;
   const unsigned grid_t = (unsigned)((T + rows_per_cta - 1) / rows_per_cta);
   prof::begin(prof::K_ROWWISE, st);
-  embed_ln_kernel<VEC><<<grid_t, 256, 0, st>>>(
+  auto embed = er == 1 ? embed_ln_kernel<VEC, 1> : er == 2 ? embed_ln_kernel<VEC, 2>
+                                                           : embed_ln_kernel<VEC, 4>;
+  embed<<<grid_t, 256, 0, st>>>(
       ids, rows, n_rows_dev, n_seq, S, cfg.vocab,
       reinterpret_cast<const __nv_bfloat16*>(w.word_emb),
       reinterpret_cast<const __nv_bfloat16*>(w.pos_emb),
