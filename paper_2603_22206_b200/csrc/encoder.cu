@@ -1706,6 +1706,310 @@ __global__ void __launch_bounds__(kFlashThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 attention for S = 256 n, v6: the two query tiles of an item PING-PONG.
+// v5 ran both tiles' softmax in lockstep, so their serial phases (TMEM loads
+// of S, the row max, the P stores) coincided and left MUFU idle for ~45 % of
+// the block period (profiles/r2_flash5_analysis.md). Here each tile has one
+// 128-key S buffer, and a tile's softmax alternates with its own MMA chain
+// while the other tile's softmax fills the gap (FlashAttention-4's schedule).
+// P_g(j) (bf16) is stored over S_g's upper 64 columns, so the lower half of
+// S_g(j + 1) (keys 0-63) is issued as soon as the softmax holds S_g(j) in
+// registers and only the upper half waits for O_g(j) to have read P_g(j).
+//   warp 0      TMA: Q (double-buffered across items), K/V ring of 128 keys
+//   warps 1, 10 MMA issuers of tile 0 / tile 1 (independent, so the tiles
+//               drift freely): S_g(j + 1) low half, O_g(j) (+ l_g), S_g(j + 1)
+//               high half
+//   warps 2-5   tile 0, warps 6-9 tile 1 (TMEM lane quarter = warp % 4)
+// TMEM: S_g at 128 g, O_g at 256 + 64 g, Q_g at 384 + 32 g, l_g at 448 + 16 g.
+// 352 threads, one CTA per SM (three warps on an SM sub-partition: 168
+// registers, the 128 scores a thread holds).
+// ---------------------------------------------------------------------------
+constexpr int kF6Keys = 128;
+constexpr int kF6Stages = 3;
+constexpr int kF6Threads = 352;
+struct Flash6Smem {
+  uint8_t q[2][2][kAttnS * 64 * 2];            // [item parity][tile] Q [128][64]
+  uint8_t kv[kF6Stages][2][kF6Keys * 64 * 2];  // [stage][K | V] [128 keys][64]
+  uint8_t ones[16 * 128];                      // bf16 1.0 (K-major B, N = 16)
+  uint64_t q_full[2], q_empty[2], kv_full[kF6Stages], kv_empty[kF6Stages];
+  uint64_t q_tmem[2], s_full[2], p_full[2], o_done[2], s_free[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kFlash6SmemBytes = sizeof(Flash6Smem) + 1024;
+
+// issue_mode bit 16: CTA 0's per-block stamps into ctx as int64 [64][4] =
+// {S0 landed, P0 stored, S1 landed, P1 stored} (ctx is not written)
+template <int kPoly>
+__global__ void __launch_bounds__(kF6Threads, 1)
+    attention_flash6_kernel(const __grid_constant__ CUtensorMap tm_qkv, int n_heads, int hidden,
+                            int S, int n_items, __nv_bfloat16* __restrict__ ctx,
+                            const int32_t* __restrict__ n_live, int issue_mode) {
+  extern __shared__ uint8_t smem_raw[];
+  Flash6Smem& s = sm100::align_smem_1024<Flash6Smem>(smem_raw);
+  const int warp = sm100::warp_id(), lane = threadIdx.x & 31;
+  const int n_kb = S / kF6Keys;
+  const int n_qp = S / (2 * kAttnS);
+  constexpr uint32_t kQTile = kAttnS * 64 * 2;
+  constexpr uint32_t kKvTile = kF6Keys * 64 * 2;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_qkv);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s.q_full[i], 1);
+      sm100::mbar_init(&s.q_empty[i], 256);  // both tiles' softmax threads copied Q out
+      sm100::mbar_init(&s.q_tmem[i], 128);
+      sm100::mbar_init(&s.s_full[i], 1);
+      sm100::mbar_init(&s.p_full[i], 128);
+      sm100::mbar_init(&s.o_done[i], 1);
+      sm100::mbar_init(&s.s_free[i], 128);
+    }
+    for (int i = 0; i < kF6Stages; ++i) {
+      sm100::mbar_init(&s.kv_full[i], 1);
+      sm100::mbar_init(&s.kv_empty[i], 2);  // O_0(j) and O_1(j)
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(&s.tmem_base);
+  for (int i = threadIdx.x; i < 16 * 128 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s.ones)[i] = 0x3F803F80u;  // two bf16 1.0
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = sm100::uniform(s.tmem_base);
+  if (n_live) n_items = min(n_items, *n_live * n_heads * n_qp);
+  const int n_my = blockIdx.x < n_items ? (n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int J = n_my * n_kb;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t kv_phase = 0;
+      for (int it = 0; it < n_my; ++it) {
+        const int item = (int)blockIdx.x + it * (int)gridDim.x;
+        const int qp = item % n_qp, sh = item / n_qp;
+        const int seq = sh / n_heads, h = sh - seq * n_heads;
+        const int row0 = seq * S;
+        const int qb = it & 1;
+        sm100::mbar_wait(&s.q_empty[qb], ((it >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&s.q_full[qb], 2 * kQTile);
+        sm100::tma_load_2d(s.q[qb][0], &tm_qkv, &s.q_full[qb], h * 64, row0 + qp * 256);
+        sm100::tma_load_2d(s.q[qb][1], &tm_qkv, &s.q_full[qb], h * 64, row0 + qp * 256 + 128);
+        for (int kb = 0; kb < n_kb; ++kb) {
+          sm100::mbar_wait(&s.kv_empty[stage], kv_phase ^ 1);
+          sm100::mbar_arrive_expect_tx(&s.kv_full[stage], 2 * kKvTile);
+          sm100::tma_load_2d(s.kv[stage][0], &tm_qkv, &s.kv_full[stage], hidden + h * 64,
+                             row0 + kb * kF6Keys);
+          sm100::tma_load_2d(s.kv[stage][1], &tm_qkv, &s.kv_full[stage], 2 * hidden + h * 64,
+                             row0 + kb * kF6Keys);
+          if (++stage == kF6Stages) { stage = 0; kv_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 10) {
+    // ---------------- MMA issuers, one warp per tile (warp-uniform) ----------------
+    // P_g(j) sits over S_g's upper 64 columns, so the lower half of S_g(j + 1)
+    // (keys 0-63) is issued once the softmax holds S_g(j) in registers
+    // (s_free) and only the upper half waits for O_g(j) to read P_g(j).
+    const int g = warp == 1 ? 0 : 1;
+    constexpr uint32_t idesc_s = sm100::umma_idesc_bf16(128, 64);
+    constexpr uint32_t idesc_o = sm100::umma_idesc_bf16(128, 64) | (1u << 16);  // V MN-major
+    constexpr uint32_t idesc_l = sm100::umma_idesc_bf16(128, 16);
+    // keys [64 half, 64 half + 64) of S_g(j) = Q_g K_j^T (A = Q_g from TMEM)
+    auto issue_s = [&](int j, int half) {
+      const int it = j / n_kb, kb = j - it * n_kb, stage = j % kF6Stages;
+      if (half == 0) {
+        sm100::mbar_wait(&s.kv_full[stage], (j / kF6Stages) & 1);
+        if (kb == 0) sm100::mbar_wait(&s.q_tmem[g], it & 1);
+      }
+      sm100::tc_fence_after();
+      const uint32_t ka = sm100::smem_u32(s.kv[stage][0]) + half * 64 * 128;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sm100::mma_bf16_ts_w(tmem + 128 * g + 64 * half, tmem + 384 + 32 * g + k * 8,
+                             sm100::umma_desc_sw128(ka + k * 32), idesc_s, k);
+      if (half == 1) sm100::mma_commit_w(&s.s_full[g]);
+    };
+    // O_g += P_g(j) V_j, l_g += P_g(j) . 1 (A = P_g from TMEM)
+    auto issue_o = [&](int j) {
+      const int kb = j % n_kb, stage = j % kF6Stages;
+      sm100::mbar_wait(&s.p_full[g], j & 1);
+      sm100::tc_fence_after();
+      const uint32_t va = sm100::smem_u32(s.kv[stage][1]);
+      const uint32_t oa = sm100::smem_u32(s.ones);
+      const uint32_t pa = tmem + 128 * g + 64;
+#pragma unroll
+      for (int kk = 0; kk < kF6Keys / 16; ++kk) {
+        sm100::mma_bf16_ts_w(tmem + 256 + 64 * g, pa + kk * 8,
+                             sm100::umma_desc_sw128(va + kk * 2048), idesc_o, (kb | kk) != 0);
+        sm100::mma_bf16_ts_w(tmem + 448 + 16 * g, pa + kk * 8,
+                             sm100::umma_desc_sw128(oa + (kk & 3) * 32), idesc_l, (kb | kk) != 0);
+      }
+      sm100::mma_commit_w(&s.o_done[g]);
+      sm100::mma_commit_w(&s.kv_empty[stage]);
+    };
+    if (J > 0) {
+      issue_s(0, 0);
+      issue_s(0, 1);
+    }
+    for (int j = 0; j < J; ++j) {
+      if (j + 1 < J) {
+        sm100::mbar_wait(&s.s_free[g], j & 1);  // S_g(j) is in the softmax's registers
+        issue_s(j + 1, 0);
+      }
+      issue_o(j);
+      if (j + 1 < J) {
+        // the upper half of S_g(j + 1) overwrites P_g(j): only after O_g(j) read it
+        sm100::mbar_wait(&s.o_done[g], j & 1);
+        issue_s(j + 1, 1);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 2 && warp < 10) {
+    // ---------------- Q -> TMEM, softmax; tile g ----------------
+    const int g = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t s_tm = lane_base + 128 * g;
+    const uint32_t o_tm = lane_base + 256 + 64 * g;
+    const uint32_t q_tm = lane_base + 384 + 32 * g;
+    const uint32_t l_tm = lane_base + 448 + 16 * g;
+    constexpr float kLog2e = 1.4426950408889634f;
+    auto copy_q = [&](int it) {
+      const int qb = it & 1;
+      sm100::mbar_wait(&s.q_full[qb], (it >> 1) & 1);
+      const uint8_t* qrow = s.q[qb][g] + r * 128;
+      uint32_t qv[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 u = *reinterpret_cast<const uint4*>(qrow + ((c ^ (r & 7)) << 4));
+        qv[4 * c] = u.x; qv[4 * c + 1] = u.y; qv[4 * c + 2] = u.z; qv[4 * c + 3] = u.w;
+      }
+      sm100::tmem_st_32x32b_x32(q_tm, qv);
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.q_tmem[g]);
+      sm100::mbar_arrive(&s.q_empty[qb]);
+    };
+    if (n_my > 0) copy_q(0);
+    float m_use = -INFINITY;
+    for (int j = 0, it = 0, kb = 0; j < J; ++j) {
+      if (kb == 0) m_use = -INFINITY;
+      sm100::mbar_wait(&s.s_full[g], j & 1);
+      sm100::tc_fence_after();
+      if ((issue_mode & 16) && blockIdx.x == 0 && quarter == 0 && lane == 0 && j < 64)
+        reinterpret_cast<long long*>(ctx)[j * 4 + 2 * g] = clock64();
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sm100::tmem_ld_32x32b_x32(s_tm + 32 * c, sv[c]);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.s_free[g]);
+      float mq[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        mq[t] = fmaxf(__uint_as_float(sv[t][0]), __uint_as_float(sv[t][1]));
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int e = 2; e < 32; e += 2)
+          mq[t] = fmaxf(mq[t], fmaxf(__uint_as_float(sv[t][e]), __uint_as_float(sv[t][e + 1])));
+      const float mxl = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * kLog2e;
+      const bool grow = mxl > m_use + 8.0f;
+      if (__any_sync(0xffffffffu, grow) && kb > 0) {
+        // O_g(j - 1) has completed: S_g(j) was issued after it
+        const float alpha = grow ? sm100::ex2_approx(m_use - mxl) : 1.f;
+        uint32_t ov[32];
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          sm100::tmem_ld_32x32b_x32(o_tm + 32 * c, ov);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          sm100::tmem_st_32x32b_x32(o_tm + 32 * c, ov);
+        }
+        uint32_t l1 = sm100::tmem_ld_32x32b_x1(l_tm);
+        sm100::tmem_ld_wait();
+        sm100::tmem_st_32x32b_x1(l_tm, __float_as_uint(__uint_as_float(l1) * alpha));
+      }
+      if (grow) m_use = mxl;
+      // x = s log2e - m in FFMA2 pairs; kPoly pairs in 8 on the FMA pipes
+      const uint64_t l2e2 = sm100::f2_pack(kLog2e, kLog2e), negm2 = sm100::f2_pack(-m_use, -m_use);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint64_t x = sm100::f2_fma(
+              sm100::f2_pack(__uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1])),
+              l2e2, negm2);
+          if ((e & 7) < kPoly) {
+            pk[e] = sm100::exp2_poly2_bf16(x);
+          } else {
+            float x0, x1;
+            sm100::f2_unpack(x, x0, x1);
+            const __nv_bfloat162 pv =
+                __floats2bfloat162_rn(sm100::ex2_approx(x0), sm100::ex2_approx(x1));
+            pk[e] = *reinterpret_cast<const uint32_t*>(&pv);
+          }
+        }
+        sm100::tmem_st_32x32b_x16(s_tm + 64 + 16 * c, pk);  // P over S columns 64-127
+      }
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s.p_full[g]);
+      if ((issue_mode & 16) && blockIdx.x == 0 && quarter == 0 && lane == 0 && j < 64)
+        reinterpret_cast<long long*>(ctx)[j * 4 + 2 * g + 1] = clock64();
+      if (++kb == n_kb) {
+        kb = 0;
+        if (++it < n_my) copy_q(it);
+        // the item's last O_g / l_g, normalised, to ctx
+        sm100::mbar_wait(&s.o_done[g], j & 1);
+        sm100::tc_fence_after();
+        uint32_t ov[2][32];
+        sm100::tmem_ld_32x32b_x32(o_tm, ov[0]);
+        sm100::tmem_ld_32x32b_x32(o_tm + 32, ov[1]);
+        const uint32_t lb = sm100::tmem_ld_32x32b_x1(l_tm);
+        sm100::tmem_ld_wait();
+        sm100::tc_fence_before();
+        if (!(issue_mode & 16)) {
+          const int item = (int)blockIdx.x + (it - 1) * (int)gridDim.x;
+          const int qp = item % n_qp, sh = item / n_qp;
+          const int seq = sh / n_heads, h = sh - seq * n_heads;
+          const float inv = 1.0f / __uint_as_float(lb);
+          __nv_bfloat16* dst =
+              ctx + ((size_t)seq * S + qp * 256 + g * kAttnS + r) * hidden + h * 64;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            __align__(16) __nv_bfloat162 pq[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c0 = c * 8 + 2 * e;
+              pq[e] = __floats2bfloat162_rn(__uint_as_float(ov[c0 >> 5][c0 & 31]) * inv,
+                                            __uint_as_float(ov[(c0 + 1) >> 5][(c0 + 1) & 31]) * inv);
+            }
+            *reinterpret_cast<uint4*>(dst + c * 8) = *reinterpret_cast<uint4*>(pq);
+          }
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem);
+  }
+}
+using Flash6Fn = void (*)(const CUtensorMap, int, int, int, int, __nv_bfloat16*, const int32_t*,
+                          int);
+static const Flash6Fn kFlash6Kernels[9] = {
+    attention_flash6_kernel<0>, attention_flash6_kernel<1>, attention_flash6_kernel<2>,
+    attention_flash6_kernel<3>, attention_flash6_kernel<4>, attention_flash6_kernel<5>,
+    attention_flash6_kernel<6>, attention_flash6_kernel<7>, attention_flash6_kernel<8>};
+
 using Flash5Fn = void (*)(const CUtensorMap, const CUtensorMap, int, int, int, int,
                           __nv_bfloat16*, const int32_t*, int);
 static const Flash5Fn kFlash5Kernels[9] = {
@@ -1961,6 +2265,8 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
                          (int)kFlash4SmemBytes);
     for (auto k : kFlash5Kernels)
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlash5SmemBytes);
+    for (auto k : kFlash6Kernels)
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlash6SmemBytes);
     attr = true;
   }
   const int NH = H / 64;
@@ -1971,10 +2277,18 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
   } else if (S % (2 * kAttnS) == 0) {
     const int items = n_seq * NH * (S / (2 * kAttnS));
     const unsigned grid = (unsigned)(items < n_sms() ? items : n_sms());
-    // CHM_FLASH: 3 = 64-key blocks, double-buffered S, O in TMEM (default);
-    // 2 = 128-key blocks with the v2 softmax; 1 = the round-1 kernel
-    static const int ver = getenv("CHM_FLASH") ? atoi(getenv("CHM_FLASH")) : 5;
-    if (ver == 5) {
+    // CHM_FLASH: 6 = ping-pong tiles, 128-key blocks (default); 5 = 64-key
+    // blocks, both tiles in lockstep; 4 / 3 / 2 / 1 = earlier versions
+    static const int ver = getenv("CHM_FLASH") ? atoi(getenv("CHM_FLASH")) : 6;
+    if (ver == 6) {
+      // pairs of 8 whose exp2 runs as a polynomial on the FMA pipes
+      static const int poly = getenv("CHM_FLASH6_POLY") ? atoi(getenv("CHM_FLASH6_POLY")) : 3;
+      auto kern = kFlash6Kernels[poly < 0 ? 0 : poly > 8 ? 8 : poly];
+      static const int issue_mode =
+          getenv("CHM_FLASH5_ISSUE") ? atoi(getenv("CHM_FLASH5_ISSUE")) : 0;
+      kern<<<grid, kF6Threads, kFlash6SmemBytes, st>>>(tm_qkv, NH, H, S, items, ctx, n_live,
+                                                       issue_mode);
+    } else if (ver == 5) {
       CUtensorMap tm_kv;
       if (!gemm::make_tmap_bf16(&tm_kv, qk, (uint64_t)T, (uint64_t)3 * H, kF3Keys, 64, 0))
         return CHM_ERR_CUDA;

@@ -64,6 +64,22 @@ def main():
         for i in range(8, 20):
             print(f"{i:4d} " + " ".join(f"{int(v) - base:8d}" for v in t[i][:11]))
         return
+    if a.flash_timeline and os.environ.get("CHM_FLASH") in ("6", "7"):
+        attn()
+        torch.cuda.synchronize()
+        t = ctx.view(-1).view(torch.int64)[:256].cpu().view(64, 4).numpy()
+        base = int(t[4, 0])
+        names = ["S0_land", "P0_done", "S1_land", "P1_done"]
+        print("blk " + " ".join(f"{n:>9s}" for n in names) + "   (cycles from block 4 S0_land)")
+        for j in range(4, 24):
+            print(f"{j:3d} " + " ".join(f"{int(v) - base:9d}" for v in t[j]))
+        d = t[8:40]
+        per = (int(d[-1, 1]) - int(d[0, 1])) / (len(d) - 1)
+        print(f"period {per:.0f} cycles per 128-key block; softmax S->P tile0 "
+              f"{float((d[:,1]-d[:,0]).mean()):.0f}, tile1 {float((d[:,3]-d[:,2]).mean()):.0f}; "
+              f"P0(j)->S0(j+1) {float((d[1:,0]-d[:-1,1]).mean()):.0f}; "
+              f"S0->S1 land offset {float((d[:,2]-d[:,0]).mean()):.0f}")
+        return
     if a.flash_timeline:
         attn()
         torch.cuda.synchronize()
