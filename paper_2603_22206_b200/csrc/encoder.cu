@@ -2336,7 +2336,15 @@ chm_status run_attention(const __nv_bfloat16* qk, __nv_bfloat16* ctx, int n_seq,
 chm_status ffn_fused(const void* x, const void* w1, const float* b1, const void* w2,
                      const float* b2, const float* gamma, const float* beta, float eps, int M,
                      int H, int F, const int32_t* live_rows, int live_mult, cudaStream_t st);
+chm_status cls_pool_build_bd(const void* wqkv, int H, void* wk_bd, void* wv_bd, cudaStream_t st);
+chm_status cls_pool(const void* x, const void* u, void* xbar, int n_seq, int S, int H,
+                    const int32_t* n_live, cudaStream_t st);
 namespace enc {
+// CHM_CLS_POOL (default 1): the last layer's CLS attention by associativity
+static bool cls_pool_on() {
+  static const int on = getenv("CHM_CLS_POOL") ? atoi(getenv("CHM_CLS_POOL")) : 1;
+  return on != 0;
+}
 // CHM_FFN_FUSED (default 1): the fused FFN sublayer for H = 256 routers
 static bool ffn_fused_on(int H, int F) {
   static const int on = getenv("CHM_FFN_FUSED") ? atoi(getenv("CHM_FFN_FUSED")) : 1;
@@ -2414,18 +2422,26 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       auto* hc = qk;
       auto* qc = qk + (size_t)n_seq * H;
       auto* kvb = ffn;
-      GemmArgs gkv;
-      gkv.live_rows = n_rows_dev;
-      gkv.live_mult = S;
-      gkv.epilogue = 1;  // bias
-      gkv.bias = bq + H;
-      gkv.stats_in = st_in;
-      gkv.n_part = P;
-      gkv.colsum = cq + H;
-      gkv.eps = eps;
-      rc = gemm_run(x, reinterpret_cast<const __nv_bfloat16*>(wq) + (size_t)H * H, kvb, (int)T,
-                    2 * H, H, gkv, st);
-      if (rc != CHM_OK) return rc;
+      // Associative CLS attention (cls_pool.cu): no [T, 2H] K|V projection;
+      // U = Q_cls Wk_bd^T, xbar = pool(x, U), ctx = xbar Wv_bd^T + b_v, all in
+      // the FFN buffer. Needs the cluster-LN stream (x normalised in place).
+      const size_t bd = (size_t)NH * H * H, uxs = (size_t)n_seq * NH * H;
+      const bool pool = cls_pool_on() && cluster_ln && H % 256 == 0 && NH <= 16 &&
+                        2 * bd + 2 * uxs <= (size_t)ws.max_tokens * F;
+      if (!pool) {
+        GemmArgs gkv;
+        gkv.live_rows = n_rows_dev;
+        gkv.live_mult = S;
+        gkv.epilogue = 1;  // bias
+        gkv.bias = bq + H;
+        gkv.stats_in = st_in;
+        gkv.n_part = P;
+        gkv.colsum = cq + H;
+        gkv.eps = eps;
+        rc = gemm_run(x, reinterpret_cast<const __nv_bfloat16*>(wq) + (size_t)H * H, kvb, (int)T,
+                      2 * H, H, gkv, st);
+        if (rc != CHM_OK) return rc;
+      }
       prof::begin(prof::K_ROWWISE, st);
       ln_rows_kernel<VEC><<<(unsigned)((n_seq + 7) / 8), 256, 0, st>>>(x, S, n_seq, st_in, P,
                                                                        g_prev, b_prev, eps, hc,
@@ -2439,17 +2455,40 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
       gq.bias = w.b_qkv[l];
       rc = gemm_run(hc, w.w_qkv[l], qc, n_seq, H, H, gq, st);
       if (rc != CHM_OK) return rc;
-      const int items = n_seq * NH;
-      const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
-      prof::begin(prof::K_ATTENTION, st);
-      switch (S) {
-        case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
-        case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
-        case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
-        default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+      if (pool) {
+        auto* wk_bd = ffn;
+        auto* wv_bd = wk_bd + bd;
+        auto* ub = wv_bd + bd;
+        auto* xb = ub + uxs;
+        rc = cls_pool_build_bd(w.w_qkv[l], H, wk_bd, wv_bd, st);
+        if (rc != CHM_OK) return rc;
+        GemmArgs gu;
+        gu.live_rows = n_rows_dev;
+        gu.live_mult = 1;
+        rc = gemm_run(qc, wk_bd, ub, n_seq, NH * H, H, gu, st);
+        if (rc != CHM_OK) return rc;
+        rc = cls_pool(x, ub, xb, n_seq, S, H, n_rows_dev, st);
+        if (rc != CHM_OK) return rc;
+        GemmArgs gv;
+        gv.live_rows = n_rows_dev;
+        gv.live_mult = 1;
+        gv.epilogue = 1;
+        gv.bias = w.b_qkv[l] + 2 * H;
+        rc = gemm_run(xb, wv_bd, ctx_c, n_seq, H, NH * H, gv, st);
+        if (rc != CHM_OK) return rc;
+      } else {
+        const int items = n_seq * NH;
+        const unsigned cls_grid = (unsigned)((items + kClsWarps - 1) / kClsWarps);
+        prof::begin(prof::K_ATTENTION, st);
+        switch (S) {
+          case 128: attention_cls_kernel<128><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+          case 256: attention_cls_kernel<256><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+          case 384: attention_cls_kernel<384><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+          default: attention_cls_kernel<512><<<cls_grid, kClsWarps * 32, 0, st>>>(qc, kvb, items, NH, H, ctx_c, n_rows_dev); break;
+        }
+        prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
+        CHM_LAUNCH_CHECK();
       }
-      prof::end(prof::K_ATTENTION, st, 4.0 * S * 64.0 * items);
-      CHM_LAUNCH_CHECK();
       GemmArgs go;
       go.live_rows = n_rows_dev;
       go.live_mult = 1;

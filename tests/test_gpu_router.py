@@ -102,6 +102,23 @@ def test_encoder_matches_fp32(cfg, head_std):
     assert np.all((got >= 0) & (got <= 1))
 
 
+@pytest.mark.parametrize("S,B", [(128, 64), (512, 40)])
+def test_encoder_cls_pool_bert_base(S, B):
+    """Enough rows for the associative last layer (cls_pool.cu) at H = 768:
+    U = Q_cls Wk_bd^T, xbar = pool(x, U), ctx = xbar Wv_bd^T + b_v."""
+    from dataclasses import replace
+    cfg = replace(EncoderConfig(n_layers=2), seq_len=S)
+    K = 5
+    r = GpuEncoderRouter(cfg, K, max_rows=B, seed=6, head_std=2 / math.sqrt(768))
+    ids = torch.as_tensor(synthetic_token_ids(B, S, seed=17), device="cuda")
+    q = torch.zeros(B * K, dtype=torch.float64, device="cuda")
+    r.forward(ids, q)
+    torch.cuda.synchronize()
+    err = np.abs(q.view(B, K).cpu().numpy() - _ref_q(r, ids)).max()
+    print(f"cls_pool S={S} B={B}: max|dq| = {err:.2e}")
+    assert err <= Q_TOL, err
+
+
 @pytest.mark.parametrize("S", [256, 512])
 def test_encoder_long_prompts(S):
     """S > 128: flash-style key-block loop with online softmax (cfg5 S=512)."""
