@@ -622,7 +622,8 @@ def run_ours(args):
     roofline["secondary"] = sec
     stage_ms = {k: v["ms"] / args.steps for k, v in prof.items() if v["timed"]}
     # executed (trimmed) FLOPs: the last layer is computed for the CLS row only
-    router_flops = B * wl.spec.encoder.flops_executed_per_request(K)
+    cls_pool = os.environ.get("CHM_CLS_POOL", "1") != "0" and args.layernorm == "cluster"
+    router_flops = B * wl.spec.encoder.flops_executed_per_request(K, cls_pool=cls_pool)
     router_ms = (prof["gemm"]["ms"] + prof["attention"]["ms"] + prof["rowwise"]["ms"] +
                  prof["qkv_attention"]["ms"])
 

@@ -2465,6 +2465,7 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
         GemmArgs gu;
         gu.live_rows = n_rows_dev;
         gu.live_mult = 1;
+        gu.work_div = NH;
         rc = gemm_run(qc, wk_bd, ub, n_seq, NH * H, H, gu, st);
         if (rc != CHM_OK) return rc;
         rc = cls_pool(x, ub, xb, n_seq, S, H, n_rows_dev, st);
@@ -2474,6 +2475,7 @@ static chm_status run_rowwise(const chm_encoder_cfg& cfg, const chm_encoder_weig
         gv.live_mult = 1;
         gv.epilogue = 1;
         gv.bias = w.b_qkv[l] + 2 * H;
+        gv.work_div = NH;
         rc = gemm_run(xb, wv_bd, ctx_c, n_seq, H, NH * H, gv, st);
         if (rc != CHM_OK) return rc;
       } else {

@@ -85,6 +85,7 @@ struct EpiParams {
   float2* stats_out;       // EPI 6: [M][N/128]
   const int32_t* live_rows;  // rows computed: min(M, *live_rows * live_mult) (nullptr: M)
   int live_mult;
+  int work_div;        // measurement only (prof): algorithmic FLOPs = 2 M N K / work_div
   int dbg;             // measurement only: 1 = epilogue drains TMEM without math/stores,
                        // 2 = also no operand loads (MMAs on stale shared memory)
 };
@@ -713,7 +714,7 @@ static chm_status launch(const void* A, const void* B, void* C, const float* bia
   cfg.gridDim = dim3(cluster * n_clusters, 1, 1);
   prof::begin(prof::K_GEMM, s);
   cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, kStages, FOLD>, ta, tb, tc, tr, bias, M, N, K, ep);
-  prof::end(prof::K_GEMM, s, 2.0 * M * N * K);
+  prof::end(prof::K_GEMM, s, 2.0 * M * N * K / (ep.work_div > 0 ? ep.work_div : 1));
   if (e != cudaSuccess) return CHM_ERR_CUDA;
   CHM_LAUNCH_CHECK();
   return CHM_OK;
@@ -756,6 +757,7 @@ chm_status gemm_run(const void* A, const void* B, void* C, int M, int N, int K,
   ep.stats_out = g.stats_out;
   ep.live_rows = g.live_rows;
   ep.live_mult = g.live_mult;
+  ep.work_div = g.work_div;
   const float* bias = g.bias;
   const void* residual = g.residual;
   // measurement overrides: CHM_GEMM_STAGES (4 or 6 operand stages for the

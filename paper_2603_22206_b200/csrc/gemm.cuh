@@ -25,6 +25,9 @@ struct GemmArgs {
   // (the routed sequences of a tick; nullptr = all M rows)
   const int32_t* live_rows = nullptr;
   int live_mult = 1;
+  // measurement only: algorithmic FLOPs = 2 M N K / work_div (block-diagonal
+  // weights: the zero blocks are executed but are not work)
+  int work_div = 1;
 };
 
 chm_status gemm_run(const void* A, const void* B, void* C, int M, int N, int K,

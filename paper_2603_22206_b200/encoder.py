@@ -39,14 +39,21 @@ class EncoderConfig:
         L, S, H, F = self.n_layers, self.seq_len, self.hidden, self.ffn
         return L * (8 * S * H * H + 4 * S * S * H + 4 * S * H * F) + 2 * H * n_models
 
-    def flops_executed_per_request(self, n_models: int) -> int:
-        """FLOPs the device actually executes: the last layer projects Q and
-        runs attention for the [CLS] query only and its out-projection / FFN
-        for the CLS row only (the head reads h_[CLS] alone); all S tokens still
-        feed K and V."""
+    def flops_executed_per_request(self, n_models: int, cls_pool: bool = True) -> int:
+        """Algorithmic FLOPs of what the device executes: the last layer serves
+        the [CLS] query only (the head reads h_[CLS] alone). With the
+        associative form (csrc/cls_pool.cu, the default) it projects Q_cls,
+        forms u_h = W_k,h^T q_h (2 H^2), pools x twice (logits and
+        xbar_h = sum_j p_hj x_j: 4 S H per head) and applies W_v,h (2 H^2);
+        without it all S tokens feed the K|V projection (4 S H^2) and the CLS
+        attention (4 S H). Out-projection / FFN run on the CLS row only."""
         L, S, H, F = self.n_layers, self.seq_len, self.hidden, self.ffn
         full = (L - 1) * (8 * S * H * H + 4 * S * S * H + 4 * S * H * F)
-        last = 4 * S * H * H + 2 * H * H + 4 * S * H + 2 * H * H + 4 * H * F
+        if cls_pool:
+            attn = 2 * H * H + 2 * H * H + 4 * S * H * self.n_heads + 2 * H * H
+        else:
+            attn = 4 * S * H * H + 2 * H * H + 4 * S * H
+        last = attn + 2 * H * H + 4 * H * F
         return full + last + 2 * H * n_models
 
 
