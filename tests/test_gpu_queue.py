@@ -144,16 +144,21 @@ def test_queue_grid_wide_matches_single_cta(n):
     assert small["promoted"].sum() > 0 and len(small["admitted0"]) > 0
 
 
-@pytest.mark.parametrize("n,capacity", [(9000, 10240), (70000, 72000), (2000000, 2097152)])
+@pytest.mark.parametrize("n,capacity", [(9000, 10240), ((9000, 15000), 20480), (70000, 72000),
+                                        (2000000, 2097152)])
 def test_queue_order_random_large(n, capacity):
     """Full-size STJF order vs a numpy lexsort of (level, priority, arrival, seq);
-    70k entries per engine exercises the global-scratch path (cfg4 stress)."""
+    70k entries per engine exercises the global-scratch path (cfg4 stress);
+    (9000, 15000) at capacity 20480: one CTA keeps its keys in shared memory,
+    the other in global scratch (queue_kernel_dual)."""
+    ns = n if isinstance(n, tuple) else (n, n)
     rng = np.random.default_rng(5)
     pool = Pool((ModelProfile("m0", 1.0, 4), ModelProfile("m1", 2.0, 4)))
     gs = GpuScheduler(pool, router=ScoreTableRouter(), predictor=PrecomputedPredictor(),
                       n_programs=16, max_rows=16, queue_capacity=capacity)
     st = gs.state
     for m in range(2):
+        n = ns[m]
         prio = rng.lognormal(5, 2, n)
         prio[rng.random(n) < 0.2] = 37.0  # ties
         arr = np.sort(rng.random(n) * 100)
@@ -168,6 +173,7 @@ def test_queue_order_random_large(n, capacity):
     gs.run_rows(e, n_iterations=0)
     gs.check_errors()
     for m in range(2):
+        n = ns[m]
         b = m * st.capacity
         pr = st.q_priority[b:b + n].cpu().numpy()
         ar = st.q_arrival[b:b + n].cpu().numpy()
