@@ -1,5 +1,7 @@
 #!/usr/bin/env bash
 # flash v8 (v6 with two threads per query row) vs v6; parity; stamps
+# (the v8 kernel was measured from a working tree and not committed; this
+# script records the commands; CHM_FLASH=8 no longer selects it)
 cd "$(dirname "$0")/../.."
 for r in 1 2; do
   for v in 6 8; do
