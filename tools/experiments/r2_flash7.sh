@@ -1,5 +1,7 @@
 #!/usr/bin/env bash
 # flash v7 (P in its own TMEM columns, S(j+1) issued once S(j) is in registers)
+# (v7 was removed after this measurement -- see profiles/r2_flash5_analysis.md;
+# CHM_FLASH=7 no longer selects it)
 # vs v6 / v5 on one box, then v7 parity and CTA 0's per-block stamps.
 cd "$(dirname "$0")/../.."
 for r in 1 2; do

@@ -1,5 +1,7 @@
 #!/usr/bin/env bash
 # flash v7 with the issuer in event order vs v6; parity; stamps
+# (v7 was removed after this measurement -- see profiles/r2_flash5_analysis.md;
+# CHM_FLASH=7 no longer selects it)
 cd "$(dirname "$0")/../.."
 for r in 1 2; do
   for v in 6 7; do

@@ -1,5 +1,7 @@
 #!/usr/bin/env bash
 # K7 dual layout (shared-memory keys when a big-capacity segment holds <= 10240 entries)
+# (the dual-layout kernel was measured from a working tree -- slower, 0.498 vs
+# 0.469 ms at cfg4 -- and not committed; CHM_QUEUE_DUAL no longer exists)
 export PYTHONUNBUFFERED=1
 timeout 900 python -m pytest tests -m gpu -q -x -k "queue or engine_clock or complete or tick or bench" 2>&1 | tail -2
 for r in 1 2; do
