@@ -25,7 +25,9 @@ def main():
 
     wl = synth.make_workload(a.config)
     gs = GpuScheduler(wl.pool, wl.balancer, wl.aging, router=wl.router, predictor=wl.predictor,
-                      n_programs=wl.n_programs, max_rows=wl.batch_size)
+                      n_programs=wl.n_programs, max_rows=wl.batch_size,
+                      queue_capacity=wl.queue_capacity)
+    wl.seed_state(gs.state)  # cfg4: 64k in flight + 64k queued (as bench.py)
     snap = gs.state.snapshot()
     batches = [wl.batch(t) for t in range(2)]
     completions = wl.completions()  # cfg4: every engine's running batch turns over (as bench.py)
