@@ -501,10 +501,6 @@ def run_ours(args):
     iev = []
     for i in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        # hold the stream (~30 ms spin) while the host enqueues the eager tick,
-        # so the per-launch events time device work, not host launch gaps
-        with torch.cuda.stream(stream):
-            torch.cuda._sleep(60_000_000)
         a.record(stream)
         tick(i, eager=True)
         b.record(stream)
