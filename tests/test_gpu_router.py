@@ -102,7 +102,7 @@ def test_encoder_matches_fp32(cfg, head_std):
     assert np.all((got >= 0) & (got <= 1))
 
 
-@pytest.mark.parametrize("S,B", [(128, 64), (512, 40)])
+@pytest.mark.parametrize("S,B", [(128, 64), (256, 48), (384, 40), (512, 40)])
 def test_encoder_cls_pool_bert_base(S, B):
     """Enough rows for the associative last layer (cls_pool.cu) at H = 768:
     U = Q_cls Wk_bd^T, xbar = pool(x, U), ctx = xbar Wv_bd^T + b_v."""
