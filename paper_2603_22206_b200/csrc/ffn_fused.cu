@@ -23,7 +23,7 @@
 //
 //   warp 0      TMA: the tile's x (4 x [128 x 64] boxes), then W1 / W2
 //               k-blocks through two rings (W1: 4 x 8 KB, W2: 2 x 16 KB)
-//   warp 1      MMA issuer (the pair leader issues for both CTAs)
+//   warp 1      G1 issuer, warp 18 G2 issuer (the pair leader issues for both CTAs)
 //   warps 2-17  epilogue: warp w owns TMEM lanes 32 (w % 4) (token rows) and
 //               column group (w - 2) / 4: 32 of a chunk's 128 columns in E1,
 //               64 of the 256 output columns in the LayerNorm
@@ -52,7 +52,7 @@ constexpr int kChunk = 128;                   // hidden units per chunk
 // TMA round trip.
 constexpr int kSlots1 = 4, kSlots2 = 2;
 constexpr int kEpiWarps = 16;
-constexpr int kThreads = 64 + kEpiWarps * 32;  // 576
+constexpr int kThreads = 64 + kEpiWarps * 32 + 32;  // 608: + the G2 issuer (warp 18)
 constexpr int kMaxF = 4096;
 constexpr uint32_t kBox = kRows * 64 * 2;      // [128 rows][64 cols] bf16, 16 KB
 constexpr uint32_t kW1Bytes = 64 * 64 * 2;     // W1 k-block half: [64 rows][64] = 8 KB
@@ -213,8 +213,12 @@ __global__ void __maxnreg__(96)
       }
       if (!progressed) __nanosleep(20);
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (the leader issues for both CTAs) ----------------
+  } else if (warp == 1 || warp == 2 + kEpiWarps) {
+    // ---------------- MMA issuers (the leader issues for both CTAs) ----------------
+    // Warp 1 issues the G1 stream, warp 18 the G2 stream. Each waits only for
+    // its own operands (W1 / W2 ring, acc_h / H buffers), so a G2 whose W2
+    // k-blocks are still in flight no longer holds back the next G1 and vice
+    // versa (one issuer serialised both behind each ring's reload).
     constexpr uint32_t idesc1 = sm100::umma_idesc_bf16(256, kChunk);
     constexpr uint32_t idesc2 = sm100::umma_idesc_bf16(256, kH);
     int slot1 = 0, slot2 = 0;
@@ -261,28 +265,29 @@ __global__ void __maxnreg__(96)
       if (lane == 0 && gc2 < 32) stamp(dbg, x, gc2, 5);
       ++gc2;
     };
-    for (int it = 0; it < (leader ? n_my : 0); ++it) {
-      sm100::mbar_wait(&s.x_full, it & 1);
-      sm100::tc_fence_after();
-      for (int c = 0; c < min(2, n_chunks); ++c) g1(c);
-      if (n_chunks <= 2) sm100::mma_commit_cg2_mc_w(&s.x_empty, 0x3);
-      // G1(c + 2) needs only E1(c)'s drain of acc_h, G2(c) all of E1(c): the
-      // tensor pipe runs G1(c + 2) while E1(c) computes its GELU
-      for (int c = 0; c < n_chunks; ++c) {
-        if (c + 2 < n_chunks) {
-          g1(c + 2);
-          if (c + 2 == n_chunks - 1) sm100::mma_commit_cg2_mc_w(&s.x_empty, 0x3);
+    if (warp == 1) {
+      for (int it = 0; it < (leader ? n_my : 0); ++it) {
+        sm100::mbar_wait(&s.x_full, it & 1);
+        sm100::tc_fence_after();
+        for (int c = 0; c < n_chunks; ++c) {
+          g1(c);
+          if (c == n_chunks - 1) sm100::mma_commit_cg2_mc_w(&s.x_empty, 0x3);
         }
-        if (c == 0) {  // acc_y free: the previous tile's LayerNorm has read it
-          sm100::mbar_wait(&s.y_empty, (it & 1) ^ 1);
-          sm100::tc_fence_after();
-        }
-        g2(c);
       }
-      sm100::mma_commit_cg2_mc_w(&s.y_full, 0x3);
+    } else {
+      for (int it = 0; it < (leader ? n_my : 0); ++it) {
+        for (int c = 0; c < n_chunks; ++c) {
+          if (c == 0) {  // acc_y free: the previous tile's LayerNorm has read it
+            sm100::mbar_wait(&s.y_empty, (it & 1) ^ 1);
+            sm100::tc_fence_after();
+          }
+          g2(c);
+        }
+        sm100::mma_commit_cg2_mc_w(&s.y_full, 0x3);
+      }
     }
     __syncwarp();
-  } else {
+  } else if (warp >= 2 && warp < 2 + kEpiWarps) {
     // ---------------- epilogue ----------------
     const int quarter = warp & 3;
     const int grp = (warp - 2) >> 2;         // column group 0..3
